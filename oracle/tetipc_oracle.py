@@ -1,0 +1,776 @@
+"""CPU oracle for the GIPC barrier hot path -- TEST INFRASTRUCTURE ONLY.
+
+A batched NumPy restatement of the reference ``tetipc`` algorithm for the path
+SURVEY.md section 8 names.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s cpu_baseline / ``--impl reference`` legs may import this module;
+the product package ``paper_2308_09400_b200`` never does (it fails loudly when
+its CUDA library is missing).
+
+Parity status: PINNED.  ``tests/golden/make_golden.py`` imports the real
+reference (``/root/reference/pkg/src``, both its ``_numpy`` backend and its
+Cython ``_core`` backend built in /tmp) in the build container, runs it on seeded
+inputs and freezes the outputs under ``tests/golden/*.npz``;
+``tests/test_oracle_golden.py`` checks this restatement against those files and
+against the reference tests' own known-answer values.
+
+Every function cites the reference file:line it follows (paths relative to
+``/root/reference/pkg/src/tetipc``).  Nothing here is copied: the reference
+evaluates one stencil per Python call through objects; this file evaluates
+whole SoA stencil tables at once.  Floating point: all arithmetic is elementwise
+NumPy mul/add/div/sqrt (never einsum/BLAS) in the scalar left-to-right order of
+``kernels/_core.pyx`` so that, on an x86-64 host without FMA contraction, the
+discrete outputs (region codes, active tests, promotion) are bit-exact with the
+reference's compiled backend.
+
+Stencil table (SoA) used by the oracle and by the CUDA path alike:
+
+    kind   uint8 (n,)   code = rank of StencilKind.value in string order, which is
+                        the reference list order (proximity.py:27-34, :82-83):
+                        0 EE, 1 EE-par, 2 PE, 3 PE-par, 4 PP, 5 PP-par, 6 PT
+    verts  int32 (n,4)  global vertex ids, -1 padded (PE: 3, PP: 2)
+    sub    uint8 (n,)   parallel kinds: local indices of the reduced stencil, two
+                        bits each, entry k at bits [2k, 2k+2)   (proximity.py:57-60)
+    eps_x  f64   (n,)   parallel tolerance, 0 for non-parallel kinds
+"""
+
+import numpy as np
+
+EE, EEP, PE, PEP, PP, PPP, PT = range(7)
+KIND_NAMES = (
+    "edge-edge",
+    "edge-edge-parallel",
+    "point-edge",
+    "point-edge-parallel",
+    "point-point",
+    "point-point-parallel",
+    "point-triangle",
+)
+#: vertices per stencil kind (proximity.py:67-75)
+KIND_SIZE = np.array([4, 4, 3, 4, 2, 4, 4], dtype=np.int64)
+#: number of entries of ``sub`` per parallel kind
+SUB_LEN = np.array([0, 4, 0, 3, 0, 2, 0], dtype=np.int64)
+IS_PARALLEL = np.array([0, 1, 0, 1, 0, 1, 0], dtype=bool)
+
+STATUS_ACTIVE, STATUS_INACTIVE, STATUS_PENETRATION = 0, 1, 2
+
+# region code -> (reduced kind, local vertex selection); proximity.py:100-127
+PT_LOCAL = {
+    0: (PT, (0, 1, 2, 3)),
+    1: (PP, (0, 1)),
+    2: (PP, (0, 2)),
+    3: (PP, (0, 3)),
+    4: (PE, (0, 1, 2)),
+    5: (PE, (0, 2, 3)),
+    6: (PE, (0, 3, 1)),
+}
+EE_LOCAL = {
+    8: (EE, (0, 1, 2, 3)),
+    2: (PE, (0, 2, 3)),
+    5: (PE, (1, 2, 3)),
+    6: (PE, (2, 0, 1)),
+    7: (PE, (3, 0, 1)),
+    0: (PP, (0, 2)),
+    1: (PP, (0, 3)),
+    3: (PP, (1, 2)),
+    4: (PP, (1, 3)),
+}
+PARALLEL_OF = {EE: EEP, PE: PEP, PP: PPP}
+
+
+def pack_sub(local):
+    """Pack a tuple of local indices (each 0..3) two bits per entry."""
+    out = 0
+    for k, loc in enumerate(local):
+        out |= (int(loc) & 3) << (2 * k)
+    return out
+
+
+def unpack_sub(byte, length):
+    return tuple((int(byte) >> (2 * k)) & 3 for k in range(length))
+
+
+# ----------------------------------------------------------------------------
+# small vector helpers, scalar left-to-right order (kernels/_core.pyx:22-35)
+# ----------------------------------------------------------------------------
+
+def _dot(a, b):
+    return a[..., 0] * b[..., 0] + a[..., 1] * b[..., 1] + a[..., 2] * b[..., 2]
+
+
+def _two_prod_err(a, b, p):
+    """Exact a*b - p (Dekker/Veltkamp split); a, b, p float64 arrays."""
+    split = 134217729.0  # 2**27 + 1
+    ca, cb = split * a, split * b
+    ah = ca - (ca - a)
+    bh = cb - (cb - b)
+    al, bl = a - ah, b - bh
+    return ((ah * bh - p) + ah * bl + al * bh) + al * bl
+
+
+def _fma(a, b, c):
+    """round(a*b + c) via error-free transformations.
+
+    Exact except for double-rounding ties (probability ~2^-53 per operation);
+    used only to mirror BLAS ddot on 3-vectors, see ``_dot_blas``.
+    """
+    p = a * b
+    e = _two_prod_err(a, b, p)
+    s = p + c
+    bb = s - p
+    t = (p - (s - bb)) + (c - bb)  # p + c == s + t exactly
+    return s + (t + e)
+
+
+def _dot_blas(a, b):
+    """3-vector dot as the reference's ``np.dot`` evaluates it.
+
+    proximity.py:172-176 (_point_edge_eval), :189 (point-point), :218 and :257-259
+    (edge_parallel_eps) call np.dot on length-3 vectors, which goes to OpenBLAS ddot
+    (0.3.30, Haswell/Zen kernels): a sequential tail loop compiled with FMA
+    contraction, i.e. fma(a2,b2, fma(a1,b1, a0*b0)).  Verified bit-for-bit against
+    np.dot on 20000 random vectors in the build container.  The kernels.* functions
+    (_core.pyx) do NOT contract; they use ``_dot``.
+    """
+    d = a[..., 0] * b[..., 0]
+    d = _fma(a[..., 1], b[..., 1], d)
+    return _fma(a[..., 2], b[..., 2], d)
+
+
+def _cross(a, b):
+    return np.stack(
+        [
+            a[..., 1] * b[..., 2] - a[..., 2] * b[..., 1],
+            a[..., 2] * b[..., 0] - a[..., 0] * b[..., 2],
+            a[..., 0] * b[..., 1] - a[..., 1] * b[..., 0],
+        ],
+        axis=-1,
+    )
+
+
+def _clamp01(v):
+    return np.where(v < 0.0, 0.0, np.where(v > 1.0, 1.0, v))
+
+
+def _f64(a):
+    return np.atleast_2d(np.asarray(a, dtype=np.float64))
+
+
+# ----------------------------------------------------------------------------
+# a4-a7: narrow-phase primitives
+# ----------------------------------------------------------------------------
+
+def pt_classify_batch(p, t1, t2, t3):
+    """Point-triangle closest feature (kernels/_core.pyx:46-106; _numpy.py:26-99).
+
+    Returns (codes i64 (n,), d2 (n,), grad (n,4,3), w (n,2)).
+    """
+    p, t1, t2, t3 = _f64(p), _f64(t1), _f64(t2), _f64(t3)
+    n = p.shape[0]
+    ab, ac, ap = t2 - t1, t3 - t1, p - t1
+    d1, d2_ = _dot(ab, ap), _dot(ac, ap)
+    bp = p - t2
+    d3, d4 = _dot(ab, bp), _dot(ac, bp)
+    cp = p - t3
+    d5, d6 = _dot(ab, cp), _dot(ac, cp)
+    vc = d1 * d4 - d3 * d2_
+    vb = d5 * d2_ - d1 * d6
+    va = d3 * d6 - d5 * d4
+
+    # priority-ordered region tests, first hit wins (_core.pyx:72-92)
+    tests = [
+        (1, (d1 <= 0.0) & (d2_ <= 0.0)),
+        (2, (d3 >= 0.0) & (d4 <= d3)),
+        (4, (vc <= 0.0) & (d1 >= 0.0) & (d3 <= 0.0)),
+        (3, (d6 >= 0.0) & (d5 <= d6)),
+        (6, (vb <= 0.0) & (d2_ >= 0.0) & (d6 <= 0.0)),
+        (5, (va <= 0.0) & (d4 - d3 >= 0.0) & (d5 - d6 >= 0.0)),
+    ]
+    codes = np.zeros(n, dtype=np.int64)
+    open_ = np.ones(n, dtype=bool)
+    for code, hit in tests:
+        take = open_ & hit
+        codes[take] = code
+        open_ &= ~take
+
+    w1 = np.zeros(n)
+    w2 = np.zeros(n)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        w1 = np.where(codes == 2, 1.0, w1)
+        w1 = np.where(codes == 4, d1 / (d1 - d3), w1)
+        w2 = np.where(codes == 3, 1.0, w2)
+        w2 = np.where(codes == 6, d2_ / (d2_ - d6), w2)
+        t = (d4 - d3) / ((d4 - d3) + (d5 - d6))
+        w1 = np.where(codes == 5, 1.0 - t, w1)
+        w2 = np.where(codes == 5, t, w2)
+        denom = va + vb + vc
+        w1 = np.where(codes == 0, vb / denom, w1)
+        w2 = np.where(codes == 0, vc / denom, w2)
+
+    w0 = 1.0 - w1 - w2
+    closest = w0[:, None] * t1 + w1[:, None] * t2 + w2[:, None] * t3
+    r = p - closest
+    d2 = _dot(r, r)
+    grad = np.empty((n, 4, 3))
+    grad[:, 0] = 2.0 * r
+    grad[:, 1] = (-2.0 * w0)[:, None] * r
+    grad[:, 2] = (-2.0 * w1)[:, None] * r
+    grad[:, 3] = (-2.0 * w2)[:, None] * r
+    return codes, d2, grad, np.stack([w1, w2], axis=1)
+
+
+def ee_classify_batch(a1, a2, b1, b2):
+    """Clamped segment-segment closest pair (kernels/_core.pyx:109-150).
+
+    Returns (codes = 3*ra+rb, d2, grad (n,4,3), (s,t)).
+    """
+    a1, a2, b1, b2 = _f64(a1), _f64(a2), _f64(b1), _f64(b2)
+    n = a1.shape[0]
+    da, db, r = a2 - a1, b2 - b1, a1 - b1
+    a, e = _dot(da, da), _dot(db, db)
+    f = _dot(db, r)
+    b = _dot(da, db)
+    c = _dot(da, r)
+    denom = a * e - b * b
+    with np.errstate(divide="ignore", invalid="ignore"):
+        pos = denom > 0.0
+        s = np.where(pos, _clamp01((b * f - c * e) / np.where(pos, denom, 1.0)), 0.0)
+        t = (b * s + f) / e
+        low, high = t < 0.0, t > 1.0
+        s = np.where(low, _clamp01(-c / a), s)
+        s = np.where(high, _clamp01((b - c) / a), s)
+        t = np.where(low, 0.0, np.where(high, 1.0, t))
+    ra = np.where(s <= 0.0, 0, np.where(s >= 1.0, 1, 2))
+    rb = np.where(t <= 0.0, 0, np.where(t >= 1.0, 1, 2))
+    codes = (3 * ra + rb).astype(np.int64)
+    rvec = (a1 + s[:, None] * da) - (b1 + t[:, None] * db)
+    d2 = _dot(rvec, rvec)
+    grad = np.empty((n, 4, 3))
+    grad[:, 0] = (2.0 * (1.0 - s))[:, None] * rvec
+    grad[:, 1] = (2.0 * s)[:, None] * rvec
+    grad[:, 2] = (-2.0 * (1.0 - t))[:, None] * rvec
+    grad[:, 3] = (-2.0 * t)[:, None] * rvec
+    return codes, d2, grad, np.stack([s, t], axis=1)
+
+
+def cross_sq_batch(a1, a2, b1, b2):
+    """c = |(a2-a1) x (b2-b1)|^2 and its gradient (kernels/_core.pyx:195-219)."""
+    a1, a2, b1, b2 = _f64(a1), _f64(a2), _f64(b1), _f64(b2)
+    u, v = a2 - a1, b2 - b1
+    w = _cross(u, v)
+    c = _dot(w, w)
+    gu, gv = _cross(v, w), _cross(w, u)
+    grad = np.stack([-2.0 * gu, 2.0 * gu, -2.0 * gv, 2.0 * gv], axis=1)
+    return c, grad
+
+
+def point_edge_batch(p, e1, e2):
+    """Point-segment distance, gradient over (p,e1,e2) (proximity.py:170-180)."""
+    p, e1, e2 = _f64(p), _f64(e1), _f64(e2)
+    e = e2 - e1
+    ee = _dot_blas(e, e)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        t = _clamp01(_dot_blas(p - e1, e) / ee)
+    r = p - e1 - t[:, None] * e
+    d2 = _dot_blas(r, r)
+    grad = np.stack([2.0 * r, (-2.0 * (1.0 - t))[:, None] * r, (-2.0 * t)[:, None] * r], axis=1)
+    return d2, grad, t
+
+
+# ----------------------------------------------------------------------------
+# a8/a9: per-stencil distance and parallel measure on a table
+# ----------------------------------------------------------------------------
+
+def _gather(positions, verts):
+    """positions[(n,4) ids] with -1 padding mapped to vertex 0 (unused rows)."""
+    idx = np.where(verts < 0, 0, verts)
+    return positions[idx]
+
+
+def stencil_distance_batch(kind, verts, sub, positions):
+    """d2 (n,) and grad_d2 padded to (n,4,3) for every table row.
+
+    Follows proximity.py:183-222: PP direct, PE a7, PT/EE full re-classification
+    (zero rows off the active branch), parallel kinds evaluated on x[sub] and
+    scattered back to the four-vertex layout.
+    """
+    kind = np.asarray(kind)
+    n = kind.shape[0]
+    x = _gather(np.asarray(positions, dtype=np.float64), np.asarray(verts))
+    d2 = np.zeros(n)
+    grad = np.zeros((n, 4, 3))
+
+    def rows(k):
+        return np.flatnonzero(kind == k)
+
+    i = rows(PP)
+    if i.size:
+        r = x[i, 0] - x[i, 1]
+        d2[i] = _dot_blas(r, r)
+        grad[i, 0], grad[i, 1] = 2.0 * r, -2.0 * r
+    i = rows(PE)
+    if i.size:
+        d2[i], g, _ = point_edge_batch(x[i, 0], x[i, 1], x[i, 2])
+        grad[i, :3] = g
+    i = rows(PT)
+    if i.size:
+        _, d2[i], grad[i], _ = pt_classify_batch(x[i, 0], x[i, 1], x[i, 2], x[i, 3])
+    i = rows(EE)
+    if i.size:
+        _, d2[i], grad[i], _ = ee_classify_batch(x[i, 0], x[i, 1], x[i, 2], x[i, 3])
+
+    sub = np.asarray(sub)
+    loc = np.stack([(sub >> (2 * k)) & 3 for k in range(4)], axis=1).astype(np.int64)
+    i = rows(EEP)
+    if i.size:
+        xs = np.take_along_axis(x[i], loc[i][:, :, None], axis=1)
+        _, d2[i], g, _ = ee_classify_batch(xs[:, 0], xs[:, 1], xs[:, 2], xs[:, 3])
+        full = np.zeros((i.size, 4, 3))
+        for row in range(4):
+            full[np.arange(i.size), loc[i, row]] = g[:, row]
+        grad[i] = full
+    i = rows(PEP)
+    if i.size:
+        xs = np.take_along_axis(x[i], loc[i][:, :, None], axis=1)
+        d2[i], g, _ = point_edge_batch(xs[:, 0], xs[:, 1], xs[:, 2])
+        full = np.zeros((i.size, 4, 3))
+        for row in range(3):
+            full[np.arange(i.size), loc[i, row]] = g[:, row]
+        grad[i] = full
+    i = rows(PPP)
+    if i.size:
+        xs = np.take_along_axis(x[i], loc[i][:, :, None], axis=1)
+        r = xs[:, 0] - xs[:, 1]
+        d2[i] = _dot_blas(r, r)
+        full = np.zeros((i.size, 4, 3))
+        full[np.arange(i.size), loc[i, 0]] = 2.0 * r
+        full[np.arange(i.size), loc[i, 1]] = -2.0 * r
+        grad[i] = full
+    return d2, grad
+
+
+def parallel_measure_batch(verts, positions):
+    """(c, grad_c (n,4,3)) on the four stencil vertices (proximity.py:225-229)."""
+    x = _gather(np.asarray(positions, dtype=np.float64), np.asarray(verts))
+    return cross_sq_batch(x[:, 0], x[:, 1], x[:, 2], x[:, 3])
+
+
+# ----------------------------------------------------------------------------
+# a13/a14: barrier scalars (qlog production form and the log diagnostic form)
+# ----------------------------------------------------------------------------
+
+def barrier_scalars(g, scale, form="qlog"):
+    """(b, b', b'') at gap g with S = kappa*d_hat^4 (barrier.py:76-101)."""
+    g = np.asarray(g, dtype=np.float64)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        lg = np.log(g)
+        om = 1.0 - g
+        if form == "qlog":
+            b = scale * om**2 * lg * lg
+            bg = scale * (-2.0 * om * lg * lg + 2.0 * om**2 * lg / g)
+            bgg = scale * (2.0 * lg * lg - 8.0 * om * lg / g + 2.0 * om**2 * (1.0 - lg) / g**2)
+        elif form == "log":
+            b = -scale * om**2 * lg
+            bg = scale * (2.0 * om * lg - om**2 / g)
+            bgg = scale * (-2.0 * lg + om * (3.0 * g + 1.0) / g**2)
+        else:
+            raise ValueError(f"unknown barrier form {form!r}")
+    return b, bg, bgg
+
+
+def lambda1(g, scale, form="qlog"):
+    """4 g b'' + 2 b' (barrier.py:104-106)."""
+    _, bg, bgg = barrier_scalars(g, scale, form)
+    return 4.0 * np.asarray(g) * bgg + 2.0 * bg
+
+
+def filtered_lambda1(g, scale, eps_g, use_filter=True, form="qlog"):
+    """lambda1 frozen at lambda1(eps_g) below the proximal limit (barrier.py:114-120)."""
+    lam = lambda1(g, scale, form)
+    if not use_filter:
+        return lam
+    return np.where(np.asarray(g) >= eps_g, lam, lambda1(eps_g, scale, form))
+
+
+# ----------------------------------------------------------------------------
+# a16-a18: mollifier and the coupled 2x2 eigen system
+# ----------------------------------------------------------------------------
+
+def mollifier(c, eps_x):
+    """(e, e', e'') of the parallel-edge mollifier (mollifier.py:55-67)."""
+    c = np.asarray(c, dtype=np.float64)
+    eps_x = np.asarray(eps_x, dtype=np.float64)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        inside = c < eps_x
+        e = np.where(inside, -(c * c) / (eps_x * eps_x) + 2.0 * c / eps_x, 1.0)
+        de = np.where(inside, -2.0 * c / (eps_x * eps_x) + 2.0 / eps_x, 0.0)
+        d2e = np.where(inside, -2.0 / (eps_x * eps_x), 0.0)
+    return e, de, d2e
+
+
+def mollified_eigensystem(g, c, eps_x, scale, form="qlog"):
+    """Closed-form retained eigenpair (lambda8', q_gamma, q_f) (mollifier.py:106-144).
+
+    Also returns the intermediates (lam_gamma1, lam_g1, t, p, lambda7') used by
+    the golden checks.
+    """
+    g = np.asarray(g, dtype=np.float64)
+    c = np.asarray(c, dtype=np.float64)
+    b, bg, bgg = barrier_scalars(g, scale, form)
+    e, de, d2e = mollifier(c, eps_x)
+    b_gamma, b_gamma2 = de * b, d2e * b
+    b_g, b_g2, b_gamma_g = e * bg, e * bgg, de * bg
+    lam_gamma1 = 2.0 * (b_gamma + 2.0 * c * b_gamma2)
+    lam_g1 = 2.0 * (b_g + 2.0 * g * b_g2)
+    t = b_gamma_g * np.sqrt(c) * np.sqrt(g)
+    p = 0.5 * np.sqrt((lam_gamma1 - lam_g1) ** 2 + 64.0 * t * t)
+    mean = 0.5 * (lam_gamma1 + lam_g1)
+    lam7, lam8 = mean - p, mean + p
+    decoupled = (np.abs(8.0 * t) < 1e-12 * (np.abs(lam_gamma1) + np.abs(lam_g1))) | (t == 0.0)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        k2 = (lam_gamma1 - lam_g1 + 2.0 * p) / (8.0 * t)
+        nrm = np.sqrt(k2 * k2 + 1.0)
+        q_gamma = np.where(decoupled, np.where(lam_gamma1 >= lam_g1, 1.0, 0.0), k2 / nrm)
+        q_f = np.where(decoupled, np.where(lam_gamma1 >= lam_g1, 0.0, 1.0), 1.0 / nrm)
+    return {
+        "lam_gamma1": lam_gamma1,
+        "lam_g1": lam_g1,
+        "t": t,
+        "p": p,
+        "lambda7p": lam7,
+        "lambda8p": lam8,
+        "q_gamma": q_gamma,
+        "q_f": q_f,
+        "b_gamma": b_gamma,
+        "b_g": b_g,
+    }
+
+
+# ----------------------------------------------------------------------------
+# a12, a15, a17, a19-a22: per-stencil energy, gradient and PSD block
+# ----------------------------------------------------------------------------
+
+def local_quadratics_batch(kind, verts, sub, eps_x, positions, d_hat, kappa,
+                           d_thr_ratio=0.1, use_filter=True, form="qlog", dt2=1.0):
+    """Energy, gradient and rank-1 PSD block of every table row.
+
+    Returns a dict with
+      status (n,) u8   0 active, 1 inactive (d2 >= d_hat^2), 2 d2 <= 0
+      energy (n,)      a20: b(g) or e(c) b(g) with g = d2/d_hat**2; NOT dt2 scaled
+                       (solver.py:127-146); 0 for inactive rows
+      grad   (n,12)    dt2-scaled gradient, padded with zeros beyond 3*s
+      hess   (n,12,12) dt2-scaled PSD block, padded
+      f, lam           diagnostics
+    Follows gap.py:56-82 (f, grad f, sqrt c, grad sqrt c), barrier.py:163-177
+    (plain kinds) and mollifier.py:89-103, :191-210 (parallel kinds); the dt2
+    scaling and the inactive skip are solver.py:202-209.
+    """
+    kind = np.asarray(kind)
+    verts = np.asarray(verts)
+    n = kind.shape[0]
+    eps_x = np.asarray(eps_x, dtype=np.float64)
+    scale = kappa * d_hat**4
+    eps_g = d_thr_ratio * d_thr_ratio
+    d2, grad_d2 = stencil_distance_batch(kind, verts, sub, positions)
+    status = np.where(d2 <= 0.0, STATUS_PENETRATION,
+                      np.where(d2 >= d_hat**2, STATUS_INACTIVE, STATUS_ACTIVE)).astype(np.uint8)
+    active = status == STATUS_ACTIVE
+    par = IS_PARALLEL[kind]
+
+    with np.errstate(divide="ignore", invalid="ignore"):
+        d = np.sqrt(d2)
+        f = d / d_hat
+        u_f = (grad_d2 / (2.0 * d * d_hat)[:, None, None]).reshape(n, 12)
+        g = f * f
+        b, bg, bgg = barrier_scalars(g, scale, form)
+
+        # plain kinds (barrier.py:172-176)
+        coef = 2.0 * f * bg
+        grad = coef[:, None] * u_f
+        lam = np.maximum(filtered_lambda1(g, scale, eps_g, use_filter, form), 0.0)
+        w = u_f.copy()
+
+        # energy uses g = d2/d_hat^2, not f*f (solver.py:141-145)
+        g_e = d2 / d_hat**2
+        energy = barrier_scalars(g_e, scale, form)[0]
+
+        if np.any(par):
+            i = np.flatnonzero(par)
+            c, grad_c = parallel_measure_batch(verts[i], positions)
+            sqrt_c = np.sqrt(c)
+            safe = np.where(sqrt_c > 0.0, sqrt_c, 1.0)
+            u_c = np.where((sqrt_c > 0.0)[:, None], grad_c.reshape(-1, 12) / (2.0 * safe)[:, None], 0.0)
+            cc = sqrt_c * sqrt_c
+            sys = mollified_eigensystem(g[i], cc, eps_x[i], scale, form)
+            grad[i] = (sys["b_gamma"] * 2.0 * sqrt_c)[:, None] * u_c + (sys["b_g"] * 2.0 * f[i])[:, None] * u_f[i]
+            w[i] = sys["q_gamma"][:, None] * u_c + sys["q_f"][:, None] * u_f[i]
+            lam[i] = np.maximum(sys["lambda8p"], 0.0)
+            energy[i] = mollifier(c, eps_x[i])[0] * energy[i]
+
+    hess = lam[:, None, None] * (w[:, :, None] * w[:, None, :])
+    grad = dt2 * grad
+    hess = dt2 * hess
+    dead = ~active
+    grad[dead] = 0.0
+    hess[dead] = 0.0
+    energy = np.where(active, energy, 0.0)
+    lam = np.where(active, lam, 0.0)
+    return {"status": status, "energy": energy, "grad": grad, "hess": hess, "f": f, "lam": lam,
+            "d2": d2}
+
+
+def barrier_energy(kind, verts, sub, eps_x, positions, d_hat, kappa, form="qlog"):
+    """Total barrier energy; raises on d2 <= 0 like solver.py:132-133."""
+    out = local_quadratics_batch(kind, verts, sub, eps_x, positions, d_hat, kappa, form=form)
+    if np.any(out["status"] == STATUS_PENETRATION):
+        raise ValueError("nonpositive distance on a stencil")
+    return float(np.sum(out["energy"]))
+
+
+def family_views(kind, verts, out):
+    """Split a padded batch result into the size families of ``group_blocks``.
+
+    solver.py:237-248 stacks blocks by stencil size (2, 3, 4 ascending) keeping
+    list order and skipping inactive rows (solver.py:204-205).  Returns
+    ``[(s, rows, vids (nb,s) i64, grad (nb,3s), hess (nb,3s,3s))]``.
+    """
+    size = KIND_SIZE[np.asarray(kind)]
+    active = out["status"] == STATUS_ACTIVE
+    fams = []
+    for s in (2, 3, 4):
+        rows = np.flatnonzero((size == s) & active)
+        if rows.size == 0:
+            continue
+        fams.append((
+            s,
+            rows,
+            np.asarray(verts)[rows, :s].astype(np.int64),
+            np.ascontiguousarray(out["grad"][rows, : 3 * s]),
+            np.ascontiguousarray(out["hess"][rows, : 3 * s, : 3 * s]),
+        ))
+    return fams
+
+
+# ----------------------------------------------------------------------------
+# a23-a29: gradient scatter, matvec, block-Jacobi, PCG, assembled matrix
+# ----------------------------------------------------------------------------
+
+def scatter_gradient(masses, fixed, x, x_tilde, families):
+    """m (x - x~) + sum scatter(grad); fixed rows zero (solver.py:218-226)."""
+    n = x.shape[0]
+    g3 = masses[:, None] * (x - x_tilde)
+    for _, _, vids, grad, _ in families:
+        np.add.at(g3, vids, grad.reshape(vids.shape[0], vids.shape[1], 3))
+    g3[fixed] = 0.0
+    return g3.reshape(3 * n)
+
+
+def matvec_blocks(hess, vids, x, out):
+    """out += scatter(H_b gather(x)), serial block order (kernels/_core.pyx:222-247)."""
+    nb = hess.shape[0]
+    if nb == 0:
+        return
+    s = vids.shape[1]
+    xg = x.reshape(-1, 3)[vids].reshape(nb, 3 * s)
+    y = (hess * xg[:, None, :]).sum(axis=2)
+    np.add.at(out.reshape(-1, 3), vids, y.reshape(nb, s, 3))
+
+
+def matvec_matrix_free(grouped, masses, fixed, v):
+    """A v with Dirichlet rows/cols as identity (solver.py:251-262)."""
+    n = masses.shape[0]
+    vin = v.copy()
+    vin.reshape(n, 3)[fixed] = 0.0
+    out = (masses[:, None] * vin.reshape(n, 3)).reshape(-1).copy()
+    for hess, vids in grouped:
+        matvec_blocks(hess, vids, vin, out)
+    out.reshape(n, 3)[fixed] = v.reshape(n, 3)[fixed]
+    return out
+
+
+def block_jacobi(grouped, masses, fixed):
+    """Inverse 3x3 diagonal blocks (solver.py:265-276)."""
+    n = masses.shape[0]
+    diag = np.zeros((n, 3, 3))
+    diag[:] = np.eye(3)[None] * masses[:, None, None]
+    for hess, vids in grouped:
+        for k in range(vids.shape[1]):
+            np.add.at(diag, vids[:, k], hess[:, 3 * k:3 * k + 3, 3 * k:3 * k + 3])
+    diag[fixed] = np.eye(3)
+    return np.linalg.inv(diag)
+
+
+def pcg_solve(grouped, masses, fixed, rhs, rel_tol, max_iters, matvec=None):
+    """Block-Jacobi PCG (solver.py:279-315). Returns (d, iters, converged)."""
+    n = masses.shape[0]
+    pinv = block_jacobi(grouped, masses, fixed)
+    if matvec is None:
+        def matvec(c):
+            return matvec_matrix_free(grouped, masses, fixed, c)
+
+    def prec(r):
+        return (pinv * r.reshape(n, 1, 3)).sum(axis=2).reshape(-1)
+
+    d = np.zeros_like(rhs)
+    r = rhs.copy()
+    r.reshape(n, 3)[fixed] = 0.0
+    s = prec(r)
+    delta_new = float(r @ s)
+    delta0 = delta_new
+    if delta0 <= 0.0:
+        return d, 0, True
+    c = s.copy()
+    iters = 0
+    while iters < max_iters and delta_new > rel_tol * delta0:
+        q = matvec(c)
+        denom = float(c @ q)
+        if denom <= 0.0:
+            break
+        alpha = delta_new / denom
+        d += alpha * c
+        r -= alpha * q
+        s = prec(r)
+        delta_old = delta_new
+        delta_new = float(r @ s)
+        c = s + (delta_new / delta_old) * c
+        iters += 1
+    return d, iters, delta_new <= rel_tol * delta0
+
+
+def assemble_dense(grouped, masses, fixed):
+    """The assembled global matrix (tests/test_solver.py:71-84 of the reference)."""
+    n = masses.shape[0]
+    a = np.zeros((3 * n, 3 * n))
+    for v in range(n):
+        a[3 * v:3 * v + 3, 3 * v:3 * v + 3] = masses[v] * np.eye(3)
+    for hess, vids in grouped:
+        for blk, ids in zip(hess, vids):
+            idx = (3 * ids[:, None] + np.arange(3)[None]).reshape(-1)
+            a[np.ix_(idx, idx)] += blk
+    fd = np.repeat(fixed, 3)
+    a[fd, :] = 0.0
+    a[:, fd] = 0.0
+    a[fd, fd] = 1.0
+    return a
+
+
+def assemble_bsr(grouped, masses, fixed):
+    """3x3-block CSR of the same matrix: (rowptr i32 (N+1), colidx i32, vals (nnzb,3,3)).
+
+    Sparsity pattern := {(i,j): i,j in some block's vert_ids} U {(i,i)}, fixed
+    rows/cols reduced to the identity diagonal.  Column indices
+    ascend within a row.  Contributions are summed in block (list) order.
+    """
+    n = masses.shape[0]
+    rows = [np.arange(n, dtype=np.int64)]
+    cols = [np.arange(n, dtype=np.int64)]
+    vals = [np.eye(3)[None] * masses[:, None, None]]
+    for hess, vids in grouped:
+        nb, s = vids.shape
+        sub = hess.reshape(nb, s, 3, s, 3).transpose(0, 1, 3, 2, 4)  # (nb, a, b, 3, 3)
+        ra = np.broadcast_to(vids[:, :, None], (nb, s, s))
+        cb = np.broadcast_to(vids[:, None, :], (nb, s, s))
+        rows.append(ra.reshape(-1))
+        cols.append(cb.reshape(-1))
+        vals.append(sub.reshape(-1, 3, 3))
+    rows, cols, vals = np.concatenate(rows), np.concatenate(cols), np.concatenate(vals)
+    keep = ~(fixed[rows] | fixed[cols]) | (rows == cols)
+    rows, cols, vals = rows[keep], cols[keep], vals[keep]
+    key = rows * n + cols
+    order = np.argsort(key, kind="stable")
+    key, vals = key[order], vals[order]
+    uniq, first = np.unique(key, return_index=True)
+    out = np.add.reduceat(vals, first, axis=0)
+    r, c = uniq // n, uniq % n
+    fx = fixed[r]
+    out[fx] = np.eye(3)
+    rowptr = np.zeros(n + 1, dtype=np.int32)
+    np.add.at(rowptr, r + 1, 1)
+    rowptr = np.cumsum(rowptr).astype(np.int32)
+    return rowptr, c.astype(np.int32), out
+
+
+def bsr_matvec(rowptr, colidx, vals, x):
+    n = rowptr.shape[0] - 1
+    rows = np.repeat(np.arange(n), np.diff(rowptr))
+    y = np.zeros((n, 3))
+    np.add.at(y, rows, (vals * x.reshape(n, 3)[colidx][:, None, :]).sum(axis=2))
+    return y.reshape(-1)
+
+
+# ----------------------------------------------------------------------------
+# a10/a11: narrow phase -> ordered contact list
+# ----------------------------------------------------------------------------
+
+def edge_parallel_eps(rest_positions, ea, eb):
+    """1e-3 |la|^2 |lb|^2 from rest positions (proximity.py:251-259).
+
+    The reference uses np.dot on 3-vectors: see ``_dot_blas``.
+    """
+    la = rest_positions[ea[:, 1]] - rest_positions[ea[:, 0]]
+    lb = rest_positions[eb[:, 1]] - rest_positions[eb[:, 0]]
+    return 1e-3 * _dot_blas(la, la) * _dot_blas(lb, lb)
+
+
+_PT_KIND = np.array([PT_LOCAL[c][0] for c in range(7)], dtype=np.uint8)
+_PT_SEL = np.array([PT_LOCAL[c][1] + (0,) * (4 - len(PT_LOCAL[c][1])) for c in range(7)], dtype=np.int64)
+_EE_KIND = np.array([EE_LOCAL[c][0] for c in range(9)], dtype=np.uint8)
+_EE_SEL = np.array([EE_LOCAL[c][1] + (0,) * (4 - len(EE_LOCAL[c][1])) for c in range(9)], dtype=np.int64)
+_EE_SUB = np.array([pack_sub(EE_LOCAL[c][1]) for c in range(9)], dtype=np.uint8)
+
+
+def narrow_phase(positions, rest_positions, vt_pairs, ee_pairs, d_hat, promote_parallel=True):
+    """Candidate queries -> the reference's ordered contact list as a table.
+
+    ``vt_pairs`` (m,4) = (vertex, t1, t2, t3), ``ee_pairs`` (k,4) = (a1,a2,b1,b2),
+    any duplicate-free superset of the near queries (incident/adjacent pairs
+    already removed).  Follows proximity.py:284-358: keep d2 < d_hat*d_hat, reduce
+    to the active branch, promote EE queries with c < eps_x, sort by
+    (kind.value, verts, origin).  Returns dict(kind, verts, sub, eps_x,
+    origin_type (1 "ee", 2 "vt"), origin (n,4)).
+    """
+    positions = np.asarray(positions, dtype=np.float64)
+    ks, vs, subs, epss, ots, ors = [], [], [], [], [], []
+    vt_pairs = np.asarray(vt_pairs, dtype=np.int64).reshape(-1, 4)
+    ee_pairs = np.asarray(ee_pairs, dtype=np.int64).reshape(-1, 4)
+    if vt_pairs.shape[0]:
+        x = positions[vt_pairs]
+        codes, d2, _, _ = pt_classify_batch(x[:, 0], x[:, 1], x[:, 2], x[:, 3])
+        near = np.flatnonzero(d2 < d_hat * d_hat)
+        k = _PT_KIND[codes[near]]
+        sel = _PT_SEL[codes[near]]
+        v = np.take_along_axis(vt_pairs[near], sel, axis=1)
+        size = KIND_SIZE[k]
+        v[np.arange(4)[None, :] >= size[:, None]] = -1
+        ks.append(k); vs.append(v); subs.append(np.zeros(near.size, np.uint8))
+        epss.append(np.zeros(near.size)); ots.append(np.full(near.size, 2, np.uint8))
+        ors.append(vt_pairs[near])
+    if ee_pairs.shape[0]:
+        x = positions[ee_pairs]
+        codes, d2, _, _ = ee_classify_batch(x[:, 0], x[:, 1], x[:, 2], x[:, 3])
+        cval, _ = cross_sq_batch(x[:, 0], x[:, 1], x[:, 2], x[:, 3])
+        near = np.flatnonzero(d2 < d_hat * d_hat)
+        q = ee_pairs[near]
+        eps = edge_parallel_eps(np.asarray(rest_positions, dtype=np.float64), q[:, 0:2], q[:, 2:4])
+        k = _EE_KIND[codes[near]]
+        prom = (cval[near] < eps) if promote_parallel else np.zeros(near.size, bool)
+        sel = _EE_SEL[codes[near]]
+        v = np.take_along_axis(q, sel, axis=1)
+        size = KIND_SIZE[k]
+        v[np.arange(4)[None, :] >= size[:, None]] = -1
+        v = np.where(prom[:, None], q, v)
+        k = np.where(prom, k + 1, k).astype(np.uint8)  # EE->EEP, PE->PEP, PP->PPP
+        ks.append(k); vs.append(v)
+        subs.append(np.where(prom, _EE_SUB[codes[near]], 0).astype(np.uint8))
+        epss.append(np.where(prom, eps, 0.0)); ots.append(np.full(near.size, 1, np.uint8))
+        ors.append(q)
+    if not ks:
+        z4 = np.zeros((0, 4), np.int32)
+        return {"kind": np.zeros(0, np.uint8), "verts": z4, "sub": np.zeros(0, np.uint8),
+                "eps_x": np.zeros(0), "origin_type": np.zeros(0, np.uint8), "origin": z4.copy()}
+    kind = np.concatenate(ks); verts = np.concatenate(vs); sub = np.concatenate(subs)
+    eps_x = np.concatenate(epss); ot = np.concatenate(ots); origin = np.concatenate(ors)
+    # tuple comparison: shorter tuples only meet within one kind, so -1 padding is inert
+    order = np.lexsort((origin[:, 3], origin[:, 2], origin[:, 1], origin[:, 0], ot,
+                        verts[:, 3], verts[:, 2], verts[:, 1], verts[:, 0], kind))
+    return {"kind": kind[order], "verts": verts[order].astype(np.int32), "sub": sub[order],
+            "eps_x": eps_x[order], "origin_type": ot[order], "origin": origin[order].astype(np.int32)}

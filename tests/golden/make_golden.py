@@ -1,0 +1,318 @@
+#!/usr/bin/env python
+"""Freeze outputs of the REAL reference (`tetipc`) into tests/golden/*.npz.
+
+Run in the build container only (needs /root/reference):
+
+    python tests/golden/make_golden.py
+
+The reference package is imported unmodified.  Its compiled backend
+(``tetipc.kernels._core``) is the canonical arithmetic (scalar, left-to-right,
+no FMA); because /root/reference is read-only the script copies ``pkg/`` to
+/tmp/refprobe and builds the extension there with the reference's own setup.py,
+then imports from that copy (``kernels.BACKEND == "core"``).  The ``_numpy``
+fallback outputs of the three classify kernels are stored next to the ``_core``
+ones: they differ in the last bits (einsum uses FMA/SIMD), region codes agree.
+
+Inputs come from ``paper_2308_09400_b200.workloads`` (seeded); every array the
+parity tests need is stored in the .npz, so the GPU box needs neither
+/root/reference nor this script.
+"""
+
+import os
+import shutil
+import subprocess
+import sys
+import types
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+REF_SRC = "/root/reference/pkg"
+PROBE = "/tmp/refprobe/pkg"
+
+
+def _import_reference():
+    so = [f for f in os.listdir(os.path.join(PROBE, "src/tetipc/kernels"))
+          if f.startswith("_core") and f.endswith(".so")] if os.path.isdir(PROBE) else []
+    if not so:
+        os.makedirs(os.path.dirname(PROBE), exist_ok=True)
+        shutil.copytree(REF_SRC, PROBE, dirs_exist_ok=True)
+        subprocess.check_call([sys.executable, "setup.py", "build_ext", "--inplace"], cwd=PROBE)
+    sys.path.insert(0, os.path.join(PROBE, "src"))
+    import tetipc  # noqa: F401
+    from tetipc import kernels
+
+    assert kernels.BACKEND == "core", kernels.BACKEND
+    return kernels
+
+
+kernels = _import_reference()
+sys.path.insert(0, ROOT)
+
+from tetipc import barrier as rb  # noqa: E402
+from tetipc import mollifier as rm  # noqa: E402
+from tetipc import proximity as rp  # noqa: E402
+from tetipc import solver as rs  # noqa: E402
+from tetipc.gap import build_diagonal_jacobian  # noqa: E402
+from tetipc.kernels import _numpy as k_numpy  # noqa: E402
+from tetipc.mesh import Scene  # noqa: E402
+
+from paper_2308_09400_b200 import workloads as wl  # noqa: E402
+
+KIND_CODE = {
+    rp.StencilKind.EDGE_EDGE: 0,
+    rp.StencilKind.EDGE_EDGE_PARALLEL: 1,
+    rp.StencilKind.POINT_EDGE: 2,
+    rp.StencilKind.POINT_EDGE_PARALLEL: 3,
+    rp.StencilKind.POINT_POINT: 4,
+    rp.StencilKind.POINT_POINT_PARALLEL: 5,
+    rp.StencilKind.POINT_TRIANGLE: 6,
+}
+
+PARAM_SETS = {
+    # name: (d_hat, kappa, dt)   second set = bundled-scene values (scenes.py:223-225)
+    "unit": (1.0, 1.0, 1.0),
+    "scene": (5e-3, 2e8, 0.01),
+}
+
+
+def save(name, **arrays):
+    path = os.path.join(HERE, name + ".npz")
+    np.savez_compressed(path, **arrays)
+    print(f"{name}.npz: {os.path.getsize(path) / 1024:.0f} KiB, keys={sorted(arrays)}")
+
+
+def table_of(stencils):
+    n = len(stencils)
+    kind = np.zeros(n, np.uint8)
+    verts = np.full((n, 4), -1, np.int32)
+    sub = np.zeros(n, np.uint8)
+    eps = np.zeros(n)
+    otype = np.zeros(n, np.uint8)
+    origin = np.full((n, 4), -1, np.int32)
+    for i, st in enumerate(stencils):
+        kind[i] = KIND_CODE[st.kind]
+        verts[i, : len(st.verts)] = st.verts
+        if st.sub is not None:
+            for k, loc in enumerate(st.sub):
+                sub[i] |= (loc & 3) << (2 * k)
+        if st.eps_x is not None:
+            eps[i] = st.eps_x
+        if st.origin is not None:
+            otype[i] = {"ee": 1, "vt": 2}[st.origin[0]]
+            origin[i] = st.origin[1:]
+    return dict(kind=kind, verts=verts, sub=sub, eps_x=eps, origin_type=otype, origin=origin)
+
+
+def fake_state(d_hat, kappa, dt, masses=None, fixed=None, **kw):
+    """Just enough of SimState for its unbound hot-path methods (solver.py:127-226)."""
+    params = rb.BarrierParams(d_hat=d_hat, kappa=kappa, **kw)
+    cfg = rs.SolverConfig(dt=dt, barrier=params)
+    scene = types.SimpleNamespace(tets=np.zeros((0, 4), np.int64))
+    st = types.SimpleNamespace(config=cfg, scene=scene, friction_data=[], masses=masses, fixed=fixed, l=1.0)
+    st._barrier_block = lambda stencil, x: rs.SimState._barrier_block(st, stencil, x)
+    return st
+
+
+def reference_blocks(stencils, x, d_hat, kappa, dt, **kw):
+    """Per-stencil reference outputs padded to 4 vertices."""
+    st = fake_state(d_hat, kappa, dt, **kw)
+    n = len(stencils)
+    energy = np.zeros(n)
+    grad = np.zeros((n, 12))
+    hess = np.zeros((n, 12, 12))
+    status = np.zeros(n, np.uint8)
+    for i, s in enumerate(stencils):
+        dist = rp.stencil_distance(s, x)
+        if dist.d2 <= 0.0:
+            status[i] = 2
+            continue
+        if dist.d2 >= d_hat**2:
+            status[i] = 1
+            continue
+        energy[i] = rs.SimState._barrier_energy(st, x, [s])
+        blk = rs.SimState.assemble_local_quadratics(st, x, x, [s])[0]
+        k = blk.grad.shape[0]
+        grad[i, :k] = blk.grad
+        hess[i, :k, :k] = blk.hess
+    return dict(ref_energy=energy, ref_grad=grad, ref_hess=hess, ref_status=status)
+
+
+# ---------------------------------------------------------------------------
+
+def golden_scalars():
+    g = np.concatenate([np.linspace(0.01, 0.99, 99), [1e-6, 1e-4, 0.0025, 0.25, 1 - 1e-6, 1 - 1e-12]])
+    out = {"g": g}
+    for name, (d_hat, kappa, _) in PARAM_SETS.items():
+        for form in ("qlog", "log"):
+            p = rb.BarrierParams(d_hat=d_hat, kappa=kappa, form=form)
+            tag = f"{name}_{form}"
+            out[tag + "_b"] = rb.barrier_value(g, p)
+            out[tag + "_bg"] = rb.barrier_dg(g, p)
+            out[tag + "_bgg"] = rb.barrier_d2g(g, p)
+            out[tag + "_lam1"] = rb.lambda1(g, p)
+            out[tag + "_lam23"] = rb.lambda23(g, p)
+            out[tag + "_lam1f"] = rb.filtered_lambda1(g, p)
+    save("scalars", **out)
+
+
+def golden_classify():
+    rng = np.random.default_rng(20240817)
+    n = 768
+    pts = [rng.normal(size=(n, 3)) for _ in range(4)]
+    # a block of exact-distance PT / EE stencils, and near-degenerate rows
+    xp = wl.gen_point_triangle(rng, 128, rng.uniform(0.1, 0.9, 128))
+    xe = wl.gen_edge_edge(rng, 128, rng.uniform(0.1, 0.9, 128))
+    xq = wl.gen_parallel_edge_edge(rng, 120, rng.uniform(0.2, 0.9, 120),
+                                   np.exp(rng.uniform(np.log(1e-7), np.log(1e-2), 120)))
+    xz = wl.gen_exact_parallel_edge_edge(rng, 8, rng.integers(13, 58, 8))
+    for j in range(4):
+        pts[j][:128] = xp[:, j]
+        pts[j][128:256] = xe[:, j]
+        pts[j][256:376] = xq[:, j]
+        pts[j][376:384] = xz[:, j]
+    out = {f"in{j}": pts[j] for j in range(4)}
+    for tag, mod in (("core", kernels.get_backend("core")), ("numpy", k_numpy)):
+        c, d2, g, w = mod.pt_classify_batch(*pts)
+        out.update({f"pt_{tag}_codes": c, f"pt_{tag}_d2": d2, f"pt_{tag}_grad": g, f"pt_{tag}_w": w})
+        c, d2, g, w = mod.ee_classify_batch(*pts)
+        out.update({f"ee_{tag}_codes": c, f"ee_{tag}_d2": d2, f"ee_{tag}_grad": g, f"ee_{tag}_w": w})
+        cv, cg = mod.cross_sq_batch(*pts)
+        out.update({f"cs_{tag}_c": cv, f"cs_{tag}_grad": cg})
+        hess = rng.normal(size=(40, 12, 12)) if tag == "core" else out["mv_hess"]
+        if tag == "core":
+            hess = hess + hess.transpose(0, 2, 1)
+            out["mv_hess"] = hess
+            out["mv_vids"] = np.stack([rng.choice(30, size=4, replace=False) for _ in range(40)]).astype(np.int64)
+            out["mv_x"] = rng.normal(size=90)
+        acc = np.zeros(90)
+        mod.matvec_blocks(out["mv_hess"], out["mv_vids"], out["mv_x"], acc)
+        out[f"mv_{tag}_out"] = acc
+    save("classify", **out)
+
+
+def golden_plain_blocks():
+    pos, ids = wl.mixed_kind_batch(n_each=48, seed=11)
+    kinds = {"pp": rp.StencilKind.POINT_POINT, "pe": rp.StencilKind.POINT_EDGE,
+             "pt": rp.StencilKind.POINT_TRIANGLE, "ee": rp.StencilKind.EDGE_EDGE}
+    stencils = []
+    for name in ("ee", "pe", "pp", "pt"):  # reference list order
+        for row in ids[name]:
+            stencils.append(rp.ContactStencil(kind=kinds[name], verts=tuple(int(v) for v in row)))
+    # off-branch PT/EE rows: move some points sideways so the closest feature is an edge/vertex
+    rng = np.random.default_rng(5)
+    x = pos.copy()
+    for row in ids["pt"][::4]:
+        x[row[0]] += (x[row[2]] - x[row[1]]) * rng.uniform(1.0, 2.0)
+    for row in ids["ee"][::4]:
+        x[row[2:]] += (x[row[1]] - x[row[0]]) * rng.uniform(0.8, 1.6)
+    out = dict(table_of(stencils), positions=x)
+    for name, (d_hat, kappa, dt) in PARAM_SETS.items():
+        xs = x * d_hat  # d/d_hat preserved; geometry shrinks with d_hat
+        ref = reference_blocks(stencils, xs, d_hat, kappa, dt)
+        out.update({f"{name}_{k}": v for k, v in ref.items()})
+        ref = reference_blocks(stencils, xs, d_hat, kappa, dt, use_filter=False)
+        out[f"{name}_nofilter_ref_hess"] = ref["ref_hess"]
+    save("blocks_plain", **out)
+
+
+def golden_parallel_blocks():
+    batch = wl.config2_batch(n=320, seed=20240818)
+    x = batch.positions
+    stencils, cvals, eig = [], [], []
+    for q in batch.ee:
+        ea, eb = q[:2], q[2:]
+        eps = rp.edge_parallel_eps(batch.rest_positions, ea, eb)
+        kind, local, res, c = rp.classify_edge_edge(x[q[0]], x[q[1]], x[q[2]], x[q[3]], eps_x=eps)
+        if res.d2 >= batch.d_hat**2:
+            continue
+        gids = tuple(int(v) for v in q)
+        if kind in rp.PARALLEL_KINDS:
+            st = rp.ContactStencil(kind=kind, verts=gids, eps_x=eps, sub=local, origin=("ee",) + gids,
+                                   edge_pair=(gids[:2], gids[2:]))
+        else:
+            st = rp.ContactStencil(kind=kind, verts=tuple(gids[k] for k in local), origin=("ee",) + gids)
+        stencils.append(st)
+        cvals.append(c)
+    stencils.sort(key=lambda s: s.sort_key())
+    out = dict(table_of(stencils), positions=x)
+    for name, (d_hat, kappa, dt) in PARAM_SETS.items():
+        if name == "scene":
+            continue  # eps_x is tied to the unit geometry
+        ref = reference_blocks(stencils, x, d_hat, kappa, dt)
+        out.update({f"{name}_{k}": v for k, v in ref.items()})
+        params = rb.BarrierParams(d_hat=d_hat, kappa=kappa)
+        rows = []
+        for s in stencils:
+            if s.kind not in rp.PARALLEL_KINDS:
+                rows.append([np.nan] * 8)
+                continue
+            jac = build_diagonal_jacobian(s, x, d_hat)
+            sysm = rm.mollified_eigensystem(jac.f * jac.f, jac.sqrt_c * jac.sqrt_c, params, s.eps_x)
+            rows.append([sysm.lambda_gamma[0], sysm.lambda_g[0], sysm.t, sysm.p, sysm.lambda7p,
+                         sysm.lambda8p, sysm.q8p[4], sysm.q8p[8]])
+        out[f"{name}_eig"] = np.array(rows)
+    save("blocks_parallel", **out)
+
+
+def _reference_scene(cloth):
+    nv = cloth.positions.shape[0]
+    return Scene(
+        bodies=[], gravity=np.array([0.0, 0.0, -9.81]), bbox_diagonal=float(np.linalg.norm(np.ptp(cloth.positions, axis=0))),
+        positions=cloth.positions, rest_positions=cloth.rest_positions, masses=cloth.masses, fixed=cloth.fixed,
+        tets=np.zeros((0, 4), np.int64), surf_tris=cloth.tris, surf_edges=cloth.edges,
+        surf_verts=np.unique(cloth.tris), body_offsets=np.array([0, nv]), tet_volumes=np.zeros(0),
+    )
+
+
+def golden_scene():
+    cloth = wl.cloth_stack(layers=3, n=6, seed=3, twist_deg=5.0)
+    scene = _reference_scene(cloth)
+    stencils = rp.find_contact_pairs(scene, cloth.positions, cloth.d_hat)
+    kinds = sorted({s.kind.value for s in stencils})
+    print(f"scene: {cloth.positions.shape[0]} verts, {len(stencils)} contacts, kinds={kinds}")
+    st = fake_state(cloth.d_hat, cloth.kappa, cloth.dt, masses=cloth.masses, fixed=cloth.fixed)
+    x = cloth.positions
+    rng = np.random.default_rng(9)
+    x_tilde = x + rng.normal(size=x.shape) * 1e-4
+    blocks = rs.SimState.assemble_local_quadratics(st, x, x, stencils)
+    grouped = rs.group_blocks(blocks)
+    grad = rs.SimState.gradient(st, x, x_tilde, blocks)
+    energy = rs.SimState._barrier_energy(st, x, stencils)
+    v = rng.normal(size=3 * x.shape[0])
+    mv = rs.matvec_matrix_free(grouped, cloth.masses, cloth.fixed, v)
+    pinv = rs.block_jacobi_preconditioner(grouped, cloth.masses, cloth.fixed)
+    d, iters, ok = rs.pcg_solve(grouped, cloth.masses, cloth.fixed, -grad, 1e-4, 2000)
+    d12, iters12, ok12 = rs.pcg_solve(grouped, cloth.masses, cloth.fixed, -grad, 1e-12, 5000)
+    # dense assembly exactly as the reference's own test oracle does it (tests/test_solver.py:71-84)
+    n = x.shape[0]
+    a = np.zeros((3 * n, 3 * n))
+    for i in range(n):
+        a[3 * i:3 * i + 3, 3 * i:3 * i + 3] = cloth.masses[i] * np.eye(3)
+    for blk in blocks:
+        idx = np.concatenate([[3 * i, 3 * i + 1, 3 * i + 2] for i in blk.vert_ids])
+        a[np.ix_(idx, idx)] += blk.hess
+    fd = np.repeat(cloth.fixed, 3)
+    a[fd, :] = 0.0
+    a[:, fd] = 0.0
+    a[fd, fd] = 1.0
+    out = dict(table_of(stencils), positions=x, rest_positions=cloth.rest_positions, tris=cloth.tris,
+               edges=cloth.edges, masses=cloth.masses, fixed=cloth.fixed, x_tilde=x_tilde,
+               d_hat=cloth.d_hat, kappa=cloth.kappa, dt=cloth.dt,
+               ref_gradient=grad, ref_energy=energy, v=v, ref_matvec=mv, ref_pinv=pinv,
+               ref_pcg_d=d, ref_pcg_iters=iters, ref_pcg_ok=ok,
+               ref_pcg12_d=d12, ref_pcg12_iters=iters12, ref_pcg12_ok=ok12,
+               ref_dense=a.astype(np.float64))
+    for s, (hess, vids) in zip((int(h.shape[1]) // 3 for h, _ in grouped), grouped):
+        out[f"fam{s}_hess"] = hess
+        out[f"fam{s}_vids"] = vids
+    save("scene", **out)
+
+
+if __name__ == "__main__":
+    golden_scalars()
+    golden_classify()
+    golden_plain_blocks()
+    golden_parallel_blocks()
+    golden_scene()
