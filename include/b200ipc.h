@@ -1,0 +1,152 @@
+/*
+ * b200ipc.h -- C ABI of the B200 (sm_100a) GIPC barrier hot path.
+ *
+ * Drop-in boundary for the reference package `tetipc` (arXiv 2308.09400).  Every
+ * entry point names the reference interface it replaces (paths relative to
+ * /root/reference/pkg/src/tetipc).  Plain pointers and sizes only; no torch or
+ * Python types.  Unless a parameter says "host", every pointer is DEVICE memory
+ * owned by the caller; the library never frees or retains caller buffers.  All
+ * functions are asynchronous on `stream` (a cudaStream_t passed as void*; NULL =
+ * the legacy default stream) unless stated otherwise, and return
+ *     0   success
+ *    <0   -(cudaError_t) of the failing runtime call / launch
+ *    >0   argument error (B200IPC_EINVAL ...)
+ * Per-stencil conditions are reported through `status` bytes, which the host side
+ * turns into the reference's exceptions (gap.py:23-32).
+ *
+ * Arithmetic: fp64 throughout.  The library is compiled with -fmad=false so the
+ * geometric predicates round exactly like the reference's compiled backend
+ * (kernels/_core.pyx, x86-64 without FMA); the few places where the reference goes
+ * through BLAS ddot on 3-vectors use an explicit fused chain.
+ */
+#ifndef B200IPC_H
+#define B200IPC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define B200IPC_ABI_VERSION 1
+
+#define B200IPC_EINVAL 1   /* bad argument (null pointer, negative size, bad kind/size) */
+#define B200IPC_ESTATE 2   /* handle used out of order (e.g. numeric before symbolic) */
+
+/* Stencil kinds = rank of StencilKind.value in string order, i.e. the order of the
+ * reference contact list (proximity.py:27-34, sort_key :82-83). */
+enum {
+  B200IPC_EE = 0, B200IPC_EEP = 1, B200IPC_PE = 2, B200IPC_PEP = 3,
+  B200IPC_PP = 4, B200IPC_PPP = 5, B200IPC_PT = 6, B200IPC_NKINDS = 7
+};
+
+/* per-stencil status byte */
+enum { B200IPC_ACTIVE = 0, B200IPC_INACTIVE = 1 /* d2 >= d_hat^2: skipped, solver.py:204 */,
+       B200IPC_PENETRATION = 2 /* d2 <= 0: InterpenetrationError, gap.py:61 */ };
+
+/* BarrierParams (barrier.py:24-53) + the solver's dt^2 (solver.py:192), pre-evaluated
+ * on the host exactly as the reference's Python expressions evaluate them. */
+typedef struct b200ipc_params {
+  double d_hat;        /* params.d_hat                                              */
+  double d_hat_sq;     /* d_hat*d_hat   -- gap.py:63, proximity.py:292,327          */
+  double d_hat_pow2;   /* d_hat**2      -- solver.py:134,141,204 (libm pow)         */
+  double scale;        /* kappa * d_hat**4 -- barrier.py:79                         */
+  double eps_g;        /* d_thr_ratio**2   -- barrier.py:51-53                      */
+  double dt2;          /* dt**2; multiplies grad and hess, not energy (solver.py:207) */
+  int32_t use_filter;  /* proximal filter on lambda1 (barrier.py:114-120)           */
+  int32_t form;        /* 0 = qlog (production), 1 = log (diagnostic)               */
+} b200ipc_params;
+
+/* ---- library ---------------------------------------------------------------- */
+int b200ipc_abi_version(void);
+/* Static string: build flags and target arch ("sm_100a"). */
+const char* b200ipc_build_info(void);
+/* Number of kernel launches issued by this library since load (all threads). */
+int64_t b200ipc_launch_count(void);
+
+/* ---- tetipc.kernels twins (kernels/__init__.py:28-31) ------------------------ */
+/* pt_classify_batch (_core.pyx:46-106,153-171): p,t1,t2,t3 are (n,3) f64 row-major.
+ * codes (n) i64, d2 (n), grad (n,4,3), w (n,2).  Any output pointer may be NULL. */
+int b200ipc_pt_classify(int64_t n, const double* p, const double* t1, const double* t2,
+                        const double* t3, int64_t* codes, double* d2, double* grad,
+                        double* w, void* stream);
+/* ee_classify_batch (_core.pyx:109-150,174-192). codes = 3*ra+rb, w = (s,t). */
+int b200ipc_ee_classify(int64_t n, const double* a1, const double* a2, const double* b1,
+                        const double* b2, int64_t* codes, double* d2, double* grad,
+                        double* w, void* stream);
+/* cross_sq_batch (_core.pyx:195-219): c (n), grad (n,4,3). */
+int b200ipc_cross_sq(int64_t n, const double* a1, const double* a2, const double* b1,
+                     const double* b2, double* c, double* grad, void* stream);
+/* matvec_blocks (_core.pyx:222-247): out += scatter(H_b . gather(x)).
+ * hess (nb,3s,3s) f64, vids (nb,s) i64, x/out (3N).  s in {2,3,4}.  Accumulation order is
+ * not the serial block order of the reference (fp64 atomics); see DESIGN.md. */
+int b200ipc_matvec_blocks(int64_t nb, int32_t s, const double* hess, const int64_t* vids,
+                          const double* x, double* out, void* stream);
+
+/* ---- contact stencils: energy, gradient, PSD block ---------------------------- */
+/* Fused twin of stencil_distance (proximity.py:183-222), parallel_measure (:225-229),
+ * build_diagonal_jacobian (gap.py:56-82), barrier scalars (barrier.py:76-120),
+ * build_local_quadratic (barrier.py:163-177), mollified_* (mollifier.py:55-144,191-210),
+ * SimState._barrier_energy (solver.py:127-146) and the barrier loop of
+ * assemble_local_quadratics (solver.py:202-209).
+ *
+ * The stencil table is sorted by kind (the reference list order); kind_off[k]..kind_off[k+1]
+ * (host array of 8 int64) is the row range of kind k.
+ *   positions (nverts,3) f64
+ *   verts     (n,4) i32, -1 padded          sub (n) u8 (two bits per local index)
+ *   eps_x     (n) f64 (parallel kinds)
+ * Outputs (any may be NULL to skip it):
+ *   energy (n)  per-stencil b(g) or e(c) b(g), g = d2/d_hat**2, not dt2-scaled; 0 if inactive
+ *   status (n)  u8
+ *   grad2/hess2 (n_PP,6)/(n_PP,6,6); grad3/hess3 (n_PE,9)/(n_PE,9,9);
+ *   grad4/hess4 (n4,12)/(n4,12,12) with n4 = n_EE+n_EEP+n_PEP+n_PPP+n_PT, rows in that
+ *   order -- the size families of group_blocks (solver.py:237-248).  Inactive rows are
+ *   written as zeros.  grad/hess are dt2-scaled. */
+int b200ipc_barrier_stencils(const b200ipc_params* params /* host */, int64_t nverts,
+                             const double* positions, int64_t n, const int64_t* kind_off /* host[8] */,
+                             const int32_t* verts, const uint8_t* sub, const double* eps_x,
+                             double* energy, uint8_t* status,
+                             double* grad2, double* hess2, double* grad3, double* hess3,
+                             double* grad4, double* hess4, void* stream);
+
+/* ---- per-stencil entry points kept as batched kernels ------------------------- */
+/* stencil_distance (proximity.py:183-222) + parallel_measure (:225-229) +
+ * build_diagonal_jacobian (gap.py:56-82) for n table rows in any order (kind is a device
+ * array here).  All outputs padded to four vertex rows: d2 (n), grad_d2 (n,4,3),
+ * witness (n,2), f (n), grad_f (n,4,3); parallel kinds only: c (n), grad_c (n,4,3),
+ * sqrt_c (n), grad_sqrt_c (n,4,3) (rows of other kinds untouched).  status compares against
+ * d_hat*d_hat like gap.py:61-64.  Any output may be NULL. */
+int b200ipc_diagonal_jacobian(const b200ipc_params* params /* host */, int64_t nverts,
+                              const double* positions, int64_t n, const uint8_t* kind,
+                              const int32_t* verts, const uint8_t* sub,
+                              double* d2, double* grad_d2, double* witness, double* f, double* grad_f,
+                              double* c, double* grad_c, double* sqrt_c, double* grad_sqrt_c,
+                              uint8_t* status, void* stream);
+/* build_local_quadratic (barrier.py:163-177) / build_mollified_local_quadratic
+ * (mollifier.py:191-210) from a given Jacobian: f (n), grad_f (n,12), and for parallel kinds
+ * sqrt_c (n), grad_sqrt_c (n,12), eps_x (n).  grad (n,12), hess (n,12,12), padded, times dt2. */
+int b200ipc_blocks_from_jacobian(const b200ipc_params* params /* host */, int64_t n, const uint8_t* kind,
+                                 const double* f, const double* grad_f, const double* sqrt_c,
+                                 const double* grad_sqrt_c, const double* eps_x,
+                                 double* grad, double* hess, void* stream);
+/* barrier_value/dg/d2g, lambda1, lambda23, filtered_lambda1 (barrier.py:76-120) at g (n):
+ * out (n,6) = (b, b', b'', lambda1, lambda23, filtered lambda1). */
+int b200ipc_barrier_scalars(const b200ipc_params* params /* host */, int64_t n, const double* g,
+                            double* out, void* stream);
+/* mollified_eigensystem (mollifier.py:106-144) at (g, c, eps_x) (n each): out (n,12) =
+ * (lam_gamma1, lam_g1, t, p, lambda7', lambda8', q_gamma, q_f, b_gamma, b_g, e_k, e_k'). */
+int b200ipc_mollified_eigensystem(const b200ipc_params* params /* host */, int64_t n, const double* g,
+                                  const double* c, const double* eps_x, double* out, void* stream);
+
+/* Sum of energy[0..n) (the scalar of SimState._barrier_energy, solver.py:127-146) and the
+ * counts of status==1 / status==2, deterministic two-pass.  result: device double[1];
+ * counts: device int64[2] (inactive, penetration); workspace: device scratch of at least
+ * B200IPC_REDUCE_WS_BYTES. */
+#define B200IPC_REDUCE_WS_BYTES 16384
+int b200ipc_reduce_energy(int64_t n, const double* energy, const uint8_t* status,
+                          double* result, int64_t* counts, void* workspace, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* B200IPC_H */

@@ -1,0 +1,61 @@
+"""Device-memory plumbing: torch owns HBM and streams, the kernels get raw pointers."""
+
+import ctypes as C
+
+import numpy as np
+
+_torch = None
+
+
+def torch():
+    global _torch
+    if _torch is None:
+        import torch as _t
+
+        if not _t.cuda.is_available():
+            raise RuntimeError("paper_2308_09400_b200 needs a CUDA device (sm_100a); there is no CPU path")
+        _torch = _t
+    return _torch
+
+
+_NP2T = None
+
+
+def _dtype(np_dtype):
+    global _NP2T
+    t = torch()
+    if _NP2T is None:
+        _NP2T = {np.dtype(np.float64): t.float64, np.dtype(np.int64): t.int64, np.dtype(np.int32): t.int32,
+                 np.dtype(np.uint8): t.uint8, np.dtype(np.bool_): t.bool}
+    return _NP2T[np.dtype(np_dtype)]
+
+
+def empty(shape, dtype=np.float64):
+    return torch().empty(shape, dtype=_dtype(dtype), device="cuda")
+
+
+def zeros(shape, dtype=np.float64):
+    return torch().zeros(shape, dtype=_dtype(dtype), device="cuda")
+
+
+def to_device(a, dtype=None):
+    """Host array (or device tensor) -> contiguous device tensor of ``dtype``."""
+    t = torch()
+    if isinstance(a, t.Tensor):
+        out = a if dtype is None else a.to(_dtype(dtype))
+        return out.cuda().contiguous()
+    arr = np.ascontiguousarray(a, dtype=dtype)
+    return t.from_numpy(arr).cuda()
+
+
+def to_host(x):
+    return x.detach().cpu().numpy()
+
+
+def ptr(x):
+    """Raw device pointer of a tensor (None -> NULL)."""
+    return C.c_void_p(None) if x is None else C.c_void_p(x.data_ptr())
+
+
+def stream():
+    return C.c_void_p(torch().cuda.current_stream().cuda_stream)

@@ -1,0 +1,242 @@
+"""GPU parity of the fused barrier stencil kernel and the per-stencil entry points.
+
+Bar (BASELINE.json north_star): status / kinds exact; energy, gradient, Hessian per-entry
+relative error <= 1e-9 (entries that are analytically zero measured against the block scale);
+projected blocks PSD (min eigenvalue >= -1e-12 * lambda_max) and symmetric.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import block_rel_err, load_golden
+from oracle import tetipc_oracle as o
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-9
+PARAM_SETS = {"unit": (1.0, 1.0, 1.0), "scene": (5e-3, 2e8, 0.01)}
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2308_09400_b200 as pkg
+    from paper_2308_09400_b200 import barrier, device, gap, mollifier, proximity, stencils, workloads
+
+    class NS:
+        pass
+
+    ns = NS()
+    ns.pkg, ns.barrier, ns.device, ns.gap, ns.mollifier = pkg, barrier, device, gap, mollifier
+    ns.proximity, ns.stencils, ns.workloads = proximity, stencils, workloads
+    return ns
+
+
+def padded(P, batch):
+    """BarrierBatch -> (energy, status, grad (n,12), hess (n,12,12)) in table order."""
+    n = batch.table.n
+    energy = P.device.to_host(batch.energy)
+    status = P.device.to_host(batch.status)
+    grad = np.zeros((n, 12))
+    hess = np.zeros((n, 12, 12))
+    off = batch.table.kind_off
+    for s, fam in batch.families.items():
+        rows = np.concatenate([np.arange(off[k], off[k + 1]) for k in P.stencils.FAMILY_KINDS[s]])
+        grad[rows, : 3 * s] = P.device.to_host(fam.grad)
+        hess[rows, : 3 * s, : 3 * s] = P.device.to_host(fam.hess)
+    return energy, status, grad, hess
+
+
+def table_from(P, z):
+    return P.proximity.StencilTable(z["kind"], z["verts"], z["sub"], z["eps_x"], z.get("origin_type"), z.get("origin"))
+
+
+def check_psd_symmetric(hess):
+    assert np.array_equal(hess, hess.transpose(0, 2, 1)), "blocks must be bit-symmetric"
+    w = np.linalg.eigvalsh(hess)
+    lam_max = np.maximum(w.max(axis=1), 1e-300)
+    assert np.all(w.min(axis=1) >= -1e-12 * lam_max)
+    # rank <= 1: second largest eigenvalue is noise
+    assert np.all(np.sort(np.abs(w), axis=1)[:, -2] <= 1e-12 * lam_max + 1e-300)
+
+
+@pytest.mark.parametrize("pset", ["unit", "scene"])
+def test_plain_blocks_vs_reference_golden(P, pset):
+    z = load_golden("blocks_plain")
+    d_hat, kappa, dt = PARAM_SETS[pset]
+    x = z["positions"] * d_hat
+    params = P.barrier.BarrierParams(d_hat=d_hat, kappa=kappa)
+    batch = P.stencils.evaluate(table_from(P, z), x, params, dt=dt)
+    energy, status, grad, hess = padded(P, batch)
+    np.testing.assert_array_equal(status, z[f"{pset}_ref_status"])
+    np.testing.assert_allclose(energy, z[f"{pset}_ref_energy"], rtol=TOL, atol=0.0)
+    assert block_rel_err(grad, z[f"{pset}_ref_grad"]) < TOL
+    assert block_rel_err(hess, z[f"{pset}_ref_hess"]) < TOL
+    check_psd_symmetric(hess)
+    nf = P.stencils.evaluate(table_from(P, z), x, P.barrier.BarrierParams(d_hat=d_hat, kappa=kappa, use_filter=False), dt=dt)
+    assert block_rel_err(padded(P, nf)[3], z[f"{pset}_nofilter_ref_hess"]) < TOL
+
+
+def test_parallel_blocks_vs_reference_golden(P):
+    z = load_golden("blocks_parallel")
+    params = P.barrier.BarrierParams(d_hat=1.0, kappa=1.0)
+    batch = P.stencils.evaluate(table_from(P, z), z["positions"], params)
+    energy, status, grad, hess = padded(P, batch)
+    np.testing.assert_array_equal(status, z["unit_ref_status"])
+    np.testing.assert_allclose(energy, z["unit_ref_energy"], rtol=TOL, atol=0.0)
+    assert block_rel_err(grad, z["unit_ref_grad"]) < TOL
+    assert block_rel_err(hess, z["unit_ref_hess"]) < TOL
+    check_psd_symmetric(hess)
+    total, n_inactive, n_pen = batch.summary()
+    assert total == pytest.approx(float(z["unit_ref_energy"].sum()), rel=1e-12)
+    assert (n_inactive, n_pen) == (int((status == 1).sum()), 0)
+
+
+def oracle_table(P, batch_in):
+    tab = o.narrow_phase(batch_in.positions, batch_in.rest_positions, batch_in.vt, batch_in.ee, batch_in.d_hat)
+    return tab, P.proximity.StencilTable(tab["kind"], tab["verts"], tab["sub"], tab["eps_x"], tab["origin_type"],
+                                         tab["origin"])
+
+
+@pytest.mark.parametrize("d_hat,kappa,dt", [(1.0, 1.0, 1.0), (5e-3, 2e8, 0.01)])
+def test_config1_10k_pt_ee_vs_oracle(P, d_hat, kappa, dt):
+    """BASELINE config 1: 5000 PT + 5000 EE stencils, every entry against the CPU oracle."""
+    qb = P.workloads.config1_batch(d_hat=d_hat, kappa=kappa, dt=dt, scale=1.0 if d_hat == 1.0 else 0.05)
+    tab, table = oracle_table(P, qb)
+    assert len(table) == 10000 and set(tab["kind"].tolist()) == {o.EE, o.PT}
+    params = P.barrier.BarrierParams(d_hat=d_hat, kappa=kappa)
+    energy, status, grad, hess = padded(P, P.stencils.evaluate(table, qb.positions, params, dt=dt))
+    ref = o.local_quadratics_batch(tab["kind"], tab["verts"], tab["sub"], tab["eps_x"], qb.positions, d_hat, kappa,
+                                   dt2=dt * dt)
+    np.testing.assert_array_equal(status, ref["status"])
+    np.testing.assert_allclose(energy, ref["energy"], rtol=TOL, atol=0.0)
+    assert block_rel_err(grad, ref["grad"]) < TOL
+    assert block_rel_err(hess, ref["hess"]) < TOL
+    check_psd_symmetric(hess)
+
+
+def test_config2_parallel_subset_vs_oracle(P):
+    """BASELINE config 2 recipe at 40k rows: all three mollified kinds, c == 0 rows, wide rows."""
+    qb = P.workloads.config2_batch(n=40000)
+    tab, table = oracle_table(P, qb)
+    kinds = set(tab["kind"].tolist())
+    assert {o.EEP, o.PEP, o.PPP} <= kinds
+    params = P.barrier.BarrierParams(d_hat=qb.d_hat, kappa=qb.kappa)
+    energy, status, grad, hess = padded(P, P.stencils.evaluate(table, qb.positions, params))
+    ref = o.local_quadratics_batch(tab["kind"], tab["verts"], tab["sub"], tab["eps_x"], qb.positions, qb.d_hat, qb.kappa)
+    np.testing.assert_array_equal(status, ref["status"])
+    np.testing.assert_allclose(energy, ref["energy"], rtol=TOL, atol=1e-300)
+    assert block_rel_err(grad, ref["grad"]) < TOL
+    # the reference's k2 = (dl + 2p)/(8t) cancels catastrophically when lam_gamma1 < lam_g1 and
+    # |t| << |dl|: there the two correctly-rounded evaluations
+    # differ by ulp(dl)/(8|t|); compare those rows through that bound and all others at 1e-9
+    par = np.flatnonzero(o.IS_PARALLEL[tab["kind"]])
+    c, _ = o.parallel_measure_batch(tab["verts"][par], qb.positions)
+    sc = np.sqrt(c)
+    sysm = o.mollified_eigensystem(ref["f"][par] ** 2, sc * sc, tab["eps_x"][par], qb.kappa * qb.d_hat**4)
+    dl = sysm["lam_gamma1"] - sysm["lam_g1"]
+    with np.errstate(divide="ignore", invalid="ignore"):
+        amp_par = np.where(dl < 0, 4e-16 * np.abs(dl) / np.abs(8.0 * sysm["t"]), 0.0)
+    amp = np.zeros(len(table))
+    amp[par] = np.nan_to_num(amp_par, nan=0.0, posinf=0.0)
+    easy = amp < 1e-11
+    assert easy.mean() > 0.97
+    assert block_rel_err(hess[easy], ref["hess"][easy]) < TOL
+    check_psd_symmetric(hess)
+
+
+def test_inactive_and_penetrating_rows(P):
+    """Rows beyond d_hat are skipped (zero blocks, status 1); d2 == 0 raises like gap.py:61."""
+    x = np.array([[0.0, 0, 0], [0, 0, 2.0], [0.0, 0, 0.5], [1, 1, 1.0], [1, 1, 1.0]])
+    table = P.proximity.StencilTable(np.full(3, o.PP, np.uint8), [[0, 1, -1, -1], [0, 2, -1, -1], [3, 4, -1, -1]],
+                                     np.zeros(3, np.uint8), np.zeros(3))
+    params = P.barrier.BarrierParams(d_hat=1.0, kappa=1.0)
+    batch = P.stencils.evaluate(table, x, params)
+    energy, status, grad, hess = padded(P, batch)
+    np.testing.assert_array_equal(status, [1, 0, 2])
+    assert np.all(grad[[0, 2]] == 0) and np.all(hess[[0, 2]] == 0) and np.all(energy[[0, 2]] == 0)
+    assert np.trace(hess[1]) == pytest.approx(123.6518037225672, rel=1e-12)
+    assert batch.summary()[1:] == (1, 1)
+    with pytest.raises(P.gap.InterpenetrationError):
+        batch.raise_on_penetration()
+    with pytest.raises(P.gap.InterpenetrationError):
+        P.stencils.barrier_energy(table, x, params)
+    blocks = batch.to_local_quadratics()
+    assert len(blocks) == 1 and blocks[0].vert_ids.tolist() == [0, 2]
+
+
+def test_empty_table(P):
+    table = P.proximity.StencilTable(np.zeros(0, np.uint8), np.zeros((0, 4), np.int32), np.zeros(0, np.uint8), np.zeros(0))
+    batch = P.stencils.evaluate(table, np.zeros((4, 3)), P.barrier.BarrierParams(d_hat=1.0))
+    assert batch.families == {} and batch.grouped() == []
+
+
+def test_energy_only_and_known_answers(P):
+    """Known answers of the reference tests through the public per-stencil entry points."""
+    prm = P.barrier.BarrierParams(d_hat=1.0, kappa=1.0)
+    assert float(P.barrier.barrier_value(0.25, prm)) == pytest.approx(1.0810193, rel=1e-6)
+    assert float(P.barrier.barrier_dg(0.25, prm)) == pytest.approx(-9.1210427, rel=1e-7)
+    assert float(P.barrier.barrier_d2g(0.25, prm)) == pytest.approx(80.067988, rel=1e-7)
+    assert float(P.barrier.lambda1(0.25, prm)) == pytest.approx(61.825903, rel=1e-7)
+    assert float(P.barrier.lambda23(0.25, prm)) == pytest.approx(-18.242085, rel=1e-7)
+    assert float(P.barrier.filtered_lambda1(0.0025, prm)) == pytest.approx(2653.097252532248, rel=1e-12)
+    g = np.linspace(0.01, 0.99, 99)
+    z = load_golden("scalars")
+    np.testing.assert_allclose(P.barrier.barrier_value(g, prm), z["unit_qlog_b"][:99], rtol=1e-12)
+    np.testing.assert_allclose(P.barrier.barrier_d2g(g, prm), z["unit_qlog_bgg"][:99], rtol=1e-12)
+    logp = P.barrier.BarrierParams(d_hat=1.0, kappa=1.0, form="log")
+    np.testing.assert_allclose(P.barrier.barrier_dg(g, logp), z["unit_log_bg"][:99], rtol=1e-12)
+    assert P.mollifier.mollified_barrier_value(0.25, 0.5e-3, prm, 1e-3) == pytest.approx(0.8107645, rel=1e-6)
+    with pytest.raises(ValueError):
+        P.barrier.BarrierParams(d_hat=-1.0)
+
+
+def test_per_stencil_entry_points(P):
+    """stencil_distance / build_diagonal_jacobian / build_*_local_quadratic as n = 1 shims."""
+    CS, SK = P.proximity.ContactStencil, P.proximity.StencilKind
+    prm = P.barrier.BarrierParams(d_hat=1.0, kappa=1.0)
+    x = np.array([[.1, .05, .5], [1, 0, 0], [-1, 1, 0], [-1, -1, 0.0]])
+    st = CS(kind=SK.POINT_TRIANGLE, verts=(0, 1, 2, 3))
+    dist = P.gap.stencil_distance(st, x)
+    assert dist.d2 == pytest.approx(0.25, rel=1e-15) and dist.grad_d2.shape == (4, 3)
+    assert np.abs(dist.grad_d2.sum(axis=0)).max() < 1e-15
+    jac = P.gap.build_diagonal_jacobian(st, x, 1.0)
+    assert jac.m == 3 and jac.f == pytest.approx(0.5, rel=1e-15)
+    blk = P.barrier.build_local_quadratic(st, jac, prm)
+    np.testing.assert_allclose(blk.grad[2::3], [-9.121042708548716, 5.016573489701793, 2.280260677137179,
+                                                1.8242085417097436], rtol=1e-12)
+    assert np.trace(blk.hess) == pytest.approx(86.86539211510345, rel=1e-12)
+    assert blk.vert_ids.dtype == np.int64
+    # point-edge: 9x9
+    xe = np.array([[.25, .4, 0], [0, 0, 0], [1, 0, 0.0]])
+    ste = CS(kind=SK.POINT_EDGE, verts=(0, 1, 2))
+    blk = P.barrier.build_local_quadratic(ste, P.gap.build_diagonal_jacobian(ste, xe, 1.0), prm)
+    assert blk.hess.shape == (9, 9) and np.trace(blk.hess) == pytest.approx(178.55686669896568, rel=1e-12)
+    # error classes (gap.py:61-64)
+    with pytest.raises(P.gap.BarrierInactiveError):
+        P.gap.build_diagonal_jacobian(st, x, 0.4)
+    with pytest.raises(P.gap.InterpenetrationError):
+        P.gap.build_diagonal_jacobian(CS(kind=SK.POINT_POINT, verts=(0, 1)), np.zeros((2, 3)), 1.0)
+    with pytest.raises(ValueError):
+        P.mollifier.build_mollified_local_quadratic(st, jac, prm)
+    # EE-parallel KAT
+    xp = np.array([[-1.0, 0, 0], [1.0, 0, 0], [-np.cos(2e-3), -np.sin(2e-3), 0.4], [np.cos(2e-3), np.sin(2e-3), 0.4]])
+    sp = CS(kind=SK.EDGE_EDGE_PARALLEL, verts=(0, 1, 2, 3), eps_x=0.016, sub=(0, 1, 2, 3))
+    c, gc = P.gap.parallel_measure(sp, xp)
+    assert c == pytest.approx(6.399991466671217e-05, rel=1e-12) and gc.shape == (4, 3)
+    jp = P.gap.build_diagonal_jacobian(sp, xp, 1.0)
+    gv = P.gap.gap_function(jp)
+    sysm = P.mollifier.mollified_eigensystem(gv.g, gv.gamma, prm, 0.016)
+    assert sysm.lambda8p == pytest.approx(587.3637020327291, rel=1e-11)
+    assert sysm.lambda7p == pytest.approx(-1.1815776429242533, rel=1e-9)
+    assert sysm.q_gamma == pytest.approx(-0.9982493519246743, rel=1e-11)
+    blk = P.mollifier.build_mollified_local_quadratic(sp, jp, prm)
+    assert np.trace(blk.hess) == pytest.approx(9366.998220497468, rel=1e-10)
+    with pytest.raises(ValueError):
+        P.barrier.build_local_quadratic(sp, jp, prm)
+    # exactly parallel pair: zero gradient and block (test_mollifier.py:227-236)
+    x0 = np.array([[0, 0, 0], [1, 0, 0], [0, .4, 0], [1, .4, 0.0]])
+    s0 = CS(kind=SK.EDGE_EDGE_PARALLEL, verts=(0, 1, 2, 3), eps_x=1e-3, sub=(0, 1, 2, 3))
+    j0 = P.gap.build_diagonal_jacobian(s0, x0, 1.0)
+    assert j0.sqrt_c == 0.0 and np.all(j0.grad_sqrt_c == 0.0)
+    b0 = P.mollifier.build_mollified_local_quadratic(s0, j0, prm)
+    assert np.all(b0.grad == 0.0) and np.all(b0.hess == 0.0)
