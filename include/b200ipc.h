@@ -82,6 +82,11 @@ int b200ipc_cross_sq(int64_t n, const double* a1, const double* a2, const double
  * not the serial block order of the reference (fp64 atomics); see DESIGN.md. */
 int b200ipc_matvec_blocks(int64_t nb, int32_t s, const double* hess, const int64_t* vids,
                           const double* x, double* out, void* stream);
+/* matvec_matrix_free (solver.py:251-262) = begin + matvec_blocks per family + end:
+ * begin: vin = v with fixed rows zeroed, out = m * vin;  end: out[fixed] = v[fixed]. */
+int b200ipc_matvec_begin(int64_t nverts, const double* masses, const uint8_t* fixed, const double* v,
+                         double* vin, double* out, void* stream);
+int b200ipc_matvec_end(int64_t nverts, const uint8_t* fixed, const double* v, double* out, void* stream);
 
 /* ---- contact stencils: energy, gradient, PSD block ---------------------------- */
 /* Fused twin of stencil_distance (proximity.py:183-222), parallel_measure (:225-229),
@@ -145,6 +150,59 @@ int b200ipc_mollified_eigensystem(const b200ipc_params* params /* host */, int64
 #define B200IPC_REDUCE_WS_BYTES 16384
 int b200ipc_reduce_energy(int64_t n, const double* energy, const uint8_t* status,
                           double* result, int64_t* counts, void* workspace, void* stream);
+
+/* ---- assembly into the 3x3-block sparse global matrix (BSR) -------------------- */
+/* The reference's production path is matrix-free; the assembled matrix is the one its tests
+ * build densely (tests/test_solver.py:71-84): A = diag(m_i I3) + sum_b scatter(H_b), fixed
+ * rows/cols zeroed, unit diagonal.  Pattern := {(i,j): i,j in one block's vert_ids} U {(i,i)},
+ * fixed rows reduced to the diagonal; columns ascend within a row.
+ *
+ * A handle owns the pattern and sort workspaces of ONE contact set (one per scene/GPU; not
+ * thread-safe).  Families are the (hess, vids) pairs of group_blocks (solver.py:237-248):
+ * fam_s[f] in {2,3,4}, fam_nb[f] blocks, fam_vids[f] device (nb,s) int64. */
+typedef struct b200ipc_assembly b200ipc_assembly;
+int b200ipc_assembly_create(b200ipc_assembly** out);
+int b200ipc_assembly_destroy(b200ipc_assembly* h);
+/* Build the pattern and the source runs (sort by key).  fixed: device u8 (nverts).  Synchronises
+ * `stream` and returns the number of 3x3 blocks in *nnzb_out (host).  The vids buffers must stay
+ * valid until the next symbolic call (the numeric phase re-reads nothing from them). */
+int b200ipc_assemble_symbolic(b200ipc_assembly* h, int64_t nverts, const uint8_t* fixed, int32_t nfam,
+                              const int32_t* fam_s /* host */, const int64_t* fam_nb /* host */,
+                              const int64_t* const* fam_vids /* host array of device ptrs */,
+                              int64_t* nnzb_out /* host */, void* stream);
+/* Copy the pattern out: rowptr (nverts+1) i32, colidx (nnzb) i32, device. */
+int b200ipc_assembly_pattern(b200ipc_assembly* h, int32_t* rowptr, int32_t* colidx, void* stream);
+/* vals (nnzb,3,3) = segmented sum of the sub-blocks in list order; no atomics, deterministic.
+ * fam_hess[f]: device (nb,3s,3s). */
+int b200ipc_assemble_numeric(b200ipc_assembly* h, const double* masses,
+                             const double* const* fam_hess /* host array of device ptrs */,
+                             double* vals, void* stream);
+/* SimState.gradient (solver.py:218-226): out (3 nverts) = m (x - x_tilde) + sum scatter(grad_b),
+ * fixed rows 0.  fam_grad[f]: device (nb,3s). */
+int b200ipc_scatter_gradient(b200ipc_assembly* h, const double* masses, const double* x,
+                             const double* x_tilde, const double* const* fam_grad /* host array */,
+                             double* out, void* stream);
+
+/* ---- solver kernels over the assembled matrix ---------------------------------- */
+/* y = A x (the assembled twin of matvec_matrix_free, solver.py:251-262). */
+int b200ipc_bsr_spmv(int64_t nverts, int64_t nnzb, const int32_t* rowptr, const int32_t* colidx,
+                     const double* vals, const double* x, double* y, void* stream);
+/* block_jacobi_preconditioner (solver.py:265-276): pinv (nverts,3,3) = inverse diagonal blocks. */
+int b200ipc_block_jacobi(int64_t nverts, const int32_t* rowptr, const int32_t* colidx,
+                         const double* vals, double* pinv, void* stream);
+typedef struct b200ipc_pcg_result {
+  int32_t iters;
+  int32_t converged;   /* delta_new <= rel_tol*delta0 (or delta0 <= 0) */
+  double delta0;
+  double delta_new;
+} b200ipc_pcg_result;
+int64_t b200ipc_pcg_workspace_bytes(int64_t nverts);
+/* pcg_solve (solver.py:279-315) as one persistent cooperative kernel.  rhs, d: (3 nverts);
+ * fixed: u8 (nverts).  Synchronises `stream`; *result is host memory. */
+int b200ipc_pcg(int64_t nverts, int64_t nnzb, const int32_t* rowptr, const int32_t* colidx,
+                const double* vals, const double* pinv, const uint8_t* fixed, const double* rhs,
+                double* d, double rel_tol, int32_t max_iters, void* workspace, int64_t workspace_bytes,
+                b200ipc_pcg_result* result /* host */, void* stream);
 
 #ifdef __cplusplus
 }

@@ -52,6 +52,8 @@ SIGNATURES = {
     "b200ipc_ee_classify": [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "b200ipc_cross_sq": [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "b200ipc_matvec_blocks": [_i64, _i32, _vp, _vp, _vp, _vp, _vp],
+    "b200ipc_matvec_begin": [_i64, _vp, _vp, _vp, _vp, _vp, _vp],
+    "b200ipc_matvec_end": [_i64, _vp, _vp, _vp, _vp],
     "b200ipc_barrier_stencils": [C.POINTER(Params), _i64, _vp, _i64, C.POINTER(_i64), _vp, _vp, _vp,
                                  _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "b200ipc_reduce_energy": [_i64, _vp, _vp, _vp, _vp, _vp, _vp],
@@ -60,8 +62,6 @@ SIGNATURES = {
     "b200ipc_blocks_from_jacobian": [C.POINTER(Params), _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "b200ipc_barrier_scalars": [C.POINTER(Params), _i64, _vp, _vp, _vp],
     "b200ipc_mollified_eigensystem": [C.POINTER(Params), _i64, _vp, _vp, _vp, _vp, _vp],
-}
-_PENDING = {
     "b200ipc_assembly_create": [C.POINTER(_vp)],
     "b200ipc_assembly_destroy": [_vp],
     "b200ipc_assemble_symbolic": [_vp, _i64, _vp, _i32, C.POINTER(_i32), C.POINTER(_i64), C.POINTER(_vp),
@@ -69,12 +69,11 @@ _PENDING = {
     "b200ipc_assembly_pattern": [_vp, _vp, _vp, _vp],
     "b200ipc_assemble_numeric": [_vp, _vp, C.POINTER(_vp), _vp, _vp],
     "b200ipc_scatter_gradient": [_vp, _vp, _vp, _vp, C.POINTER(_vp), _vp, _vp],
-    "b200ipc_bsr_spmv": [_i64, _vp, _vp, _vp, _vp, _vp, _vp],
+    "b200ipc_bsr_spmv": [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp],
     "b200ipc_block_jacobi": [_i64, _vp, _vp, _vp, _vp, _vp],
     "b200ipc_pcg_workspace_bytes": [_i64],
-    "b200ipc_pcg": [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _dbl, _i32, _vp, _i64, C.POINTER(PcgResult), _vp],
-    "b200ipc_narrow_phase": [_i64, _vp, _vp, _i64, _vp, _i64, _vp, _dbl, _i32, _vp, _vp, _vp, _vp, _vp, _vp,
-                             _vp, _vp],
+    "b200ipc_pcg": [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _dbl, _i32, _vp, _i64, C.POINTER(PcgResult),
+                    _vp],
 }
 _RESTYPE = {"b200ipc_build_info": C.c_char_p, "b200ipc_launch_count": _i64,
             "b200ipc_pcg_workspace_bytes": _i64}

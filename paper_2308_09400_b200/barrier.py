@@ -74,8 +74,9 @@ def _scalars(g, params):
     flat = np.ascontiguousarray(g_arr.reshape(-1))
     out = device.empty((flat.shape[0], 6))
     prm = c_params(params)
-    _lib.check(_lib.lib().b200ipc_barrier_scalars(prm, flat.shape[0], device.ptr(device.to_device(flat)),
-                                                  device.ptr(out), device.stream()), "barrier_scalars")
+    d_g = device.to_device(flat)
+    _lib.check(_lib.lib().b200ipc_barrier_scalars(prm, flat.shape[0], device.ptr(d_g), device.ptr(out),
+                                                  device.stream()), "barrier_scalars")
     return device.to_host(out), g_arr.shape
 
 
@@ -132,8 +133,9 @@ def _blocks_from_jac(stencil, jac, params, parallel):
         eps = device.to_device(np.array([stencil.eps_x], np.float64))
     grad, hess = device.empty((1, 12)), device.empty((1, 12, 12))
     prm = c_params(params)
+    d_gf = device.to_device(gf)
     _lib.check(_lib.lib().b200ipc_blocks_from_jacobian(
-        prm, 1, device.ptr(kind), device.ptr(f), device.ptr(device.to_device(gf)), device.ptr(sc),
+        prm, 1, device.ptr(kind), device.ptr(f), device.ptr(d_gf), device.ptr(sc),
         device.ptr(gsc), device.ptr(eps), device.ptr(grad), device.ptr(hess), device.stream()),
         "blocks_from_jacobian")
     g, h = device.to_host(grad)[0, : 3 * s], device.to_host(hess)[0, : 3 * s, : 3 * s]

@@ -1,0 +1,434 @@
+// Scatter-assembly of the 6x6 / 9x9 / 12x12 local blocks into the 3x3-block sparse global
+// matrix (BSR), and the gradient scatter -- both WITHOUT atomics.
+//
+// The reference never assembles (matvec is matrix-free, solver.py:251-262); the assembled matrix
+// is defined by its test oracle (tests/test_solver.py:71-84): A = diag(m_i I3) + sum of blocks at
+// ix_(idx, idx), fixed rows/cols zeroed with a unit diagonal.
+//
+// symbolic (once per contact set): every (block, a, b) sub-block slot and every diagonal mass
+//   slot gets the key row*N+col; a stable LSD radix sort (CUB) of (key, slot) gives, per unique
+//   key, a contiguous run of source slots in list order; run heads -> colidx / rowptr.
+// numeric (once per Newton iteration): one thread per (unique block, entry) walks its run and sums
+//   the 3x3 sub-blocks in list order -- a segmented reduction by gather, deterministic, bitwise
+//   reproducible, no contention.  Threads of a warp write consecutive doubles of vals.
+// The gradient scatter (SimState.gradient, solver.py:218-226) reuses the same machinery keyed by
+// vertex.
+#include <cub/cub.cuh>
+
+#include "launch.cuh"
+#include "../../include/b200ipc.h"
+
+namespace b200ipc {
+
+constexpr int kMaxFam = 8;
+constexpr int kAT = 256;
+
+struct FamDesc {
+  int32_t s[kMaxFam];
+  int64_t nb[kMaxFam];
+  int64_t ent_off[kMaxFam + 1];   // prefix of nb*s*s  (matrix slots, after the N diagonal slots)
+  int64_t vert_off[kMaxFam + 1];  // prefix of nb*s    (gradient slots)
+  const int64_t* vids[kMaxFam];
+  int32_t nfam;
+};
+
+struct HessPtrs {
+  const double* p[kMaxFam];
+};
+
+template <typename T>
+struct DevBuf {
+  T* ptr = nullptr;
+  size_t cap = 0;
+  cudaError_t reserve(size_t n) {
+    if (n <= cap) return cudaSuccess;
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    cap = 0;
+    cudaError_t e = cudaMalloc(&ptr, n * sizeof(T));
+    if (e == cudaSuccess) cap = n;
+    return e;
+  }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    cap = 0;
+  }
+};
+
+}  // namespace b200ipc
+
+struct b200ipc_assembly {
+  int64_t nverts = 0;
+  int64_t nslots = 0;      // N + sum nb*s*s
+  int64_t nvalid = 0;      // slots that survive the fixed-vertex filter
+  int64_t nnzb = 0;
+  int64_t ngslots = 0;     // sum nb*s
+  bool ready = false;
+  b200ipc::FamDesc fam;
+  b200ipc::DevBuf<uint8_t> fixed;
+  b200ipc::DevBuf<uint64_t> keys_a, keys_b;
+  b200ipc::DevBuf<uint32_t> slot_a, slot_b;   // slot_b ends up as the sorted permutation
+  b200ipc::DevBuf<int32_t> head, useg;        // head flags / scan, run starts (nnzb+1)
+  b200ipc::DevBuf<int32_t> rowptr, colidx;
+  b200ipc::DevBuf<uint32_t> gkeys_a, gkeys_b, gslot_a, gslot_b;
+  b200ipc::DevBuf<int32_t> gseg;              // (N+1) run starts per vertex
+  b200ipc::DevBuf<uint8_t> temp;
+  b200ipc::DevBuf<int64_t> scalars;           // device scratch for counts
+};
+
+namespace b200ipc {
+
+__device__ __forceinline__ void decode_slot(const FamDesc& fd, int64_t q, int& f, int64_t& b, int& a, int& c) {
+  f = 0;
+#pragma unroll
+  for (int k = 1; k < kMaxFam; ++k)
+    if (k < fd.nfam && q >= fd.ent_off[k]) f = k;
+  const int s = fd.s[f];
+  const int64_t r = q - fd.ent_off[f];
+  b = r / (s * s);
+  const int rem = (int)(r - b * (s * s));
+  a = rem / s;
+  c = rem - a * s;
+}
+
+// keys for matrix slots: slot < N is the diagonal mass slot of vertex `slot`
+__global__ void __launch_bounds__(kAT) matrix_keys_kernel(FamDesc fd, int64_t nverts, int64_t nslots,
+                                                          const uint8_t* __restrict__ fixed,
+                                                          uint64_t* __restrict__ keys, uint32_t* __restrict__ slots) {
+  const int64_t e = (int64_t)blockIdx.x * kAT + threadIdx.x;
+  if (e >= nslots) return;
+  int64_t row, col;
+  if (e < nverts) {
+    row = col = e;
+  } else {
+    int f, a, c;
+    int64_t b;
+    decode_slot(fd, e - nverts, f, b, a, c);
+    const int64_t* v = fd.vids[f] + b * fd.s[f];
+    row = v[a];
+    col = v[c];
+  }
+  uint64_t key = (uint64_t)row * (uint64_t)nverts + (uint64_t)col;
+  if (row != col && (fixed[row] | fixed[col])) key = (uint64_t)nverts * (uint64_t)nverts;  // Dirichlet: dropped (sorts last)
+  keys[e] = key;
+  slots[e] = (uint32_t)e;
+}
+
+__global__ void __launch_bounds__(kAT) head_flags_kernel(int64_t n, uint64_t sentinel,
+                                                         const uint64_t* __restrict__ keys,
+                                                         int32_t* __restrict__ head) {
+  const int64_t i = (int64_t)blockIdx.x * kAT + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t k = keys[i];
+  head[i] = (k != sentinel && (i == 0 || keys[i - 1] != k)) ? 1 : 0;
+}
+
+// keys are sorted with the sentinel last: index of the first sentinel = number of kept slots
+__global__ void first_sentinel_kernel(int64_t n, uint64_t sentinel, const uint64_t* keys, int64_t* out) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (keys[mid] != sentinel) lo = mid + 1;
+    else hi = mid;
+  }
+  out[0] = lo;
+}
+
+// scan[i] = inclusive count of heads; heads write colidx / run start; count valid slots
+__global__ void __launch_bounds__(kAT) emit_pattern_kernel(int64_t n, int64_t nverts, const uint64_t* __restrict__ keys,
+                                                           const int32_t* __restrict__ scan,
+                                                           int32_t* __restrict__ colidx, int32_t* __restrict__ useg,
+                                                           int32_t* __restrict__ rowmark) {
+  const int64_t i = (int64_t)blockIdx.x * kAT + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t k = keys[i];
+  if (k == (uint64_t)nverts * (uint64_t)nverts) return;
+  const bool is_head = i == 0 || keys[i - 1] != k;
+  if (is_head) {
+    const int32_t u = scan[i] - 1;
+    const int64_t row = (int64_t)(k / (uint64_t)nverts);
+    colidx[u] = (int32_t)(k - (uint64_t)row * (uint64_t)nverts);
+    useg[u] = (int32_t)i;
+    // first block of a row: every row has its diagonal, so each row owns >= 1 block
+    const bool row_head = i == 0 || (int64_t)(keys[i - 1] / (uint64_t)nverts) != row;
+    if (row_head) rowmark[row] = u;
+  }
+}
+
+__global__ void finish_pattern_kernel(int64_t nverts, int64_t nnzb, int64_t nvalid, int32_t* rowptr, int32_t* useg) {
+  rowptr[nverts] = (int32_t)nnzb;
+  useg[nnzb] = (int32_t)nvalid;
+}
+
+struct NumericArgs {
+  FamDesc fd;
+  HessPtrs hp;
+  int64_t nverts, nnzb;
+  const uint8_t* fixed;
+  const double* masses;
+  const int32_t* useg;
+  const int32_t* colidx;
+  const uint32_t* perm;
+  const int32_t* rowptr;
+  double* vals;
+};
+
+// thread = (unique block u, entry e in 0..8); consecutive threads -> consecutive doubles of vals
+__global__ void __launch_bounds__(kAT) assemble_numeric_kernel(const NumericArgs a) {
+  const int64_t t = (int64_t)blockIdx.x * kAT + threadIdx.x;
+  if (t >= 9 * a.nnzb) return;
+  const int64_t u = t / 9;
+  const int e = (int)(t - 9 * u);
+  const int er = e / 3, ec = e - 3 * er;
+  const int32_t j0 = a.useg[u], j1 = a.useg[u + 1];
+  double acc = 0.0;
+  bool identity = false;
+  for (int32_t j = j0; j < j1; ++j) {
+    const int64_t slot = a.perm[j];
+    if (slot < a.nverts) {  // diagonal mass slot; a fixed vertex keeps a unit diagonal instead
+      if (a.fixed[slot]) identity = true;
+      else acc += (er == ec) ? a.masses[slot] : 0.0;
+    } else {
+      int f, sa, sc;
+      int64_t b;
+      decode_slot(a.fd, slot - a.nverts, f, b, sa, sc);
+      const int D = 3 * a.fd.s[f];
+      acc += __ldg(a.hp.p[f] + (b * D + 3 * sa + er) * D + 3 * sc + ec);
+    }
+  }
+  a.vals[t] = identity ? (er == ec ? 1.0 : 0.0) : acc;
+}
+
+// ---- gradient ---------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kAT) gradient_keys_kernel(FamDesc fd, int64_t ngslots, uint32_t* __restrict__ keys,
+                                                            uint32_t* __restrict__ slots) {
+  const int64_t q = (int64_t)blockIdx.x * kAT + threadIdx.x;
+  if (q >= ngslots) return;
+  int f = 0;
+#pragma unroll
+  for (int k = 1; k < kMaxFam; ++k)
+    if (k < fd.nfam && q >= fd.vert_off[k]) f = k;
+  keys[q] = (uint32_t)fd.vids[f][q - fd.vert_off[f]];
+  slots[q] = (uint32_t)q;
+}
+
+__global__ void __launch_bounds__(kAT) lower_bound_kernel(int64_t nverts, int64_t n, const uint32_t* __restrict__ keys,
+                                                          int32_t* __restrict__ seg) {
+  const int64_t v = (int64_t)blockIdx.x * kAT + threadIdx.x;
+  if (v > nverts) return;
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if ((int64_t)keys[mid] < v) lo = mid + 1;
+    else hi = mid;
+  }
+  seg[v] = (int32_t)lo;
+}
+
+struct GradArgs {
+  FamDesc fd;
+  HessPtrs gp;
+  int64_t nverts;
+  const uint8_t* fixed;
+  const double *masses, *x, *x_tilde;
+  const int32_t* gseg;
+  const uint32_t* gperm;
+  double* out;
+};
+
+// thread = (vertex, component): m (x - x~) + contributions in list order; fixed rows -> 0
+__global__ void __launch_bounds__(kAT) scatter_gradient_kernel(const GradArgs a) {
+  const int64_t t = (int64_t)blockIdx.x * kAT + threadIdx.x;
+  if (t >= 3 * a.nverts) return;
+  const int64_t v = t / 3;
+  const int k = (int)(t - 3 * v);
+  if (a.fixed[v]) {
+    a.out[t] = 0.0;
+    return;
+  }
+  double acc = a.masses[v] * (a.x[t] - a.x_tilde[t]);
+  for (int32_t j = a.gseg[v]; j < a.gseg[v + 1]; ++j) {
+    const int64_t q = a.gperm[j];
+    int f = 0;
+#pragma unroll
+    for (int kk = 1; kk < kMaxFam; ++kk)
+      if (kk < a.fd.nfam && q >= a.fd.vert_off[kk]) f = kk;
+    // slot q - vert_off[f] = b*s + a  ->  grad_f[b][3a + k] = base[3*(b*s+a) + k]
+    acc += __ldg(a.gp.p[f] + 3 * (q - a.fd.vert_off[f]) + k);
+  }
+  a.out[t] = acc;
+}
+
+static inline unsigned blocks_for(int64_t n) { return (unsigned)((n + kAT - 1) / kAT); }
+
+static int bits_for(uint64_t maxval) {
+  int b = 1;
+  while (b < 64 && (maxval >> b)) ++b;
+  return b;
+}
+
+}  // namespace b200ipc
+
+using namespace b200ipc;
+
+extern "C" int b200ipc_assembly_create(b200ipc_assembly** out) {
+  if (!out) return B200IPC_EINVAL;
+  *out = new (std::nothrow) b200ipc_assembly();
+  return *out ? 0 : B200IPC_EINVAL;
+}
+
+extern "C" int b200ipc_assembly_destroy(b200ipc_assembly* h) {
+  if (!h) return 0;
+  h->fixed.release(); h->keys_a.release(); h->keys_b.release(); h->slot_a.release(); h->slot_b.release();
+  h->head.release(); h->useg.release(); h->rowptr.release(); h->colidx.release();
+  h->gkeys_a.release(); h->gkeys_b.release(); h->gslot_a.release(); h->gslot_b.release(); h->gseg.release();
+  h->temp.release(); h->scalars.release();
+  delete h;
+  return 0;
+}
+
+#define CK(expr)                                  \
+  do {                                            \
+    cudaError_t _e = (expr);                      \
+    if (_e != cudaSuccess) return -(int)_e;       \
+  } while (0)
+#define RC(expr)            \
+  do {                      \
+    int _r = (expr);        \
+    if (_r) return _r;      \
+  } while (0)
+
+extern "C" int b200ipc_assemble_symbolic(b200ipc_assembly* h, int64_t nverts, const uint8_t* fixed, int32_t nfam,
+                                         const int32_t* fam_s, const int64_t* fam_nb, const int64_t* const* fam_vids,
+                                         int64_t* nnzb_out, void* stream) {
+  if (!h || nverts <= 0 || nfam < 0 || nfam > kMaxFam || !fixed) return B200IPC_EINVAL;
+  if (nfam && (!fam_s || !fam_nb || !fam_vids)) return B200IPC_EINVAL;
+  if (nverts >= (1ll << 31)) return B200IPC_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  h->ready = false;
+  FamDesc& fd = h->fam;
+  fd.nfam = nfam;
+  fd.ent_off[0] = fd.vert_off[0] = 0;
+  for (int f = 0; f < nfam; ++f) {
+    if (fam_s[f] < 2 || fam_s[f] > 4 || fam_nb[f] < 0 || (fam_nb[f] && !fam_vids[f])) return B200IPC_EINVAL;
+    fd.s[f] = fam_s[f];
+    fd.nb[f] = fam_nb[f];
+    fd.vids[f] = fam_vids[f];
+    fd.ent_off[f + 1] = fd.ent_off[f] + fam_nb[f] * fam_s[f] * fam_s[f];
+    fd.vert_off[f + 1] = fd.vert_off[f] + fam_nb[f] * fam_s[f];
+  }
+  h->nverts = nverts;
+  h->nslots = nverts + fd.ent_off[nfam];
+  h->ngslots = fd.vert_off[nfam];
+  if (h->nslots >= (1ll << 31)) return B200IPC_EINVAL;  // int32 run offsets
+  const int64_t n = h->nslots;
+
+  CK(h->fixed.reserve(nverts));
+  CK(cudaMemcpyAsync(h->fixed.ptr, fixed, nverts, cudaMemcpyDeviceToDevice, st));
+  CK(h->keys_a.reserve(n)); CK(h->keys_b.reserve(n)); CK(h->slot_a.reserve(n)); CK(h->slot_b.reserve(n));
+  CK(h->head.reserve(n)); CK(h->rowptr.reserve(nverts + 1)); CK(h->scalars.reserve(4));
+
+  matrix_keys_kernel<<<blocks_for(n), kAT, 0, st>>>(fd, nverts, n, h->fixed.ptr, h->keys_a.ptr, h->slot_a.ptr);
+  RC(post_launch());
+
+  // stable LSD radix sort over the significant bits only; the sentinel N*N is the largest key
+  const uint64_t sentinel = (uint64_t)nverts * (uint64_t)nverts;
+  const int end_bit = bits_for(sentinel);
+  size_t tb = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, h->keys_a.ptr, h->keys_b.ptr, h->slot_a.ptr, h->slot_b.ptr, (int)n,
+                                     0, end_bit, st));
+  size_t tb2 = 0;
+  CK(cub::DeviceScan::InclusiveSum(nullptr, tb2, h->head.ptr, h->head.ptr, (int)n, st));
+  CK(h->temp.reserve(tb > tb2 ? tb : tb2));
+  CK(cub::DeviceRadixSort::SortPairs(h->temp.ptr, tb, h->keys_a.ptr, h->keys_b.ptr, h->slot_a.ptr, h->slot_b.ptr,
+                                     (int)n, 0, end_bit, st));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+
+  head_flags_kernel<<<blocks_for(n), kAT, 0, st>>>(n, sentinel, h->keys_b.ptr, h->head.ptr);
+  RC(post_launch());
+  CK(cub::DeviceScan::InclusiveSum(h->temp.ptr, tb2, h->head.ptr, h->head.ptr, (int)n, st));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  // nnzb = scan[n-1]
+  int32_t nnzb32 = 0;
+  CK(cudaMemcpyAsync(&nnzb32, h->head.ptr + (n - 1), sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  h->nnzb = nnzb32;
+  CK(h->colidx.reserve(h->nnzb)); CK(h->useg.reserve(h->nnzb + 1));
+  emit_pattern_kernel<<<blocks_for(n), kAT, 0, st>>>(n, nverts, h->keys_b.ptr, h->head.ptr, h->colidx.ptr,
+                                                     h->useg.ptr, h->rowptr.ptr);
+  RC(post_launch());
+  {
+    first_sentinel_kernel<<<1, 1, 0, st>>>(n, sentinel, h->keys_b.ptr, h->scalars.ptr);
+    RC(post_launch());
+    int64_t nvalid = 0;
+    CK(cudaMemcpyAsync(&nvalid, h->scalars.ptr, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    h->nvalid = nvalid;
+  }
+  finish_pattern_kernel<<<1, 1, 0, st>>>(nverts, h->nnzb, h->nvalid, h->rowptr.ptr, h->useg.ptr);
+  RC(post_launch());
+
+  // gradient runs: sort vertex slots by vertex id
+  const int64_t ng = h->ngslots;
+  CK(h->gseg.reserve(nverts + 1));
+  if (ng > 0) {
+    CK(h->gkeys_a.reserve(ng)); CK(h->gkeys_b.reserve(ng)); CK(h->gslot_a.reserve(ng)); CK(h->gslot_b.reserve(ng));
+    gradient_keys_kernel<<<blocks_for(ng), kAT, 0, st>>>(fd, ng, h->gkeys_a.ptr, h->gslot_a.ptr);
+    RC(post_launch());
+    size_t tg = 0;
+    const int vbits = bits_for((uint64_t)nverts);
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tg, h->gkeys_a.ptr, h->gkeys_b.ptr, h->gslot_a.ptr, h->gslot_b.ptr,
+                                       (int)ng, 0, vbits, st));
+    CK(h->temp.reserve(tg));
+    CK(cub::DeviceRadixSort::SortPairs(h->temp.ptr, tg, h->gkeys_a.ptr, h->gkeys_b.ptr, h->gslot_a.ptr,
+                                       h->gslot_b.ptr, (int)ng, 0, vbits, st));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+  }
+  lower_bound_kernel<<<blocks_for(nverts + 1), kAT, 0, st>>>(nverts, ng, h->gkeys_b.ptr, h->gseg.ptr);
+  RC(post_launch());
+  h->ready = true;
+  if (nnzb_out) *nnzb_out = h->nnzb;
+  return 0;
+}
+
+extern "C" int b200ipc_assembly_pattern(b200ipc_assembly* h, int32_t* rowptr, int32_t* colidx, void* stream) {
+  if (!h || !h->ready) return B200IPC_ESTATE;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (rowptr) CK(cudaMemcpyAsync(rowptr, h->rowptr.ptr, (h->nverts + 1) * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+  if (colidx) CK(cudaMemcpyAsync(colidx, h->colidx.ptr, h->nnzb * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+  return 0;
+}
+
+extern "C" int b200ipc_assemble_numeric(b200ipc_assembly* h, const double* masses, const double* const* fam_hess,
+                                        double* vals, void* stream) {
+  if (!h || !h->ready) return B200IPC_ESTATE;
+  if (!masses || !vals || (h->fam.nfam && !fam_hess)) return B200IPC_EINVAL;
+  NumericArgs a;
+  a.fd = h->fam;
+  for (int f = 0; f < h->fam.nfam; ++f) {
+    if (h->fam.nb[f] && !fam_hess[f]) return B200IPC_EINVAL;
+    a.hp.p[f] = fam_hess[f];
+  }
+  a.nverts = h->nverts; a.nnzb = h->nnzb; a.fixed = h->fixed.ptr; a.masses = masses;
+  a.useg = h->useg.ptr; a.colidx = h->colidx.ptr; a.perm = h->slot_b.ptr; a.rowptr = h->rowptr.ptr; a.vals = vals;
+  assemble_numeric_kernel<<<blocks_for(9 * h->nnzb), kAT, 0, (cudaStream_t)stream>>>(a);
+  return post_launch();
+}
+
+extern "C" int b200ipc_scatter_gradient(b200ipc_assembly* h, const double* masses, const double* x,
+                                        const double* x_tilde, const double* const* fam_grad, double* out,
+                                        void* stream) {
+  if (!h || !h->ready) return B200IPC_ESTATE;
+  if (!masses || !x || !x_tilde || !out || (h->fam.nfam && !fam_grad)) return B200IPC_EINVAL;
+  GradArgs a;
+  a.fd = h->fam;
+  for (int f = 0; f < h->fam.nfam; ++f) {
+    if (h->fam.nb[f] && !fam_grad[f]) return B200IPC_EINVAL;
+    a.gp.p[f] = fam_grad[f];
+  }
+  a.nverts = h->nverts; a.fixed = h->fixed.ptr; a.masses = masses; a.x = x; a.x_tilde = x_tilde;
+  a.gseg = h->gseg.ptr; a.gperm = h->gslot_b.ptr; a.out = out;
+  scatter_gradient_kernel<<<blocks_for(3 * h->nverts), kAT, 0, (cudaStream_t)stream>>>(a);
+  return post_launch();
+}

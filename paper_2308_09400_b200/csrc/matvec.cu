@@ -40,9 +40,47 @@ __global__ void __launch_bounds__(kMvThreads) matvec_blocks_kernel(int64_t nb, c
   }
 }
 
+// matvec_matrix_free prologue/epilogue (solver.py:255-261): vin = v with fixed rows zeroed,
+// out = m * vin; afterwards out[fixed] = v[fixed].
+__global__ void __launch_bounds__(256) matvec_begin_kernel(int64_t n, const double* __restrict__ masses,
+                                                           const uint8_t* __restrict__ fixed,
+                                                           const double* __restrict__ v, double* __restrict__ vin,
+                                                           double* __restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (t >= 3 * n) return;
+  const int64_t i = t / 3;
+  const double x = fixed[i] ? 0.0 : v[t];
+  vin[t] = x;
+  out[t] = masses[i] * x;
+}
+
+__global__ void __launch_bounds__(256) matvec_end_kernel(int64_t n, const uint8_t* __restrict__ fixed,
+                                                         const double* __restrict__ v, double* __restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (t >= 3 * n) return;
+  if (fixed[t / 3]) out[t] = v[t];
+}
+
 }  // namespace b200ipc
 
 using namespace b200ipc;
+
+extern "C" int b200ipc_matvec_begin(int64_t n, const double* masses, const uint8_t* fixed, const double* v,
+                                    double* vin, double* out, void* stream) {
+  if (n < 0) return B200IPC_EINVAL;
+  if (n == 0) return 0;
+  if (!masses || !fixed || !v || !vin || !out) return B200IPC_EINVAL;
+  matvec_begin_kernel<<<(unsigned)((3 * n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(n, masses, fixed, v, vin, out);
+  return post_launch();
+}
+
+extern "C" int b200ipc_matvec_end(int64_t n, const uint8_t* fixed, const double* v, double* out, void* stream) {
+  if (n < 0) return B200IPC_EINVAL;
+  if (n == 0) return 0;
+  if (!fixed || !v || !out) return B200IPC_EINVAL;
+  matvec_end_kernel<<<(unsigned)((3 * n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(n, fixed, v, out);
+  return post_launch();
+}
 
 extern "C" int b200ipc_matvec_blocks(int64_t nb, int32_t s, const double* hess, const int64_t* vids, const double* x,
                                      double* out, void* stream) {

@@ -1,0 +1,218 @@
+// Block-Jacobi preconditioned CG (pcg_solve, solver.py:279-315) over the assembled BSR matrix,
+// as ONE persistent cooperative kernel: the whole iteration loop runs on the device with three
+// grid barriers per iteration and a device-side convergence test, so there is no launch or host
+// round trip per iteration (vectors of a 100k-vertex scene are L2 resident; launch latency would
+// dominate otherwise).  Dot products are reduced in two fixed-order stages (per-CTA partials, then
+// every CTA sums the partials in the same order): results are bitwise reproducible and every CTA
+// takes the same branch.
+//
+//   r = rhs (fixed -> 0); s = P r; delta = r.s; c = s
+//   loop: q = A c; denom = c.q; stop if denom <= 0; alpha = delta/denom
+//         d += alpha c; r -= alpha q; s = P r; delta' = r.s; c = s + (delta'/delta) c
+//   until delta' <= tol*delta0 or the cap.
+#include <cooperative_groups.h>
+
+#include "spmv.cuh"
+#include "launch.cuh"
+#include "../../include/b200ipc.h"
+
+namespace cg = cooperative_groups;
+
+namespace b200ipc {
+
+constexpr int kPT = 256;
+constexpr int kMaxParts = 4096;
+
+struct PcgArgs {
+  int64_t n;
+  const int32_t* rowptr;
+  const int32_t* colidx;
+  const double* vals;
+  const double* pinv;
+  const uint8_t* fixed;
+  const double* rhs;
+  double* d;
+  double *r, *s, *c, *q;    // workspace vectors (3n each)
+  double* part;             // 2 * kMaxParts partial sums (ping-pong)
+  double rel_tol;
+  int32_t max_iters;
+  b200ipc_pcg_result* result;  // device
+};
+
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < kPT / 32; ++w) t += sh[w];
+  return t;  // valid in thread 0
+}
+
+// every CTA sums all partials in the same order -> identical value everywhere
+__device__ __forceinline__ double sum_parts(const double* part, int nparts, double* sh) {
+  double v = 0.0;
+  for (int i = threadIdx.x; i < nparts; i += kPT) v += part[i];
+  const double t = block_sum(v, sh);
+  __shared__ double bc;
+  if (threadIdx.x == 0) bc = t;
+  __syncthreads();
+  return bc;
+}
+
+__device__ __forceinline__ void apply_pinv(const double* __restrict__ p, double r0, double r1, double r2, double& s0,
+                                           double& s1, double& s2) {
+  s0 = p[0] * r0 + p[1] * r1 + p[2] * r2;
+  s1 = p[3] * r0 + p[4] * r1 + p[5] * r2;
+  s2 = p[6] * r0 + p[7] * r1 + p[8] * r2;
+}
+
+template <int LPR>
+__global__ void __launch_bounds__(kPT) pcg_kernel(const PcgArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sh[kPT / 32];
+  const int64_t tid = (int64_t)blockIdx.x * kPT + threadIdx.x;
+  const int64_t nthreads = (int64_t)gridDim.x * kPT;
+  const int nparts = gridDim.x;
+  double* part0 = a.part;
+  double* part1 = a.part + kMaxParts;
+
+  // ---- init: d = 0, r = rhs (fixed -> 0), s = P r, c = s, delta0 = r.s ------------------------
+  double acc = 0.0;
+  for (int64_t v = tid; v < a.n; v += nthreads) {
+    const bool fx = a.fixed[v];
+    const double r0 = fx ? 0.0 : a.rhs[3 * v], r1 = fx ? 0.0 : a.rhs[3 * v + 1], r2 = fx ? 0.0 : a.rhs[3 * v + 2];
+    double s0, s1, s2;
+    apply_pinv(a.pinv + 9 * v, r0, r1, r2, s0, s1, s2);
+    a.d[3 * v] = a.d[3 * v + 1] = a.d[3 * v + 2] = 0.0;
+    a.r[3 * v] = r0; a.r[3 * v + 1] = r1; a.r[3 * v + 2] = r2;
+    a.s[3 * v] = s0; a.s[3 * v + 1] = s1; a.s[3 * v + 2] = s2;
+    a.c[3 * v] = s0; a.c[3 * v + 1] = s1; a.c[3 * v + 2] = s2;
+    acc += r0 * s0 + r1 * s1 + r2 * s2;
+  }
+  {
+    const double t = block_sum(acc, sh);
+    if (threadIdx.x == 0) part0[blockIdx.x] = t;
+  }
+  grid.sync();
+  const double delta0 = sum_parts(part0, nparts, sh);
+  double delta_new = delta0;
+  int iters = 0;
+  bool broke = false;
+
+  if (delta0 > 0.0) {
+    while (iters < a.max_iters && delta_new > a.rel_tol * delta0) {
+      // ---- q = A c, denom = c.q ------------------------------------------------------------------
+      acc = 0.0;
+      const int lane = threadIdx.x % LPR;
+      for (int64_t row = tid / LPR; row < a.n; row += nthreads / LPR) {
+        double y0, y1, y2;
+        bsr_row_product<LPR>(row, lane, a.rowptr, a.colidx, a.vals, a.c, y0, y1, y2);
+        if (lane == 0) {
+          a.q[3 * row] = y0; a.q[3 * row + 1] = y1; a.q[3 * row + 2] = y2;
+          acc += a.c[3 * row] * y0 + a.c[3 * row + 1] * y1 + a.c[3 * row + 2] * y2;
+        }
+      }
+      {
+        const double t = block_sum(acc, sh);
+        if (threadIdx.x == 0) part1[blockIdx.x] = t;
+      }
+      grid.sync();
+      const double denom = sum_parts(part1, nparts, sh);
+      if (denom <= 0.0) {  // solver.py:305-306
+        broke = true;
+        break;
+      }
+      const double alpha = delta_new / denom;
+      // ---- d += alpha c; r -= alpha q; s = P r; delta' = r.s -------------------------------------
+      acc = 0.0;
+      for (int64_t v = tid; v < a.n; v += nthreads) {
+        double rr[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          a.d[3 * v + k] += alpha * a.c[3 * v + k];
+          rr[k] = a.r[3 * v + k] - alpha * a.q[3 * v + k];
+          a.r[3 * v + k] = rr[k];
+        }
+        double s0, s1, s2;
+        apply_pinv(a.pinv + 9 * v, rr[0], rr[1], rr[2], s0, s1, s2);
+        a.s[3 * v] = s0; a.s[3 * v + 1] = s1; a.s[3 * v + 2] = s2;
+        acc += rr[0] * s0 + rr[1] * s1 + rr[2] * s2;
+      }
+      {
+        const double t = block_sum(acc, sh);
+        if (threadIdx.x == 0) part0[blockIdx.x] = t;
+      }
+      grid.sync();
+      const double delta_old = delta_new;
+      delta_new = sum_parts(part0, nparts, sh);
+      const double beta = delta_new / delta_old;
+      // ---- c = s + beta c ---------------------------------------------------------------------------
+      for (int64_t i = tid; i < 3 * a.n; i += nthreads) a.c[i] = a.s[i] + beta * a.c[i];
+      ++iters;
+      grid.sync();
+    }
+  }
+  (void)broke;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    a.result->iters = iters;
+    a.result->converged = (delta0 <= 0.0) || (delta_new <= a.rel_tol * delta0);
+    a.result->delta0 = delta0;
+    a.result->delta_new = delta_new;
+  }
+}
+
+int pick_lpr(int64_t n, int64_t nnzb);  // spmv.cu
+
+}  // namespace b200ipc
+
+using namespace b200ipc;
+
+extern "C" int64_t b200ipc_pcg_workspace_bytes(int64_t n) {
+  if (n < 0) return 0;
+  return (int64_t)sizeof(double) * (4 * 3 * n + 2 * kMaxParts) + 256;
+}
+
+extern "C" int b200ipc_pcg(int64_t n, int64_t nnzb, const int32_t* rowptr, const int32_t* colidx, const double* vals,
+                           const double* pinv, const uint8_t* fixed, const double* rhs, double* d, double rel_tol,
+                           int32_t max_iters, void* workspace, int64_t workspace_bytes, b200ipc_pcg_result* result,
+                           void* stream) {
+  if (n <= 0 || nnzb < n || !rowptr || !colidx || !vals || !pinv || !fixed || !rhs || !d || !workspace || !result)
+    return B200IPC_EINVAL;
+  if (workspace_bytes < b200ipc_pcg_workspace_bytes(n) || max_iters < 0) return B200IPC_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  PcgArgs a;
+  a.n = n; a.rowptr = rowptr; a.colidx = colidx; a.vals = vals; a.pinv = pinv; a.fixed = fixed; a.rhs = rhs; a.d = d;
+  double* w = static_cast<double*>(workspace);
+  a.r = w; a.s = w + 3 * n; a.c = w + 6 * n; a.q = w + 9 * n;
+  a.part = w + 12 * n;
+  a.result = reinterpret_cast<b200ipc_pcg_result*>(a.part + 2 * kMaxParts);
+  a.rel_tol = rel_tol; a.max_iters = max_iters;
+
+  const int lpr = pick_lpr(n, nnzb);
+  const void* fn = lpr == 32 ? (const void*)pcg_kernel<32> : (lpr == 16 ? (const void*)pcg_kernel<16> : (const void*)pcg_kernel<8>);
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return -(int)e;
+  e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e != cudaSuccess) return -(int)e;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kPT, 0);
+  if (e != cudaSuccess) return -(int)e;
+  if (per_sm < 1) return B200IPC_ESTATE;
+  int64_t grid = (int64_t)sms * per_sm;
+  const int64_t want = (n * lpr + kPT - 1) / kPT;  // no more CTAs than rows need
+  if (grid > want) grid = want;
+  if (grid > kMaxParts) grid = kMaxParts;
+  if (grid < 1) grid = 1;
+  void* args[] = {(void*)&a};
+  e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)grid), dim3(kPT), args, 0, st);
+  if (e != cudaSuccess) return -(int)e;
+  int rc = post_launch();
+  if (rc) return rc;
+  e = cudaMemcpyAsync(result, a.result, sizeof(b200ipc_pcg_result), cudaMemcpyDeviceToHost, st);
+  if (e != cudaSuccess) return -(int)e;
+  e = cudaStreamSynchronize(st);
+  return e == cudaSuccess ? 0 : -(int)e;
+}

@@ -45,6 +45,8 @@ def to_device(a, dtype=None):
         out = a if dtype is None else a.to(_dtype(dtype))
         return out.cuda().contiguous()
     arr = np.ascontiguousarray(a, dtype=dtype)
+    if not arr.flags.writeable:
+        arr = arr.copy()
     return t.from_numpy(arr).cuda()
 
 
@@ -53,7 +55,11 @@ def to_host(x):
 
 
 def ptr(x):
-    """Raw device pointer of a tensor (None -> NULL)."""
+    """Raw device pointer of a tensor (None -> NULL).
+
+    The caller must keep ``x`` referenced until the kernel is launched: a temporary created
+    inside the argument list can be recycled by the caching allocator for the next temporary.
+    """
     return C.c_void_p(None) if x is None else C.c_void_p(x.data_ptr())
 
 

@@ -53,9 +53,10 @@ def diagonal_jacobian_batch(table, positions, d_hat):
     t = device.torch()
     bufs = {k: t.full(shapes[k], float("nan"), dtype=t.float64, device="cuda") for k in names}
     status = device.empty((n,), np.uint8)
+    d_kind, d_verts, d_sub = (device.to_device(table.kind), device.to_device(table.verts),
+                              device.to_device(table.sub))  # named: temporaries would alias before the launch
     _lib.check(_lib.lib().b200ipc_diagonal_jacobian(
-        prm, pos.shape[0], device.ptr(pos), n, device.ptr(device.to_device(table.kind)),
-        device.ptr(device.to_device(table.verts)), device.ptr(device.to_device(table.sub)),
+        prm, pos.shape[0], device.ptr(pos), n, device.ptr(d_kind), device.ptr(d_verts), device.ptr(d_sub),
         *[device.ptr(bufs[k]) for k in names], device.ptr(status), device.stream()), "diagonal_jacobian")
     out = {k: device.to_host(v) for k, v in bufs.items()}
     out["status"] = device.to_host(status)

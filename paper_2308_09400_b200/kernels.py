@@ -85,7 +85,8 @@ def matvec_blocks(hess, vids, x, out):
     if not (isinstance(out, np.ndarray) and out.dtype == np.float64 and out.flags.c_contiguous):
         raise ValueError("out must be a C-contiguous float64 array")  # _core.pyx:226 typed memoryview
     d_out = device.to_device(out)
-    matvec_blocks_device(device.to_device(hess), device.to_device(vids), device.to_device(x, np.float64), d_out)
+    d_hess, d_vids, d_x = device.to_device(hess), device.to_device(vids), device.to_device(x, np.float64)
+    matvec_blocks_device(d_hess, d_vids, d_x, d_out)
     out[...] = device.to_host(d_out).reshape(out.shape)
 
 

@@ -39,9 +39,10 @@ def mollified_eigensystem_batch(g, c, eps_x, params):
     if np.any(c < 0.0):
         raise ValueError("parallelness measure must be nonnegative")
     out = device.empty((g.shape[0], 12))
+    d_g, d_c, d_eps = device.to_device(g), device.to_device(c), device.to_device(eps)  # keep alive until launch
     _lib.check(_lib.lib().b200ipc_mollified_eigensystem(
-        c_params(params), g.shape[0], device.ptr(device.to_device(g)), device.ptr(device.to_device(c)),
-        device.ptr(device.to_device(eps)), device.ptr(out), device.stream()), "mollified_eigensystem")
+        c_params(params), g.shape[0], device.ptr(d_g), device.ptr(d_c), device.ptr(d_eps), device.ptr(out),
+        device.stream()), "mollified_eigensystem")
     return device.to_host(out)
 
 
