@@ -151,6 +151,22 @@ int b200ipc_mollified_eigensystem(const b200ipc_params* params /* host */, int64
 int b200ipc_reduce_energy(int64_t n, const double* energy, const uint8_t* status,
                           double* result, int64_t* counts, void* workspace, void* stream);
 
+/* ---- narrow phase: candidate queries -> ordered contact list ------------------- */
+/* find_contact_pairs without its broad phase (proximity.py:284-358).  vt (n_vt,4) i32 =
+ * (vertex, t1, t2, t3) and ee (n_ee,4) i32 = (a1, a2, b1, b2): any duplicate-free superset of
+ * the near queries with incident / adjacent pairs already removed.  Keeps d2 < d_hat_sq
+ * (= d_hat*d_hat), reduces to the active branch, promotes edge pairs with c < eps_x
+ * (edge_parallel_eps from rest_positions) when promote_parallel, and sorts by the reference key
+ * (kind.value, verts, origin).  Outputs have capacity n_vt+n_ee rows: kind u8, verts (.,4) i32
+ * (-1 padded), sub u8, eps_x f64, origin_type u8 (1 "ee", 2 "vt"; may be NULL), origin (.,4) i32
+ * (may be NULL).  *n_out and kind_off[8] are host; synchronises `stream`. */
+int b200ipc_narrow_phase(int64_t nverts, const double* positions, const double* rest_positions,
+                         int64_t n_vt, const int32_t* vt, int64_t n_ee, const int32_t* ee,
+                         double d_hat_sq, int32_t promote_parallel,
+                         uint8_t* kind, int32_t* verts, uint8_t* sub, double* eps_x,
+                         uint8_t* origin_type, int32_t* origin,
+                         int64_t* n_out /* host */, int64_t* kind_off /* host[8] */, void* stream);
+
 /* ---- assembly into the 3x3-block sparse global matrix (BSR) -------------------- */
 /* The reference's production path is matrix-free; the assembled matrix is the one its tests
  * build densely (tests/test_solver.py:71-84): A = diag(m_i I3) + sum_b scatter(H_b), fixed

@@ -62,6 +62,8 @@ SIGNATURES = {
     "b200ipc_blocks_from_jacobian": [C.POINTER(Params), _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "b200ipc_barrier_scalars": [C.POINTER(Params), _i64, _vp, _vp, _vp],
     "b200ipc_mollified_eigensystem": [C.POINTER(Params), _i64, _vp, _vp, _vp, _vp, _vp],
+    "b200ipc_narrow_phase": [_i64, _vp, _vp, _i64, _vp, _i64, _vp, _dbl, _i32, _vp, _vp, _vp, _vp, _vp, _vp,
+                             C.POINTER(_i64), C.POINTER(_i64), _vp],
     "b200ipc_assembly_create": [C.POINTER(_vp)],
     "b200ipc_assembly_destroy": [_vp],
     "b200ipc_assemble_symbolic": [_vp, _i64, _vp, _i32, C.POINTER(_i32), C.POINTER(_i64), C.POINTER(_vp),

@@ -274,7 +274,7 @@ def cloth_stack(layers=4, n=64, seed=1, h=0.01, gap_rel=0.6, d_hat_rel=0.5, jitt
 
 
 def _cells_of_boxes(lo, hi, cell, origin):
-    """All (box, cell-key) incidences of axis-aligned boxes on a uniform grid."""
+    """All (box, cell) incidences of axis-aligned boxes on a uniform grid."""
     ilo = np.floor((lo - origin) / cell).astype(np.int64)
     ihi = np.floor((hi - origin) / cell).astype(np.int64)
     span = ihi - ilo + 1
@@ -286,32 +286,45 @@ def _cells_of_boxes(lo, hi, cell, origin):
     cx = ilo[box, 0] + local % sx
     cy = ilo[box, 1] + (local // sx) % sy
     cz = ilo[box, 2] + local // (sx * sy)
-    return box, cx, cy, cz
+    return box, (cx << 42) | (cy << 21) | cz
 
 
-def _pair_join(box_a, key_a, box_b, key_b):
-    """All (a,b) sharing a cell key; duplicates removed."""
-    oa, ob = np.argsort(key_a, kind="stable"), np.argsort(key_b, kind="stable")
-    ka, kb = key_a[oa], key_b[ob]
-    ua, sa, ca = np.unique(ka, return_index=True, return_counts=True)
-    pos = np.searchsorted(kb, ua, side="left")
-    end = np.searchsorted(kb, ua, side="right")
-    cb = end - pos
-    hit = cb > 0
-    sa, ca, pos, cb = sa[hit], ca[hit], pos[hit], cb[hit]
-    if sa.size == 0:
-        return np.zeros((0, 2), np.int64)
-    per_cell = ca * cb
-    cell_of = np.repeat(np.arange(sa.size), per_cell)
-    start = np.cumsum(per_cell) - per_cell
-    local = np.arange(per_cell.sum(), dtype=np.int64) - np.repeat(start, per_cell)
-    ia = oa[sa[cell_of] + local // cb[cell_of]]
-    ib = ob[pos[cell_of] + local % cb[cell_of]]
-    pairs = np.stack([box_a[ia], box_b[ib]], axis=1)
-    return np.unique(pairs, axis=0)
+def _overlap_join(lo_a, hi_a, lo_b, hi_b, cell, origin, chunk=4_000_000):
+    """All (a, b) with overlapping boxes, each exactly once.
+
+    Boxes are binned into grid cells; a pair that shares several cells is reported only from the
+    cell holding the lower corner of the boxes' intersection, so no de-duplication pass is needed.
+    """
+    box_a, key_a = _cells_of_boxes(lo_a, hi_a, cell, origin)
+    box_b, key_b = _cells_of_boxes(lo_b, hi_b, cell, origin)
+    ob = np.argsort(key_b, kind="stable")
+    kb, box_b = key_b[ob], box_b[ob]
+    first = np.searchsorted(kb, key_a, side="left")
+    cnt = np.searchsorted(kb, key_a, side="right") - first
+    out = []
+    order = np.flatnonzero(cnt > 0)
+    csum = np.cumsum(cnt[order])
+    lo_i = 0
+    while lo_i < order.size:
+        base = csum[lo_i - 1] if lo_i else 0
+        hi_i = int(np.searchsorted(csum, base + chunk, side="right"))
+        hi_i = max(hi_i, lo_i + 1)
+        sel = order[lo_i:hi_i]
+        c = cnt[sel]
+        rep = np.repeat(np.arange(sel.size), c)
+        local = np.arange(c.sum(), dtype=np.int64) - np.repeat(np.cumsum(c) - c, c)
+        ia = box_a[sel][rep]
+        ib = box_b[first[sel][rep] + local]
+        lo_int = np.maximum(lo_a[ia], lo_b[ib])
+        ok = np.all(lo_int <= np.minimum(hi_a[ia], hi_b[ib]), axis=1)
+        own = np.floor((lo_int - origin) / cell).astype(np.int64)
+        ok &= ((own[:, 0] << 42) | (own[:, 1] << 21) | own[:, 2]) == key_a[sel][rep]
+        out.append(np.stack([ia[ok], ib[ok]], axis=1))
+        lo_i = hi_i
+    return np.concatenate(out) if out else np.zeros((0, 2), np.int64)
 
 
-def broad_phase(scene, positions=None, margin=None):
+def broad_phase(scene, positions=None, surf_verts=None):
     """Conservative uniform-grid broad phase -> (vt (m,4), ee (k,4)) candidate queries.
 
     Replaces the reference's O(n^2) AABB sweep (proximity.py:232-248, :275-319) with
@@ -323,32 +336,27 @@ def broad_phase(scene, positions=None, margin=None):
     x = scene.positions if positions is None else positions
     d_hat = scene.d_hat
     tris, edges = scene.tris, scene.edges
-    verts = np.unique(tris)
+    if tris.shape[0] == 0 and edges.shape[0] < 2:
+        return np.zeros((0, 4), np.int64), np.zeros((0, 4), np.int64)
+    verts = np.unique(tris) if surf_verts is None else np.asarray(surf_verts)
     tx = x[tris]
     elen = np.linalg.norm(x[edges[:, 1]] - x[edges[:, 0]], axis=1)
-    cell = max(2.0 * d_hat, 1.5 * float(np.median(elen)))
+    cell = max(2.0 * d_hat, 1.0 * float(np.median(elen)))
     origin = x.min(axis=0) - 2.0 * cell
-    key = lambda cx, cy, cz: (cx << 42) | (cy << 21) | cz  # noqa: E731
-
-    bv, *cv = _cells_of_boxes(x[verts] - d_hat, x[verts] + d_hat, cell, origin)
-    bt, *ct = _cells_of_boxes(tx.min(axis=1), tx.max(axis=1), cell, origin)
-    pairs = _pair_join(bv, key(*cv), bt, key(*ct))
+    lo_v, hi_v = x[verts] - d_hat, x[verts] + d_hat
+    pairs = _overlap_join(lo_v, hi_v, tx.min(axis=1), tx.max(axis=1), cell, origin)
     vid, tv = verts[pairs[:, 0]], tris[pairs[:, 1]]
-    lo_v, hi_v = x[vid] - d_hat, x[vid] + d_hat
-    ttx = x[tv]
-    ok = np.all((lo_v <= ttx.max(axis=1)) & (ttx.min(axis=1) <= hi_v), axis=1)
-    ok &= (vid != tv[:, 0]) & (vid != tv[:, 1]) & (vid != tv[:, 2])
+    ok = (vid != tv[:, 0]) & (vid != tv[:, 1]) & (vid != tv[:, 2])
     vt = np.concatenate([vid[ok, None], tv[ok]], axis=1)
+    vt = vt[np.lexsort((pairs[ok, 1], pairs[ok, 0]))]
 
     e1, e2 = x[edges[:, 0]], x[edges[:, 1]]
     lo_e = np.minimum(e1, e2) - 0.5 * d_hat
     hi_e = np.maximum(e1, e2) + 0.5 * d_hat
-    be, *ce = _cells_of_boxes(lo_e, hi_e, cell, origin)
-    pairs = _pair_join(be, key(*ce), be, key(*ce))
+    pairs = _overlap_join(lo_e, hi_e, lo_e, hi_e, cell, origin)
     pairs = pairs[pairs[:, 0] < pairs[:, 1]]
-    i, j = pairs[:, 0], pairs[:, 1]
-    ok = np.all((lo_e[i] <= hi_e[j]) & (lo_e[j] <= hi_e[i]), axis=1)
-    ea, eb = edges[i], edges[j]
-    ok &= (ea[:, 0] != eb[:, 0]) & (ea[:, 0] != eb[:, 1]) & (ea[:, 1] != eb[:, 0]) & (ea[:, 1] != eb[:, 1])
+    ea, eb = edges[pairs[:, 0]], edges[pairs[:, 1]]
+    ok = (ea[:, 0] != eb[:, 0]) & (ea[:, 0] != eb[:, 1]) & (ea[:, 1] != eb[:, 0]) & (ea[:, 1] != eb[:, 1])
     ee = np.concatenate([ea[ok], eb[ok]], axis=1)
+    ee = ee[np.lexsort((pairs[ok, 1], pairs[ok, 0]))]
     return vt, ee
