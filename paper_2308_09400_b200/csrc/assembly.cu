@@ -20,7 +20,7 @@
 
 namespace b200ipc {
 
-constexpr int kMaxFam = 8;
+constexpr int kMaxFam = 7;  // family ids 0..6; 7 tags the diagonal mass slot in source descriptors
 constexpr int kAT = 256;
 
 struct FamDesc {
@@ -70,6 +70,7 @@ struct b200ipc_assembly {
   b200ipc::DevBuf<uint64_t> keys_a, keys_b;
   b200ipc::DevBuf<uint32_t> slot_a, slot_b;   // slot_b ends up as the sorted permutation
   b200ipc::DevBuf<int32_t> head, useg;        // head flags / scan, run starts (nnzb+1)
+  b200ipc::DevBuf<uint64_t> desc;             // per sorted source: (element offset << 3) | family, 7 = mass slot
   b200ipc::DevBuf<int32_t> rowptr, colidx;
   b200ipc::DevBuf<uint32_t> gkeys_a, gkeys_b, gslot_a, gslot_b;
   b200ipc::DevBuf<int32_t> gseg;              // (N+1) run starts per vertex
@@ -161,43 +162,82 @@ __global__ void finish_pattern_kernel(int64_t nverts, int64_t nnzb, int64_t nval
   useg[nnzb] = (int32_t)nvalid;
 }
 
+// Source descriptors, written once per pattern in sorted order: the numeric phase then needs no
+// integer division and no family search per source.
+__global__ void __launch_bounds__(kAT) source_desc_kernel(FamDesc fd, int64_t nverts, int64_t nvalid,
+                                                          const uint32_t* __restrict__ perm,
+                                                          uint64_t* __restrict__ desc) {
+  const int64_t j = (int64_t)blockIdx.x * kAT + threadIdx.x;
+  if (j >= nvalid) return;
+  const int64_t slot = perm[j];
+  if (slot < nverts) {
+    desc[j] = ((uint64_t)slot << 3) | 7ull;
+  } else {
+    int f, a, c;
+    int64_t b;
+    decode_slot(fd, slot - nverts, f, b, a, c);
+    const int64_t D = 3 * fd.s[f];
+    desc[j] = ((uint64_t)((b * D + 3 * a) * D + 3 * c) << 3) | (uint64_t)f;
+  }
+}
+
 struct NumericArgs {
-  FamDesc fd;
   HessPtrs hp;
-  int64_t nverts, nnzb;
+  int32_t ld[kMaxFam];   // row length 3s of each family
+  int64_t nnzb;
   const uint8_t* fixed;
   const double* masses;
   const int32_t* useg;
-  const int32_t* colidx;
-  const uint32_t* perm;
-  const int32_t* rowptr;
+  const uint64_t* desc;
   double* vals;
 };
 
-// thread = (unique block u, entry e in 0..8); consecutive threads -> consecutive doubles of vals
-__global__ void __launch_bounds__(kAT) assemble_numeric_kernel(const NumericArgs a) {
-  const int64_t t = (int64_t)blockIdx.x * kAT + threadIdx.x;
-  if (t >= 9 * a.nnzb) return;
-  const int64_t u = t / 9;
-  const int e = (int)(t - 9 * u);
+constexpr int kNumWarps = 8;
+
+__device__ __forceinline__ double source_value(const NumericArgs& a, uint64_t d, int er, int ec, bool& identity) {
+  const int f = (int)(d & 7ull);
+  const int64_t off = (int64_t)(d >> 3);
+  if (f == 7) {  // diagonal mass slot; a fixed vertex keeps a unit diagonal instead
+    if (a.fixed[off]) {
+      identity = true;
+      return 0.0;
+    }
+    return er == ec ? a.masses[off] : 0.0;
+  }
+  return __ldg(a.hp.p[f] + off + er * a.ld[f] + ec);
+}
+
+// One warp per output block: lanes (g, e) = (lane / 9, lane % 9), g < 3, walk the block's run of
+// sources three at a time (two iterations in flight), entry e of each 3x3 sub-block per lane; the
+// three partial sums are combined in fixed order with two shuffles.  Lanes 0..8 write the block:
+// nine consecutive doubles per warp, 72-byte rows back to back across the CTA's warps.
+__global__ void __launch_bounds__(32 * kNumWarps) assemble_numeric_kernel(const NumericArgs a) {
+  const int64_t u = (int64_t)blockIdx.x * kNumWarps + (threadIdx.x >> 5);
+  if (u >= a.nnzb) return;
+  const int lane = threadIdx.x & 31;
+  const int g = lane / 9, e = lane - 9 * g;
   const int er = e / 3, ec = e - 3 * er;
   const int32_t j0 = a.useg[u], j1 = a.useg[u + 1];
   double acc = 0.0;
   bool identity = false;
-  for (int32_t j = j0; j < j1; ++j) {
-    const int64_t slot = a.perm[j];
-    if (slot < a.nverts) {  // diagonal mass slot; a fixed vertex keeps a unit diagonal instead
-      if (a.fixed[slot]) identity = true;
-      else acc += (er == ec) ? a.masses[slot] : 0.0;
-    } else {
-      int f, sa, sc;
-      int64_t b;
-      decode_slot(a.fd, slot - a.nverts, f, b, sa, sc);
-      const int D = 3 * a.fd.s[f];
-      acc += __ldg(a.hp.p[f] + (b * D + 3 * sa + er) * D + 3 * sc + ec);
+  if (g < 3) {
+    int32_t j = j0 + g;
+    for (; j + 3 < j1; j += 6) {
+      const uint64_t d0 = a.desc[j], d1 = a.desc[j + 3];
+      const double v0 = source_value(a, d0, er, ec, identity);
+      const double v1 = source_value(a, d1, er, ec, identity);
+      acc += v0;
+      acc += v1;
     }
+    if (j < j1) acc += source_value(a, a.desc[j], er, ec, identity);
   }
-  a.vals[t] = identity ? (er == ec ? 1.0 : 0.0) : acc;
+  const double s1 = __shfl_down_sync(0xffffffffu, acc, 9);   // group 1's partial sum (lanes 0..8)
+  const double s2 = __shfl_down_sync(0xffffffffu, acc, 18);  // group 2's
+  const bool any_identity = __any_sync(0xffffffffu, identity);
+  if (lane < 9) {
+    const double total = (acc + s1) + s2;
+    a.vals[9 * u + lane] = any_identity ? (er == ec ? 1.0 : 0.0) : total;
+  }
 }
 
 // ---- gradient ---------------------------------------------------------------------------------
@@ -281,7 +321,7 @@ extern "C" int b200ipc_assembly_create(b200ipc_assembly** out) {
 extern "C" int b200ipc_assembly_destroy(b200ipc_assembly* h) {
   if (!h) return 0;
   h->fixed.release(); h->keys_a.release(); h->keys_b.release(); h->slot_a.release(); h->slot_b.release();
-  h->head.release(); h->useg.release(); h->rowptr.release(); h->colidx.release();
+  h->head.release(); h->useg.release(); h->desc.release(); h->rowptr.release(); h->colidx.release();
   h->gkeys_a.release(); h->gkeys_b.release(); h->gslot_a.release(); h->gslot_b.release(); h->gseg.release();
   h->temp.release(); h->scalars.release();
   delete h;
@@ -368,6 +408,9 @@ extern "C" int b200ipc_assemble_symbolic(b200ipc_assembly* h, int64_t nverts, co
   }
   finish_pattern_kernel<<<1, 1, 0, st>>>(nverts, h->nnzb, h->nvalid, h->rowptr.ptr, h->useg.ptr);
   RC(post_launch());
+  CK(h->desc.reserve(h->nvalid));
+  source_desc_kernel<<<blocks_for(h->nvalid), kAT, 0, st>>>(fd, nverts, h->nvalid, h->slot_b.ptr, h->desc.ptr);
+  RC(post_launch());
 
   // gradient runs: sort vertex slots by vertex id
   const int64_t ng = h->ngslots;
@@ -405,14 +448,19 @@ extern "C" int b200ipc_assemble_numeric(b200ipc_assembly* h, const double* masse
   if (!h || !h->ready) return B200IPC_ESTATE;
   if (!masses || !vals || (h->fam.nfam && !fam_hess)) return B200IPC_EINVAL;
   NumericArgs a;
-  a.fd = h->fam;
+  for (int f = 0; f < kMaxFam; ++f) {
+    a.hp.p[f] = nullptr;
+    a.ld[f] = 0;
+  }
   for (int f = 0; f < h->fam.nfam; ++f) {
     if (h->fam.nb[f] && !fam_hess[f]) return B200IPC_EINVAL;
     a.hp.p[f] = fam_hess[f];
+    a.ld[f] = 3 * h->fam.s[f];
   }
-  a.nverts = h->nverts; a.nnzb = h->nnzb; a.fixed = h->fixed.ptr; a.masses = masses;
-  a.useg = h->useg.ptr; a.colidx = h->colidx.ptr; a.perm = h->slot_b.ptr; a.rowptr = h->rowptr.ptr; a.vals = vals;
-  assemble_numeric_kernel<<<blocks_for(9 * h->nnzb), kAT, 0, (cudaStream_t)stream>>>(a);
+  a.nnzb = h->nnzb; a.fixed = h->fixed.ptr; a.masses = masses;
+  a.useg = h->useg.ptr; a.desc = h->desc.ptr; a.vals = vals;
+  const unsigned grid = (unsigned)((h->nnzb + kNumWarps - 1) / kNumWarps);
+  assemble_numeric_kernel<<<grid, 32 * kNumWarps, 0, (cudaStream_t)stream>>>(a);
   return post_launch();
 }
 

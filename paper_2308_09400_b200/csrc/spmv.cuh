@@ -22,14 +22,24 @@ __device__ __forceinline__ void bsr_row_product(int64_t row, int lane, const int
   const double* v = vals + 9ll * b0;
   const int nelem = 9 * (b1 - b0);
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-  for (int q = lane; q < nelem; q += LPR) {
-    const int blk = q / 9;
-    const int e = q - 9 * blk;
+  // two elements per lane in flight per trip (independent loads), accumulated in element order
+  for (int q = lane; q < nelem; q += 2 * LPR) {
+    const int q2 = q + LPR;
+    const bool two = q2 < nelem;
+    const int blk = q / 9, blk2 = two ? q2 / 9 : blk;
+    const int e = q - 9 * blk, e2 = two ? q2 - 9 * blk2 : 0;
     const int i = e / 3, j = e - 3 * i;
-    const double p = v[q] * __ldg(x + 3ll * __ldg(colidx + b0 + blk) + j);
+    const int i2 = e2 / 3, j2 = e2 - 3 * i2;
+    const int c1 = __ldg(colidx + b0 + blk), c2 = __ldg(colidx + b0 + blk2);
+    const double v1 = v[q], v2 = two ? v[q2] : 0.0;
+    const double p = v1 * __ldg(x + 3ll * c1 + j);
+    const double p2 = v2 * __ldg(x + 3ll * c2 + j2);
     a0 += i == 0 ? p : 0.0;
     a1 += i == 1 ? p : 0.0;
     a2 += i == 2 ? p : 0.0;
+    a0 += (two && i2 == 0) ? p2 : 0.0;
+    a1 += (two && i2 == 1) ? p2 : 0.0;
+    a2 += (two && i2 == 2) ? p2 : 0.0;
   }
 #pragma unroll
   // only this group's lanes take part: neighbouring groups in the warp may run other trip counts

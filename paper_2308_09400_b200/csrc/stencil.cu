@@ -1,6 +1,7 @@
 // Per-contact barrier energy / gradient / analytically PSD-projected Hessian block.
 //
-// One launch per stencil kind (the table is kind-sorted, so a launch is branch-uniform).
+// One launch per table; the table is kind-sorted and every CTA owns a 128-stencil tile of a
+// single kind, so CTAs are branch-uniform.
 // Phase 1: thread-per-stencil -- gather the 2..4 vertex positions, evaluate the distance
 // branch, f = d/d_hat and its gradient, the barrier scalars and the closed-form retained
 // eigenpair (lambda, w); everything stays in registers, no numerical eigendecomposition.
@@ -30,9 +31,7 @@ template <> struct KindTraits<B200IPC_PP>  { static constexpr int S = 2; static 
 template <> struct KindTraits<B200IPC_PPP> { static constexpr int S = 4; static constexpr bool PAR = true; };
 template <> struct KindTraits<B200IPC_PT>  { static constexpr int S = 4; static constexpr bool PAR = false; };
 
-struct StencilArgs {
-  b200ipc_params prm;
-  const double* positions;
+struct KindArgs {
   int64_t n;                 // rows of this kind
   const int32_t* verts;      // (n,4)
   const uint8_t* sub;        // (n)
@@ -43,29 +42,37 @@ struct StencilArgs {
   double* hess;              // (n,D,D) or null
 };
 
+// One launch covers every kind: CTA b works on tile (b - tile_off[kind]) of the kind whose tile
+// range contains b, so a CTA is still branch-uniform while the step pays one launch and one tail.
+struct StencilArgs {
+  b200ipc_params prm;
+  const double* positions;
+  KindArgs k[B200IPC_NKINDS];
+  uint32_t tile_off[B200IPC_NKINDS + 1];
+};
+
+constexpr int kPad = kTile + 1;  // odd stride: bank = 2(k*P + i) mod 32 is distinct across k and i
+
 template <int KIND, int FORM>
-__global__ void __launch_bounds__(kTile) barrier_stencil_kernel(const StencilArgs a) {
+__device__ __forceinline__ void stencil_tile(const b200ipc_params& prm, const double* __restrict__ positions,
+                                             const KindArgs& a, int64_t tile, double* sm_z, double* sm_g) {
   using KT = KindTraits<KIND>;
   constexpr int S = KT::S;
   constexpr int D = 3 * S;
   constexpr int DD = D * D;
-  constexpr int P = kTile + 1;  // odd stride: bank = 2(k*P + i) mod 32 is distinct across k and i
-
-  __shared__ double sm_z[D * P];
-  __shared__ double sm_g[D * P];
+  constexpr int P = kPad;
 
   const int tid = threadIdx.x;
-  const int64_t tile0 = (int64_t)blockIdx.x * kTile;
+  const int64_t tile0 = tile * kTile;
   const int64_t i = tile0 + tid;
-  const b200ipc_params& prm = a.prm;
 
   if (i < a.n) {
     const int4 vid = __ldg(reinterpret_cast<const int4*>(a.verts) + i);
     V3 x[4];
-    x[0] = load3(a.positions, vid.x);
-    x[1] = load3(a.positions, vid.y);
-    if (S >= 3) x[2] = load3(a.positions, vid.z);
-    if (S >= 4) x[3] = load3(a.positions, vid.w);
+    x[0] = load3(positions, vid.x);
+    x[1] = load3(positions, vid.y);
+    if (S >= 3) x[2] = load3(positions, vid.z);
+    if (S >= 4) x[3] = load3(positions, vid.w);
 
     V3 gd[4];
     double wit0, wit1;
@@ -188,15 +195,25 @@ __global__ void __launch_bounds__(kTile) barrier_stencil_kernel(const StencilArg
   }
 }
 
-template <int KIND>
-static int launch_kind(const StencilArgs& a, cudaStream_t stream) {
-  if (a.n <= 0) return 0;
-  const unsigned grid = (unsigned)((a.n + kTile - 1) / kTile);
-  if (a.prm.form == 0)
-    barrier_stencil_kernel<KIND, 0><<<grid, kTile, 0, stream>>>(a);
-  else
-    barrier_stencil_kernel<KIND, 1><<<grid, kTile, 0, stream>>>(a);
-  return post_launch();
+template <int FORM>
+__global__ void __launch_bounds__(kTile) barrier_stencil_kernel(const StencilArgs a) {
+  __shared__ double sm_z[12 * kPad];
+  __shared__ double sm_g[12 * kPad];
+  const uint32_t b = blockIdx.x;
+  int kind = 0;
+#pragma unroll
+  for (int k = 1; k < B200IPC_NKINDS; ++k)
+    if (b >= a.tile_off[k]) kind = k;
+  const int64_t tile = b - a.tile_off[kind];
+  switch (kind) {
+    case B200IPC_EE: stencil_tile<B200IPC_EE, FORM>(a.prm, a.positions, a.k[B200IPC_EE], tile, sm_z, sm_g); break;
+    case B200IPC_EEP: stencil_tile<B200IPC_EEP, FORM>(a.prm, a.positions, a.k[B200IPC_EEP], tile, sm_z, sm_g); break;
+    case B200IPC_PE: stencil_tile<B200IPC_PE, FORM>(a.prm, a.positions, a.k[B200IPC_PE], tile, sm_z, sm_g); break;
+    case B200IPC_PEP: stencil_tile<B200IPC_PEP, FORM>(a.prm, a.positions, a.k[B200IPC_PEP], tile, sm_z, sm_g); break;
+    case B200IPC_PP: stencil_tile<B200IPC_PP, FORM>(a.prm, a.positions, a.k[B200IPC_PP], tile, sm_z, sm_g); break;
+    case B200IPC_PPP: stencil_tile<B200IPC_PPP, FORM>(a.prm, a.positions, a.k[B200IPC_PPP], tile, sm_z, sm_g); break;
+    default: stencil_tile<B200IPC_PT, FORM>(a.prm, a.positions, a.k[B200IPC_PT], tile, sm_z, sm_g); break;
+  }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -305,40 +322,35 @@ extern "C" int b200ipc_barrier_stencils(const b200ipc_params* params, int64_t nv
     row4[fam4_order[j]] = acc;
     acc += kind_off[fam4_order[j] + 1] - kind_off[fam4_order[j]];
   }
+  StencilArgs a;
+  a.prm = *params;
+  a.positions = positions;
+  uint64_t tiles = 0;
   for (int k = 0; k < B200IPC_NKINDS; ++k) {
     const int64_t off = kind_off[k], cnt = kind_off[k + 1] - off;
-    if (cnt == 0) continue;
-    StencilArgs a;
-    a.prm = *params;
-    a.positions = positions;
-    a.n = cnt;
-    a.verts = verts + 4 * off;
-    a.sub = sub ? sub + off : nullptr;
-    a.eps_x = eps_x ? eps_x + off : nullptr;
-    a.energy = energy ? energy + off : nullptr;
-    a.status = status ? status + off : nullptr;
-    int rc = 0;
-    switch (k) {
-      case B200IPC_PP:
-        a.grad = grad2; a.hess = hess2;
-        rc = launch_kind<B200IPC_PP>(a, s);
-        break;
-      case B200IPC_PE:
-        a.grad = grad3; a.hess = hess3;
-        rc = launch_kind<B200IPC_PE>(a, s);
-        break;
-      default:
-        a.grad = grad4 ? grad4 + 12 * row4[k] : nullptr;
-        a.hess = hess4 ? hess4 + 144 * row4[k] : nullptr;
-        if (k == B200IPC_EE) rc = launch_kind<B200IPC_EE>(a, s);
-        else if (k == B200IPC_EEP) rc = launch_kind<B200IPC_EEP>(a, s);
-        else if (k == B200IPC_PEP) rc = launch_kind<B200IPC_PEP>(a, s);
-        else if (k == B200IPC_PPP) rc = launch_kind<B200IPC_PPP>(a, s);
-        else rc = launch_kind<B200IPC_PT>(a, s);
+    KindArgs& ka = a.k[k];
+    ka.n = cnt;
+    ka.verts = verts + 4 * off;
+    ka.sub = sub ? sub + off : nullptr;
+    ka.eps_x = eps_x ? eps_x + off : nullptr;
+    ka.energy = energy ? energy + off : nullptr;
+    ka.status = status ? status + off : nullptr;
+    if (k == B200IPC_PP) {
+      ka.grad = grad2; ka.hess = hess2;
+    } else if (k == B200IPC_PE) {
+      ka.grad = grad3; ka.hess = hess3;
+    } else {
+      ka.grad = grad4 ? grad4 + 12 * row4[k] : nullptr;
+      ka.hess = hess4 ? hess4 + 144 * row4[k] : nullptr;
     }
-    if (rc) return rc;
+    a.tile_off[k] = (uint32_t)tiles;
+    tiles += (uint64_t)((cnt + kTile - 1) / kTile);
   }
-  return 0;
+  a.tile_off[B200IPC_NKINDS] = (uint32_t)tiles;
+  if (tiles >= (1ull << 31)) return B200IPC_EINVAL;
+  if (params->form == 0) barrier_stencil_kernel<0><<<(unsigned)tiles, kTile, 0, s>>>(a);
+  else barrier_stencil_kernel<1><<<(unsigned)tiles, kTile, 0, s>>>(a);
+  return post_launch();
 }
 
 extern "C" int b200ipc_reduce_energy(int64_t n, const double* energy, const uint8_t* status, double* result,

@@ -6,7 +6,7 @@ TAG=${1:-r1}
 mkdir -p gpurun_out
 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches_${TAG}.csv \
     python bench.py --steps 2 --warmup 3 --skip-cpu > gpurun_out/launches_${TAG}.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:barrier_stencil_kernel -s 12 -c 6 \
+ncu --set full --clock-control none --import-source on -k regex:barrier_stencil_kernel -s 4 -c 2 \
     -o gpurun_out/prof_stencil_${TAG} -f python bench.py --steps 1 --warmup 3 --skip-newton --skip-cpu \
     > gpurun_out/prof_stencil_${TAG}.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:'assemble_numeric|bsr_spmv|pcg_kernel|scatter_gradient' -c 8 \

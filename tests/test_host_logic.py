@@ -1,0 +1,116 @@
+"""Host-side logic that needs no GPU: stencil table, kind order, broad phase, generators, params."""
+
+import numpy as np
+import pytest
+
+from oracle import tetipc_oracle as o
+from paper_2308_09400_b200 import barrier, proximity, scene_batch, solver, workloads
+from paper_2308_09400_b200.proximity import ContactStencil, StencilKind, StencilTable
+
+
+def test_kind_codes_follow_reference_list_order():
+    assert [k.value for k in proximity.KIND_ORDER] == list(o.KIND_NAMES)
+    assert (proximity.EE, proximity.EEP, proximity.PE, proximity.PEP, proximity.PP, proximity.PPP, proximity.PT) == (
+        o.EE, o.EEP, o.PE, o.PEP, o.PP, o.PPP, o.PT)
+    np.testing.assert_array_equal(proximity.KIND_SIZE, o.KIND_SIZE)
+    np.testing.assert_array_equal(proximity.IS_PARALLEL, o.IS_PARALLEL)
+
+
+def test_table_roundtrip_and_validation():
+    stencils = [
+        ContactStencil(kind=StencilKind.POINT_TRIANGLE, verts=(3, 0, 1, 2), origin=("vt", 3, 0, 1, 2)),
+        ContactStencil(kind=StencilKind.EDGE_EDGE, verts=(0, 1, 4, 5), origin=("ee", 0, 1, 4, 5)),
+        ContactStencil(kind=StencilKind.POINT_EDGE_PARALLEL, verts=(0, 1, 6, 7), eps_x=1e-3, sub=(2, 0, 1),
+                       edge_pair=((0, 1), (6, 7)), origin=("ee", 0, 1, 6, 7)),
+        ContactStencil(kind=StencilKind.POINT_POINT, verts=(1, 6), origin=("ee", 0, 1, 6, 7)),
+    ]
+    table = StencilTable.from_stencils(stencils, sort=True)
+    assert table.kind.tolist() == [0, 3, 4, 6]
+    assert table.verts[2].tolist() == [1, 6, -1, -1]
+    assert table.sub[1] == o.pack_sub((2, 0, 1)) and table.eps_x[1] == 1e-3
+    back = table.to_stencils()
+    assert back == sorted(stencils, key=lambda s: s.sort_key())
+    np.testing.assert_array_equal(table.kind_offsets(), [0, 1, 1, 1, 2, 3, 3, 4])
+    assert table.family_rows(4).tolist() == [0, 1, 3] and table.family_rows(2).tolist() == [2]
+    with pytest.raises(proximity.ProximityError):
+        StencilTable([6, 0], np.zeros((2, 4)), np.zeros(2), np.zeros(2))  # not kind sorted
+    with pytest.raises(proximity.ProximityError):
+        ContactStencil(kind=StencilKind.POINT_EDGE, verts=(0, 1))
+    with pytest.raises(proximity.ProximityError):
+        ContactStencil(kind=StencilKind.EDGE_EDGE_PARALLEL, verts=(0, 1, 2, 3))
+
+
+def test_params_mirror_reference_expressions():
+    with pytest.raises(ValueError):
+        barrier.BarrierParams(d_hat=1.0, d_thr_ratio=1.5)
+    with pytest.raises(ValueError):
+        barrier.BarrierParams(d_hat=1.0, form="cubic")
+    p = barrier.BarrierParams(d_hat=5e-3, kappa=2e8)
+    assert p.eps_g == 0.1 * 0.1 and p.d_thr == 0.1 * 5e-3
+    c = barrier.c_params(p, dt=0.01)
+    assert c.d_hat_sq == 5e-3 * 5e-3 and c.d_hat_pow2 == 5e-3**2 and c.scale == 2e8 * 5e-3**4
+    assert c.dt2 == 0.01**2 and c.use_filter == 1 and c.form == 0
+
+
+def all_pairs(tris, edges):
+    verts = np.unique(tris)
+    vv, tt = np.meshgrid(verts, np.arange(tris.shape[0]), indexing="ij")
+    vt = np.concatenate([vv.reshape(-1, 1), tris[tt.reshape(-1)]], axis=1)
+    vt = vt[(vt[:, :1] != vt[:, 1:]).all(axis=1)]
+    i, j = np.triu_indices(edges.shape[0], 1)
+    ee = np.concatenate([edges[i], edges[j]], axis=1)
+    return vt, ee[(ee[:, 0] != ee[:, 2]) & (ee[:, 0] != ee[:, 3]) & (ee[:, 1] != ee[:, 2]) & (ee[:, 1] != ee[:, 3])]
+
+
+@pytest.mark.parametrize("seed,layers,n", [(5, 4, 9), (2, 2, 12)])
+def test_grid_broad_phase_is_a_duplicate_free_superset(seed, layers, n):
+    cloth = workloads.cloth_stack(layers=layers, n=n, seed=seed)
+    vt, ee = workloads.broad_phase(cloth)
+    assert len(np.unique(vt, axis=0)) == len(vt) and len(np.unique(ee, axis=0)) == len(ee)
+    vt_all, ee_all = all_pairs(cloth.tris, cloth.edges)
+    ref = o.narrow_phase(cloth.positions, cloth.rest_positions, vt_all, ee_all, cloth.d_hat)
+    got = o.narrow_phase(cloth.positions, cloth.rest_positions, vt, ee, cloth.d_hat)
+    for key in ref:
+        np.testing.assert_array_equal(got[key], ref[key], err_msg=key)
+    assert len(ref["kind"]) > 500 and len(vt) < len(vt_all) // 4
+
+
+def test_generators_are_seeded_and_hit_their_distances():
+    a, b = workloads.config1_batch(n_pt=50, n_ee=50), workloads.config1_batch(n_pt=50, n_ee=50)
+    np.testing.assert_array_equal(a.positions, b.positions)
+    tab = o.narrow_phase(a.positions, a.rest_positions, a.vt, a.ee, a.d_hat)
+    assert np.bincount(tab["kind"], minlength=7).tolist() == [50, 0, 0, 0, 0, 0, 50]
+    rng = np.random.default_rng(0)
+    d = rng.uniform(0.1, 0.9, 200)
+    x = workloads.gen_point_triangle(rng, 200, d)
+    codes, d2, _, _ = o.pt_classify_batch(x[:, 0], x[:, 1], x[:, 2], x[:, 3])
+    assert np.all(codes == 0)
+    np.testing.assert_allclose(np.sqrt(d2), d, rtol=1e-9)
+    x = workloads.gen_edge_edge(rng, 200, d)
+    codes, d2, _, _ = o.ee_classify_batch(x[:, 0], x[:, 1], x[:, 2], x[:, 3])
+    assert np.all(codes == 8)
+    np.testing.assert_allclose(np.sqrt(d2), d, rtol=1e-9)
+    x = workloads.gen_exact_parallel_edge_edge(rng, 50, rng.integers(13, 58, 50))
+    c, _ = o.cross_sq_batch(x[:, 0], x[:, 1], x[:, 2], x[:, 3])
+    assert np.all(c == 0.0)
+    qb = workloads.config2_batch(n=4000)
+    kinds = set(o.narrow_phase(qb.positions, qb.rest_positions, qb.vt, qb.ee, qb.d_hat)["kind"].tolist())
+    assert {o.EEP, o.PEP, o.PPP} <= kinds
+
+
+def test_group_blocks_layout():
+    rng = np.random.default_rng(1)
+    blocks = []
+    for s in (4, 2, 3, 4, 2):
+        blocks.append(barrier.LocalQuadratic(vert_ids=np.arange(s, dtype=np.int64), grad=rng.normal(size=3 * s),
+                                             hess=rng.normal(size=(3 * s, 3 * s))))
+    grouped = solver.group_blocks(blocks)
+    assert [h.shape for h, _ in grouped] == [(2, 6, 6), (1, 9, 9), (2, 12, 12)]
+    np.testing.assert_array_equal(grouped[2][0][1], blocks[3].hess)
+    assert solver.group_blocks([]) == []
+
+
+def test_scene_batch_single_process():
+    assert scene_batch.replica_seed(10, 3) == 13
+    assert scene_batch.aggregate(5.0, 2.0) == (5.0, 2.0)
+    assert scene_batch.throughput(8e6, 2.0, 4) == pytest.approx(1.6e10)
