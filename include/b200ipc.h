@@ -179,6 +179,10 @@ int b200ipc_narrow_phase(int64_t nverts, const double* positions, const double* 
 typedef struct b200ipc_assembly b200ipc_assembly;
 int b200ipc_assembly_create(b200ipc_assembly** out);
 int b200ipc_assembly_destroy(b200ipc_assembly* h);
+/* Numeric kernel choice: 0 (default) row-wise -- one warp per block-row reads every dense block
+ * exactly once as contiguous three-row runs; 1 per-block runs -- one warp per output block gathers
+ * its 3x3 sub-blocks.  Both are atomic-free and deterministic; results agree to round-off. */
+int b200ipc_assembly_set_variant(b200ipc_assembly* h, int32_t variant);
 /* Build the pattern and the source runs (sort by key).  fixed: device u8 (nverts).  Synchronises
  * `stream` and returns the number of 3x3 blocks in *nnzb_out (host).  The vids buffers must stay
  * valid until the next symbolic call (the numeric phase re-reads nothing from them). */

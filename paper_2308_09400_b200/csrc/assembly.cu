@@ -65,6 +65,7 @@ struct b200ipc_assembly {
   int64_t nnzb = 0;
   int64_t ngslots = 0;     // sum nb*s
   bool ready = false;
+  int variant = 0;         // numeric kernel: 0 row-wise (default), 1 per-block runs
   b200ipc::FamDesc fam;
   b200ipc::DevBuf<uint8_t> fixed;
   b200ipc::DevBuf<uint64_t> keys_a, keys_b;
@@ -74,6 +75,7 @@ struct b200ipc_assembly {
   b200ipc::DevBuf<int32_t> rowptr, colidx;
   b200ipc::DevBuf<uint32_t> gkeys_a, gkeys_b, gslot_a, gslot_b;
   b200ipc::DevBuf<int32_t> gseg;              // (N+1) run starts per vertex
+  b200ipc::DevBuf<uint64_t> rs_desc, rs_dst;  // per row-source: chunk offset|family, 4 x u16 destination block
   b200ipc::DevBuf<uint8_t> temp;
   b200ipc::DevBuf<int64_t> scalars;           // device scratch for counts
 };
@@ -240,6 +242,145 @@ __global__ void __launch_bounds__(32 * kNumWarps) assemble_numeric_kernel(const 
   }
 }
 
+// ---- row-wise numeric assembly ------------------------------------------------------------------
+// A "row-source" is (block b of family f, local vertex a): rows 3a..3a+2 of the dense block are ONE
+// contiguous run of 3*D doubles.  For output block-row i the row-sources are the gradient runs
+// (vertex i's incidences in list order).  rs_desc = (element offset of the run << 3) | family,
+// rs_dst = four u16: index of column vertex v_c inside row i's block list (0xffff = dropped).
+__global__ void __launch_bounds__(kAT) row_source_kernel(FamDesc fd, int64_t nverts, int64_t ng,
+                                                         const uint32_t* __restrict__ gperm,
+                                                         const uint8_t* __restrict__ fixed,
+                                                         const int32_t* __restrict__ rowptr,
+                                                         const int32_t* __restrict__ colidx,
+                                                         uint64_t* __restrict__ rs_desc, uint64_t* __restrict__ rs_dst) {
+  const int64_t j = (int64_t)blockIdx.x * kAT + threadIdx.x;
+  if (j >= ng) return;
+  const int64_t q = gperm[j];
+  int f = 0;
+#pragma unroll
+  for (int k = 1; k < kMaxFam; ++k)
+    if (k < fd.nfam && q >= fd.vert_off[k]) f = k;
+  const int s = fd.s[f];
+  const int64_t r = q - fd.vert_off[f];
+  const int64_t b = r / s;
+  const int a = (int)(r - b * s);
+  const int64_t D = 3 * s;
+  const int64_t* v = fd.vids[f] + b * s;
+  const int64_t row = v[a];
+  rs_desc[j] = ((uint64_t)((b * D + 3 * a) * D) << 3) | (uint64_t)f;
+  uint64_t dst = 0;
+  const int32_t r0 = rowptr[row], r1 = rowptr[row + 1];
+  for (int c = 0; c < 4; ++c) {
+    uint64_t rel = 0xffffull;
+    if (c < s && !fixed[row]) {
+      const int64_t col = v[c];
+      if (col == row || !fixed[col]) {
+        int32_t lo = r0, hi = r1;
+        while (lo < hi) {
+          const int32_t mid = (lo + hi) >> 1;
+          if (colidx[mid] < col) lo = mid + 1;
+          else hi = mid;
+        }
+        rel = (uint64_t)(lo - r0);
+      }
+    }
+    dst |= rel << (16 * c);
+  }
+  rs_dst[j] = dst;
+}
+
+struct RowArgs {
+  HessPtrs hp;
+  int32_t fs[kMaxFam];   // stencil size s per family
+  int64_t nverts;
+  const uint8_t* fixed;
+  const double* masses;
+  const int32_t* rowptr;
+  const int32_t* colidx;
+  const int32_t* gseg;
+  const uint64_t* rs_desc;
+  const uint64_t* rs_dst;
+  double* vals;
+};
+
+constexpr int kRowWarps = 8;
+constexpr int kRowWin = 64;   // blocks of one row accumulated per pass in shared memory
+
+// One warp per block-row.  Every row-source is read as one contiguous run (full sectors, each dense
+// block is read exactly once over the whole kernel) and its s sub-blocks are added into the row's
+// accumulators in shared memory in list order -- no atomics, bitwise reproducible.  The finished
+// row (72 bytes per block, contiguous) is written with consecutive lanes on consecutive doubles.
+__global__ void __launch_bounds__(32 * kRowWarps) assemble_rows_kernel(const RowArgs a) {
+  __shared__ double sm[kRowWarps][kRowWin * 9];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * kRowWarps + w;
+  if (row >= a.nverts) return;
+  double* acc = sm[w];
+  const int32_t r0 = a.rowptr[row], len = a.rowptr[row + 1] - r0;
+  double* out = a.vals + 9ll * r0;
+  if (a.fixed[row]) {  // Dirichlet row: identity diagonal only
+    if (lane < 9) out[lane] = (lane == 0 || lane == 4 || lane == 8) ? 1.0 : 0.0;
+    return;
+  }
+  // diagonal block position inside the row
+  int32_t lo = 0, hi = len;
+  while (lo < hi) {
+    const int32_t mid = (lo + hi) >> 1;
+    if (a.colidx[r0 + mid] < row) lo = mid + 1;
+    else hi = mid;
+  }
+  const int drel = lo;
+  const double mass = a.masses[row];
+  const int32_t j0 = a.gseg[row], j1 = a.gseg[row + 1];
+
+  for (int win = 0; win < len; win += kRowWin) {
+    const int wlen = min(kRowWin, len - win);
+    for (int t = lane; t < 9 * wlen; t += 32) acc[t] = 0.0;
+    __syncwarp();
+    if (lane < 3 && drel >= win && drel < win + wlen) acc[(drel - win) * 9 + 4 * lane] = mass;
+    __syncwarp();
+    // two row-sources in flight: loads of j+1 are issued before j is accumulated
+    for (int32_t j = j0; j < j1; j += 2) {
+      const bool two = j + 1 < j1;
+      const uint64_t dA = a.rs_desc[j], mA = a.rs_dst[j];
+      const uint64_t dB = two ? a.rs_desc[j + 1] : dA, mB = two ? a.rs_dst[j + 1] : 0xffffffffffffffffull;
+      const int fA = (int)(dA & 7), fB = (int)(dB & 7);
+      const int DA = 3 * a.fs[fA], DB = 3 * a.fs[fB];
+      const double* pA = a.hp.p[fA] + (dA >> 3);
+      const double* pB = a.hp.p[fB] + (dB >> 3);
+      const int nA = 3 * DA, nB = two ? 3 * DB : 0;
+      const double vA0 = lane < nA ? __ldg(pA + lane) : 0.0;
+      const double vA1 = lane + 32 < nA ? __ldg(pA + lane + 32) : 0.0;
+      const double vB0 = lane < nB ? __ldg(pB + lane) : 0.0;
+      const double vB1 = lane + 32 < nB ? __ldg(pB + lane + 32) : 0.0;
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const int t = lane + 32 * half;
+        if (t < nA) {
+          const int er = t / DA, cc = t - er * DA;
+          const int c = cc / 3, ec = cc - 3 * c;
+          const int rel = (int)((mA >> (16 * c)) & 0xffff) - win;
+          if (rel >= 0 && rel < wlen) acc[rel * 9 + er * 3 + ec] += half ? vA1 : vA0;
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const int t = lane + 32 * half;
+        if (t < nB) {
+          const int er = t / DB, cc = t - er * DB;
+          const int c = cc / 3, ec = cc - 3 * c;
+          const int rel = (int)((mB >> (16 * c)) & 0xffff) - win;
+          if (rel >= 0 && rel < wlen) acc[rel * 9 + er * 3 + ec] += half ? vB1 : vB0;
+        }
+      }
+      __syncwarp();
+    }
+    for (int t = lane; t < 9 * wlen; t += 32) out[9 * win + t] = acc[t];
+    __syncwarp();
+  }
+}
+
 // ---- gradient ---------------------------------------------------------------------------------
 __global__ void __launch_bounds__(kAT) gradient_keys_kernel(FamDesc fd, int64_t ngslots, uint32_t* __restrict__ keys,
                                                             uint32_t* __restrict__ slots) {
@@ -318,11 +459,17 @@ extern "C" int b200ipc_assembly_create(b200ipc_assembly** out) {
   return *out ? 0 : B200IPC_EINVAL;
 }
 
+extern "C" int b200ipc_assembly_set_variant(b200ipc_assembly* h, int32_t variant) {
+  if (!h || variant < 0 || variant > 1) return B200IPC_EINVAL;
+  h->variant = variant;
+  return 0;
+}
+
 extern "C" int b200ipc_assembly_destroy(b200ipc_assembly* h) {
   if (!h) return 0;
   h->fixed.release(); h->keys_a.release(); h->keys_b.release(); h->slot_a.release(); h->slot_b.release();
   h->head.release(); h->useg.release(); h->desc.release(); h->rowptr.release(); h->colidx.release();
-  h->gkeys_a.release(); h->gkeys_b.release(); h->gslot_a.release(); h->gslot_b.release(); h->gseg.release();
+  h->gkeys_a.release(); h->gkeys_b.release(); h->gslot_a.release(); h->gslot_b.release(); h->gseg.release(); h->rs_desc.release(); h->rs_dst.release();
   h->temp.release(); h->scalars.release();
   delete h;
   return 0;
@@ -430,6 +577,12 @@ extern "C" int b200ipc_assemble_symbolic(b200ipc_assembly* h, int64_t nverts, co
   }
   lower_bound_kernel<<<blocks_for(nverts + 1), kAT, 0, st>>>(nverts, ng, h->gkeys_b.ptr, h->gseg.ptr);
   RC(post_launch());
+  if (ng > 0) {
+    CK(h->rs_desc.reserve(ng)); CK(h->rs_dst.reserve(ng));
+    row_source_kernel<<<blocks_for(ng), kAT, 0, st>>>(fd, nverts, ng, h->gslot_b.ptr, h->fixed.ptr, h->rowptr.ptr,
+                                                     h->colidx.ptr, h->rs_desc.ptr, h->rs_dst.ptr);
+    RC(post_launch());
+  }
   h->ready = true;
   if (nnzb_out) *nnzb_out = h->nnzb;
   return 0;
@@ -459,8 +612,18 @@ extern "C" int b200ipc_assemble_numeric(b200ipc_assembly* h, const double* masse
   }
   a.nnzb = h->nnzb; a.fixed = h->fixed.ptr; a.masses = masses;
   a.useg = h->useg.ptr; a.desc = h->desc.ptr; a.vals = vals;
-  const unsigned grid = (unsigned)((h->nnzb + kNumWarps - 1) / kNumWarps);
-  assemble_numeric_kernel<<<grid, 32 * kNumWarps, 0, (cudaStream_t)stream>>>(a);
+  if (h->variant == 1) {  // per-block runs (gather of 3x3 sub-blocks)
+    const unsigned grid = (unsigned)((h->nnzb + kNumWarps - 1) / kNumWarps);
+    assemble_numeric_kernel<<<grid, 32 * kNumWarps, 0, (cudaStream_t)stream>>>(a);
+    return post_launch();
+  }
+  RowArgs r;
+  r.hp = a.hp;
+  for (int f = 0; f < kMaxFam; ++f) r.fs[f] = f < h->fam.nfam ? h->fam.s[f] : 0;
+  r.nverts = h->nverts; r.fixed = h->fixed.ptr; r.masses = masses; r.rowptr = h->rowptr.ptr; r.colidx = h->colidx.ptr;
+  r.gseg = h->gseg.ptr; r.rs_desc = h->rs_desc.ptr; r.rs_dst = h->rs_dst.ptr; r.vals = vals;
+  const unsigned grid = (unsigned)((h->nverts + kRowWarps - 1) / kRowWarps);
+  assemble_rows_kernel<<<grid, 32 * kRowWarps, 0, (cudaStream_t)stream>>>(r);
   return post_launch();
 }
 

@@ -57,6 +57,10 @@ class NewtonSystem:
         self._fam = []        # [(s, nb, vids tensor)]
         self._pcg_ws = None
 
+    def set_numeric_variant(self, variant):
+        """0 = row-wise numeric kernel (default), 1 = per-block runs."""
+        _lib.check(_lib.lib().b200ipc_assembly_set_variant(self._h, int(variant)), "assembly_set_variant")
+
     def close(self):
         if getattr(self, "_h", None) is not None and self._h:
             _lib.lib().b200ipc_assembly_destroy(self._h)
@@ -161,8 +165,9 @@ class NewtonSystem:
         return device.to_host(self.rowptr), device.to_host(self.colidx), device.to_host(self.vals)
 
 
-def _system_from_grouped(grouped, masses, fixed):
+def _system_from_grouped(grouped, masses, fixed, variant=0):
     sysm = NewtonSystem(masses, fixed)
+    sysm.set_numeric_variant(variant)
     fams = [(int(v.shape[1]), v) for _, v in grouped if len(v)]
     sysm.set_pattern(fams)
     sysm.assemble([h for h, v in grouped if len(v)])

@@ -116,7 +116,10 @@ def test_gradient_scatter(S, scene):
 def test_pcg_matches_reference(S, scene):
     rhs = -scene["ref_gradient"]
     d, iters, ok = S.solver.pcg_solve(scene["grouped"], scene["masses"], scene["fixed"], rhs, 1e-4, 2000)
-    assert ok == bool(scene["ref_pcg_ok"]) and abs(iters - int(scene["ref_pcg_iters"])) <= 2
+    # kappa = 2e8: round-off (summation order of the assembly, of the dot products) moves the stopping
+    # iteration by a few percent; the iterate is compared in the energy norm below
+    ref_it = int(scene["ref_pcg_iters"])
+    assert ok == bool(scene["ref_pcg_ok"]) and abs(iters - ref_it) <= 2 + 0.05 * ref_it, (iters, ref_it)
     assert np.all(d.reshape(-1, 3)[scene["fixed"]] == 0.0)
     # same Krylov iterate up to round-off amplified by the conditioning: compare in the energy norm
     a = scene["ref_dense"]
@@ -163,12 +166,21 @@ def test_random_blocks_assembly_vs_oracle(S, n, nb):
         hess = u[:, :, None] * u[:, None, :] * rng.uniform(0.1, 5.0, size=(cnt, 1, 1))
         base = rng.integers(0, n - 8, size=(cnt, 1))
         vids = (base + np.stack([rng.permutation(8)[:s] for _ in range(cnt)])).astype(np.int64)
+        if s == 4:  # a hub vertex with several hundred neighbours: rows longer than one smem window
+            hub = np.stack([np.concatenate([[7], rng.choice(np.arange(8, n), size=3, replace=False)]) for _ in range(300)])
+            vids[:300] = hub
         grouped.append((hess, vids))
+    fixed[7] = False
     rowptr, colidx, vals = S.solver.assemble_bsr(grouped, masses, fixed)
     o_rowptr, o_colidx, o_vals = o.assemble_bsr(grouped, masses, fixed)
     np.testing.assert_array_equal(rowptr, o_rowptr)
     np.testing.assert_array_equal(colidx, o_colidx)
+    assert rowptr[8] - rowptr[7] > 500
     assert block_rel_err(vals, o_vals) < 1e-12
+    # the per-block-run numeric kernel gives the same matrix
+    alt = S.solver._system_from_grouped(grouped, masses, fixed, variant=1)
+    assert block_rel_err(S.device.to_host(alt.vals), o_vals) < 1e-12
+    alt.close()
     x = rng.normal(size=3 * n)
     sysm = S.solver._system_from_grouped(grouped, masses, fixed)
     y = S.device.to_host(sysm.spmv(x))
