@@ -306,6 +306,37 @@ struct RowArgs {
 constexpr int kRowWarps = 8;
 constexpr int kRowWin = 64;   // blocks of one row accumulated per pass in shared memory
 
+// Per-lane constants of the element -> (sub-block, entry) map of a run of 3*D doubles.
+template <int D>
+struct LaneMap {
+  int k0, sh0, k1, sh1;  // entry index er*3+ec and shift 16*c for elements lane and lane+32
+  __device__ __forceinline__ explicit LaneMap(int lane) {
+    const int t0 = lane < 3 * D ? lane : 0;
+    const int er0 = t0 / D, cc0 = t0 - er0 * D;
+    k0 = er0 * 3 + cc0 % 3;
+    sh0 = 16 * (cc0 / 3);
+    const int t1 = lane + 32 < 3 * D ? lane + 32 : 0;
+    const int er1 = t1 / D, cc1 = t1 - er1 * D;
+    k1 = er1 * 3 + cc1 % 3;
+    sh1 = 16 * (cc1 / 3);
+  }
+};
+
+template <int D>
+__device__ __forceinline__ void row_add(double* acc, const LaneMap<D>& m, int lane, uint64_t dst, int win, int wlen,
+                                        double v0, double v1) {
+  if (lane < 3 * D) {
+    const unsigned rel = (unsigned)((dst >> m.sh0) & 0xffff) - (unsigned)win;
+    if (rel < (unsigned)wlen) acc[rel * 9 + m.k0] += v0;
+  }
+  if (3 * D > 32) {
+    if (lane + 32 < 3 * D) {
+      const unsigned rel = (unsigned)((dst >> m.sh1) & 0xffff) - (unsigned)win;
+      if (rel < (unsigned)wlen) acc[rel * 9 + m.k1] += v1;
+    }
+  }
+}
+
 // One warp per block-row.  Every row-source is read as one contiguous run (full sectors, each dense
 // block is read exactly once over the whole kernel) and its s sub-blocks are added into the row's
 // accumulators in shared memory in list order -- no atomics, bitwise reproducible.  The finished
@@ -332,6 +363,9 @@ __global__ void __launch_bounds__(32 * kRowWarps) assemble_rows_kernel(const Row
   const int drel = lo;
   const double mass = a.masses[row];
   const int32_t j0 = a.gseg[row], j1 = a.gseg[row + 1];
+  const LaneMap<6> m6(lane);
+  const LaneMap<9> m9(lane);
+  const LaneMap<12> m12(lane);
 
   for (int win = 0; win < len; win += kRowWin) {
     const int wlen = min(kRowWin, len - win);
@@ -339,41 +373,26 @@ __global__ void __launch_bounds__(32 * kRowWarps) assemble_rows_kernel(const Row
     __syncwarp();
     if (lane < 3 && drel >= win && drel < win + wlen) acc[(drel - win) * 9 + 4 * lane] = mass;
     __syncwarp();
-    // two row-sources in flight: loads of j+1 are issued before j is accumulated
+    // two row-sources in flight: the loads of source j+1 are issued before source j is accumulated
     for (int32_t j = j0; j < j1; j += 2) {
       const bool two = j + 1 < j1;
       const uint64_t dA = a.rs_desc[j], mA = a.rs_dst[j];
-      const uint64_t dB = two ? a.rs_desc[j + 1] : dA, mB = two ? a.rs_dst[j + 1] : 0xffffffffffffffffull;
-      const int fA = (int)(dA & 7), fB = (int)(dB & 7);
-      const int DA = 3 * a.fs[fA], DB = 3 * a.fs[fB];
-      const double* pA = a.hp.p[fA] + (dA >> 3);
-      const double* pB = a.hp.p[fB] + (dB >> 3);
-      const int nA = 3 * DA, nB = two ? 3 * DB : 0;
+      const uint64_t dB = two ? a.rs_desc[j + 1] : dA, mB = two ? a.rs_dst[j + 1] : ~0ull;
+      const int sA = a.fs[dA & 7], sB = two ? a.fs[dB & 7] : 0;
+      const double* pA = a.hp.p[dA & 7] + (dA >> 3);
+      const double* pB = a.hp.p[dB & 7] + (dB >> 3);
+      const int nA = 9 * sA, nB = 9 * sB;
       const double vA0 = lane < nA ? __ldg(pA + lane) : 0.0;
       const double vA1 = lane + 32 < nA ? __ldg(pA + lane + 32) : 0.0;
       const double vB0 = lane < nB ? __ldg(pB + lane) : 0.0;
       const double vB1 = lane + 32 < nB ? __ldg(pB + lane + 32) : 0.0;
-#pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        const int t = lane + 32 * half;
-        if (t < nA) {
-          const int er = t / DA, cc = t - er * DA;
-          const int c = cc / 3, ec = cc - 3 * c;
-          const int rel = (int)((mA >> (16 * c)) & 0xffff) - win;
-          if (rel >= 0 && rel < wlen) acc[rel * 9 + er * 3 + ec] += half ? vA1 : vA0;
-        }
-      }
+      if (sA == 4) row_add<12>(acc, m12, lane, mA, win, wlen, vA0, vA1);
+      else if (sA == 3) row_add<9>(acc, m9, lane, mA, win, wlen, vA0, vA1);
+      else row_add<6>(acc, m6, lane, mA, win, wlen, vA0, vA1);
       __syncwarp();
-#pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        const int t = lane + 32 * half;
-        if (t < nB) {
-          const int er = t / DB, cc = t - er * DB;
-          const int c = cc / 3, ec = cc - 3 * c;
-          const int rel = (int)((mB >> (16 * c)) & 0xffff) - win;
-          if (rel >= 0 && rel < wlen) acc[rel * 9 + er * 3 + ec] += half ? vB1 : vB0;
-        }
-      }
+      if (sB == 4) row_add<12>(acc, m12, lane, mB, win, wlen, vB0, vB1);
+      else if (sB == 3) row_add<9>(acc, m9, lane, mB, win, wlen, vB0, vB1);
+      else if (sB == 2) row_add<6>(acc, m6, lane, mB, win, wlen, vB0, vB1);
       __syncwarp();
     }
     for (int t = lane; t < 9 * wlen; t += 32) out[9 * win + t] = acc[t];

@@ -11,6 +11,7 @@
 //         d += alpha c; r -= alpha q; s = P r; delta' = r.s; c = s + (delta'/delta) c
 //   until delta' <= tol*delta0 or the cap.
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 #include "spmv.cuh"
 #include "launch.cuh"
@@ -201,6 +202,10 @@ extern "C" int b200ipc_pcg(int64_t n, int64_t nnzb, const int32_t* rowptr, const
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kPT, 0);
   if (e != cudaSuccess) return -(int)e;
   if (per_sm < 1) return B200IPC_ESTATE;
+  if (const char* env = getenv("B200IPC_PCG_CTAS_PER_SM")) {  // tuning knob: fewer CTAs = cheaper grid barriers
+    const int want_per_sm = atoi(env);
+    if (want_per_sm >= 1 && want_per_sm < per_sm) per_sm = want_per_sm;
+  }
   int64_t grid = (int64_t)sms * per_sm;
   const int64_t want = (n * lpr + kPT - 1) / kPT;  // no more CTAs than rows need
   if (grid > want) grid = want;

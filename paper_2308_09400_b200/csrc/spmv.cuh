@@ -22,24 +22,31 @@ __device__ __forceinline__ void bsr_row_product(int64_t row, int lane, const int
   const double* v = vals + 9ll * b0;
   const int nelem = 9 * (b1 - b0);
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-  // two elements per lane in flight per trip (independent loads), accumulated in element order
-  for (int q = lane; q < nelem; q += 2 * LPR) {
-    const int q2 = q + LPR;
-    const bool two = q2 < nelem;
-    const int blk = q / 9, blk2 = two ? q2 / 9 : blk;
-    const int e = q - 9 * blk, e2 = two ? q2 - 9 * blk2 : 0;
-    const int i = e / 3, j = e - 3 * i;
-    const int i2 = e2 / 3, j2 = e2 - 3 * i2;
-    const int c1 = __ldg(colidx + b0 + blk), c2 = __ldg(colidx + b0 + blk2);
-    const double v1 = v[q], v2 = two ? v[q2] : 0.0;
-    const double p = v1 * __ldg(x + 3ll * c1 + j);
-    const double p2 = v2 * __ldg(x + 3ll * c2 + j2);
-    a0 += i == 0 ? p : 0.0;
-    a1 += i == 1 ? p : 0.0;
-    a2 += i == 2 ? p : 0.0;
-    a0 += (two && i2 == 0) ? p2 : 0.0;
-    a1 += (two && i2 == 1) ? p2 : 0.0;
-    a2 += (two && i2 == 2) ? p2 : 0.0;
+  // four elements per lane per trip: all value / column loads are issued before the dependent x
+  // gathers, and those before the adds (rows are short -- latency, not bandwidth, is the enemy)
+  for (int base = lane; base < nelem; base += 4 * LPR) {
+    double val[4], xv[4];
+    int col[4], ei[4], ej[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int q = base + u * LPR;
+      const bool ok = q < nelem;
+      const int blk = ok ? q / 9 : 0;
+      const int e = ok ? q - 9 * blk : 0;
+      ei[u] = ok ? e / 3 : 3;  // 3 = no row: contributes nowhere
+      ej[u] = e - 3 * (e / 3);
+      col[u] = __ldg(colidx + b0 + blk);
+      val[u] = ok ? v[q] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) xv[u] = __ldg(x + 3ll * col[u] + ej[u]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double p = val[u] * xv[u];
+      a0 += ei[u] == 0 ? p : 0.0;
+      a1 += ei[u] == 1 ? p : 0.0;
+      a2 += ei[u] == 2 ? p : 0.0;
+    }
   }
 #pragma unroll
   // only this group's lanes take part: neighbouring groups in the warp may run other trip counts
