@@ -33,7 +33,7 @@ struct FamDesc {
 };
 
 struct HessPtrs {
-  const double* p[kMaxFam];
+  const double* p[kMaxFam + 1];  // slot 7 = "no source" (null)
 };
 
 template <typename T>
@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(kAT) row_source_kernel(FamDesc fd, int64_t nve
 
 struct RowArgs {
   HessPtrs hp;
-  int32_t fs[kMaxFam];   // stencil size s per family
+  int32_t fs[kMaxFam + 1];   // stencil size s per family; fs[7] = 0 tags an absent source
   int64_t nverts;
   const uint8_t* fixed;
   const double* masses;
@@ -373,27 +373,49 @@ __global__ void __launch_bounds__(32 * kRowWarps) assemble_rows_kernel(const Row
     __syncwarp();
     if (lane < 3 && drel >= win && drel < win + wlen) acc[(drel - win) * 9 + 4 * lane] = mass;
     __syncwarp();
-    // two row-sources in flight: the loads of source j+1 are issued before source j is accumulated
+    // Software pipeline over pairs of row-sources: descriptors are loaded two pairs ahead and the
+    // dense runs one pair ahead of the accumulation, so neither memory latency sits on the
+    // critical path of the (ordered) shared-memory adds.
+    auto load_desc = [&](int32_t j, uint64_t& d, uint64_t& m) {
+      const bool ok = j < j1;
+      d = ok ? a.rs_desc[j] : 7ull;
+      m = ok ? a.rs_dst[j] : ~0ull;
+    };
+    auto fetch = [&](uint64_t d, int& sz, double& v0, double& v1) {
+      sz = a.fs[d & 7];
+      const double* p = a.hp.p[d & 7] + (d >> 3);
+      v0 = lane < 9 * sz ? __ldg(p + lane) : 0.0;
+      v1 = lane + 32 < 9 * sz ? __ldg(p + lane + 32) : 0.0;
+    };
+    auto add = [&](int sz, uint64_t m, double v0, double v1) {
+      if (sz == 4) row_add<12>(acc, m12, lane, m, win, wlen, v0, v1);
+      else if (sz == 3) row_add<9>(acc, m9, lane, m, win, wlen, v0, v1);
+      else if (sz == 2) row_add<6>(acc, m6, lane, m, win, wlen, v0, v1);
+    };
+    uint64_t dA, mA, dB, mB, ndA, nmA, ndB, nmB;
+    load_desc(j0, dA, mA);
+    load_desc(j0 + 1, dB, mB);
+    load_desc(j0 + 2, ndA, nmA);
+    load_desc(j0 + 3, ndB, nmB);
+    int sA, sB;
+    double vA0, vA1, vB0, vB1;
+    fetch(dA, sA, vA0, vA1);
+    fetch(dB, sB, vB0, vB1);
     for (int32_t j = j0; j < j1; j += 2) {
-      const bool two = j + 1 < j1;
-      const uint64_t dA = a.rs_desc[j], mA = a.rs_dst[j];
-      const uint64_t dB = two ? a.rs_desc[j + 1] : dA, mB = two ? a.rs_dst[j + 1] : ~0ull;
-      const int sA = a.fs[dA & 7], sB = two ? a.fs[dB & 7] : 0;
-      const double* pA = a.hp.p[dA & 7] + (dA >> 3);
-      const double* pB = a.hp.p[dB & 7] + (dB >> 3);
-      const int nA = 9 * sA, nB = 9 * sB;
-      const double vA0 = lane < nA ? __ldg(pA + lane) : 0.0;
-      const double vA1 = lane + 32 < nA ? __ldg(pA + lane + 32) : 0.0;
-      const double vB0 = lane < nB ? __ldg(pB + lane) : 0.0;
-      const double vB1 = lane + 32 < nB ? __ldg(pB + lane + 32) : 0.0;
-      if (sA == 4) row_add<12>(acc, m12, lane, mA, win, wlen, vA0, vA1);
-      else if (sA == 3) row_add<9>(acc, m9, lane, mA, win, wlen, vA0, vA1);
-      else row_add<6>(acc, m6, lane, mA, win, wlen, vA0, vA1);
+      uint64_t fdA, fmA, fdB, fmB;  // two pairs ahead
+      load_desc(j + 4, fdA, fmA);
+      load_desc(j + 5, fdB, fmB);
+      int nsA, nsB;                 // one pair ahead
+      double nA0, nA1, nB0, nB1;
+      fetch(ndA, nsA, nA0, nA1);
+      fetch(ndB, nsB, nB0, nB1);
+      add(sA, mA, vA0, vA1);
       __syncwarp();
-      if (sB == 4) row_add<12>(acc, m12, lane, mB, win, wlen, vB0, vB1);
-      else if (sB == 3) row_add<9>(acc, m9, lane, mB, win, wlen, vB0, vB1);
-      else if (sB == 2) row_add<6>(acc, m6, lane, mB, win, wlen, vB0, vB1);
+      add(sB, mB, vB0, vB1);
       __syncwarp();
+      sA = nsA; mA = nmA; vA0 = nA0; vA1 = nA1;
+      sB = nsB; mB = nmB; vB0 = nB0; vB1 = nB1;
+      ndA = fdA; nmA = fmA; ndB = fdB; nmB = fmB;
     }
     for (int t = lane; t < 9 * wlen; t += 32) out[9 * win + t] = acc[t];
     __syncwarp();
@@ -620,10 +642,8 @@ extern "C" int b200ipc_assemble_numeric(b200ipc_assembly* h, const double* masse
   if (!h || !h->ready) return B200IPC_ESTATE;
   if (!masses || !vals || (h->fam.nfam && !fam_hess)) return B200IPC_EINVAL;
   NumericArgs a;
-  for (int f = 0; f < kMaxFam; ++f) {
-    a.hp.p[f] = nullptr;
-    a.ld[f] = 0;
-  }
+  for (int f = 0; f < kMaxFam; ++f) a.ld[f] = 0;
+  for (int f = 0; f <= kMaxFam; ++f) a.hp.p[f] = nullptr;
   for (int f = 0; f < h->fam.nfam; ++f) {
     if (h->fam.nb[f] && !fam_hess[f]) return B200IPC_EINVAL;
     a.hp.p[f] = fam_hess[f];
@@ -638,7 +658,7 @@ extern "C" int b200ipc_assemble_numeric(b200ipc_assembly* h, const double* masse
   }
   RowArgs r;
   r.hp = a.hp;
-  for (int f = 0; f < kMaxFam; ++f) r.fs[f] = f < h->fam.nfam ? h->fam.s[f] : 0;
+  for (int f = 0; f <= kMaxFam; ++f) r.fs[f] = f < h->fam.nfam ? h->fam.s[f] : 0;
   r.nverts = h->nverts; r.fixed = h->fixed.ptr; r.masses = masses; r.rowptr = h->rowptr.ptr; r.colidx = h->colidx.ptr;
   r.gseg = h->gseg.ptr; r.rs_desc = h->rs_desc.ptr; r.rs_dst = h->rs_dst.ptr; r.vals = vals;
   const unsigned grid = (unsigned)((h->nverts + kRowWarps - 1) / kRowWarps);

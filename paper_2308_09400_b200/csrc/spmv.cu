@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(kST) block_jacobi_kernel(int64_t n, const int3
 
 int pick_lpr(int64_t n, int64_t nnzb) {
   const double avg = n > 0 ? (double)nnzb / (double)n : 0.0;
-  return avg >= 10.0 ? 32 : (avg >= 5.0 ? 16 : 8);
+  return avg >= 6.0 ? 32 : (avg >= 3.0 ? 16 : 8);
 }
 
 }  // namespace b200ipc

@@ -12,12 +12,52 @@
 
 namespace b200ipc {
 
+// Full-warp variant: lane = 9*g + 3*i + j with g < 3 owns entry (i,j) of every third block of the
+// row, so the entry index, the x component and the accumulator are lane constants -- no index
+// arithmetic, no selects.  27 of 32 lanes work; each trip reads three whole blocks (216 contiguous
+// bytes) and two trips are in flight.  Five shuffles finish the row.
+__device__ __forceinline__ void bsr_row_product_warp(int64_t row, int lane, const int32_t* __restrict__ rowptr,
+                                                     const int32_t* __restrict__ colidx,
+                                                     const double* __restrict__ vals, const double* __restrict__ x,
+                                                     double& y0, double& y1, double& y2) {
+  const int32_t b0 = rowptr[row], nblk = rowptr[row + 1] - b0;
+  const int g = lane / 9, e = lane - 9 * g;
+  const int j = e % 3;
+  const double* v = vals + 9ll * b0 + e;
+  const int32_t* ci = colidx + b0;
+  double acc = 0.0;
+  if (g < 3) {
+    int blk = g;
+    for (; blk + 3 < nblk; blk += 6) {
+      const int c0 = __ldg(ci + blk), c1 = __ldg(ci + blk + 3);
+      const double v0 = v[9 * blk], v1 = v[9 * (blk + 3)];
+      const double x0 = __ldg(x + 3ll * c0 + j), x1 = __ldg(x + 3ll * c1 + j);
+      acc += v0 * x0;
+      acc += v1 * x1;
+    }
+    if (blk < nblk) acc += v[9 * blk] * __ldg(x + 3ll * __ldg(ci + blk) + j);
+  }
+  const double s1 = __shfl_down_sync(0xffffffffu, acc, 9);
+  const double s2 = __shfl_down_sync(0xffffffffu, acc, 18);
+  const double t = (acc + s1) + s2;               // lanes 0..8: entry sums over all blocks
+  const double t1 = __shfl_down_sync(0xffffffffu, t, 1);
+  const double t2 = __shfl_down_sync(0xffffffffu, t, 2);
+  const double u = (t + t1) + t2;                 // lanes 0, 3, 6: row components
+  y0 = __shfl_sync(0xffffffffu, u, 0);
+  y1 = __shfl_sync(0xffffffffu, u, 3);
+  y2 = __shfl_sync(0xffffffffu, u, 6);
+}
+
 // Returns (y0,y1,y2) of block row `row` in every lane of the group.
 template <int LPR>
 __device__ __forceinline__ void bsr_row_product(int64_t row, int lane, const int32_t* __restrict__ rowptr,
                                                 const int32_t* __restrict__ colidx,
                                                 const double* __restrict__ vals, const double* __restrict__ x,
                                                 double& y0, double& y1, double& y2) {
+  if (LPR == 32) {
+    bsr_row_product_warp(row, lane, rowptr, colidx, vals, x, y0, y1, y2);
+    return;
+  }
   const int32_t b0 = rowptr[row], b1 = rowptr[row + 1];
   const double* v = vals + 9ll * b0;
   const int nelem = 9 * (b1 - b0);
