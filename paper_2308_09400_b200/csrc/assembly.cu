@@ -75,7 +75,9 @@ struct b200ipc_assembly {
   b200ipc::DevBuf<int32_t> rowptr, colidx;
   b200ipc::DevBuf<uint32_t> gkeys_a, gkeys_b, gslot_a, gslot_b;
   b200ipc::DevBuf<int32_t> gseg;              // (N+1) run starts per vertex
-  b200ipc::DevBuf<uint64_t> rs_desc, rs_dst;  // per row-source: chunk offset|family, 4 x u16 destination block
+  b200ipc::DevBuf<uint32_t> rs_idx;           // per row-source: b*s + a inside its family (run = 9s doubles at 9s*idx)
+  b200ipc::DevBuf<uint16_t> rs_dst;           // per row-source x 4: destination block inside the row (0xffff = dropped)
+  b200ipc::DevBuf<int32_t> rseg;              // (N, nfam+1): row-source range of each family inside each row
   b200ipc::DevBuf<uint8_t> temp;
   b200ipc::DevBuf<int64_t> scalars;           // device scratch for counts
 };
@@ -244,15 +246,16 @@ __global__ void __launch_bounds__(32 * kNumWarps) assemble_numeric_kernel(const 
 
 // ---- row-wise numeric assembly ------------------------------------------------------------------
 // A "row-source" is (block b of family f, local vertex a): rows 3a..3a+2 of the dense block are ONE
-// contiguous run of 3*D doubles.  For output block-row i the row-sources are the gradient runs
-// (vertex i's incidences in list order).  rs_desc = (element offset of the run << 3) | family,
-// rs_dst = four u16: index of column vertex v_c inside row i's block list (0xffff = dropped).
+// contiguous run of 9s doubles at element offset 9s*(b*s+a).  For output block-row i the row-sources
+// are vertex i's incidences in list order (the gradient runs), family-major.  Per row-source the
+// symbolic phase stores idx = b*s+a and, for each local column c, the index of vertex v_c inside
+// row i's block list (0xffff = dropped: fixed row or fixed column).
 __global__ void __launch_bounds__(kAT) row_source_kernel(FamDesc fd, int64_t nverts, int64_t ng,
                                                          const uint32_t* __restrict__ gperm,
                                                          const uint8_t* __restrict__ fixed,
                                                          const int32_t* __restrict__ rowptr,
                                                          const int32_t* __restrict__ colidx,
-                                                         uint64_t* __restrict__ rs_desc, uint64_t* __restrict__ rs_dst) {
+                                                         uint32_t* __restrict__ rs_idx, uint16_t* __restrict__ rs_dst) {
   const int64_t j = (int64_t)blockIdx.x * kAT + threadIdx.x;
   if (j >= ng) return;
   const int64_t q = gperm[j];
@@ -264,14 +267,12 @@ __global__ void __launch_bounds__(kAT) row_source_kernel(FamDesc fd, int64_t nve
   const int64_t r = q - fd.vert_off[f];
   const int64_t b = r / s;
   const int a = (int)(r - b * s);
-  const int64_t D = 3 * s;
   const int64_t* v = fd.vids[f] + b * s;
   const int64_t row = v[a];
-  rs_desc[j] = ((uint64_t)((b * D + 3 * a) * D) << 3) | (uint64_t)f;
-  uint64_t dst = 0;
+  rs_idx[j] = (uint32_t)r;
   const int32_t r0 = rowptr[row], r1 = rowptr[row + 1];
   for (int c = 0; c < 4; ++c) {
-    uint64_t rel = 0xffffull;
+    uint16_t rel = 0xffff;
     if (c < s && !fixed[row]) {
       const int64_t col = v[c];
       if (col == row || !fixed[col]) {
@@ -281,63 +282,99 @@ __global__ void __launch_bounds__(kAT) row_source_kernel(FamDesc fd, int64_t nve
           if (colidx[mid] < col) lo = mid + 1;
           else hi = mid;
         }
-        rel = (uint64_t)(lo - r0);
+        rel = (uint16_t)(lo - r0);
       }
     }
-    dst |= rel << (16 * c);
+    rs_dst[4 * j + c] = rel;
   }
-  rs_dst[j] = dst;
+}
+
+// rseg[row*(nfam+1) + f] = first row-source of family >= f inside row's run (slots ascend family-major)
+__global__ void __launch_bounds__(kAT) row_family_split_kernel(FamDesc fd, int64_t nverts,
+                                                               const int32_t* __restrict__ gseg,
+                                                               const uint32_t* __restrict__ gperm,
+                                                               int32_t* __restrict__ rseg) {
+  const int64_t t = (int64_t)blockIdx.x * kAT + threadIdx.x;
+  const int nf1 = fd.nfam + 1;
+  if (t >= nverts * nf1) return;
+  const int64_t row = t / nf1;
+  const int f = (int)(t - row * nf1);
+  int32_t lo = gseg[row], hi = gseg[row + 1];
+  if (f == fd.nfam) {
+    rseg[t] = hi;
+    return;
+  }
+  const int64_t first_slot = fd.vert_off[f];
+  while (lo < hi) {
+    const int32_t mid = (lo + hi) >> 1;
+    if ((int64_t)gperm[mid] < first_slot) lo = mid + 1;
+    else hi = mid;
+  }
+  rseg[t] = lo;
 }
 
 struct RowArgs {
   HessPtrs hp;
-  int32_t fs[kMaxFam + 1];   // stencil size s per family; fs[7] = 0 tags an absent source
+  int32_t fs[kMaxFam];   // stencil size s per family
+  int32_t nfam;
   int64_t nverts;
   const uint8_t* fixed;
   const double* masses;
   const int32_t* rowptr;
   const int32_t* colidx;
-  const int32_t* gseg;
-  const uint64_t* rs_desc;
-  const uint64_t* rs_dst;
+  const int32_t* rseg;
+  const uint32_t* rs_idx;
+  const uint16_t* rs_dst;
   double* vals;
 };
 
 constexpr int kRowWarps = 8;
 constexpr int kRowWin = 64;   // blocks of one row accumulated per pass in shared memory
 
-// Per-lane constants of the element -> (sub-block, entry) map of a run of 3*D doubles.
+// All row-sources of one family inside one row: runs of N = 9s doubles, element t of a run belongs
+// to sub-block c = (t % D) / 3, entry k = 3*(t / D) + t % 3 -- lane constants.  Software pipeline:
+// indices are loaded two sources ahead, the dense run one source ahead of the ordered adds.
 template <int D>
-struct LaneMap {
-  int k0, sh0, k1, sh1;  // entry index er*3+ec and shift 16*c for elements lane and lane+32
-  __device__ __forceinline__ explicit LaneMap(int lane) {
-    const int t0 = lane < 3 * D ? lane : 0;
-    const int er0 = t0 / D, cc0 = t0 - er0 * D;
-    k0 = er0 * 3 + cc0 % 3;
-    sh0 = 16 * (cc0 / 3);
-    const int t1 = lane + 32 < 3 * D ? lane + 32 : 0;
-    const int er1 = t1 / D, cc1 = t1 - er1 * D;
-    k1 = er1 * 3 + cc1 % 3;
-    sh1 = 16 * (cc1 / 3);
-  }
-};
-
-template <int D>
-__device__ __forceinline__ void row_add(double* acc, const LaneMap<D>& m, int lane, uint64_t dst, int win, int wlen,
-                                        double v0, double v1) {
-  if (lane < 3 * D) {
-    const unsigned rel = (unsigned)((dst >> m.sh0) & 0xffff) - (unsigned)win;
-    if (rel < (unsigned)wlen) acc[rel * 9 + m.k0] += v0;
-  }
-  if (3 * D > 32) {
-    if (lane + 32 < 3 * D) {
-      const unsigned rel = (unsigned)((dst >> m.sh1) & 0xffff) - (unsigned)win;
-      if (rel < (unsigned)wlen) acc[rel * 9 + m.k1] += v1;
+__device__ __forceinline__ void row_family(double* acc, int lane, int win, int wlen, const double* __restrict__ base,
+                                           const uint32_t* __restrict__ rs_idx, const uint16_t* __restrict__ rs_dst,
+                                           int32_t jb, int32_t je) {
+  constexpr int N = 3 * D;
+  const bool on0 = lane < N, on1 = lane + 32 < N;
+  const int t0 = on0 ? lane : 0, t1 = on1 ? lane + 32 : 0;
+  const int c0 = (t0 % D) / 3, k0 = 3 * (t0 / D) + t0 % 3;
+  const int c1 = (t1 % D) / 3, k1 = 3 * (t1 / D) + t1 % 3;
+  if (jb >= je) return;
+  // stage 2 (indices) for jb and jb+1, stage 1 (values) for jb
+  uint32_t idxN = rs_idx[jb];
+  unsigned relN0 = rs_dst[4 * jb + c0], relN1 = N > 32 ? rs_dst[4 * jb + c1] : 0xffffu;
+  const double* p = base + (int64_t)N * idxN;
+  double v0 = on0 ? __ldg(p + t0) : 0.0, v1 = on1 ? __ldg(p + t1) : 0.0;
+  unsigned rel0 = relN0, rel1 = relN1;
+  const int32_t j1 = jb + 1 < je ? jb + 1 : jb;
+  idxN = rs_idx[j1];
+  relN0 = rs_dst[4 * j1 + c0];
+  relN1 = N > 32 ? rs_dst[4 * j1 + c1] : 0xffffu;
+  for (int32_t j = jb; j < je; ++j) {
+    // issue: indices of j+2, values of j+1
+    const int32_t j2 = j + 2 < je ? j + 2 : je - 1;
+    const uint32_t idxF = rs_idx[j2];
+    const unsigned relF0 = rs_dst[4 * j2 + c0], relF1 = N > 32 ? rs_dst[4 * j2 + c1] : 0xffffu;
+    const double* pn = base + (int64_t)N * idxN;
+    const double n0 = on0 ? __ldg(pn + t0) : 0.0, n1 = on1 ? __ldg(pn + t1) : 0.0;
+    // ordered adds of source j
+    const unsigned a0 = rel0 - (unsigned)win;
+    if (on0 && a0 < (unsigned)wlen) acc[a0 * 9 + k0] += v0;
+    if (N > 32) {
+      const unsigned a1 = rel1 - (unsigned)win;
+      if (on1 && a1 < (unsigned)wlen) acc[a1 * 9 + k1] += v1;
     }
+    __syncwarp();
+    v0 = n0; v1 = n1; rel0 = relN0; rel1 = relN1;
+    idxN = idxF; relN0 = relF0; relN1 = relF1;
   }
 }
 
-// One warp per block-row.  Every row-source is read as one contiguous run (full sectors, each dense
+// One warp per block-row.  Every row-source is read as one contiguous run (full sectors; each dense
 // block is read exactly once over the whole kernel) and its s sub-blocks are added into the row's
 // accumulators in shared memory in list order -- no atomics, bitwise reproducible.  The finished
 // row (72 bytes per block, contiguous) is written with consecutive lanes on consecutive doubles.
@@ -362,10 +399,7 @@ __global__ void __launch_bounds__(32 * kRowWarps) assemble_rows_kernel(const Row
   }
   const int drel = lo;
   const double mass = a.masses[row];
-  const int32_t j0 = a.gseg[row], j1 = a.gseg[row + 1];
-  const LaneMap<6> m6(lane);
-  const LaneMap<9> m9(lane);
-  const LaneMap<12> m12(lane);
+  const int32_t* seg = a.rseg + row * (a.nfam + 1);
 
   for (int win = 0; win < len; win += kRowWin) {
     const int wlen = min(kRowWin, len - win);
@@ -373,49 +407,12 @@ __global__ void __launch_bounds__(32 * kRowWarps) assemble_rows_kernel(const Row
     __syncwarp();
     if (lane < 3 && drel >= win && drel < win + wlen) acc[(drel - win) * 9 + 4 * lane] = mass;
     __syncwarp();
-    // Software pipeline over pairs of row-sources: descriptors are loaded two pairs ahead and the
-    // dense runs one pair ahead of the accumulation, so neither memory latency sits on the
-    // critical path of the (ordered) shared-memory adds.
-    auto load_desc = [&](int32_t j, uint64_t& d, uint64_t& m) {
-      const bool ok = j < j1;
-      d = ok ? a.rs_desc[j] : 7ull;
-      m = ok ? a.rs_dst[j] : ~0ull;
-    };
-    auto fetch = [&](uint64_t d, int& sz, double& v0, double& v1) {
-      sz = a.fs[d & 7];
-      const double* p = a.hp.p[d & 7] + (d >> 3);
-      v0 = lane < 9 * sz ? __ldg(p + lane) : 0.0;
-      v1 = lane + 32 < 9 * sz ? __ldg(p + lane + 32) : 0.0;
-    };
-    auto add = [&](int sz, uint64_t m, double v0, double v1) {
-      if (sz == 4) row_add<12>(acc, m12, lane, m, win, wlen, v0, v1);
-      else if (sz == 3) row_add<9>(acc, m9, lane, m, win, wlen, v0, v1);
-      else if (sz == 2) row_add<6>(acc, m6, lane, m, win, wlen, v0, v1);
-    };
-    uint64_t dA, mA, dB, mB, ndA, nmA, ndB, nmB;
-    load_desc(j0, dA, mA);
-    load_desc(j0 + 1, dB, mB);
-    load_desc(j0 + 2, ndA, nmA);
-    load_desc(j0 + 3, ndB, nmB);
-    int sA, sB;
-    double vA0, vA1, vB0, vB1;
-    fetch(dA, sA, vA0, vA1);
-    fetch(dB, sB, vB0, vB1);
-    for (int32_t j = j0; j < j1; j += 2) {
-      uint64_t fdA, fmA, fdB, fmB;  // two pairs ahead
-      load_desc(j + 4, fdA, fmA);
-      load_desc(j + 5, fdB, fmB);
-      int nsA, nsB;                 // one pair ahead
-      double nA0, nA1, nB0, nB1;
-      fetch(ndA, nsA, nA0, nA1);
-      fetch(ndB, nsB, nB0, nB1);
-      add(sA, mA, vA0, vA1);
-      __syncwarp();
-      add(sB, mB, vB0, vB1);
-      __syncwarp();
-      sA = nsA; mA = nmA; vA0 = nA0; vA1 = nA1;
-      sB = nsB; mB = nmB; vB0 = nB0; vB1 = nB1;
-      ndA = fdA; nmA = fmA; ndB = fdB; nmB = fmB;
+    for (int f = 0; f < a.nfam; ++f) {
+      const int32_t jb = seg[f], je = seg[f + 1];
+      const int sz = a.fs[f];
+      if (sz == 4) row_family<12>(acc, lane, win, wlen, a.hp.p[f], a.rs_idx, a.rs_dst, jb, je);
+      else if (sz == 3) row_family<9>(acc, lane, win, wlen, a.hp.p[f], a.rs_idx, a.rs_dst, jb, je);
+      else row_family<6>(acc, lane, win, wlen, a.hp.p[f], a.rs_idx, a.rs_dst, jb, je);
     }
     for (int t = lane; t < 9 * wlen; t += 32) out[9 * win + t] = acc[t];
     __syncwarp();
@@ -510,7 +507,7 @@ extern "C" int b200ipc_assembly_destroy(b200ipc_assembly* h) {
   if (!h) return 0;
   h->fixed.release(); h->keys_a.release(); h->keys_b.release(); h->slot_a.release(); h->slot_b.release();
   h->head.release(); h->useg.release(); h->desc.release(); h->rowptr.release(); h->colidx.release();
-  h->gkeys_a.release(); h->gkeys_b.release(); h->gslot_a.release(); h->gslot_b.release(); h->gseg.release(); h->rs_desc.release(); h->rs_dst.release();
+  h->gkeys_a.release(); h->gkeys_b.release(); h->gslot_a.release(); h->gslot_b.release(); h->gseg.release(); h->rs_idx.release(); h->rs_dst.release(); h->rseg.release();
   h->temp.release(); h->scalars.release();
   delete h;
   return 0;
@@ -618,12 +615,16 @@ extern "C" int b200ipc_assemble_symbolic(b200ipc_assembly* h, int64_t nverts, co
   }
   lower_bound_kernel<<<blocks_for(nverts + 1), kAT, 0, st>>>(nverts, ng, h->gkeys_b.ptr, h->gseg.ptr);
   RC(post_launch());
+  CK(h->rseg.reserve((size_t)nverts * (nfam + 1)));
   if (ng > 0) {
-    CK(h->rs_desc.reserve(ng)); CK(h->rs_dst.reserve(ng));
+    CK(h->rs_idx.reserve(ng)); CK(h->rs_dst.reserve(4 * ng));
     row_source_kernel<<<blocks_for(ng), kAT, 0, st>>>(fd, nverts, ng, h->gslot_b.ptr, h->fixed.ptr, h->rowptr.ptr,
-                                                     h->colidx.ptr, h->rs_desc.ptr, h->rs_dst.ptr);
+                                                     h->colidx.ptr, h->rs_idx.ptr, h->rs_dst.ptr);
     RC(post_launch());
   }
+  row_family_split_kernel<<<blocks_for(nverts * (nfam + 1)), kAT, 0, st>>>(fd, nverts, h->gseg.ptr, h->gslot_b.ptr,
+                                                                          h->rseg.ptr);
+  RC(post_launch());
   h->ready = true;
   if (nnzb_out) *nnzb_out = h->nnzb;
   return 0;
@@ -658,9 +659,10 @@ extern "C" int b200ipc_assemble_numeric(b200ipc_assembly* h, const double* masse
   }
   RowArgs r;
   r.hp = a.hp;
-  for (int f = 0; f <= kMaxFam; ++f) r.fs[f] = f < h->fam.nfam ? h->fam.s[f] : 0;
+  for (int f = 0; f < kMaxFam; ++f) r.fs[f] = f < h->fam.nfam ? h->fam.s[f] : 0;
+  r.nfam = h->fam.nfam;
   r.nverts = h->nverts; r.fixed = h->fixed.ptr; r.masses = masses; r.rowptr = h->rowptr.ptr; r.colidx = h->colidx.ptr;
-  r.gseg = h->gseg.ptr; r.rs_desc = h->rs_desc.ptr; r.rs_dst = h->rs_dst.ptr; r.vals = vals;
+  r.rseg = h->rseg.ptr; r.rs_idx = h->rs_idx.ptr; r.rs_dst = h->rs_dst.ptr; r.vals = vals;
   const unsigned grid = (unsigned)((h->nverts + kRowWarps - 1) / kRowWarps);
   assemble_rows_kernel<<<grid, 32 * kRowWarps, 0, (cudaStream_t)stream>>>(r);
   return post_launch();
