@@ -329,49 +329,81 @@ struct RowArgs {
 };
 
 constexpr int kRowWarps = 8;
-constexpr int kRowWin = 64;   // blocks of one row accumulated per pass in shared memory
+constexpr int kRowWin = 64;       // blocks of one row accumulated per pass in shared memory
+constexpr int kRingGroup = 4;     // row-sources per cp.async group
+constexpr int kRingGroups = 3;    // groups in flight per warp (2 in flight while 1 is consumed)
+constexpr int kRingSlot = 37;     // doubles per slot: 36 run values + 4 x u16 destinations
+constexpr int kRowSmemPerWarp = kRowWin * 9 + kRingGroup * kRingGroups * kRingSlot;  // doubles
 
-// All row-sources of one family inside one row: runs of N = 9s doubles, element t of a run belongs
-// to sub-block c = (t % D) / 3, entry k = 3*(t / D) + t % 3 -- lane constants.  Software pipeline:
-// indices are loaded two sources ahead, the dense run one source ahead of the ordered adds.
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int NLEFT>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(NLEFT));
+}
+
+// All row-sources of one family inside one row: runs of N = 9s doubles; element t of a run belongs
+// to sub-block c = (t % D) / 3, entry k = 3*(t / D) + t % 3 -- lane constants.  The runs are staged
+// through a per-warp shared-memory ring with cp.async (LDGSTS): twelve slots in three groups keep
+// ~2.3 KB of contiguous dense-block reads in flight per warp without holding registers, which is
+// what an HBM-latency-bound gather needs; the adds then run in list order out of shared memory.
 template <int D>
-__device__ __forceinline__ void row_family(double* acc, int lane, int win, int wlen, const double* __restrict__ base,
-                                           const uint32_t* __restrict__ rs_idx, const uint16_t* __restrict__ rs_dst,
-                                           int32_t jb, int32_t je) {
+__device__ __forceinline__ void row_family(double* acc, double* ring, int lane, int win, int wlen,
+                                           const double* __restrict__ base, const uint32_t* __restrict__ rs_idx,
+                                           const uint16_t* __restrict__ rs_dst, int32_t jb, int32_t je) {
   constexpr int N = 3 * D;
+  constexpr int G = kRingGroup, NG = kRingGroups;
   const bool on0 = lane < N, on1 = lane + 32 < N;
   const int t0 = on0 ? lane : 0, t1 = on1 ? lane + 32 : 0;
   const int c0 = (t0 % D) / 3, k0 = 3 * (t0 / D) + t0 % 3;
   const int c1 = (t1 % D) / 3, k1 = 3 * (t1 / D) + t1 % 3;
   if (jb >= je) return;
-  // stage 2 (indices) for jb and jb+1, stage 1 (values) for jb
-  uint32_t idxN = rs_idx[jb];
-  unsigned relN0 = rs_dst[4 * jb + c0], relN1 = N > 32 ? rs_dst[4 * jb + c1] : 0xffffu;
-  const double* p = base + (int64_t)N * idxN;
-  double v0 = on0 ? __ldg(p + t0) : 0.0, v1 = on1 ? __ldg(p + t1) : 0.0;
-  unsigned rel0 = relN0, rel1 = relN1;
-  const int32_t j1 = jb + 1 < je ? jb + 1 : jb;
-  idxN = rs_idx[j1];
-  relN0 = rs_dst[4 * j1 + c0];
-  relN1 = N > 32 ? rs_dst[4 * j1 + c1] : 0xffffu;
-  for (int32_t j = jb; j < je; ++j) {
-    // issue: indices of j+2, values of j+1
-    const int32_t j2 = j + 2 < je ? j + 2 : je - 1;
-    const uint32_t idxF = rs_idx[j2];
-    const unsigned relF0 = rs_dst[4 * j2 + c0], relF1 = N > 32 ? rs_dst[4 * j2 + c1] : 0xffffu;
-    const double* pn = base + (int64_t)N * idxN;
-    const double n0 = on0 ? __ldg(pn + t0) : 0.0, n1 = on1 ? __ldg(pn + t1) : 0.0;
-    // ordered adds of source j
-    const unsigned a0 = rel0 - (unsigned)win;
-    if (on0 && a0 < (unsigned)wlen) acc[a0 * 9 + k0] += v0;
-    if (N > 32) {
-      const unsigned a1 = rel1 - (unsigned)win;
-      if (on1 && a1 < (unsigned)wlen) acc[a1 * 9 + k1] += v1;
+  const int ngroups = (je - jb + G - 1) / G;
+
+  auto issue = [&](int gi) {
+    if (gi < ngroups) {
+#pragma unroll
+      for (int u = 0; u < G; ++u) {
+        const int32_t j = jb + gi * G + u;
+        if (j < je) {
+          double* slot = ring + ((gi % NG) * G + u) * kRingSlot;
+          const double* p = base + (int64_t)N * rs_idx[j];
+          if (on0) cp_async8(slot + t0, p + t0);
+          if (on1) cp_async8(slot + t1, p + t1);
+          if (lane == 0) cp_async8(slot + 36, rs_dst + 4 * (int64_t)j);
+        }
+      }
     }
-    __syncwarp();
-    v0 = n0; v1 = n1; rel0 = relN0; rel1 = relN1;
-    idxN = idxF; relN0 = relF0; relN1 = relF1;
+    cp_async_commit();  // empty groups keep the group count uniform
+  };
+
+#pragma unroll
+  for (int gi = 0; gi < NG; ++gi) issue(gi);
+  for (int gi = 0; gi < ngroups; ++gi) {
+    cp_async_wait<NG - 1>();  // this lane's copies of the oldest group have landed ...
+    __syncwarp();             // ... and so have every other lane's
+#pragma unroll
+    for (int u = 0; u < G; ++u) {
+      const int32_t j = jb + gi * G + u;
+      if (j < je) {
+        const double* slot = ring + ((gi % NG) * G + u) * kRingSlot;
+        const uint16_t* dst = reinterpret_cast<const uint16_t*>(slot + 36);
+        const unsigned a0 = (unsigned)dst[c0] - (unsigned)win;
+        if (on0 && a0 < (unsigned)wlen) acc[a0 * 9 + k0] += slot[t0];
+        if (N > 32) {
+          const unsigned a1 = (unsigned)dst[c1] - (unsigned)win;
+          if (on1 && a1 < (unsigned)wlen) acc[a1 * 9 + k1] += slot[t1];
+        }
+      }
+      __syncwarp();  // adds of one source finish before the next source touches the same entries
+    }
+    issue(gi + NG);  // refill the ring slots just consumed
   }
+  cp_async_wait<0>();
+  __syncwarp();
 }
 
 // One warp per block-row.  Every row-source is read as one contiguous run (full sectors; each dense
@@ -379,11 +411,12 @@ __device__ __forceinline__ void row_family(double* acc, int lane, int win, int w
 // accumulators in shared memory in list order -- no atomics, bitwise reproducible.  The finished
 // row (72 bytes per block, contiguous) is written with consecutive lanes on consecutive doubles.
 __global__ void __launch_bounds__(32 * kRowWarps) assemble_rows_kernel(const RowArgs a) {
-  __shared__ double sm[kRowWarps][kRowWin * 9];
+  extern __shared__ double sm_rows[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * kRowWarps + w;
   if (row >= a.nverts) return;
-  double* acc = sm[w];
+  double* acc = sm_rows + w * kRowSmemPerWarp;
+  double* ring = acc + kRowWin * 9;
   const int32_t r0 = a.rowptr[row], len = a.rowptr[row + 1] - r0;
   double* out = a.vals + 9ll * r0;
   if (a.fixed[row]) {  // Dirichlet row: identity diagonal only
@@ -410,9 +443,9 @@ __global__ void __launch_bounds__(32 * kRowWarps) assemble_rows_kernel(const Row
     for (int f = 0; f < a.nfam; ++f) {
       const int32_t jb = seg[f], je = seg[f + 1];
       const int sz = a.fs[f];
-      if (sz == 4) row_family<12>(acc, lane, win, wlen, a.hp.p[f], a.rs_idx, a.rs_dst, jb, je);
-      else if (sz == 3) row_family<9>(acc, lane, win, wlen, a.hp.p[f], a.rs_idx, a.rs_dst, jb, je);
-      else row_family<6>(acc, lane, win, wlen, a.hp.p[f], a.rs_idx, a.rs_dst, jb, je);
+      if (sz == 4) row_family<12>(acc, ring, lane, win, wlen, a.hp.p[f], a.rs_idx, a.rs_dst, jb, je);
+      else if (sz == 3) row_family<9>(acc, ring, lane, win, wlen, a.hp.p[f], a.rs_idx, a.rs_dst, jb, je);
+      else row_family<6>(acc, ring, lane, win, wlen, a.hp.p[f], a.rs_idx, a.rs_dst, jb, je);
     }
     for (int t = lane; t < 9 * wlen; t += 32) out[9 * win + t] = acc[t];
     __syncwarp();
@@ -664,7 +697,13 @@ extern "C" int b200ipc_assemble_numeric(b200ipc_assembly* h, const double* masse
   r.nverts = h->nverts; r.fixed = h->fixed.ptr; r.masses = masses; r.rowptr = h->rowptr.ptr; r.colidx = h->colidx.ptr;
   r.rseg = h->rseg.ptr; r.rs_idx = h->rs_idx.ptr; r.rs_dst = h->rs_dst.ptr; r.vals = vals;
   const unsigned grid = (unsigned)((h->nverts + kRowWarps - 1) / kRowWarps);
-  assemble_rows_kernel<<<grid, 32 * kRowWarps, 0, (cudaStream_t)stream>>>(r);
+  constexpr size_t smem = (size_t)kRowWarps * kRowSmemPerWarp * sizeof(double);
+  static bool smem_set = false;
+  if (!smem_set) {
+    CK(cudaFuncSetAttribute(assemble_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    smem_set = true;
+  }
+  assemble_rows_kernel<<<grid, 32 * kRowWarps, smem, (cudaStream_t)stream>>>(r);
   return post_launch();
 }
 
