@@ -75,9 +75,7 @@ struct b200ipc_assembly {
   b200ipc::DevBuf<int32_t> rowptr, colidx;
   b200ipc::DevBuf<uint32_t> gkeys_a, gkeys_b, gslot_a, gslot_b;
   b200ipc::DevBuf<int32_t> gseg;              // (N+1) run starts per vertex
-  b200ipc::DevBuf<uint32_t> rs_idx;           // per row-source: b*s + a inside its family (run = 9s doubles at 9s*idx)
-  b200ipc::DevBuf<uint16_t> rs_dst;           // per row-source x 4: destination block inside the row (0xffff = dropped)
-  b200ipc::DevBuf<int32_t> rseg;              // (N, nfam+1): row-source range of each family inside each row
+  b200ipc::DevBuf<uint64_t> rs_desc, rs_dst;  // per row-source: chunk offset|family, 4 x u16 destination block
   b200ipc::DevBuf<uint8_t> temp;
   b200ipc::DevBuf<int64_t> scalars;           // device scratch for counts
 };
@@ -168,8 +166,6 @@ __global__ void finish_pattern_kernel(int64_t nverts, int64_t nnzb, int64_t nval
 
 // Source descriptors, written once per pattern in sorted order: the numeric phase then needs no
 // integer division and no family search per source.
-//   block source : (element offset of the 3x3 sub-block << 16) | (row length D << 8) | family
-//   mass slot    : (vertex << 16) | 0xff      (always the first source of a diagonal block's run)
 __global__ void __launch_bounds__(kAT) source_desc_kernel(FamDesc fd, int64_t nverts, int64_t nvalid,
                                                           const uint32_t* __restrict__ perm,
                                                           uint64_t* __restrict__ desc) {
@@ -177,18 +173,19 @@ __global__ void __launch_bounds__(kAT) source_desc_kernel(FamDesc fd, int64_t nv
   if (j >= nvalid) return;
   const int64_t slot = perm[j];
   if (slot < nverts) {
-    desc[j] = ((uint64_t)slot << 16) | 0xffull;
+    desc[j] = ((uint64_t)slot << 3) | 7ull;
   } else {
     int f, a, c;
     int64_t b;
     decode_slot(fd, slot - nverts, f, b, a, c);
     const int64_t D = 3 * fd.s[f];
-    desc[j] = ((uint64_t)((b * D + 3 * a) * D + 3 * c) << 16) | ((uint64_t)D << 8) | (uint64_t)f;
+    desc[j] = ((uint64_t)((b * D + 3 * a) * D + 3 * c) << 3) | (uint64_t)f;
   }
 }
 
 struct NumericArgs {
   HessPtrs hp;
+  int32_t ld[kMaxFam];   // row length 3s of each family
   int64_t nnzb;
   const uint8_t* fixed;
   const double* masses;
@@ -199,65 +196,63 @@ struct NumericArgs {
 
 constexpr int kNumWarps = 8;
 
+__device__ __forceinline__ double source_value(const NumericArgs& a, uint64_t d, int er, int ec, bool& identity) {
+  const int f = (int)(d & 7ull);
+  const int64_t off = (int64_t)(d >> 3);
+  if (f == 7) {  // diagonal mass slot; a fixed vertex keeps a unit diagonal instead
+    if (a.fixed[off]) {
+      identity = true;
+      return 0.0;
+    }
+    return er == ec ? a.masses[off] : 0.0;
+  }
+  return __ldg(a.hp.p[f] + off + er * a.ld[f] + ec);
+}
+
 // One warp per output block: lanes (g, e) = (lane / 9, lane % 9), g < 3, walk the block's run of
-// sources three at a time, entry e of each 3x3 sub-block per lane, four trips (twelve sub-blocks)
-// of loads in flight before the adds; the three partial sums are combined in fixed order with two
-// shuffles.  Lanes 0..8 write the block: nine consecutive doubles.
+// sources three at a time (two iterations in flight), entry e of each 3x3 sub-block per lane; the
+// three partial sums are combined in fixed order with two shuffles.  Lanes 0..8 write the block:
+// nine consecutive doubles per warp, 72-byte rows back to back across the CTA's warps.
 __global__ void __launch_bounds__(32 * kNumWarps) assemble_numeric_kernel(const NumericArgs a) {
-  __shared__ const double* fam_base[kMaxFam + 1];  // dynamic family lookup without a local-memory copy
-  if (threadIdx.x <= kMaxFam) fam_base[threadIdx.x] = a.hp.p[threadIdx.x];
-  __syncthreads();
   const int64_t u = (int64_t)blockIdx.x * kNumWarps + (threadIdx.x >> 5);
   if (u >= a.nnzb) return;
   const int lane = threadIdx.x & 31;
   const int g = lane / 9, e = lane - 9 * g;
   const int er = e / 3, ec = e - 3 * er;
-  int32_t j0 = a.useg[u];
-  const int32_t j1 = a.useg[u + 1];
+  const int32_t j0 = a.useg[u], j1 = a.useg[u + 1];
   double acc = 0.0;
-  const uint64_t first = a.desc[j0];
-  if ((first & 0xff) == 0xff) {  // diagonal block: mass slot first
-    const int64_t v = (int64_t)(first >> 16);
-    if (a.fixed[v]) {  // Dirichlet vertex: unit diagonal, nothing else
-      if (lane < 9) a.vals[9 * u + lane] = er == ec ? 1.0 : 0.0;
-      return;
-    }
-    if (g == 0 && er == ec) acc = a.masses[v];
-    ++j0;
-  }
+  bool identity = false;
   if (g < 3) {
-    for (int32_t j = j0 + g; j < j1; j += 12) {
-      uint64_t d[4];
-      double v[4];
-#pragma unroll
-      for (int t = 0; t < 4; ++t) d[t] = j + 3 * t < j1 ? a.desc[j + 3 * t] : ~0ull;
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int D = (int)(d[t] >> 8) & 0xff;
-        const double* p = fam_base[d[t] & 7] + (d[t] >> 16) + er * D + ec;
-        v[t] = d[t] != ~0ull ? __ldg(p) : 0.0;
-      }
-#pragma unroll
-      for (int t = 0; t < 4; ++t) acc += v[t];
+    int32_t j = j0 + g;
+    for (; j + 3 < j1; j += 6) {
+      const uint64_t d0 = a.desc[j], d1 = a.desc[j + 3];
+      const double v0 = source_value(a, d0, er, ec, identity);
+      const double v1 = source_value(a, d1, er, ec, identity);
+      acc += v0;
+      acc += v1;
     }
+    if (j < j1) acc += source_value(a, a.desc[j], er, ec, identity);
   }
   const double s1 = __shfl_down_sync(0xffffffffu, acc, 9);   // group 1's partial sum (lanes 0..8)
   const double s2 = __shfl_down_sync(0xffffffffu, acc, 18);  // group 2's
-  if (lane < 9) a.vals[9 * u + lane] = (acc + s1) + s2;
+  const bool any_identity = __any_sync(0xffffffffu, identity);
+  if (lane < 9) {
+    const double total = (acc + s1) + s2;
+    a.vals[9 * u + lane] = any_identity ? (er == ec ? 1.0 : 0.0) : total;
+  }
 }
 
 // ---- row-wise numeric assembly ------------------------------------------------------------------
 // A "row-source" is (block b of family f, local vertex a): rows 3a..3a+2 of the dense block are ONE
-// contiguous run of 9s doubles at element offset 9s*(b*s+a).  For output block-row i the row-sources
-// are vertex i's incidences in list order (the gradient runs), family-major.  Per row-source the
-// symbolic phase stores idx = b*s+a and, for each local column c, the index of vertex v_c inside
-// row i's block list (0xffff = dropped: fixed row or fixed column).
+// contiguous run of 3*D doubles.  For output block-row i the row-sources are the gradient runs
+// (vertex i's incidences in list order).  rs_desc = (element offset of the run << 3) | family,
+// rs_dst = four u16: index of column vertex v_c inside row i's block list (0xffff = dropped).
 __global__ void __launch_bounds__(kAT) row_source_kernel(FamDesc fd, int64_t nverts, int64_t ng,
                                                          const uint32_t* __restrict__ gperm,
                                                          const uint8_t* __restrict__ fixed,
                                                          const int32_t* __restrict__ rowptr,
                                                          const int32_t* __restrict__ colidx,
-                                                         uint32_t* __restrict__ rs_idx, uint16_t* __restrict__ rs_dst) {
+                                                         uint64_t* __restrict__ rs_desc, uint64_t* __restrict__ rs_dst) {
   const int64_t j = (int64_t)blockIdx.x * kAT + threadIdx.x;
   if (j >= ng) return;
   const int64_t q = gperm[j];
@@ -269,12 +264,14 @@ __global__ void __launch_bounds__(kAT) row_source_kernel(FamDesc fd, int64_t nve
   const int64_t r = q - fd.vert_off[f];
   const int64_t b = r / s;
   const int a = (int)(r - b * s);
+  const int64_t D = 3 * s;
   const int64_t* v = fd.vids[f] + b * s;
   const int64_t row = v[a];
-  rs_idx[j] = (uint32_t)r;
+  rs_desc[j] = ((uint64_t)((b * D + 3 * a) * D) << 3) | (uint64_t)f;
+  uint64_t dst = 0;
   const int32_t r0 = rowptr[row], r1 = rowptr[row + 1];
   for (int c = 0; c < 4; ++c) {
-    uint16_t rel = 0xffff;
+    uint64_t rel = 0xffffull;
     if (c < s && !fixed[row]) {
       const int64_t col = v[c];
       if (col == row || !fixed[col]) {
@@ -284,141 +281,72 @@ __global__ void __launch_bounds__(kAT) row_source_kernel(FamDesc fd, int64_t nve
           if (colidx[mid] < col) lo = mid + 1;
           else hi = mid;
         }
-        rel = (uint16_t)(lo - r0);
+        rel = (uint64_t)(lo - r0);
       }
     }
-    rs_dst[4 * j + c] = rel;
+    dst |= rel << (16 * c);
   }
-}
-
-// rseg[row*(nfam+1) + f] = first row-source of family >= f inside row's run (slots ascend family-major)
-__global__ void __launch_bounds__(kAT) row_family_split_kernel(FamDesc fd, int64_t nverts,
-                                                               const int32_t* __restrict__ gseg,
-                                                               const uint32_t* __restrict__ gperm,
-                                                               int32_t* __restrict__ rseg) {
-  const int64_t t = (int64_t)blockIdx.x * kAT + threadIdx.x;
-  const int nf1 = fd.nfam + 1;
-  if (t >= nverts * nf1) return;
-  const int64_t row = t / nf1;
-  const int f = (int)(t - row * nf1);
-  int32_t lo = gseg[row], hi = gseg[row + 1];
-  if (f == fd.nfam) {
-    rseg[t] = hi;
-    return;
-  }
-  const int64_t first_slot = fd.vert_off[f];
-  while (lo < hi) {
-    const int32_t mid = (lo + hi) >> 1;
-    if ((int64_t)gperm[mid] < first_slot) lo = mid + 1;
-    else hi = mid;
-  }
-  rseg[t] = lo;
+  rs_dst[j] = dst;
 }
 
 struct RowArgs {
   HessPtrs hp;
-  int32_t fs[kMaxFam];   // stencil size s per family
-  int32_t nfam;
+  int32_t fs[kMaxFam + 1];   // stencil size s per family; fs[7] = 0 tags an absent source
   int64_t nverts;
   const uint8_t* fixed;
   const double* masses;
   const int32_t* rowptr;
   const int32_t* colidx;
-  const int32_t* rseg;
-  const uint32_t* rs_idx;
-  const uint16_t* rs_dst;
+  const int32_t* gseg;
+  const uint64_t* rs_desc;
+  const uint64_t* rs_dst;
   double* vals;
 };
 
 constexpr int kRowWarps = 8;
-constexpr int kRowWin = 64;       // blocks of one row accumulated per pass in shared memory
-constexpr int kRingGroup = 4;     // row-sources per cp.async group
-constexpr int kRingGroups = 3;    // groups in flight per warp (2 in flight while 1 is consumed)
-constexpr int kRingSlot = 37;     // doubles per slot: 36 run values + 4 x u16 destinations
-constexpr int kRowSmemPerWarp = kRowWin * 9 + kRingGroup * kRingGroups * kRingSlot;  // doubles
+constexpr int kRowWin = 64;   // blocks of one row accumulated per pass in shared memory
 
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int NLEFT>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(NLEFT));
-}
-
-// All row-sources of one family inside one row: runs of N = 9s doubles; element t of a run belongs
-// to sub-block c = (t % D) / 3, entry k = 3*(t / D) + t % 3 -- lane constants.  The runs are staged
-// through a per-warp shared-memory ring with cp.async (LDGSTS): twelve slots in three groups keep
-// ~2.3 KB of contiguous dense-block reads in flight per warp without holding registers, which is
-// what an HBM-latency-bound gather needs; the adds then run in list order out of shared memory.
+// Per-lane constants of the element -> (sub-block, entry) map of a run of 3*D doubles.
 template <int D>
-__device__ __forceinline__ void row_family(double* acc, double* ring, int lane, int win, int wlen,
-                                           const double* __restrict__ base, const uint32_t* __restrict__ rs_idx,
-                                           const uint16_t* __restrict__ rs_dst, int32_t jb, int32_t je) {
-  constexpr int N = 3 * D;
-  constexpr int G = kRingGroup, NG = kRingGroups;
-  const bool on0 = lane < N, on1 = lane + 32 < N;
-  const int t0 = on0 ? lane : 0, t1 = on1 ? lane + 32 : 0;
-  const int c0 = (t0 % D) / 3, k0 = 3 * (t0 / D) + t0 % 3;
-  const int c1 = (t1 % D) / 3, k1 = 3 * (t1 / D) + t1 % 3;
-  if (jb >= je) return;
-  const int ngroups = (je - jb + G - 1) / G;
-
-  auto issue = [&](int gi) {
-    if (gi < ngroups) {
-#pragma unroll
-      for (int u = 0; u < G; ++u) {
-        const int32_t j = jb + gi * G + u;
-        if (j < je) {
-          double* slot = ring + ((gi % NG) * G + u) * kRingSlot;
-          const double* p = base + (int64_t)N * rs_idx[j];
-          if (on0) cp_async8(slot + t0, p + t0);
-          if (on1) cp_async8(slot + t1, p + t1);
-          if (lane == 0) cp_async8(slot + 36, rs_dst + 4 * (int64_t)j);
-        }
-      }
-    }
-    cp_async_commit();  // empty groups keep the group count uniform
-  };
-
-#pragma unroll
-  for (int gi = 0; gi < NG; ++gi) issue(gi);
-  for (int gi = 0; gi < ngroups; ++gi) {
-    cp_async_wait<NG - 1>();  // this lane's copies of the oldest group have landed ...
-    __syncwarp();             // ... and so have every other lane's
-#pragma unroll
-    for (int u = 0; u < G; ++u) {
-      const int32_t j = jb + gi * G + u;
-      if (j < je) {
-        const double* slot = ring + ((gi % NG) * G + u) * kRingSlot;
-        const uint16_t* dst = reinterpret_cast<const uint16_t*>(slot + 36);
-        const unsigned a0 = (unsigned)dst[c0] - (unsigned)win;
-        if (on0 && a0 < (unsigned)wlen) acc[a0 * 9 + k0] += slot[t0];
-        if (N > 32) {
-          const unsigned a1 = (unsigned)dst[c1] - (unsigned)win;
-          if (on1 && a1 < (unsigned)wlen) acc[a1 * 9 + k1] += slot[t1];
-        }
-      }
-      __syncwarp();  // adds of one source finish before the next source touches the same entries
-    }
-    issue(gi + NG);  // refill the ring slots just consumed
+struct LaneMap {
+  int k0, sh0, k1, sh1;  // entry index er*3+ec and shift 16*c for elements lane and lane+32
+  __device__ __forceinline__ explicit LaneMap(int lane) {
+    const int t0 = lane < 3 * D ? lane : 0;
+    const int er0 = t0 / D, cc0 = t0 - er0 * D;
+    k0 = er0 * 3 + cc0 % 3;
+    sh0 = 16 * (cc0 / 3);
+    const int t1 = lane + 32 < 3 * D ? lane + 32 : 0;
+    const int er1 = t1 / D, cc1 = t1 - er1 * D;
+    k1 = er1 * 3 + cc1 % 3;
+    sh1 = 16 * (cc1 / 3);
   }
-  cp_async_wait<0>();
-  __syncwarp();
+};
+
+template <int D>
+__device__ __forceinline__ void row_add(double* acc, const LaneMap<D>& m, int lane, uint64_t dst, int win, int wlen,
+                                        double v0, double v1) {
+  if (lane < 3 * D) {
+    const unsigned rel = (unsigned)((dst >> m.sh0) & 0xffff) - (unsigned)win;
+    if (rel < (unsigned)wlen) acc[rel * 9 + m.k0] += v0;
+  }
+  if (3 * D > 32) {
+    if (lane + 32 < 3 * D) {
+      const unsigned rel = (unsigned)((dst >> m.sh1) & 0xffff) - (unsigned)win;
+      if (rel < (unsigned)wlen) acc[rel * 9 + m.k1] += v1;
+    }
+  }
 }
 
-// One warp per block-row.  Every row-source is read as one contiguous run (full sectors; each dense
+// One warp per block-row.  Every row-source is read as one contiguous run (full sectors, each dense
 // block is read exactly once over the whole kernel) and its s sub-blocks are added into the row's
 // accumulators in shared memory in list order -- no atomics, bitwise reproducible.  The finished
 // row (72 bytes per block, contiguous) is written with consecutive lanes on consecutive doubles.
 __global__ void __launch_bounds__(32 * kRowWarps) assemble_rows_kernel(const RowArgs a) {
-  extern __shared__ double sm_rows[];
+  __shared__ double sm[kRowWarps][kRowWin * 9];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * kRowWarps + w;
   if (row >= a.nverts) return;
-  double* acc = sm_rows + w * kRowSmemPerWarp;
-  double* ring = acc + kRowWin * 9;
+  double* acc = sm[w];
   const int32_t r0 = a.rowptr[row], len = a.rowptr[row + 1] - r0;
   double* out = a.vals + 9ll * r0;
   if (a.fixed[row]) {  // Dirichlet row: identity diagonal only
@@ -434,7 +362,10 @@ __global__ void __launch_bounds__(32 * kRowWarps) assemble_rows_kernel(const Row
   }
   const int drel = lo;
   const double mass = a.masses[row];
-  const int32_t* seg = a.rseg + row * (a.nfam + 1);
+  const int32_t j0 = a.gseg[row], j1 = a.gseg[row + 1];
+  const LaneMap<6> m6(lane);
+  const LaneMap<9> m9(lane);
+  const LaneMap<12> m12(lane);
 
   for (int win = 0; win < len; win += kRowWin) {
     const int wlen = min(kRowWin, len - win);
@@ -442,12 +373,49 @@ __global__ void __launch_bounds__(32 * kRowWarps) assemble_rows_kernel(const Row
     __syncwarp();
     if (lane < 3 && drel >= win && drel < win + wlen) acc[(drel - win) * 9 + 4 * lane] = mass;
     __syncwarp();
-    for (int f = 0; f < a.nfam; ++f) {
-      const int32_t jb = seg[f], je = seg[f + 1];
-      const int sz = a.fs[f];
-      if (sz == 4) row_family<12>(acc, ring, lane, win, wlen, a.hp.p[f], a.rs_idx, a.rs_dst, jb, je);
-      else if (sz == 3) row_family<9>(acc, ring, lane, win, wlen, a.hp.p[f], a.rs_idx, a.rs_dst, jb, je);
-      else row_family<6>(acc, ring, lane, win, wlen, a.hp.p[f], a.rs_idx, a.rs_dst, jb, je);
+    // Software pipeline over pairs of row-sources: descriptors are loaded two pairs ahead and the
+    // dense runs one pair ahead of the accumulation, so neither memory latency sits on the
+    // critical path of the (ordered) shared-memory adds.
+    auto load_desc = [&](int32_t j, uint64_t& d, uint64_t& m) {
+      const bool ok = j < j1;
+      d = ok ? a.rs_desc[j] : 7ull;
+      m = ok ? a.rs_dst[j] : ~0ull;
+    };
+    auto fetch = [&](uint64_t d, int& sz, double& v0, double& v1) {
+      sz = a.fs[d & 7];
+      const double* p = a.hp.p[d & 7] + (d >> 3);
+      v0 = lane < 9 * sz ? __ldg(p + lane) : 0.0;
+      v1 = lane + 32 < 9 * sz ? __ldg(p + lane + 32) : 0.0;
+    };
+    auto add = [&](int sz, uint64_t m, double v0, double v1) {
+      if (sz == 4) row_add<12>(acc, m12, lane, m, win, wlen, v0, v1);
+      else if (sz == 3) row_add<9>(acc, m9, lane, m, win, wlen, v0, v1);
+      else if (sz == 2) row_add<6>(acc, m6, lane, m, win, wlen, v0, v1);
+    };
+    uint64_t dA, mA, dB, mB, ndA, nmA, ndB, nmB;
+    load_desc(j0, dA, mA);
+    load_desc(j0 + 1, dB, mB);
+    load_desc(j0 + 2, ndA, nmA);
+    load_desc(j0 + 3, ndB, nmB);
+    int sA, sB;
+    double vA0, vA1, vB0, vB1;
+    fetch(dA, sA, vA0, vA1);
+    fetch(dB, sB, vB0, vB1);
+    for (int32_t j = j0; j < j1; j += 2) {
+      uint64_t fdA, fmA, fdB, fmB;  // two pairs ahead
+      load_desc(j + 4, fdA, fmA);
+      load_desc(j + 5, fdB, fmB);
+      int nsA, nsB;                 // one pair ahead
+      double nA0, nA1, nB0, nB1;
+      fetch(ndA, nsA, nA0, nA1);
+      fetch(ndB, nsB, nB0, nB1);
+      add(sA, mA, vA0, vA1);
+      __syncwarp();
+      add(sB, mB, vB0, vB1);
+      __syncwarp();
+      sA = nsA; mA = nmA; vA0 = nA0; vA1 = nA1;
+      sB = nsB; mB = nmB; vB0 = nB0; vB1 = nB1;
+      ndA = fdA; nmA = fmA; ndB = fdB; nmB = fmB;
     }
     for (int t = lane; t < 9 * wlen; t += 32) out[9 * win + t] = acc[t];
     __syncwarp();
@@ -542,7 +510,7 @@ extern "C" int b200ipc_assembly_destroy(b200ipc_assembly* h) {
   if (!h) return 0;
   h->fixed.release(); h->keys_a.release(); h->keys_b.release(); h->slot_a.release(); h->slot_b.release();
   h->head.release(); h->useg.release(); h->desc.release(); h->rowptr.release(); h->colidx.release();
-  h->gkeys_a.release(); h->gkeys_b.release(); h->gslot_a.release(); h->gslot_b.release(); h->gseg.release(); h->rs_idx.release(); h->rs_dst.release(); h->rseg.release();
+  h->gkeys_a.release(); h->gkeys_b.release(); h->gslot_a.release(); h->gslot_b.release(); h->gseg.release(); h->rs_desc.release(); h->rs_dst.release();
   h->temp.release(); h->scalars.release();
   delete h;
   return 0;
@@ -650,16 +618,12 @@ extern "C" int b200ipc_assemble_symbolic(b200ipc_assembly* h, int64_t nverts, co
   }
   lower_bound_kernel<<<blocks_for(nverts + 1), kAT, 0, st>>>(nverts, ng, h->gkeys_b.ptr, h->gseg.ptr);
   RC(post_launch());
-  CK(h->rseg.reserve((size_t)nverts * (nfam + 1)));
   if (ng > 0) {
-    CK(h->rs_idx.reserve(ng)); CK(h->rs_dst.reserve(4 * ng));
+    CK(h->rs_desc.reserve(ng)); CK(h->rs_dst.reserve(ng));
     row_source_kernel<<<blocks_for(ng), kAT, 0, st>>>(fd, nverts, ng, h->gslot_b.ptr, h->fixed.ptr, h->rowptr.ptr,
-                                                     h->colidx.ptr, h->rs_idx.ptr, h->rs_dst.ptr);
+                                                     h->colidx.ptr, h->rs_desc.ptr, h->rs_dst.ptr);
     RC(post_launch());
   }
-  row_family_split_kernel<<<blocks_for(nverts * (nfam + 1)), kAT, 0, st>>>(fd, nverts, h->gseg.ptr, h->gslot_b.ptr,
-                                                                          h->rseg.ptr);
-  RC(post_launch());
   h->ready = true;
   if (nnzb_out) *nnzb_out = h->nnzb;
   return 0;
@@ -678,10 +642,12 @@ extern "C" int b200ipc_assemble_numeric(b200ipc_assembly* h, const double* masse
   if (!h || !h->ready) return B200IPC_ESTATE;
   if (!masses || !vals || (h->fam.nfam && !fam_hess)) return B200IPC_EINVAL;
   NumericArgs a;
+  for (int f = 0; f < kMaxFam; ++f) a.ld[f] = 0;
   for (int f = 0; f <= kMaxFam; ++f) a.hp.p[f] = nullptr;
   for (int f = 0; f < h->fam.nfam; ++f) {
     if (h->fam.nb[f] && !fam_hess[f]) return B200IPC_EINVAL;
     a.hp.p[f] = fam_hess[f];
+    a.ld[f] = 3 * h->fam.s[f];
   }
   a.nnzb = h->nnzb; a.fixed = h->fixed.ptr; a.masses = masses;
   a.useg = h->useg.ptr; a.desc = h->desc.ptr; a.vals = vals;
@@ -692,18 +658,11 @@ extern "C" int b200ipc_assemble_numeric(b200ipc_assembly* h, const double* masse
   }
   RowArgs r;
   r.hp = a.hp;
-  for (int f = 0; f < kMaxFam; ++f) r.fs[f] = f < h->fam.nfam ? h->fam.s[f] : 0;
-  r.nfam = h->fam.nfam;
+  for (int f = 0; f <= kMaxFam; ++f) r.fs[f] = f < h->fam.nfam ? h->fam.s[f] : 0;
   r.nverts = h->nverts; r.fixed = h->fixed.ptr; r.masses = masses; r.rowptr = h->rowptr.ptr; r.colidx = h->colidx.ptr;
-  r.rseg = h->rseg.ptr; r.rs_idx = h->rs_idx.ptr; r.rs_dst = h->rs_dst.ptr; r.vals = vals;
+  r.gseg = h->gseg.ptr; r.rs_desc = h->rs_desc.ptr; r.rs_dst = h->rs_dst.ptr; r.vals = vals;
   const unsigned grid = (unsigned)((h->nverts + kRowWarps - 1) / kRowWarps);
-  constexpr size_t smem = (size_t)kRowWarps * kRowSmemPerWarp * sizeof(double);
-  static bool smem_set = false;
-  if (!smem_set) {
-    CK(cudaFuncSetAttribute(assemble_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    smem_set = true;
-  }
-  assemble_rows_kernel<<<grid, 32 * kRowWarps, smem, (cudaStream_t)stream>>>(r);
+  assemble_rows_kernel<<<grid, 32 * kRowWarps, 0, (cudaStream_t)stream>>>(r);
   return post_launch();
 }
 

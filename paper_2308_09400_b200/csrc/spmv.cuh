@@ -23,21 +23,19 @@ __device__ __forceinline__ void bsr_row_product_warp(int64_t row, int lane, cons
   const int32_t b0 = rowptr[row], nblk = rowptr[row + 1] - b0;
   const int g = lane / 9, e = lane - 9 * g;
   const int j = e % 3;
+  const double* v = vals + 9ll * b0 + e;
+  const int32_t* ci = colidx + b0;
   double acc = 0.0;
-  // Up to 32 blocks per chunk: the column indices are fetched with ONE coalesced load and handed
-  // to the owning lanes by shuffle, so the x gathers do not wait on a dependent index load and all
-  // value / x loads of the chunk are independent (three memory latencies per row in total).
-  for (int c0 = 0; c0 < nblk; c0 += 32) {
-    const int cn = min(32, nblk - c0);
-    const int mycol = lane < cn ? __ldg(colidx + b0 + c0 + lane) : 0;
-    const double* v = vals + 9ll * (b0 + c0) + e;
-    const int trips = (cn + 2) / 3;
-#pragma unroll 4
-    for (int t = 0; t < trips; ++t) {
-      const int blk = 3 * t + g;                       // g == 3 (lanes 27..31): idle
-      const int col = __shfl_sync(0xffffffffu, mycol, blk & 31);
-      if (g < 3 && blk < cn) acc += v[9 * blk] * __ldg(x + 3ll * col + j);
+  if (g < 3) {
+    int blk = g;
+    for (; blk + 3 < nblk; blk += 6) {
+      const int c0 = __ldg(ci + blk), c1 = __ldg(ci + blk + 3);
+      const double v0 = v[9 * blk], v1 = v[9 * (blk + 3)];
+      const double x0 = __ldg(x + 3ll * c0 + j), x1 = __ldg(x + 3ll * c1 + j);
+      acc += v0 * x0;
+      acc += v1 * x1;
     }
+    if (blk < nblk) acc += v[9 * blk] * __ldg(x + 3ll * __ldg(ci + blk) + j);
   }
   const double s1 = __shfl_down_sync(0xffffffffu, acc, 9);
   const double s2 = __shfl_down_sync(0xffffffffu, acc, 18);
