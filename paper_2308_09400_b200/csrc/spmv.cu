@@ -9,7 +9,7 @@ namespace b200ipc {
 constexpr int kST = 256;
 
 template <int LPR>
-__global__ void __launch_bounds__(kST) bsr_spmv_kernel(int64_t n, const int32_t* __restrict__ rowptr,
+__global__ void __launch_bounds__(kST, 8) bsr_spmv_kernel(int64_t n, const int32_t* __restrict__ rowptr,
                                                        const int32_t* __restrict__ colidx,
                                                        const double* __restrict__ vals, const double* __restrict__ x,
                                                        double* __restrict__ y) {
