@@ -177,10 +177,11 @@ def test_random_blocks_assembly_vs_oracle(S, n, nb):
     np.testing.assert_array_equal(colidx, o_colidx)
     assert rowptr[8] - rowptr[7] > 500
     assert block_rel_err(vals, o_vals) < 1e-12
-    # the per-block-run numeric kernel gives the same matrix
-    alt = S.solver._system_from_grouped(grouped, masses, fixed, variant=1)
-    assert block_rel_err(S.device.to_host(alt.vals), o_vals) < 1e-12
-    alt.close()
+    # the alternative numeric kernels give the same matrix
+    for variant in (1, 2, 3):
+        alt = S.solver._system_from_grouped(grouped, masses, fixed, variant=variant)
+        assert block_rel_err(S.device.to_host(alt.vals), o_vals) < 1e-12, variant
+        alt.close()
     x = rng.normal(size=3 * n)
     sysm = S.solver._system_from_grouped(grouped, masses, fixed)
     y = S.device.to_host(sysm.spmv(x))
