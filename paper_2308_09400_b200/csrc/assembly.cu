@@ -475,61 +475,40 @@ __device__ __forceinline__ void row_family_regs(double* acc, int lane, int win, 
   const int t0 = on0 ? lane : 0, t1 = on1 ? lane + 32 : 0;
   const int sh0 = 16 * ((t0 % D) / 3), k0 = 3 * (t0 / D) + t0 % 3;
   const int sh1 = 16 * ((t1 % D) / 3), k1 = 3 * (t1 / D) + t1 % 3;
-  if (jb >= je) return;
-  const int32_t jl = je - 1;
-  uint64_t offB[PF], dstA[PF], dstB[PF];
-  double va0[PF], va1[PF];
-#pragma unroll
-  for (int u = 0; u < PF; ++u) {
-    const int32_t j = min(jb + u, jl);
-    const double* p = base + (rs_desc[j] >> 3);
-    dstA[u] = rs_dst[j];
-    va0[u] = on0 ? __ldg(p + t0) : 0.0;
-    va1[u] = on1 ? __ldg(p + t1) : 0.0;
-  }
-#pragma unroll
-  for (int u = 0; u < PF; ++u) {
-    const int32_t j = min(jb + PF + u, jl);
-    offB[u] = rs_desc[j] >> 3;
-    dstB[u] = rs_dst[j];
-  }
+  // batches of PF sources, no cross-iteration state: descriptors, then the PF dense runs (all
+  // independent loads), then the ordered adds; other warps of the SM cover the two latencies
   for (int32_t j = jb; j < je; j += PF) {
-    uint64_t offC[PF], dstC[PF];
-    double vb0[PF], vb1[PF];
+    uint64_t off[PF], dst[PF];
+    double v0[PF], v1[PF];
 #pragma unroll
     for (int u = 0; u < PF; ++u) {
-      const int32_t jj = min(j + 2 * PF + u, jl);
-      offC[u] = rs_desc[jj] >> 3;
-      dstC[u] = rs_dst[jj];
+      const int32_t jj = min(j + u, je - 1);
+      off[u] = rs_desc[jj] >> 3;
+      dst[u] = rs_dst[jj];
     }
 #pragma unroll
     for (int u = 0; u < PF; ++u) {
-      const double* p = base + offB[u];
-      vb0[u] = on0 ? __ldg(p + t0) : 0.0;
-      vb1[u] = on1 ? __ldg(p + t1) : 0.0;
+      const double* p = base + off[u];
+      v0[u] = on0 ? __ldg(p + t0) : 0.0;
+      v1[u] = on1 ? __ldg(p + t1) : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < PF; ++u) {
       if (j + u < je) {
-        const unsigned a0 = (unsigned)((dstA[u] >> sh0) & 0xffff) - (unsigned)win;
-        if (on0 && a0 < (unsigned)wlen) acc[a0 * 9 + k0] += va0[u];
+        const unsigned a0 = (unsigned)((dst[u] >> sh0) & 0xffff) - (unsigned)win;
+        if (on0 && a0 < (unsigned)wlen) acc[a0 * 9 + k0] += v0[u];
         if (N > 32) {
-          const unsigned a1 = (unsigned)((dstA[u] >> sh1) & 0xffff) - (unsigned)win;
-          if (on1 && a1 < (unsigned)wlen) acc[a1 * 9 + k1] += va1[u];
+          const unsigned a1 = (unsigned)((dst[u] >> sh1) & 0xffff) - (unsigned)win;
+          if (on1 && a1 < (unsigned)wlen) acc[a1 * 9 + k1] += v1[u];
         }
       }
       __syncwarp();
-    }
-#pragma unroll
-    for (int u = 0; u < PF; ++u) {
-      va0[u] = vb0[u]; va1[u] = vb1[u]; dstA[u] = dstB[u];
-      offB[u] = offC[u]; dstB[u] = dstC[u];
     }
   }
 }
 
 template <int PF>
-__global__ void __launch_bounds__(32 * kRowWarps, PF <= 2 ? 4 : 2) assemble_rows_family_kernel(const RowFamArgs a) {
+__global__ void __launch_bounds__(32 * kRowWarps, 4) assemble_rows_family_kernel(const RowFamArgs a) {
   __shared__ double sm[kRowWarps][kRowWin * 9];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * kRowWarps + w;
@@ -819,8 +798,8 @@ extern "C" int b200ipc_assemble_numeric(b200ipc_assembly* h, const double* masse
     q.rowptr = h->rowptr.ptr; q.colidx = h->colidx.ptr; q.rseg = h->rseg.ptr; q.rs_desc = h->rs_desc.ptr;
     q.rs_dst = h->rs_dst.ptr; q.vals = vals;
     const unsigned grid = (unsigned)((h->nverts + kRowWarps - 1) / kRowWarps);
-    if (h->variant == 2) assemble_rows_family_kernel<2><<<grid, 32 * kRowWarps, 0, (cudaStream_t)stream>>>(q);
-    else assemble_rows_family_kernel<4><<<grid, 32 * kRowWarps, 0, (cudaStream_t)stream>>>(q);
+    if (h->variant == 2) assemble_rows_family_kernel<4><<<grid, 32 * kRowWarps, 0, (cudaStream_t)stream>>>(q);
+    else assemble_rows_family_kernel<8><<<grid, 32 * kRowWarps, 0, (cudaStream_t)stream>>>(q);
     return post_launch();
   }
   RowArgs r;
