@@ -507,8 +507,13 @@ __device__ __forceinline__ void row_family_regs(double* acc, int lane, int win, 
   }
 }
 
-template <int PF>
-__global__ void __launch_bounds__(32 * kRowWarps, 4) assemble_rows_family_kernel(const RowFamArgs a) {
+// PF sources per batch, WIN blocks of a row per shared-memory window, MINB resident CTAs per SM.
+// The gather is latency-bound: what buys bandwidth is resident warps (a 288-byte random-run probe
+// reaches 2.6 / 4.4 / 5.1 TB/s at 16 / 32 / 64 warps per SM, independent of per-warp prefetch depth),
+// so the production instantiation trades per-warp state for occupancy.
+template <int PF, int WIN, int MINB>
+__global__ void __launch_bounds__(32 * kRowWarps, MINB) assemble_rows_family_kernel(const RowFamArgs a) {
+  constexpr int kRowWin = WIN;
   __shared__ double sm[kRowWarps][kRowWin * 9];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * kRowWarps + w;
@@ -798,8 +803,8 @@ extern "C" int b200ipc_assemble_numeric(b200ipc_assembly* h, const double* masse
     q.rowptr = h->rowptr.ptr; q.colidx = h->colidx.ptr; q.rseg = h->rseg.ptr; q.rs_desc = h->rs_desc.ptr;
     q.rs_dst = h->rs_dst.ptr; q.vals = vals;
     const unsigned grid = (unsigned)((h->nverts + kRowWarps - 1) / kRowWarps);
-    if (h->variant == 2) assemble_rows_family_kernel<4><<<grid, 32 * kRowWarps, 0, (cudaStream_t)stream>>>(q);
-    else assemble_rows_family_kernel<8><<<grid, 32 * kRowWarps, 0, (cudaStream_t)stream>>>(q);
+    if (h->variant == 2) assemble_rows_family_kernel<1, 48, 8><<<grid, 32 * kRowWarps, 0, (cudaStream_t)stream>>>(q);
+    else assemble_rows_family_kernel<2, 48, 6><<<grid, 32 * kRowWarps, 0, (cudaStream_t)stream>>>(q);
     return post_launch();
   }
   RowArgs r;
