@@ -167,6 +167,8 @@ __global__ void finish_pattern_kernel(int64_t nverts, int64_t nnzb, int64_t nval
 
 // Source descriptors, written once per pattern in sorted order: the numeric phase then needs no
 // integer division and no family search per source.
+//   block source : (element offset of the 3x3 sub-block << 16) | (row length D << 8) | family
+//   mass slot    : (vertex << 16) | 0xff      (always the first source of a diagonal block's run)
 __global__ void __launch_bounds__(kAT) source_desc_kernel(FamDesc fd, int64_t nverts, int64_t nvalid,
                                                           const uint32_t* __restrict__ perm,
                                                           uint64_t* __restrict__ desc) {
@@ -174,19 +176,18 @@ __global__ void __launch_bounds__(kAT) source_desc_kernel(FamDesc fd, int64_t nv
   if (j >= nvalid) return;
   const int64_t slot = perm[j];
   if (slot < nverts) {
-    desc[j] = ((uint64_t)slot << 3) | 7ull;
+    desc[j] = ((uint64_t)slot << 16) | 0xffull;
   } else {
     int f, a, c;
     int64_t b;
     decode_slot(fd, slot - nverts, f, b, a, c);
     const int64_t D = 3 * fd.s[f];
-    desc[j] = ((uint64_t)((b * D + 3 * a) * D + 3 * c) << 3) | (uint64_t)f;
+    desc[j] = ((uint64_t)((b * D + 3 * a) * D + 3 * c) << 16) | ((uint64_t)D << 8) | (uint64_t)f;
   }
 }
 
 struct NumericArgs {
   HessPtrs hp;
-  int32_t ld[kMaxFam];   // row length 3s of each family
   int64_t nnzb;
   const uint8_t* fixed;
   const double* masses;
@@ -197,50 +198,48 @@ struct NumericArgs {
 
 constexpr int kNumWarps = 8;
 
-__device__ __forceinline__ double source_value(const NumericArgs& a, uint64_t d, int er, int ec, bool& identity) {
-  const int f = (int)(d & 7ull);
-  const int64_t off = (int64_t)(d >> 3);
-  if (f == 7) {  // diagonal mass slot; a fixed vertex keeps a unit diagonal instead
-    if (a.fixed[off]) {
-      identity = true;
-      return 0.0;
-    }
-    return er == ec ? a.masses[off] : 0.0;
-  }
-  return __ldg(a.hp.p[f] + off + er * a.ld[f] + ec);
-}
-
 // One warp per output block: lanes (g, e) = (lane / 9, lane % 9), g < 3, walk the block's run of
-// sources three at a time (two iterations in flight), entry e of each 3x3 sub-block per lane; the
-// three partial sums are combined in fixed order with two shuffles.  Lanes 0..8 write the block:
-// nine consecutive doubles per warp, 72-byte rows back to back across the CTA's warps.
-__global__ void __launch_bounds__(32 * kNumWarps) assemble_numeric_kernel(const NumericArgs a) {
+// sources three at a time, entry e of each 3x3 sub-block per lane, four trips (twelve sub-blocks)
+// of loads in flight before the adds; the three partial sums are combined in fixed order with two
+// shuffles.  Lanes 0..8 write the block: nine consecutive doubles.
+__global__ void __launch_bounds__(32 * kNumWarps, 8) assemble_numeric_kernel(const __grid_constant__ NumericArgs a) {
   const int64_t u = (int64_t)blockIdx.x * kNumWarps + (threadIdx.x >> 5);
   if (u >= a.nnzb) return;
   const int lane = threadIdx.x & 31;
   const int g = lane / 9, e = lane - 9 * g;
   const int er = e / 3, ec = e - 3 * er;
-  const int32_t j0 = a.useg[u], j1 = a.useg[u + 1];
+  int32_t j0 = a.useg[u];
+  const int32_t j1 = a.useg[u + 1];
   double acc = 0.0;
-  bool identity = false;
-  if (g < 3) {
-    int32_t j = j0 + g;
-    for (; j + 3 < j1; j += 6) {
-      const uint64_t d0 = a.desc[j], d1 = a.desc[j + 3];
-      const double v0 = source_value(a, d0, er, ec, identity);
-      const double v1 = source_value(a, d1, er, ec, identity);
-      acc += v0;
-      acc += v1;
+  const uint64_t first = a.desc[j0];
+  if ((first & 0xff) == 0xff) {  // diagonal block: mass slot first
+    const int64_t v = (int64_t)(first >> 16);
+    if (a.fixed[v]) {  // Dirichlet vertex: unit diagonal, nothing else
+      if (lane < 9) a.vals[9 * u + lane] = er == ec ? 1.0 : 0.0;
+      return;
     }
-    if (j < j1) acc += source_value(a, a.desc[j], er, ec, identity);
+    if (g == 0 && er == ec) acc = a.masses[v];
+    ++j0;
+  }
+  if (g < 3) {
+    for (int32_t j = j0 + g; j < j1; j += 12) {
+      uint64_t d[4];
+      double v[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) d[t] = j + 3 * t < j1 ? a.desc[j + 3 * t] : ~0ull;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int D = (int)(d[t] >> 8) & 0xff;
+        const double* p = a.hp.p[d[t] & 7] + (d[t] >> 16) + er * D + ec;
+        v[t] = d[t] != ~0ull ? __ldg(p) : 0.0;
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) acc += v[t];
+    }
   }
   const double s1 = __shfl_down_sync(0xffffffffu, acc, 9);   // group 1's partial sum (lanes 0..8)
   const double s2 = __shfl_down_sync(0xffffffffu, acc, 18);  // group 2's
-  const bool any_identity = __any_sync(0xffffffffu, identity);
-  if (lane < 9) {
-    const double total = (acc + s1) + s2;
-    a.vals[9 * u + lane] = any_identity ? (er == ec ? 1.0 : 0.0) : total;
-  }
+  if (lane < 9) a.vals[9 * u + lane] = (acc + s1) + s2;
 }
 
 // ---- row-wise numeric assembly ------------------------------------------------------------------
@@ -342,7 +341,7 @@ __device__ __forceinline__ void row_add(double* acc, const LaneMap<D>& m, int la
 // block is read exactly once over the whole kernel) and its s sub-blocks are added into the row's
 // accumulators in shared memory in list order -- no atomics, bitwise reproducible.  The finished
 // row (72 bytes per block, contiguous) is written with consecutive lanes on consecutive doubles.
-__global__ void __launch_bounds__(32 * kRowWarps) assemble_rows_kernel(const RowArgs a) {
+__global__ void __launch_bounds__(32 * kRowWarps) assemble_rows_kernel(const __grid_constant__ RowArgs a) {
   __shared__ double sm[kRowWarps][kRowWin * 9];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * kRowWarps + w;
@@ -512,7 +511,7 @@ __device__ __forceinline__ void row_family_regs(double* acc, int lane, int win, 
 // reaches 2.6 / 4.4 / 5.1 TB/s at 16 / 32 / 64 warps per SM, independent of per-warp prefetch depth),
 // so the production instantiation trades per-warp state for occupancy.
 template <int PF, int WIN, int MINB>
-__global__ void __launch_bounds__(32 * kRowWarps, MINB) assemble_rows_family_kernel(const RowFamArgs a) {
+__global__ void __launch_bounds__(32 * kRowWarps, MINB) assemble_rows_family_kernel(const __grid_constant__ RowFamArgs a) {
   constexpr int kRowWin = WIN;
   __shared__ double sm[kRowWarps][kRowWin * 9];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -593,7 +592,7 @@ struct GradArgs {
 };
 
 // thread = (vertex, component): m (x - x~) + contributions in list order; fixed rows -> 0
-__global__ void __launch_bounds__(kAT) scatter_gradient_kernel(const GradArgs a) {
+__global__ void __launch_bounds__(kAT) scatter_gradient_kernel(const __grid_constant__ GradArgs a) {
   const int64_t t = (int64_t)blockIdx.x * kAT + threadIdx.x;
   if (t >= 3 * a.nverts) return;
   const int64_t v = t / 3;
@@ -779,12 +778,10 @@ extern "C" int b200ipc_assemble_numeric(b200ipc_assembly* h, const double* masse
   if (!h || !h->ready) return B200IPC_ESTATE;
   if (!masses || !vals || (h->fam.nfam && !fam_hess)) return B200IPC_EINVAL;
   NumericArgs a;
-  for (int f = 0; f < kMaxFam; ++f) a.ld[f] = 0;
   for (int f = 0; f <= kMaxFam; ++f) a.hp.p[f] = nullptr;
   for (int f = 0; f < h->fam.nfam; ++f) {
     if (h->fam.nb[f] && !fam_hess[f]) return B200IPC_EINVAL;
     a.hp.p[f] = fam_hess[f];
-    a.ld[f] = 3 * h->fam.s[f];
   }
   a.nnzb = h->nnzb; a.fixed = h->fixed.ptr; a.masses = masses;
   a.useg = h->useg.ptr; a.desc = h->desc.ptr; a.vals = vals;
