@@ -71,7 +71,7 @@ struct b200ipc_assembly {
   b200ipc::DevBuf<uint64_t> keys_a, keys_b;
   b200ipc::DevBuf<uint32_t> slot_a, slot_b;   // slot_b ends up as the sorted permutation
   b200ipc::DevBuf<int32_t> head, useg;        // head flags / scan, run starts (nnzb+1)
-  b200ipc::DevBuf<uint64_t> desc;             // per sorted source: (element offset << 3) | family, 7 = mass slot
+  b200ipc::DevBuf<uint32_t> desc;             // per sorted source: family << 30 | element offset / 3 (3 = mass slot)
   b200ipc::DevBuf<int32_t> rowptr, colidx;
   b200ipc::DevBuf<uint32_t> gkeys_a, gkeys_b, gslot_a, gslot_b;
   b200ipc::DevBuf<int32_t> gseg;              // (N+1) run starts per vertex
@@ -165,43 +165,54 @@ __global__ void finish_pattern_kernel(int64_t nverts, int64_t nnzb, int64_t nval
   useg[nnzb] = (int32_t)nvalid;
 }
 
-// Source descriptors, written once per pattern in sorted order: the numeric phase then needs no
-// integer division and no family search per source.
-//   block source : (element offset of the 3x3 sub-block << 16) | (row length D << 8) | family
-//   mass slot    : (vertex << 16) | 0xff      (always the first source of a diagonal block's run)
+// Source descriptors, written once per pattern in sorted order, 32 bits each: the numeric phase then
+// needs no integer division, no family search and a single address computation per source.
+//   block source : family (2 bits) << 30 | (element offset of the 3x3 sub-block) / 3
+//   mass slot    : 3 << 30 | vertex          (always the first source of a diagonal block's run)
+// (needs nfam <= 3 and family arrays below 2^30 * 24 bytes; otherwise the row-wise kernel is used)
 __global__ void __launch_bounds__(kAT) source_desc_kernel(FamDesc fd, int64_t nverts, int64_t nvalid,
                                                           const uint32_t* __restrict__ perm,
-                                                          uint64_t* __restrict__ desc) {
+                                                          uint32_t* __restrict__ desc) {
   const int64_t j = (int64_t)blockIdx.x * kAT + threadIdx.x;
   if (j >= nvalid) return;
   const int64_t slot = perm[j];
   if (slot < nverts) {
-    desc[j] = ((uint64_t)slot << 16) | 0xffull;
+    desc[j] = 0xC0000000u | (uint32_t)slot;
   } else {
     int f, a, c;
     int64_t b;
     decode_slot(fd, slot - nverts, f, b, a, c);
-    const int64_t D = 3 * fd.s[f];
-    desc[j] = ((uint64_t)((b * D + 3 * a) * D + 3 * c) << 16) | ((uint64_t)D << 8) | (uint64_t)f;
+    const int64_t s = fd.s[f];
+    // ((b*D + 3a)*D + 3c) / 3 with D = 3s
+    desc[j] = ((uint32_t)f << 30) | (uint32_t)((b * 3 * s + 3 * a) * s + c);
   }
 }
 
 struct NumericArgs {
   HessPtrs hp;
+  int32_t ld[4];        // row length D of families 0..2 (slot 3 unused)
   int64_t nnzb;
   const uint8_t* fixed;
   const double* masses;
   const int32_t* useg;
-  const uint64_t* desc;
+  const uint32_t* desc;
   double* vals;
 };
 
 constexpr int kNumWarps = 8;
 
+__device__ __forceinline__ double gather_entry(const NumericArgs& a, uint32_t d, int er, int ec) {
+  const uint32_t f = d >> 30;
+  const uint32_t e = (d & 0x3fffffffu) * 3u + (uint32_t)(er * a.ld[f] + ec);
+  return __ldg(a.hp.p[f] + e);
+}
+
 // One warp per output block: lanes (g, e) = (lane / 9, lane % 9), g < 3, walk the block's run of
-// sources three at a time, entry e of each 3x3 sub-block per lane, four trips (twelve sub-blocks)
-// of loads in flight before the adds; the three partial sums are combined in fixed order with two
-// shuffles.  Lanes 0..8 write the block: nine consecutive doubles.
+// sources three at a time, entry e of each 3x3 sub-block per lane, accumulating in a register; four
+// trips (twelve sub-blocks) of loads are in flight before the adds; the three partial sums are
+// combined in fixed order with two shuffles.  Lanes 0..8 write the block: nine consecutive doubles.
+// 32 registers, no shared memory: 64 resident warps per SM, which is what this latency-bound gather
+// needs (scripts/probes/gather_probe.cu).
 __global__ void __launch_bounds__(32 * kNumWarps, 8) assemble_numeric_kernel(const __grid_constant__ NumericArgs a) {
   const int64_t u = (int64_t)blockIdx.x * kNumWarps + (threadIdx.x >> 5);
   if (u >= a.nnzb) return;
@@ -211,9 +222,9 @@ __global__ void __launch_bounds__(32 * kNumWarps, 8) assemble_numeric_kernel(con
   int32_t j0 = a.useg[u];
   const int32_t j1 = a.useg[u + 1];
   double acc = 0.0;
-  const uint64_t first = a.desc[j0];
-  if ((first & 0xff) == 0xff) {  // diagonal block: mass slot first
-    const int64_t v = (int64_t)(first >> 16);
+  const uint32_t first = a.desc[j0];
+  if (first >= 0xC0000000u) {  // diagonal block: mass slot first
+    const uint32_t v = first & 0x3fffffffu;
     if (a.fixed[v]) {  // Dirichlet vertex: unit diagonal, nothing else
       if (lane < 9) a.vals[9 * u + lane] = er == ec ? 1.0 : 0.0;
       return;
@@ -222,20 +233,17 @@ __global__ void __launch_bounds__(32 * kNumWarps, 8) assemble_numeric_kernel(con
     ++j0;
   }
   if (g < 3) {
-    for (int32_t j = j0 + g; j < j1; j += 12) {
-      uint64_t d[4];
-      double v[4];
-#pragma unroll
-      for (int t = 0; t < 4; ++t) d[t] = j + 3 * t < j1 ? a.desc[j + 3 * t] : ~0ull;
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int D = (int)(d[t] >> 8) & 0xff;
-        const double* p = a.hp.p[d[t] & 7] + (d[t] >> 16) + er * D + ec;
-        v[t] = d[t] != ~0ull ? __ldg(p) : 0.0;
-      }
-#pragma unroll
-      for (int t = 0; t < 4; ++t) acc += v[t];
+    int32_t j = j0 + g;
+    for (; j + 9 < j1; j += 12) {
+      const uint32_t d0 = a.desc[j], d1 = a.desc[j + 3], d2 = a.desc[j + 6], d3 = a.desc[j + 9];
+      const double v0 = gather_entry(a, d0, er, ec), v1 = gather_entry(a, d1, er, ec);
+      const double v2 = gather_entry(a, d2, er, ec), v3 = gather_entry(a, d3, er, ec);
+      acc += v0;
+      acc += v1;
+      acc += v2;
+      acc += v3;
     }
+    for (; j < j1; j += 3) acc += gather_entry(a, a.desc[j], er, ec);
   }
   const double s1 = __shfl_down_sync(0xffffffffu, acc, 9);   // group 1's partial sum (lanes 0..8)
   const double s2 = __shfl_down_sync(0xffffffffu, acc, 18);  // group 2's
@@ -779,13 +787,17 @@ extern "C" int b200ipc_assemble_numeric(b200ipc_assembly* h, const double* masse
   if (!masses || !vals || (h->fam.nfam && !fam_hess)) return B200IPC_EINVAL;
   NumericArgs a;
   for (int f = 0; f <= kMaxFam; ++f) a.hp.p[f] = nullptr;
+  for (int f = 0; f < 4; ++f) a.ld[f] = 0;
+  bool packed_ok = h->fam.nfam <= 3;
   for (int f = 0; f < h->fam.nfam; ++f) {
     if (h->fam.nb[f] && !fam_hess[f]) return B200IPC_EINVAL;
     a.hp.p[f] = fam_hess[f];
+    if (f < 3) a.ld[f] = 3 * h->fam.s[f];
+    if (h->fam.nb[f] * 9 * h->fam.s[f] * h->fam.s[f] >= (3ll << 30)) packed_ok = false;
   }
   a.nnzb = h->nnzb; a.fixed = h->fixed.ptr; a.masses = masses;
   a.useg = h->useg.ptr; a.desc = h->desc.ptr; a.vals = vals;
-  if (h->variant == 1) {  // per-block runs (gather of 3x3 sub-blocks)
+  if (h->variant == 1 && packed_ok) {  // per-block runs (gather of 3x3 sub-blocks)
     const unsigned grid = (unsigned)((h->nnzb + kNumWarps - 1) / kNumWarps);
     assemble_numeric_kernel<<<grid, 32 * kNumWarps, 0, (cudaStream_t)stream>>>(a);
     return post_launch();
