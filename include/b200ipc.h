@@ -143,6 +143,18 @@ int b200ipc_barrier_scalars(const b200ipc_params* params /* host */, int64_t n, 
 int b200ipc_mollified_eigensystem(const b200ipc_params* params /* host */, int64_t n, const double* g,
                                   const double* c, const double* eps_x, double* out, void* stream);
 
+/* Same as b200ipc_barrier_stencils plus the rank-1 factors of the blocks: fac2 (n_PP,6), fac3
+ * (n_PE,9), fac4 (n4,12) with hess_b = fac_b fac_b^T exactly (the dense entries are those products).
+ * Pass hess* = NULL to skip the dense blocks when only the assembled matrix is needed
+ * (b200ipc_assemble_numeric_factors): the step then writes 24 s instead of 72 s^2 bytes per block. */
+int b200ipc_barrier_stencils_ex(const b200ipc_params* params /* host */, int64_t nverts,
+                                const double* positions, int64_t n, const int64_t* kind_off /* host[8] */,
+                                const int32_t* verts, const uint8_t* sub, const double* eps_x,
+                                double* energy, uint8_t* status,
+                                double* grad2, double* hess2, double* grad3, double* hess3,
+                                double* grad4, double* hess4,
+                                double* fac2, double* fac3, double* fac4, void* stream);
+
 /* Sum of energy[0..n) (the scalar of SimState._barrier_energy, solver.py:127-146) and the
  * counts of status==1 / status==2, deterministic two-pass.  result: device double[1];
  * counts: device int64[2] (inactive, penetration); workspace: device scratch of at least
@@ -197,6 +209,12 @@ int b200ipc_assembly_pattern(b200ipc_assembly* h, int32_t* rowptr, int32_t* coli
 int b200ipc_assemble_numeric(b200ipc_assembly* h, const double* masses,
                              const double* const* fam_hess /* host array of device ptrs */,
                              double* vals, void* stream);
+/* Numeric assembly straight from the rank-1 factors of b200ipc_barrier_stencils_ex (barrier
+ * families only; fam_fac[f]: device (nb,3s)); at most 3 families.  Bitwise identical to
+ * b200ipc_assemble_numeric variant 1 on the dense blocks of the same factors. */
+int b200ipc_assemble_numeric_factors(b200ipc_assembly* h, const double* masses,
+                                     const double* const* fam_fac /* host array of device ptrs */,
+                                     double* vals, void* stream);
 /* SimState.gradient (solver.py:218-226): out (3 nverts) = m (x - x_tilde) + sum scatter(grad_b),
  * fixed rows 0.  fam_grad[f]: device (nb,3s). */
 int b200ipc_scatter_gradient(b200ipc_assembly* h, const double* masses, const double* x,

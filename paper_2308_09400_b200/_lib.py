@@ -56,6 +56,8 @@ SIGNATURES = {
     "b200ipc_matvec_end": [_i64, _vp, _vp, _vp, _vp],
     "b200ipc_barrier_stencils": [C.POINTER(Params), _i64, _vp, _i64, C.POINTER(_i64), _vp, _vp, _vp,
                                  _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "b200ipc_barrier_stencils_ex": [C.POINTER(Params), _i64, _vp, _i64, C.POINTER(_i64), _vp, _vp, _vp,
+                                    _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "b200ipc_reduce_energy": [_i64, _vp, _vp, _vp, _vp, _vp, _vp],
     "b200ipc_diagonal_jacobian": [C.POINTER(Params), _i64, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                   _vp, _vp, _vp, _vp, _vp, _vp],
@@ -71,6 +73,7 @@ SIGNATURES = {
                                   C.POINTER(_i64), _vp],
     "b200ipc_assembly_pattern": [_vp, _vp, _vp, _vp],
     "b200ipc_assemble_numeric": [_vp, _vp, C.POINTER(_vp), _vp, _vp],
+    "b200ipc_assemble_numeric_factors": [_vp, _vp, C.POINTER(_vp), _vp, _vp],
     "b200ipc_scatter_gradient": [_vp, _vp, _vp, _vp, C.POINTER(_vp), _vp, _vp],
     "b200ipc_bsr_spmv": [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp],
     "b200ipc_block_jacobi": [_i64, _vp, _vp, _vp, _vp, _vp],

@@ -72,6 +72,7 @@ struct b200ipc_assembly {
   b200ipc::DevBuf<uint32_t> slot_a, slot_b;   // slot_b ends up as the sorted permutation
   b200ipc::DevBuf<int32_t> head, useg;        // head flags / scan, run starts (nnzb+1)
   b200ipc::DevBuf<uint32_t> desc;             // per sorted source: family << 30 | element offset / 3 (3 = mass slot)
+  b200ipc::DevBuf<uint32_t> fdesc;            // per sorted source, factor form: family | c-a+3 | b*D+3a
   b200ipc::DevBuf<int32_t> rowptr, colidx;
   b200ipc::DevBuf<uint32_t> gkeys_a, gkeys_b, gslot_a, gslot_b;
   b200ipc::DevBuf<int32_t> gseg;              // (N+1) run starts per vertex
@@ -247,6 +248,82 @@ __global__ void __launch_bounds__(32 * kNumWarps, 8) assemble_numeric_kernel(con
   }
   const double s1 = __shfl_down_sync(0xffffffffu, acc, 9);   // group 1's partial sum (lanes 0..8)
   const double s2 = __shfl_down_sync(0xffffffffu, acc, 18);  // group 2's
+  if (lane < 9) a.vals[9 * u + lane] = (acc + s1) + s2;
+}
+
+// ---- numeric assembly straight from the rank-1 factors ---------------------------------------------
+// Barrier blocks are z z^T (stencil.cu), so sub-block (a,c) of block b is z_a z_c^T: instead of the
+// dense block (72 s^2 bytes) the gather reads two 3-vectors of the factor array (24 s bytes per block,
+// ~0.1 GB for 1M contacts: L2-resident).  Entries are the same products the dense block holds, summed
+// in the same order as assemble_numeric_kernel, so both paths give bitwise identical matrices.
+//   fdesc : family (2 bits) << 30 | (c - a + 3) << 27 | element index of z_a = b*D + 3a   (27 bits)
+__global__ void __launch_bounds__(kAT) factor_desc_kernel(FamDesc fd, int64_t nverts, int64_t nvalid,
+                                                          const uint32_t* __restrict__ perm,
+                                                          uint32_t* __restrict__ fdesc) {
+  const int64_t j = (int64_t)blockIdx.x * kAT + threadIdx.x;
+  if (j >= nvalid) return;
+  const int64_t slot = perm[j];
+  if (slot < nverts) {
+    fdesc[j] = 0xC0000000u | (uint32_t)slot;
+  } else {
+    int f, a, c;
+    int64_t b;
+    decode_slot(fd, slot - nverts, f, b, a, c);
+    const int64_t D = 3 * fd.s[f];
+    fdesc[j] = ((uint32_t)f << 30) | ((uint32_t)(c - a + 3) << 27) | (uint32_t)(b * D + 3 * a);
+  }
+}
+
+struct FactorArgs {
+  HessPtrs fp;          // factor arrays (nb, D) per family
+  int64_t nnzb;
+  const uint8_t* fixed;
+  const double* masses;
+  const int32_t* useg;
+  const uint32_t* fdesc;
+  double* vals;
+};
+
+__device__ __forceinline__ double factor_entry(const FactorArgs& a, uint32_t d, int er, int ec) {
+  const double* z = a.fp.p[d >> 30] + (d & 0x07ffffffu);
+  const int dc = 3 * ((int)((d >> 27) & 7u) - 3);
+  return __ldg(z + er) * __ldg(z + dc + ec);
+}
+
+__global__ void __launch_bounds__(32 * kNumWarps, 8) assemble_factors_kernel(const __grid_constant__ FactorArgs a) {
+  const int64_t u = (int64_t)blockIdx.x * kNumWarps + (threadIdx.x >> 5);
+  if (u >= a.nnzb) return;
+  const int lane = threadIdx.x & 31;
+  const int g = lane / 9, e = lane - 9 * g;
+  const int er = e / 3, ec = e - 3 * er;
+  int32_t j0 = a.useg[u];
+  const int32_t j1 = a.useg[u + 1];
+  double acc = 0.0;
+  const uint32_t first = a.fdesc[j0];
+  if (first >= 0xC0000000u) {
+    const uint32_t v = first & 0x3fffffffu;
+    if (a.fixed[v]) {
+      if (lane < 9) a.vals[9 * u + lane] = er == ec ? 1.0 : 0.0;
+      return;
+    }
+    if (g == 0 && er == ec) acc = a.masses[v];
+    ++j0;
+  }
+  if (g < 3) {
+    int32_t j = j0 + g;
+    for (; j + 9 < j1; j += 12) {
+      const uint32_t d0 = a.fdesc[j], d1 = a.fdesc[j + 3], d2 = a.fdesc[j + 6], d3 = a.fdesc[j + 9];
+      const double v0 = factor_entry(a, d0, er, ec), v1 = factor_entry(a, d1, er, ec);
+      const double v2 = factor_entry(a, d2, er, ec), v3 = factor_entry(a, d3, er, ec);
+      acc += v0;
+      acc += v1;
+      acc += v2;
+      acc += v3;
+    }
+    for (; j < j1; j += 3) acc += factor_entry(a, a.fdesc[j], er, ec);
+  }
+  const double s1 = __shfl_down_sync(0xffffffffu, acc, 9);
+  const double s2 = __shfl_down_sync(0xffffffffu, acc, 18);
   if (lane < 9) a.vals[9 * u + lane] = (acc + s1) + s2;
 }
 
@@ -649,7 +726,7 @@ extern "C" int b200ipc_assembly_set_variant(b200ipc_assembly* h, int32_t variant
 extern "C" int b200ipc_assembly_destroy(b200ipc_assembly* h) {
   if (!h) return 0;
   h->fixed.release(); h->keys_a.release(); h->keys_b.release(); h->slot_a.release(); h->slot_b.release();
-  h->head.release(); h->useg.release(); h->desc.release(); h->rowptr.release(); h->colidx.release();
+  h->head.release(); h->useg.release(); h->desc.release(); h->fdesc.release(); h->rowptr.release(); h->colidx.release();
   h->gkeys_a.release(); h->gkeys_b.release(); h->gslot_a.release(); h->gslot_b.release(); h->gseg.release(); h->rs_desc.release(); h->rs_dst.release(); h->rseg.release();
   h->temp.release(); h->scalars.release();
   delete h;
@@ -739,6 +816,9 @@ extern "C" int b200ipc_assemble_symbolic(b200ipc_assembly* h, int64_t nverts, co
   CK(h->desc.reserve(h->nvalid));
   source_desc_kernel<<<blocks_for(h->nvalid), kAT, 0, st>>>(fd, nverts, h->nvalid, h->slot_b.ptr, h->desc.ptr);
   RC(post_launch());
+  CK(h->fdesc.reserve(h->nvalid));
+  factor_desc_kernel<<<blocks_for(h->nvalid), kAT, 0, st>>>(fd, nverts, h->nvalid, h->slot_b.ptr, h->fdesc.ptr);
+  RC(post_launch());
 
   // gradient runs: sort vertex slots by vertex id
   const int64_t ng = h->ngslots;
@@ -823,6 +903,25 @@ extern "C" int b200ipc_assemble_numeric(b200ipc_assembly* h, const double* masse
   r.gseg = h->gseg.ptr; r.rs_desc = h->rs_desc.ptr; r.rs_dst = h->rs_dst.ptr; r.vals = vals;
   const unsigned grid = (unsigned)((h->nverts + kRowWarps - 1) / kRowWarps);
   assemble_rows_kernel<<<grid, 32 * kRowWarps, 0, (cudaStream_t)stream>>>(r);
+  return post_launch();
+}
+
+extern "C" int b200ipc_assemble_numeric_factors(b200ipc_assembly* h, const double* masses,
+                                                const double* const* fam_fac, double* vals, void* stream) {
+  if (!h || !h->ready) return B200IPC_ESTATE;
+  if (!masses || !vals || (h->fam.nfam && !fam_fac)) return B200IPC_EINVAL;
+  if (h->fam.nfam > 3) return B200IPC_EINVAL;  // 2-bit family field
+  FactorArgs a;
+  for (int f = 0; f <= kMaxFam; ++f) a.fp.p[f] = nullptr;
+  for (int f = 0; f < h->fam.nfam; ++f) {
+    if (h->fam.nb[f] && !fam_fac[f]) return B200IPC_EINVAL;
+    if (h->fam.nb[f] * 3 * h->fam.s[f] >= (1ll << 27)) return B200IPC_EINVAL;  // 27-bit element index
+    a.fp.p[f] = fam_fac[f];
+  }
+  a.nnzb = h->nnzb; a.fixed = h->fixed.ptr; a.masses = masses; a.useg = h->useg.ptr; a.fdesc = h->fdesc.ptr;
+  a.vals = vals;
+  const unsigned grid = (unsigned)((h->nnzb + kNumWarps - 1) / kNumWarps);
+  assemble_factors_kernel<<<grid, 32 * kNumWarps, 0, (cudaStream_t)stream>>>(a);
   return post_launch();
 }
 

@@ -40,6 +40,7 @@ struct KindArgs {
   uint8_t* status;           // (n) or null
   double* grad;              // (n,D) or null
   double* hess;              // (n,D,D) or null
+  double* fac;               // (n,D) or null: rank-1 factor z with hess = z z^T
 };
 
 // One launch covers every kind: CTA b works on tile (b - tile_off[kind]) of the kind whose tile
@@ -144,17 +145,21 @@ __device__ __forceinline__ void stencil_tile(const b200ipc_params& prm, const do
   const int64_t left = a.n - tile0;
   const int ntile = left < kTile ? (int)left : kTile;
 
-  // ---- phase 2a: gradient tile, (ntile, D) contiguous ----------------------------------
-  if (a.grad) {
-    double* out = a.grad + tile0 * D;
+  // ---- phase 2a: gradient tile and factor tile, (ntile, D) contiguous each ------------------
+#pragma unroll
+  for (int which = 0; which < 2; ++which) {
+    double* base = which == 0 ? a.grad : a.fac;
+    const double* sm = which == 0 ? sm_g : sm_z;
+    if (!base) continue;
+    double* out = base + tile0 * D;
     const int total = ntile * D;
     for (int e = 2 * tid; e < total; e += 2 * kTile) {
       const int b0 = e / D, k0 = e - b0 * D;
-      const double v0 = sm_g[k0 * P + b0];
+      const double v0 = sm[k0 * P + b0];
       if (e + 1 < total) {
         const int k1 = (k0 + 1 == D) ? 0 : k0 + 1;
         const int b1 = (k0 + 1 == D) ? b0 + 1 : b0;
-        const double v1 = sm_g[k1 * P + b1];
+        const double v1 = sm[k1 * P + b1];
         *reinterpret_cast<double2*>(out + e) = make_double2(v0, v1);
       } else {
         out[e] = v0;
@@ -293,11 +298,11 @@ __global__ void reduce_energy_pass2(int nparts, const double* __restrict__ part_
 
 using namespace b200ipc;
 
-extern "C" int b200ipc_barrier_stencils(const b200ipc_params* params, int64_t nverts, const double* positions,
-                                        int64_t n, const int64_t* kind_off, const int32_t* verts, const uint8_t* sub,
-                                        const double* eps_x, double* energy, uint8_t* status, double* grad2,
-                                        double* hess2, double* grad3, double* hess3, double* grad4, double* hess4,
-                                        void* stream) {
+extern "C" int b200ipc_barrier_stencils_ex(const b200ipc_params* params, int64_t nverts, const double* positions,
+                                           int64_t n, const int64_t* kind_off, const int32_t* verts,
+                                           const uint8_t* sub, const double* eps_x, double* energy, uint8_t* status,
+                                           double* grad2, double* hess2, double* grad3, double* hess3, double* grad4,
+                                           double* hess4, double* fac2, double* fac3, double* fac4, void* stream) {
   if (!params || !kind_off || n < 0 || nverts < 0) return B200IPC_EINVAL;
   if (n == 0) return 0;
   if (!positions || !verts) return B200IPC_EINVAL;
@@ -310,7 +315,8 @@ extern "C" int b200ipc_barrier_stencils(const b200ipc_params* params, int64_t nv
   if (has_par && (!sub || !eps_x)) return B200IPC_EINVAL;
   if (params->form != 0 && params->form != 1) return B200IPC_EINVAL;
   const uintptr_t align = (uintptr_t)verts | (uintptr_t)grad2 | (uintptr_t)hess2 | (uintptr_t)grad3 |
-                          (uintptr_t)hess3 | (uintptr_t)grad4 | (uintptr_t)hess4;
+                          (uintptr_t)hess3 | (uintptr_t)grad4 | (uintptr_t)hess4 | (uintptr_t)fac2 |
+                          (uintptr_t)fac3 | (uintptr_t)fac4;
   if (align & 15) return B200IPC_EINVAL;  // int4 loads / double2 stores
 
   cudaStream_t s = (cudaStream_t)stream;
@@ -336,12 +342,13 @@ extern "C" int b200ipc_barrier_stencils(const b200ipc_params* params, int64_t nv
     ka.energy = energy ? energy + off : nullptr;
     ka.status = status ? status + off : nullptr;
     if (k == B200IPC_PP) {
-      ka.grad = grad2; ka.hess = hess2;
+      ka.grad = grad2; ka.hess = hess2; ka.fac = fac2;
     } else if (k == B200IPC_PE) {
-      ka.grad = grad3; ka.hess = hess3;
+      ka.grad = grad3; ka.hess = hess3; ka.fac = fac3;
     } else {
       ka.grad = grad4 ? grad4 + 12 * row4[k] : nullptr;
       ka.hess = hess4 ? hess4 + 144 * row4[k] : nullptr;
+      ka.fac = fac4 ? fac4 + 12 * row4[k] : nullptr;
     }
     a.tile_off[k] = (uint32_t)tiles;
     tiles += (uint64_t)((cnt + kTile - 1) / kTile);
@@ -351,6 +358,15 @@ extern "C" int b200ipc_barrier_stencils(const b200ipc_params* params, int64_t nv
   if (params->form == 0) barrier_stencil_kernel<0><<<(unsigned)tiles, kTile, 0, s>>>(a);
   else barrier_stencil_kernel<1><<<(unsigned)tiles, kTile, 0, s>>>(a);
   return post_launch();
+}
+
+extern "C" int b200ipc_barrier_stencils(const b200ipc_params* params, int64_t nverts, const double* positions,
+                                        int64_t n, const int64_t* kind_off, const int32_t* verts, const uint8_t* sub,
+                                        const double* eps_x, double* energy, uint8_t* status, double* grad2,
+                                        double* hess2, double* grad3, double* hess3, double* grad4, double* hess4,
+                                        void* stream) {
+  return b200ipc_barrier_stencils_ex(params, nverts, positions, n, kind_off, verts, sub, eps_x, energy, status, grad2,
+                                     hess2, grad3, hess3, grad4, hess4, nullptr, nullptr, nullptr, stream);
 }
 
 extern "C" int b200ipc_reduce_energy(int64_t n, const double* energy, const uint8_t* status, double* result,

@@ -60,6 +60,7 @@ class Family:
     vids: object   # (nb,s) int64 device
     grad: object   # (nb,3s) device or None
     hess: object   # (nb,3s,3s) device or None
+    fac: object = None   # (nb,3s) device or None: rank-1 factor z, hess == z z^T
 
 
 @dataclass
@@ -114,13 +115,16 @@ def _lib_ws_doubles():
     return 16384 // 8
 
 
-def evaluate(table, positions, params, dt=1.0, want_energy=True, want_grad=True, want_hess=True, out=None):
+def evaluate(table, positions, params, dt=1.0, want_energy=True, want_grad=True, want_hess=True,
+             want_factors=False, out=None):
     """Evaluate every stencil of ``table`` at ``positions``.
 
     ``table``: ``StencilTable`` or ``DeviceStencilTable``; ``positions``: (N,3) host array or
     device tensor; ``params``: ``BarrierParams``; ``dt``: time step (grad/hess are scaled by
     dt**2, energy is not, like solver.py:207-208).  ``out``: a previous ``BarrierBatch`` for the
-    same table whose buffers are reused.  Returns a ``BarrierBatch`` (asynchronous).
+    same table whose buffers are reused.  ``want_factors`` adds the rank-1 factors z (hess = z z^T);
+    with ``want_hess=False`` the dense blocks are skipped and ``NewtonSystem.assemble_from_factors``
+    builds the matrix from z alone.  Returns a ``BarrierBatch`` (asynchronous).
     """
     if isinstance(table, StencilTable):
         table = DeviceStencilTable.from_host(table)
@@ -138,7 +142,8 @@ def evaluate(table, positions, params, dt=1.0, want_energy=True, want_grad=True,
                 continue
             fams[s] = Family(s, table.family_vids(s),
                              device.empty((nb, 3 * s)) if want_grad else None,
-                             device.empty((nb, 3 * s, 3 * s)) if want_hess else None)
+                             device.empty((nb, 3 * s, 3 * s)) if want_hess else None,
+                             device.empty((nb, 3 * s)) if want_factors else None)
         out = BarrierBatch(table, device.empty((n,)) if want_energy else None, device.empty((n,), np.uint8), fams)
     out._summary = None
     prm = c_params(params, dt)
@@ -148,11 +153,12 @@ def evaluate(table, positions, params, dt=1.0, want_energy=True, want_grad=True,
         fam = out.families.get(s)
         return device.ptr(getattr(fam, name) if fam is not None else None)
 
-    _lib.check(_lib.lib().b200ipc_barrier_stencils(
+    _lib.check(_lib.lib().b200ipc_barrier_stencils_ex(
         prm, pos.shape[0], device.ptr(pos), n, koff, device.ptr(table.verts), device.ptr(table.sub),
         device.ptr(table.eps_x), device.ptr(out.energy), device.ptr(out.status),
         fam_ptr(2, "grad"), fam_ptr(2, "hess"), fam_ptr(3, "grad"), fam_ptr(3, "hess"),
-        fam_ptr(4, "grad"), fam_ptr(4, "hess"), device.stream()), "barrier_stencils")
+        fam_ptr(4, "grad"), fam_ptr(4, "hess"), fam_ptr(2, "fac"), fam_ptr(3, "fac"), fam_ptr(4, "fac"),
+        device.stream()), "barrier_stencils")
     return out
 
 

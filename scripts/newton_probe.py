@@ -11,7 +11,7 @@ vt, ee = workloads.broad_phase(cloth)
 params = barrier.BarrierParams(d_hat=cloth.d_hat, kappa=cloth.kappa)
 pos = device.to_device(cloth.positions)
 table, _ = contacts.narrow_phase_device(pos, cloth.rest_positions, vt, ee, cloth.d_hat, want_origin=False)
-batch = stencils.evaluate(table, pos, params, dt=cloth.dt)
+batch = stencils.evaluate(table, pos, params, dt=cloth.dt, want_factors=True)
 fams = [batch.families[s] for s in sorted(batch.families)]
 sysm = solver.NewtonSystem(cloth.masses, cloth.fixed)
 nnzb = sysm.set_pattern([(f.s, f.vids) for f in fams])
@@ -21,6 +21,11 @@ for variant in (0, 1, 2, 3):
     sysm.set_numeric_variant(variant)
     ms = bench.time_steps(torch, lambda: sysm.assemble(hess), 20, 3, noop) / 20
     print("assemble variant", variant, "ms", ms, flush=True)
+fac = [f.fac for f in fams]
+print("assemble from factors ms", bench.time_steps(torch, lambda: sysm.assemble_from_factors(fac), 20, 3, noop) / 20, flush=True)
+lean = stencils.evaluate(table, pos, params, dt=cloth.dt, want_hess=False, want_factors=True)
+print("stencils factors-only ms", bench.time_steps(torch, lambda: stencils.evaluate(table, pos, params, dt=cloth.dt, want_hess=False, want_factors=True, out=lean), 20, 3, noop) / 20, flush=True)
+print("stencils dense ms", bench.time_steps(torch, lambda: stencils.evaluate(table, pos, params, dt=cloth.dt, want_factors=True, out=batch), 20, 3, noop) / 20, flush=True)
 sysm.set_numeric_variant(0); sysm.assemble(hess)
 x = device.to_device(np.random.default_rng(0).normal(size=3 * sysm.n)); y = device.empty((3 * sysm.n,))
 print("spmv ms", bench.time_steps(torch, lambda: sysm.spmv(x, out=y), 50, 5, noop) / 50, flush=True)

@@ -113,6 +113,33 @@ def test_gradient_scatter(S, scene):
     sysm.close()
 
 
+def test_factor_path_equals_dense_path(S, scene):
+    """Rank-1 factors: hess == z z^T bit for bit, and the matrix assembled from z alone equals the
+    one assembled from the dense blocks (bitwise for the per-block-run kernel, 1e-13 otherwise)."""
+    table = S.proximity.StencilTable(scene["kind"], scene["verts"], scene["sub"], scene["eps_x"])
+    params = S.barrier.BarrierParams(d_hat=float(scene["d_hat"]), kappa=float(scene["kappa"]))
+    full = S.stencils.evaluate(table, scene["positions"], params, dt=float(scene["dt"]), want_factors=True)
+    lean = S.stencils.evaluate(table, scene["positions"], params, dt=float(scene["dt"]), want_hess=False,
+                               want_factors=True)
+    fams = [full.families[s] for s in sorted(full.families)]
+    for f, g in zip(fams, [lean.families[s] for s in sorted(lean.families)]):
+        z = S.device.to_host(f.fac)
+        assert g.hess is None and np.array_equal(z, S.device.to_host(g.fac))
+        assert np.array_equal(S.device.to_host(f.hess), z[:, :, None] * z[:, None, :])
+    sysm = S.solver.NewtonSystem(scene["masses"], scene["fixed"])
+    sysm.set_pattern([(f.s, f.vids) for f in fams])
+    sysm.set_numeric_variant(1)
+    dense = S.device.to_host(sysm.assemble([f.hess for f in fams])).copy()
+    fused = S.device.to_host(sysm.assemble_from_factors([f.fac for f in fams])).copy()
+    assert np.array_equal(dense, fused)
+    sysm.set_numeric_variant(0)
+    rows = S.device.to_host(sysm.assemble([f.hess for f in fams]))
+    assert block_rel_err(fused, rows) < 1e-12
+    got = bsr_to_dense(sysm.n, S.device.to_host(sysm.rowptr), S.device.to_host(sysm.colidx), fused)
+    assert np.abs(got - scene["ref_dense"]).max() <= TOL * np.abs(scene["ref_dense"]).max()
+    sysm.close()
+
+
 def test_pcg_matches_reference(S, scene):
     rhs = -scene["ref_gradient"]
     d, iters, ok = S.solver.pcg_solve(scene["grouped"], scene["masses"], scene["fixed"], rhs, 1e-4, 2000)
