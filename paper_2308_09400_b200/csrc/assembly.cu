@@ -201,6 +201,7 @@ struct NumericArgs {
 };
 
 constexpr int kNumWarps = 8;
+constexpr int kBlocksPerWarp = 8;   // consecutive output blocks per warp (one descriptor prefetch for all)
 
 __device__ __forceinline__ double gather_entry(const NumericArgs& a, uint32_t d, int er, int ec) {
   const uint32_t f = d >> 30;
@@ -208,47 +209,66 @@ __device__ __forceinline__ double gather_entry(const NumericArgs& a, uint32_t d,
   return __ldg(a.hp.p[f] + e);
 }
 
-// One warp per output block: lanes (g, e) = (lane / 9, lane % 9), g < 3, walk the block's run of
-// sources three at a time, entry e of each 3x3 sub-block per lane, accumulating in a register; four
-// trips (twelve sub-blocks) of loads are in flight before the adds; the three partial sums are
-// combined in fixed order with two shuffles.  Lanes 0..8 write the block: nine consecutive doubles.
-// 32 registers, no shared memory: 64 resident warps per SM, which is what this latency-bound gather
-// needs (scripts/probes/gather_probe.cu).
-__global__ void __launch_bounds__(32 * kNumWarps, 8) assemble_numeric_kernel(const __grid_constant__ NumericArgs a) {
-  const int64_t u = (int64_t)blockIdx.x * kNumWarps + (threadIdx.x >> 5);
-  if (u >= a.nnzb) return;
+__device__ __forceinline__ void touch_l1(const void* p) {
+  unsigned tmp;
+  asm volatile("ld.global.ca.u32 %0, [%1];" : "=r"(tmp) : "l"(p));
+  (void)tmp;
+}
+
+// Shared walker of the per-block runs.  A warp owns kBlocksPerWarp consecutive output blocks, whose
+// sources are one contiguous span of descriptors: the span is pulled into L1 with coalesced loads up
+// front (one DRAM latency for the whole warp instead of one dependent miss per block), then each
+// block is reduced with lanes (g, e) = (lane / 9, lane % 9), g < 3: entry e of every third source,
+// twelve sub-blocks of loads in flight before the adds, three partial sums combined in fixed order by
+// two shuffles.  Lanes 0..8 write the block: nine consecutive doubles.  32 registers, no shared
+// memory: 64 resident warps per SM.  ENTRY(desc, er, ec) returns one entry of one source.
+template <typename ARGS, typename ENTRY>
+__device__ __forceinline__ void walk_runs(const ARGS& a, const uint32_t* __restrict__ desc, ENTRY entry) {
+  const int64_t u0 = ((int64_t)blockIdx.x * kNumWarps + (threadIdx.x >> 5)) * kBlocksPerWarp;
+  if (u0 >= a.nnzb) return;
   const int lane = threadIdx.x & 31;
+  const int nb = (int)min((int64_t)kBlocksPerWarp, a.nnzb - u0);
+  const int32_t mine = a.useg[u0 + min(lane, nb)];
+  const int32_t span0 = __shfl_sync(0xffffffffu, mine, 0), span1 = __shfl_sync(0xffffffffu, mine, nb);
+  for (int32_t t = span0 + lane; t < span1; t += 32) touch_l1(desc + t);  // 128-byte lines, fire and forget
   const int g = lane / 9, e = lane - 9 * g;
   const int er = e / 3, ec = e - 3 * er;
-  int32_t j0 = a.useg[u];
-  const int32_t j1 = a.useg[u + 1];
-  double acc = 0.0;
-  const uint32_t first = a.desc[j0];
-  if (first >= 0xC0000000u) {  // diagonal block: mass slot first
-    const uint32_t v = first & 0x3fffffffu;
-    if (a.fixed[v]) {  // Dirichlet vertex: unit diagonal, nothing else
-      if (lane < 9) a.vals[9 * u + lane] = er == ec ? 1.0 : 0.0;
-      return;
+  for (int i = 0; i < nb; ++i) {
+    int32_t j0 = __shfl_sync(0xffffffffu, mine, i);
+    const int32_t j1 = __shfl_sync(0xffffffffu, mine, i + 1);
+    const int64_t u = u0 + i;
+    double acc = 0.0;
+    const uint32_t first = desc[j0];
+    if (first >= 0xC0000000u) {  // diagonal block: mass slot first
+      const uint32_t v = first & 0x3fffffffu;
+      if (a.fixed[v]) {  // Dirichlet vertex: unit diagonal, nothing else
+        if (lane < 9) a.vals[9 * u + lane] = er == ec ? 1.0 : 0.0;
+        continue;
+      }
+      if (g == 0 && er == ec) acc = a.masses[v];
+      ++j0;
     }
-    if (g == 0 && er == ec) acc = a.masses[v];
-    ++j0;
-  }
-  if (g < 3) {
-    int32_t j = j0 + g;
-    for (; j + 9 < j1; j += 12) {
-      const uint32_t d0 = a.desc[j], d1 = a.desc[j + 3], d2 = a.desc[j + 6], d3 = a.desc[j + 9];
-      const double v0 = gather_entry(a, d0, er, ec), v1 = gather_entry(a, d1, er, ec);
-      const double v2 = gather_entry(a, d2, er, ec), v3 = gather_entry(a, d3, er, ec);
-      acc += v0;
-      acc += v1;
-      acc += v2;
-      acc += v3;
+    if (g < 3) {
+      int32_t j = j0 + g;
+      for (; j + 9 < j1; j += 12) {
+        const uint32_t d0 = desc[j], d1 = desc[j + 3], d2 = desc[j + 6], d3 = desc[j + 9];
+        const double v0 = entry(d0, er, ec), v1 = entry(d1, er, ec);
+        const double v2 = entry(d2, er, ec), v3 = entry(d3, er, ec);
+        acc += v0;
+        acc += v1;
+        acc += v2;
+        acc += v3;
+      }
+      for (; j < j1; j += 3) acc += entry(desc[j], er, ec);
     }
-    for (; j < j1; j += 3) acc += gather_entry(a, a.desc[j], er, ec);
+    const double s1 = __shfl_down_sync(0xffffffffu, acc, 9);   // group 1's partial sum (lanes 0..8)
+    const double s2 = __shfl_down_sync(0xffffffffu, acc, 18);  // group 2's
+    if (lane < 9) a.vals[9 * u + lane] = (acc + s1) + s2;
   }
-  const double s1 = __shfl_down_sync(0xffffffffu, acc, 9);   // group 1's partial sum (lanes 0..8)
-  const double s2 = __shfl_down_sync(0xffffffffu, acc, 18);  // group 2's
-  if (lane < 9) a.vals[9 * u + lane] = (acc + s1) + s2;
+}
+
+__global__ void __launch_bounds__(32 * kNumWarps, 8) assemble_numeric_kernel(const __grid_constant__ NumericArgs a) {
+  walk_runs(a, a.desc, [&](uint32_t d, int er, int ec) { return gather_entry(a, d, er, ec); });
 }
 
 // ---- numeric assembly straight from the rank-1 factors ---------------------------------------------
@@ -291,40 +311,7 @@ __device__ __forceinline__ double factor_entry(const FactorArgs& a, uint32_t d, 
 }
 
 __global__ void __launch_bounds__(32 * kNumWarps, 8) assemble_factors_kernel(const __grid_constant__ FactorArgs a) {
-  const int64_t u = (int64_t)blockIdx.x * kNumWarps + (threadIdx.x >> 5);
-  if (u >= a.nnzb) return;
-  const int lane = threadIdx.x & 31;
-  const int g = lane / 9, e = lane - 9 * g;
-  const int er = e / 3, ec = e - 3 * er;
-  int32_t j0 = a.useg[u];
-  const int32_t j1 = a.useg[u + 1];
-  double acc = 0.0;
-  const uint32_t first = a.fdesc[j0];
-  if (first >= 0xC0000000u) {
-    const uint32_t v = first & 0x3fffffffu;
-    if (a.fixed[v]) {
-      if (lane < 9) a.vals[9 * u + lane] = er == ec ? 1.0 : 0.0;
-      return;
-    }
-    if (g == 0 && er == ec) acc = a.masses[v];
-    ++j0;
-  }
-  if (g < 3) {
-    int32_t j = j0 + g;
-    for (; j + 9 < j1; j += 12) {
-      const uint32_t d0 = a.fdesc[j], d1 = a.fdesc[j + 3], d2 = a.fdesc[j + 6], d3 = a.fdesc[j + 9];
-      const double v0 = factor_entry(a, d0, er, ec), v1 = factor_entry(a, d1, er, ec);
-      const double v2 = factor_entry(a, d2, er, ec), v3 = factor_entry(a, d3, er, ec);
-      acc += v0;
-      acc += v1;
-      acc += v2;
-      acc += v3;
-    }
-    for (; j < j1; j += 3) acc += factor_entry(a, a.fdesc[j], er, ec);
-  }
-  const double s1 = __shfl_down_sync(0xffffffffu, acc, 9);
-  const double s2 = __shfl_down_sync(0xffffffffu, acc, 18);
-  if (lane < 9) a.vals[9 * u + lane] = (acc + s1) + s2;
+  walk_runs(a, a.fdesc, [&](uint32_t d, int er, int ec) { return factor_entry(a, d, er, ec); });
 }
 
 // ---- row-wise numeric assembly ------------------------------------------------------------------
@@ -878,7 +865,7 @@ extern "C" int b200ipc_assemble_numeric(b200ipc_assembly* h, const double* masse
   a.nnzb = h->nnzb; a.fixed = h->fixed.ptr; a.masses = masses;
   a.useg = h->useg.ptr; a.desc = h->desc.ptr; a.vals = vals;
   if (h->variant == 1 && packed_ok) {  // per-block runs (gather of 3x3 sub-blocks)
-    const unsigned grid = (unsigned)((h->nnzb + kNumWarps - 1) / kNumWarps);
+    const unsigned grid = (unsigned)((h->nnzb + kNumWarps * kBlocksPerWarp - 1) / (kNumWarps * kBlocksPerWarp));
     assemble_numeric_kernel<<<grid, 32 * kNumWarps, 0, (cudaStream_t)stream>>>(a);
     return post_launch();
   }
@@ -920,7 +907,7 @@ extern "C" int b200ipc_assemble_numeric_factors(b200ipc_assembly* h, const doubl
   }
   a.nnzb = h->nnzb; a.fixed = h->fixed.ptr; a.masses = masses; a.useg = h->useg.ptr; a.fdesc = h->fdesc.ptr;
   a.vals = vals;
-  const unsigned grid = (unsigned)((h->nnzb + kNumWarps - 1) / kNumWarps);
+  const unsigned grid = (unsigned)((h->nnzb + kNumWarps * kBlocksPerWarp - 1) / (kNumWarps * kBlocksPerWarp));
   assemble_factors_kernel<<<grid, 32 * kNumWarps, 0, (cudaStream_t)stream>>>(a);
   return post_launch();
 }
