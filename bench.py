@@ -218,7 +218,7 @@ def newton_section(torch, pkg, steps, warmup, peak, seed):
     table, _ = contacts.narrow_phase_device(pos, d_rest, d_vt, d_ee, cloth.d_hat, want_origin=False)
     torch.cuda.synchronize()
     t_narrow = time.perf_counter() - t0
-    batch = stencils.evaluate(table, pos, params, dt=cloth.dt)
+    batch = stencils.evaluate(table, pos, params, dt=cloth.dt, want_factors=True)
     batch.raise_on_penetration()
     fams = [batch.families[s] for s in sorted(batch.families)]
     sysm = solver.NewtonSystem(cloth.masses, cloth.fixed)
@@ -232,9 +232,16 @@ def newton_section(torch, pkg, steps, warmup, peak, seed):
     ms_symbolic = (time.perf_counter() - t0) * 1e3
     hess = [f.hess for f in fams]
     ms_numeric = time_steps(torch, lambda: sysm.assemble(hess), steps, warmup, noop) / steps
-    sysm.set_numeric_variant(1)
-    ms_numeric_runs = time_steps(torch, lambda: sysm.assemble(hess), steps, warmup, noop) / steps
+    sysm.set_numeric_variant(4)
+    ms_numeric_rows = time_steps(torch, lambda: sysm.assemble(hess), steps, warmup, noop) / steps
     sysm.set_numeric_variant(0)
+    # fused path: the matrix straight from the rank-1 factors, dense blocks never materialised
+    fac = [f.fac for f in fams]
+    ms_factors = time_steps(torch, lambda: sysm.assemble_from_factors(fac), steps, warmup, noop) / steps
+    lean = stencils.evaluate(table, pos, params, dt=cloth.dt, want_hess=False, want_factors=True)
+    ms_stencil_lean = time_steps(torch, lambda: stencils.evaluate(table, pos, params, dt=cloth.dt, want_hess=False,
+                                                                   want_factors=True, out=lean), steps, warmup, noop) / steps
+    del lean
     sysm.assemble(hess)
     x = device.to_device(np.random.default_rng(0).normal(size=3 * sysm.n))
     y = device.empty((3 * sysm.n,))
@@ -261,7 +268,10 @@ def newton_section(torch, pkg, steps, warmup, peak, seed):
         "workload": cloth.name + f" d_hat={cloth.d_hat:.3g} (teaser-style cloth stack)",
         "vertices": sysm.n, "contacts": n_c, "kinds": np.diff(table.kind_off).tolist(), "nnzb": nnzb,
         "host_broad_phase_s": t_broad, "narrow_phase_ms": t_narrow * 1e3,
-        "stencils_ms": ms_stencil, "symbolic_ms": ms_symbolic, "assembly_numeric_ms": ms_numeric, "assembly_numeric_block_runs_ms": ms_numeric_runs, "spmv_ms": ms_spmv,
+        "stencils_ms": ms_stencil, "symbolic_ms": ms_symbolic, "assembly_numeric_ms": ms_numeric, "assembly_numeric_rowwise_ms": ms_numeric_rows, "spmv_ms": ms_spmv,
+        "fused": {"stencils_factors_only_ms": ms_stencil_lean, "assembly_from_factors_ms": ms_factors,
+                  "note": "rank-1 path: the stencil kernel writes z (24 s bytes) instead of the dense block and the "
+                          "assembly gathers from z; same matrix bit for bit"},
         "assembly_plus_spmv_ms": ms_numeric + ms_spmv, "gradient_scatter_ms": ms_grad,
         "pcg_ms_per_iter": ms_pcg_iter, "pcg_solve_ms": ms_pcg_full, "pcg_iters": it_full, "pcg_converged": ok_full,
         "roofline_assembly": {"bound": "hbm", "achieved": num_bytes / ms_numeric / 1e6, "peak": peak, "unit": "GB/s",

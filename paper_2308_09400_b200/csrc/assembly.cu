@@ -65,7 +65,7 @@ struct b200ipc_assembly {
   int64_t nnzb = 0;
   int64_t ngslots = 0;     // sum nb*s
   bool ready = false;
-  int variant = 0;         // numeric kernel: 0 row-wise (default), 1 per-block runs
+  int variant = 0;         // numeric kernel: 0 auto (per-block runs when applicable), 1 runs, 2/3 row-wise family, 4 row-wise
   b200ipc::FamDesc fam;
   b200ipc::DevBuf<uint8_t> fixed;
   b200ipc::DevBuf<uint64_t> keys_a, keys_b;
@@ -705,7 +705,7 @@ extern "C" int b200ipc_assembly_create(b200ipc_assembly** out) {
 }
 
 extern "C" int b200ipc_assembly_set_variant(b200ipc_assembly* h, int32_t variant) {
-  if (!h || variant < 0 || variant > 3) return B200IPC_EINVAL;
+  if (!h || variant < 0 || variant > 4) return B200IPC_EINVAL;
   h->variant = variant;
   return 0;
 }
@@ -864,12 +864,12 @@ extern "C" int b200ipc_assemble_numeric(b200ipc_assembly* h, const double* masse
   }
   a.nnzb = h->nnzb; a.fixed = h->fixed.ptr; a.masses = masses;
   a.useg = h->useg.ptr; a.desc = h->desc.ptr; a.vals = vals;
-  if (h->variant == 1 && packed_ok) {  // per-block runs (gather of 3x3 sub-blocks)
+  if ((h->variant == 0 || h->variant == 1) && packed_ok) {  // per-block runs (gather of 3x3 sub-blocks)
     const unsigned grid = (unsigned)((h->nnzb + kNumWarps * kBlocksPerWarp - 1) / (kNumWarps * kBlocksPerWarp));
     assemble_numeric_kernel<<<grid, 32 * kNumWarps, 0, (cudaStream_t)stream>>>(a);
     return post_launch();
   }
-  if (h->variant >= 2) {  // family-specialised row-wise kernels
+  if (h->variant == 2 || h->variant == 3) {  // family-specialised row-wise kernels
     RowFamArgs q;
     for (int f = 0; f < kMaxFam; ++f) {
       q.base[f] = f < h->fam.nfam ? fam_hess[f] : nullptr;

@@ -108,12 +108,23 @@ __global__ void __launch_bounds__(kPT) pcg_kernel(const PcgArgs a) {
       // ---- q = A c, denom = c.q ------------------------------------------------------------------
       acc = 0.0;
       const int lane = threadIdx.x % LPR;
-      for (int64_t row = tid / LPR; row < a.n; row += nthreads / LPR) {
-        double y0, y1, y2;
-        bsr_row_product<LPR>(row, lane, a.rowptr, a.colidx, a.vals, a.c, y0, y1, y2);
-        if (lane == 0) {
-          a.q[3 * row] = y0; a.q[3 * row + 1] = y1; a.q[3 * row + 2] = y2;
-          acc += a.c[3 * row] * y0 + a.c[3 * row + 1] * y1 + a.c[3 * row + 2] * y2;
+      if (LPR == 32) {
+        for (int64_t row0 = (tid >> 5) * kSpmvRowsPerWarp; row0 < a.n; row0 += (nthreads >> 5) * kSpmvRowsPerWarp) {
+          bsr_rows_warp(row0, a.n, lane, a.rowptr, a.colidx, a.vals, a.c, [&](int64_t r, double y0, double y1, double y2) {
+            if (lane == 0) {
+              a.q[3 * r] = y0; a.q[3 * r + 1] = y1; a.q[3 * r + 2] = y2;
+              acc += a.c[3 * r] * y0 + a.c[3 * r + 1] * y1 + a.c[3 * r + 2] * y2;
+            }
+          });
+        }
+      } else {
+        for (int64_t row = tid / LPR; row < a.n; row += nthreads / LPR) {
+          double y0, y1, y2;
+          bsr_row_product<LPR>(row, lane, a.rowptr, a.colidx, a.vals, a.c, y0, y1, y2);
+          if (lane == 0) {
+            a.q[3 * row] = y0; a.q[3 * row + 1] = y1; a.q[3 * row + 2] = y2;
+            acc += a.c[3 * row] * y0 + a.c[3 * row + 1] * y1 + a.c[3 * row + 2] * y2;
+          }
         }
       }
       {
@@ -207,7 +218,7 @@ extern "C" int b200ipc_pcg(int64_t n, int64_t nnzb, const int32_t* rowptr, const
     if (want_per_sm >= 1 && want_per_sm < per_sm) per_sm = want_per_sm;
   }
   int64_t grid = (int64_t)sms * per_sm;
-  const int64_t want = (n * lpr + kPT - 1) / kPT;  // no more CTAs than rows need
+  const int64_t want = ((lpr == 32 ? (n + kSpmvRowsPerWarp - 1) / kSpmvRowsPerWarp : n) * lpr + kPT - 1) / kPT;
   if (grid > want) grid = want;
   if (grid > kMaxParts) grid = kMaxParts;
   if (grid < 1) grid = 1;

@@ -14,6 +14,14 @@ __global__ void __launch_bounds__(kST, 8) bsr_spmv_kernel(int64_t n, const int32
                                                        const double* __restrict__ vals, const double* __restrict__ x,
                                                        double* __restrict__ y) {
   const int lane = threadIdx.x % LPR;
+  if (LPR == 32) {
+    const int64_t row0 = (((int64_t)blockIdx.x * kST + threadIdx.x) >> 5) * kSpmvRowsPerWarp;
+    if (row0 >= n) return;
+    bsr_rows_warp(row0, n, lane, rowptr, colidx, vals, x, [&](int64_t r, double y0, double y1, double y2) {
+      if (lane < 3) y[3 * r + lane] = lane == 0 ? y0 : (lane == 1 ? y1 : y2);
+    });
+    return;
+  }
   const int64_t row = ((int64_t)blockIdx.x * kST + threadIdx.x) / LPR;
   if (row >= n) return;  // whole groups exit together (kST % LPR == 0)
   double y0, y1, y2;
@@ -68,7 +76,8 @@ extern "C" int b200ipc_bsr_spmv(int64_t n, int64_t nnzb, const int32_t* rowptr, 
   if (!rowptr || !colidx || !vals || !x || !y) return B200IPC_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
   const int lpr = pick_lpr(n, nnzb);
-  const unsigned grid = (unsigned)((n * lpr + kST - 1) / kST);
+  const int64_t groups = lpr == 32 ? (n + kSpmvRowsPerWarp - 1) / kSpmvRowsPerWarp : n;
+  const unsigned grid = (unsigned)((groups * lpr + kST - 1) / kST);
   if (lpr == 32) bsr_spmv_kernel<32><<<grid, kST, 0, st>>>(n, rowptr, colidx, vals, x, y);
   else if (lpr == 16) bsr_spmv_kernel<16><<<grid, kST, 0, st>>>(n, rowptr, colidx, vals, x, y);
   else bsr_spmv_kernel<8><<<grid, kST, 0, st>>>(n, rowptr, colidx, vals, x, y);

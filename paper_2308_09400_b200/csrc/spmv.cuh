@@ -16,11 +16,10 @@ namespace b200ipc {
 // row, so the entry index, the x component and the accumulator are lane constants -- no index
 // arithmetic, no selects.  27 of 32 lanes work; each trip reads three whole blocks (216 contiguous
 // bytes) and two trips are in flight.  Five shuffles finish the row.
-__device__ __forceinline__ void bsr_row_product_warp(int64_t row, int lane, const int32_t* __restrict__ rowptr,
+__device__ __forceinline__ void bsr_row_product_span(int32_t b0, int32_t nblk, int lane,
                                                      const int32_t* __restrict__ colidx,
                                                      const double* __restrict__ vals, const double* __restrict__ x,
                                                      double& y0, double& y1, double& y2) {
-  const int32_t b0 = rowptr[row], nblk = rowptr[row + 1] - b0;
   const int g = lane / 9, e = lane - 9 * g;
   const int j = e % 3;
   const double* v = vals + 9ll * b0 + e;
@@ -46,6 +45,45 @@ __device__ __forceinline__ void bsr_row_product_warp(int64_t row, int lane, cons
   y0 = __shfl_sync(0xffffffffu, u, 0);
   y1 = __shfl_sync(0xffffffffu, u, 3);
   y2 = __shfl_sync(0xffffffffu, u, 6);
+}
+
+__device__ __forceinline__ void bsr_row_product_warp(int64_t row, int lane, const int32_t* __restrict__ rowptr,
+                                                     const int32_t* __restrict__ colidx,
+                                                     const double* __restrict__ vals, const double* __restrict__ x,
+                                                     double& y0, double& y1, double& y2) {
+  const int32_t b0 = rowptr[row];
+  bsr_row_product_span(b0, rowptr[row + 1] - b0, lane, colidx, vals, x, y0, y1, y2);
+}
+
+__device__ __forceinline__ void spmv_touch(const void* p) {
+  unsigned tmp;
+  asm volatile("ld.global.ca.u32 %0, [%1];" : "=r"(tmp) : "l"(p));
+  (void)tmp;
+}
+
+constexpr int kSpmvRowsPerWarp = 4;
+
+// A warp owns kSpmvRowsPerWarp consecutive block rows: their values and column indices are ONE
+// contiguous span, pulled towards L1 with one round of coalesced line touches before the rows are
+// reduced one after the other -- one exposed DRAM/L2 latency per warp instead of one per row.
+// emit(row, y0, y1, y2) is called (by all lanes) once per row.
+template <typename EMIT>
+__device__ __forceinline__ void bsr_rows_warp(int64_t row0, int64_t n, int lane, const int32_t* __restrict__ rowptr,
+                                              const int32_t* __restrict__ colidx, const double* __restrict__ vals,
+                                              const double* __restrict__ x, EMIT emit) {
+  const int nr = (int)min((int64_t)kSpmvRowsPerWarp, n - row0);
+  const int32_t mine = rowptr[row0 + min(lane, nr)];
+  const int32_t s0 = __shfl_sync(0xffffffffu, mine, 0), s1 = __shfl_sync(0xffffffffu, mine, nr);
+  const char* vb = reinterpret_cast<const char*>(vals + 9ll * s0);
+  const int64_t vbytes = 72ll * (s1 - s0);
+  for (int64_t t = 128ll * lane; t < vbytes; t += 128 * 32) spmv_touch(vb + t);
+  if (4ll * lane * 32 < 4ll * (s1 - s0)) spmv_touch(colidx + s0 + 32 * lane);
+  for (int i = 0; i < nr; ++i) {
+    const int32_t b0 = __shfl_sync(0xffffffffu, mine, i), b1 = __shfl_sync(0xffffffffu, mine, i + 1);
+    double y0, y1, y2;
+    bsr_row_product_span(b0, b1 - b0, lane, colidx, vals, x, y0, y1, y2);
+    emit(row0 + i, y0, y1, y2);
+  }
 }
 
 // Returns (y0,y1,y2) of block row `row` in every lane of the group.

@@ -132,7 +132,7 @@ def test_factor_path_equals_dense_path(S, scene):
     dense = S.device.to_host(sysm.assemble([f.hess for f in fams])).copy()
     fused = S.device.to_host(sysm.assemble_from_factors([f.fac for f in fams])).copy()
     assert np.array_equal(dense, fused)
-    sysm.set_numeric_variant(0)
+    sysm.set_numeric_variant(4)
     rows = S.device.to_host(sysm.assemble([f.hess for f in fams]))
     assert block_rel_err(fused, rows) < 1e-12
     got = bsr_to_dense(sysm.n, S.device.to_host(sysm.rowptr), S.device.to_host(sysm.colidx), fused)
@@ -205,7 +205,7 @@ def test_random_blocks_assembly_vs_oracle(S, n, nb):
     assert rowptr[8] - rowptr[7] > 500
     assert block_rel_err(vals, o_vals) < 1e-12
     # the alternative numeric kernels give the same matrix
-    for variant in (1, 2, 3):
+    for variant in (1, 2, 3, 4):
         alt = S.solver._system_from_grouped(grouped, masses, fixed, variant=variant)
         assert block_rel_err(S.device.to_host(alt.vals), o_vals) < 1e-12, variant
         alt.close()
