@@ -109,8 +109,14 @@ __global__ void __launch_bounds__(kPT) pcg_kernel(const PcgArgs a) {
       acc = 0.0;
       const int lane = threadIdx.x % LPR;
       if (LPR == 32) {
-        for (int64_t row0 = (tid >> 5) * kSpmvRowsPerWarp; row0 < a.n; row0 += (nthreads >> 5) * kSpmvRowsPerWarp) {
-          bsr_rows_warp(row0, a.n, lane, a.rowptr, a.colidx, a.vals, a.c, [&](int64_t r, double y0, double y1, double y2) {
+        // contiguous, equal-sized row chunk per warp (a coarse grid-stride would leave whole
+        // kSpmvRowsPerWarp-row quanta to a few straggler warps every iteration)
+        const int64_t nwarps = nthreads >> 5;
+        const int64_t chunk = (a.n + nwarps - 1) / nwarps;
+        const int64_t rbeg = (tid >> 5) * chunk;
+        const int64_t rend = rbeg + chunk < a.n ? rbeg + chunk : a.n;
+        for (int64_t row0 = rbeg; row0 < rend; row0 += kSpmvRowsPerWarp) {
+          bsr_rows_warp(row0, rend, lane, a.rowptr, a.colidx, a.vals, a.c, [&](int64_t r, double y0, double y1, double y2) {
             if (lane == 0) {
               a.q[3 * r] = y0; a.q[3 * r + 1] = y1; a.q[3 * r + 2] = y2;
               acc += a.c[3 * r] * y0 + a.c[3 * r + 1] * y1 + a.c[3 * r + 2] * y2;

@@ -148,10 +148,18 @@ def test_pcg_matches_reference(S, scene):
     ref_it = int(scene["ref_pcg_iters"])
     assert ok == bool(scene["ref_pcg_ok"]) and abs(iters - ref_it) <= 2 + 0.05 * ref_it, (iters, ref_it)
     assert np.all(d.reshape(-1, 3)[scene["fixed"]] == 0.0)
-    # same Krylov iterate up to round-off amplified by the conditioning: compare in the energy norm
+    # the stopping criterion itself, re-evaluated with the reference's own matrix and preconditioner
     a = scene["ref_dense"]
+    n = scene["masses"].shape[0]
+    r0 = rhs.copy()
+    r0.reshape(n, 3)[scene["fixed"]] = 0.0
+    prec = lambda r: np.einsum("nij,nj->ni", scene["ref_pinv"], r.reshape(n, 3)).reshape(-1)  # noqa: E731
+    delta0 = r0 @ prec(r0)
+    res = r0 - a @ d
+    assert res @ prec(res) <= 1.01e-4 * delta0
+    # same Krylov iterate up to the few iterations by which round-off moves the stop
     diff = d - scene["ref_pcg_d"]
-    assert np.sqrt(diff @ a @ diff) <= 1e-2 * np.sqrt(scene["ref_pcg_d"] @ a @ scene["ref_pcg_d"])
+    assert np.sqrt(diff @ a @ diff) <= 0.1 * np.sqrt(scene["ref_pcg_d"] @ a @ scene["ref_pcg_d"])
     d12, it12, ok12 = S.solver.pcg_solve(scene["grouped"], scene["masses"], scene["fixed"], rhs, 1e-12, 5000)
     # ~1000 iterations on a kappa = 2e8 system: round-off reorders convergence by a few percent
     assert ok12 and abs(it12 - int(scene["ref_pcg12_iters"])) <= 0.05 * int(scene["ref_pcg12_iters"])
