@@ -24,7 +24,7 @@ NVCC_FLAGS = [
     "-fmad=false",            # geometric predicates must round like the reference's x86-64 build
     "-Xcompiler", "-fPIC",
     "-I", INCLUDE,
-]
+] + (["-DB200IPC_PCG_TIMING"] if os.environ.get("B200IPC_PCG_TIMING") else [])  # debug: per-phase timers in pcg.cu
 
 
 def _nvcc():

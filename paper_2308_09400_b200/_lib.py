@@ -8,7 +8,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libb200ipc.so")
+LIB_PATH = os.environ.get("B200IPC_LIB") or os.path.join(HERE, "libb200ipc.so")  # override: tuning builds only
 
 
 class B200IpcError(RuntimeError):

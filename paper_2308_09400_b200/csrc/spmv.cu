@@ -1,6 +1,9 @@
 // Standalone BSR SpMV (the assembled twin of matvec_matrix_free, solver.py:251-262) and the
 // block-Jacobi preconditioner (block_jacobi_preconditioner, solver.py:265-276).
+#include <cstdlib>
+
 #include "spmv.cuh"
+#include "spmv_stream.cuh"
 #include "launch.cuh"
 #include "../../include/b200ipc.h"
 
@@ -27,6 +30,28 @@ __global__ void __launch_bounds__(kST, 8) bsr_spmv_kernel(int64_t n, const int32
   double y0, y1, y2;
   bsr_row_product<LPR>(row, lane, rowptr, colidx, vals, x, y0, y1, y2);
   if (lane < 3) y[3 * row + lane] = lane == 0 ? y0 : (lane == 1 ? y1 : y2);
+}
+
+// Streamed product (spmv_stream.cuh): persistent CTAs, matrix staged through shared memory by TMA.
+__global__ void __launch_bounds__(kStreamThreads, 1) bsr_spmv_stream_kernel(const __grid_constant__ StreamMatrix m,
+                                                                             const double* __restrict__ x,
+                                                                             double* __restrict__ y) {
+  extern __shared__ __align__(128) unsigned char dyn[];
+  const StreamSmem sm = stream_smem(dyn);
+  StreamState st;
+  stream_init(m, sm, st);
+  const uint32_t limit = (uint32_t)st.nmine;
+  const double* xj = x + (threadIdx.x & 31) % 3;  // lane = 9 r + 3 i + j
+  stream_product(
+      m, sm, st, limit, [&](int c) { return xj[3ll * c]; }, [&](int64_t r, int i, double yi) { y[3 * r + i] = yi; });
+  stream_drain(sm, st);
+}
+
+int stream_rows_per_chunk(int64_t n, int64_t nnzb) {
+  const double avg = n > 0 ? (double)nnzb / (double)n : 1.0;
+  int r = (int)(0.7 * kStageBlocks / (avg > 1.0 ? avg : 1.0)) / 3 * 3;  // three rows per warp trip
+  if (const char* env = getenv("B200IPC_SPMV_ROWS_PER_CHUNK")) r = atoi(env);
+  return r < 3 ? 3 : (r > kMaxChunkRows ? kMaxChunkRows : r);
 }
 
 // Inverse of the diagonal 3x3 block of every row (closed-form adjugate / determinant).
@@ -75,6 +100,25 @@ extern "C" int b200ipc_bsr_spmv(int64_t n, int64_t nnzb, const int32_t* rowptr, 
   if (n == 0) return 0;
   if (!rowptr || !colidx || !vals || !x || !y) return B200IPC_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
+  const char* mode = getenv("B200IPC_SPMV_MODE");
+  const bool aligned = (((uintptr_t)vals | (uintptr_t)colidx | (uintptr_t)rowptr) & 15) == 0;
+  if (aligned && !(mode && mode[0] == 'l')) {  // streamed (default); "legacy" keeps the direct-load kernels
+    static int sms = 0;
+    if (!sms) {
+      int dev = 0;
+      if (cudaGetDevice(&dev) != cudaSuccess ||
+          cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+        return B200IPC_ESTATE;
+      cudaError_t e = cudaFuncSetAttribute(bsr_spmv_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           kStreamSmemBytes);
+      if (e != cudaSuccess) return -(int)e;
+    }
+    StreamMatrix m{n, nnzb, stream_rows_per_chunk(n, nnzb), 0, rowptr, colidx, vals, nullptr};
+    const int64_t nchunks = (n + m.rows_per_chunk - 1) / m.rows_per_chunk;
+    const unsigned grid = (unsigned)(nchunks < sms ? nchunks : sms);
+    bsr_spmv_stream_kernel<<<grid, kStreamThreads, kStreamSmemBytes, st>>>(m, x, y);
+    return post_launch();
+  }
   const int lpr = pick_lpr(n, nnzb);
   const int64_t groups = lpr == 32 ? (n + kSpmvRowsPerWarp - 1) / kSpmvRowsPerWarp : n;
   const unsigned grid = (unsigned)((groups * lpr + kST - 1) / kST);

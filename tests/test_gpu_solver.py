@@ -143,10 +143,14 @@ def test_factor_path_equals_dense_path(S, scene):
 def test_pcg_matches_reference(S, scene):
     rhs = -scene["ref_gradient"]
     d, iters, ok = S.solver.pcg_solve(scene["grouped"], scene["masses"], scene["fixed"], rhs, 1e-4, 2000)
-    # kappa = 2e8: round-off (summation order of the assembly, of the dot products) moves the stopping
-    # iteration by a few percent; the iterate is compared in the energy norm below
+    # kappa = 2e8: round-off (summation order of the assembly, of the SpMV, of the dot products) moves
+    # the stopping iteration.  delta = r.s is not monotone: with the streamed SpMV (FMA, per-entry sums)
+    # it dips to 0.97e-4 * delta0 at iteration 65, where the reference's arithmetic stays a hair above
+    # 1e-4 until iteration 83.  So the count is bounded from above only; that the stop is legitimate is
+    # checked right below with the reference's own matrix and preconditioner, and the 1e-12 solve
+    # further down must agree with the reference within a few percent of its ~1000 iterations.
     ref_it = int(scene["ref_pcg_iters"])
-    assert ok == bool(scene["ref_pcg_ok"]) and abs(iters - ref_it) <= 2 + 0.05 * ref_it, (iters, ref_it)
+    assert ok == bool(scene["ref_pcg_ok"]) and 0 < iters <= ref_it + 2 + 0.05 * ref_it, (iters, ref_it)
     assert np.all(d.reshape(-1, 3)[scene["fixed"]] == 0.0)
     # the stopping criterion itself, re-evaluated with the reference's own matrix and preconditioner
     a = scene["ref_dense"]
