@@ -163,6 +163,30 @@ int b200ipc_barrier_stencils_ex(const b200ipc_params* params /* host */, int64_t
 int b200ipc_reduce_energy(int64_t n, const double* energy, const uint8_t* status,
                           double* result, int64_t* counts, void* workspace, void* stream);
 
+/* ---- broad phase: scene -> candidate queries ------------------------------------ */
+/* The AABB stage of find_contact_pairs (proximity.py:232-248, :275-319) as a uniform-grid join.
+ * VT candidates: every (surface vertex v, triangle t) whose boxes [x_v - d_hat, x_v + d_hat] and
+ * AABB(t) overlap and v is not a corner of t (:278-287).  EE candidates: every pair of edges i < j
+ * whose AABBs, each inflated by d_hat/2, overlap and that share no endpoint (:305-317).  The overlap
+ * predicate is the reference's own (lo_a <= hi_b && lo_b <= hi_a on the same fp64 corners), so the
+ * candidate SETS equal the reference's; each pair is reported exactly once.  surf_verts (n_sv) i32,
+ * tris (n_tri,3) i32, edges (n_edge,2) i32, positions (nverts,3) f64: device.  `cell` (> 0, typically
+ * max(2 d_hat, median edge length)) and origin[3] (host; at or below the scene's lower corner) define
+ * the grid; they affect speed only.
+ * _count bins and joins once to size the outputs (*n_vt, *n_ee: host; synchronises `stream`);
+ * _fill writes vt (n_vt,4) = (v, t1, t2, t3) and ee (n_ee,4) = (a1, a2, b1, b2), both 16-byte
+ * aligned i32, ready for b200ipc_narrow_phase.  The input arrays must stay alive and unchanged
+ * between the two calls.  One handle per scene/GPU; not thread-safe. */
+typedef struct b200ipc_broad b200ipc_broad;
+int b200ipc_broad_create(b200ipc_broad** out);
+int b200ipc_broad_destroy(b200ipc_broad* h);
+int b200ipc_broad_phase_count(b200ipc_broad* h, int64_t nverts, const double* positions,
+                              int64_t n_sv, const int32_t* surf_verts, int64_t n_tri, const int32_t* tris,
+                              int64_t n_edge, const int32_t* edges, double d_hat, double cell,
+                              const double* origin /* host[3] */, int64_t* n_vt /* host */,
+                              int64_t* n_ee /* host */, void* stream);
+int b200ipc_broad_phase_fill(b200ipc_broad* h, int32_t* vt, int32_t* ee, void* stream);
+
 /* ---- narrow phase: candidate queries -> ordered contact list ------------------- */
 /* find_contact_pairs without its broad phase (proximity.py:284-358).  vt (n_vt,4) i32 =
  * (vertex, t1, t2, t3) and ee (n_ee,4) i32 = (a1, a2, b1, b2): any duplicate-free superset of

@@ -718,6 +718,47 @@ _EE_SEL = np.array([EE_LOCAL[c][1] + (0,) * (4 - len(EE_LOCAL[c][1])) for c in r
 _EE_SUB = np.array([pack_sub(EE_LOCAL[c][1]) for c in range(9)], dtype=np.uint8)
 
 
+def aabb_candidates(positions, surf_verts, tris, edges, d_hat):
+    """The reference's broad phase, all pairs (proximity.py:232-248, :275-287, :303-317).
+
+    Returns (vt (m,4), ee (k,4)): every (surface vertex, triangle) whose boxes
+    [p - d_hat, p + d_hat] and AABB(triangle) overlap with the vertex not a corner, and every
+    edge pair i < j whose AABBs inflated by d_hat/2 overlap and that share no endpoint -- rows in
+    the reference's order (by first box, then second).  O(n^2) memory: small scenes only.
+    """
+    x = np.asarray(positions, dtype=np.float64)
+    tris = np.asarray(tris, dtype=np.int64).reshape(-1, 3)
+    edges = np.asarray(edges, dtype=np.int64).reshape(-1, 2)
+    verts = np.asarray(surf_verts, dtype=np.int64)
+
+    def overlap(lo_a, hi_a, lo_b, hi_b):
+        ok = np.ones((lo_a.shape[0], lo_b.shape[0]), dtype=bool)
+        for k in range(3):
+            ok &= lo_a[:, k:k + 1] <= hi_b[None, :, k]
+            ok &= lo_b[None, :, k] <= hi_a[:, k:k + 1]
+        return np.argwhere(ok)
+
+    vt = np.zeros((0, 4), np.int64)
+    if verts.size and tris.size:
+        p = x[verts]
+        tx = x[tris]
+        pairs = overlap(p - d_hat, p + d_hat, tx.min(axis=1), tx.max(axis=1))
+        vid, tv = verts[pairs[:, 0]], tris[pairs[:, 1]]
+        keep = (vid != tv[:, 0]) & (vid != tv[:, 1]) & (vid != tv[:, 2])
+        vt = np.concatenate([vid[keep, None], tv[keep]], axis=1)
+    ee = np.zeros((0, 4), np.int64)
+    if edges.shape[0] > 1:
+        e1, e2 = x[edges[:, 0]], x[edges[:, 1]]
+        lo_e = np.minimum(e1, e2) - d_hat * 0.5
+        hi_e = np.maximum(e1, e2) + d_hat * 0.5
+        pairs = overlap(lo_e, hi_e, lo_e, hi_e)
+        pairs = pairs[pairs[:, 0] < pairs[:, 1]]
+        ea, eb = edges[pairs[:, 0]], edges[pairs[:, 1]]
+        keep = (ea[:, 0] != eb[:, 0]) & (ea[:, 0] != eb[:, 1]) & (ea[:, 1] != eb[:, 0]) & (ea[:, 1] != eb[:, 1])
+        ee = np.concatenate([ea[keep], eb[keep]], axis=1)
+    return vt, ee
+
+
 def narrow_phase(positions, rest_positions, vt_pairs, ee_pairs, d_hat, promote_parallel=True):
     """Candidate queries -> the reference's ordered contact list as a table.
 

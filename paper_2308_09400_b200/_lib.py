@@ -66,6 +66,11 @@ SIGNATURES = {
     "b200ipc_mollified_eigensystem": [C.POINTER(Params), _i64, _vp, _vp, _vp, _vp, _vp],
     "b200ipc_narrow_phase": [_i64, _vp, _vp, _i64, _vp, _i64, _vp, _dbl, _i32, _vp, _vp, _vp, _vp, _vp, _vp,
                              C.POINTER(_i64), C.POINTER(_i64), _vp],
+    "b200ipc_broad_create": [C.POINTER(_vp)],
+    "b200ipc_broad_destroy": [_vp],
+    "b200ipc_broad_phase_count": [_vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _dbl, _dbl, C.POINTER(_dbl),
+                                  C.POINTER(_i64), C.POINTER(_i64), _vp],
+    "b200ipc_broad_phase_fill": [_vp, _vp, _vp, _vp],
     "b200ipc_assembly_create": [C.POINTER(_vp)],
     "b200ipc_assembly_destroy": [_vp],
     "b200ipc_assembly_set_variant": [_vp, _i32],

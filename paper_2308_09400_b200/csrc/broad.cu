@@ -1,0 +1,360 @@
+// Broad phase of find_contact_pairs (proximity.py:232-248, :275-319) on the device: the candidate
+// point-triangle and edge-edge queries the narrow phase (narrow.cu) classifies.
+//
+// The reference tests every (surface vertex, triangle) and every (edge, edge) pair for AABB overlap --
+// O(n^2) boolean matrices.  Here both joins run on a uniform grid:
+//   1. every "B" box (triangle AABB; edge AABB inflated by d_hat/2) is binned into the cells it
+//      overlaps: count, scan, fill (cell key, box), stable radix sort by cell key;
+//   2. every "A" box (vertex box [p - d_hat, p + d_hat]; inflated edge AABB) walks its cells, finds
+//      each cell's run of B boxes by binary search, and keeps a pair when
+//        - the boxes overlap (the reference's own predicate lo_a <= hi_b && lo_b <= hi_a on the same
+//          fp64 box corners, so the candidate SET equals the reference's),
+//        - this cell holds the lower corner of the boxes' intersection (a pair sharing several
+//          cells is reported exactly once: no de-duplication pass),
+//        - the reference's incidence filters pass (vertex not a corner of the triangle, :286;
+//          edge index i < j and no shared endpoint, :311-317);
+//      first to count, then -- after a scan -- to write (A, B) as global vertex ids.
+// Output order is deterministic (by A box, cell, B box) but irrelevant: the narrow phase sorts.
+#include <cub/cub.cuh>
+
+#include "launch.cuh"
+#include "../../include/b200ipc.h"
+
+namespace b200ipc {
+
+constexpr int kBT = 256;
+
+template <typename T>
+struct BroadBuf {
+  T* ptr = nullptr;
+  size_t cap = 0;
+  cudaError_t reserve(size_t n) {
+    if (n <= cap) return cudaSuccess;
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    cap = 0;
+    const size_t want = n + n / 4 + 64;  // head-room: contact sets drift from step to step
+    cudaError_t e = cudaMalloc(&ptr, want * sizeof(T));
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    cap = 0;
+  }
+};
+
+struct Grid {
+  double ox, oy, oz;  // origin
+  double inv;         // 1 / cell
+};
+
+struct Box {
+  double lx, ly, lz, hx, hy, hz;
+};
+
+__device__ __forceinline__ int cell_of(double x, double o, double inv) {
+  const double c = floor((x - o) * inv);
+  return c < 0.0 ? 0 : (c > 2097151.0 ? 2097151 : (int)c);  // 21 bits per axis
+}
+__device__ __forceinline__ uint64_t cell_key(int cx, int cy, int cz) {
+  return ((uint64_t)cx << 42) | ((uint64_t)cy << 21) | (uint64_t)cz;
+}
+__device__ __forceinline__ void ld3(const double* p, int v, double& x, double& y, double& z) {
+  x = p[3ll * v];
+  y = p[3ll * v + 1];
+  z = p[3ll * v + 2];
+}
+
+// KIND 0: vertex box, 1: triangle AABB, 2: inflated edge AABB  (proximity.py:278-281, :305-307)
+template <int KIND>
+__device__ __forceinline__ Box make_box(const double* __restrict__ pos, const int32_t* __restrict__ elems, int64_t i,
+                                        double d_hat) {
+  Box b;
+  if (KIND == 0) {
+    double x, y, z;
+    ld3(pos, elems[i], x, y, z);
+    b.lx = x - d_hat; b.ly = y - d_hat; b.lz = z - d_hat;
+    b.hx = x + d_hat; b.hy = y + d_hat; b.hz = z + d_hat;
+  } else if (KIND == 1) {
+    double x0, y0, z0, x1, y1, z1, x2, y2, z2;
+    ld3(pos, elems[3 * i], x0, y0, z0);
+    ld3(pos, elems[3 * i + 1], x1, y1, z1);
+    ld3(pos, elems[3 * i + 2], x2, y2, z2);
+    b.lx = fmin(fmin(x0, x1), x2); b.ly = fmin(fmin(y0, y1), y2); b.lz = fmin(fmin(z0, z1), z2);
+    b.hx = fmax(fmax(x0, x1), x2); b.hy = fmax(fmax(y0, y1), y2); b.hz = fmax(fmax(z0, z1), z2);
+  } else {
+    double x0, y0, z0, x1, y1, z1;
+    ld3(pos, elems[2 * i], x0, y0, z0);
+    ld3(pos, elems[2 * i + 1], x1, y1, z1);
+    const double h = d_hat * 0.5;
+    b.lx = fmin(x0, x1) - h; b.ly = fmin(y0, y1) - h; b.lz = fmin(z0, z1) - h;
+    b.hx = fmax(x0, x1) + h; b.hy = fmax(y0, y1) + h; b.hz = fmax(z0, z1) + h;
+  }
+  return b;
+}
+
+struct Span {
+  int x0, y0, z0, x1, y1, z1;
+  __device__ __forceinline__ int64_t count() const { return (int64_t)(x1 - x0 + 1) * (y1 - y0 + 1) * (z1 - z0 + 1); }
+};
+__device__ __forceinline__ Span span_of(const Box& b, const Grid& g) {
+  Span s;
+  s.x0 = cell_of(b.lx, g.ox, g.inv); s.y0 = cell_of(b.ly, g.oy, g.inv); s.z0 = cell_of(b.lz, g.oz, g.inv);
+  s.x1 = cell_of(b.hx, g.ox, g.inv); s.y1 = cell_of(b.hy, g.oy, g.inv); s.z1 = cell_of(b.hz, g.oz, g.inv);
+  return s;
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kBT) bin_count_kernel(const double* __restrict__ pos, const int32_t* __restrict__ elems,
+                                                        int64_t n, double d_hat, Grid g, int32_t* __restrict__ cnt) {
+  const int64_t i = (int64_t)blockIdx.x * kBT + threadIdx.x;
+  if (i >= n) return;
+  const int64_t c = span_of(make_box<KIND>(pos, elems, i, d_hat), g).count();
+  cnt[i] = (int32_t)(c > 0x7fffffff ? 0x7fffffff : c);
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kBT) bin_fill_kernel(const double* __restrict__ pos, const int32_t* __restrict__ elems,
+                                                       int64_t n, double d_hat, Grid g, const int64_t* __restrict__ off,
+                                                       uint64_t* __restrict__ keys, uint32_t* __restrict__ ids) {
+  const int64_t i = (int64_t)blockIdx.x * kBT + threadIdx.x;
+  if (i >= n) return;
+  const Span s = span_of(make_box<KIND>(pos, elems, i, d_hat), g);
+  int64_t o = off[i];
+  for (int cx = s.x0; cx <= s.x1; ++cx)
+    for (int cy = s.y0; cy <= s.y1; ++cy)
+      for (int cz = s.z0; cz <= s.z1; ++cz) {
+        keys[o] = cell_key(cx, cy, cz);
+        ids[o] = (uint32_t)i;
+        ++o;
+      }
+}
+
+__device__ __forceinline__ int64_t lower_bound_u64(const uint64_t* __restrict__ a, int64_t n, uint64_t key) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (a[mid] < key) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+struct JoinArgs {
+  const double* pos;
+  const int32_t* a_elems;   // surf_verts (VT) or edges (EE)
+  const int32_t* b_elems;   // tris (VT) or edges (EE)
+  int64_t na, nbins;        // A boxes; sorted (cell, B box) incidences
+  double d_hat;
+  Grid g;
+  const uint64_t* keys;     // sorted
+  const uint32_t* ids;
+  const int64_t* off;       // per A box output offset (fill pass)
+  int32_t* cnt;             // per A box pair count (count pass)
+  int4* out;                // (pairs, 4) global vertex ids (fill pass)
+};
+
+// EE = false: A = vertex boxes, B = triangles.  EE = true: A = B = inflated edge boxes.
+template <bool EE, bool FILL>
+__global__ void __launch_bounds__(kBT) join_kernel(const __grid_constant__ JoinArgs a) {
+  const int64_t i = (int64_t)blockIdx.x * kBT + threadIdx.x;
+  if (i >= a.na) return;
+  const Box A = EE ? make_box<2>(a.pos, a.a_elems, i, a.d_hat) : make_box<0>(a.pos, a.a_elems, i, a.d_hat);
+  const Span s = span_of(A, a.g);
+  int av0, av1 = -1;
+  if (EE) {
+    av0 = a.a_elems[2 * i];
+    av1 = a.a_elems[2 * i + 1];
+  } else {
+    av0 = a.a_elems[i];
+  }
+  int32_t n = 0;
+  int64_t o = FILL ? a.off[i] : 0;
+  for (int cx = s.x0; cx <= s.x1; ++cx)
+    for (int cy = s.y0; cy <= s.y1; ++cy) {
+      // cells (cx, cy, z0..z1) are consecutive keys: one search, one walk
+      const uint64_t k0 = cell_key(cx, cy, s.z0), k1 = cell_key(cx, cy, s.z1);
+      for (int64_t t = lower_bound_u64(a.keys, a.nbins, k0); t < a.nbins; ++t) {
+        const uint64_t key = a.keys[t];
+        if (key > k1) break;
+        const int64_t j = a.ids[t];
+        if (EE && j <= i) continue;  // each unordered pair once, lower edge index first (:310)
+        const Box B = EE ? make_box<2>(a.pos, a.b_elems, j, a.d_hat) : make_box<1>(a.pos, a.b_elems, j, a.d_hat);
+        if (!(A.lx <= B.hx && B.lx <= A.hx && A.ly <= B.hy && B.ly <= A.hy && A.lz <= B.hz && B.lz <= A.hz)) continue;
+        // owner cell = cell of the lower corner of the intersection
+        const int ox = cell_of(fmax(A.lx, B.lx), a.g.ox, a.g.inv), oy = cell_of(fmax(A.ly, B.ly), a.g.oy, a.g.inv),
+                  oz = cell_of(fmax(A.lz, B.lz), a.g.oz, a.g.inv);
+        if (cell_key(ox, oy, oz) != key) continue;
+        int4 q;
+        if (EE) {
+          const int b0 = a.b_elems[2 * j], b1 = a.b_elems[2 * j + 1];
+          if (av0 == b0 || av0 == b1 || av1 == b0 || av1 == b1) continue;
+          q = make_int4(av0, av1, b0, b1);
+        } else {
+          const int t0 = a.b_elems[3 * j], t1 = a.b_elems[3 * j + 1], t2 = a.b_elems[3 * j + 2];
+          if (av0 == t0 || av0 == t1 || av0 == t2) continue;
+          q = make_int4(av0, t0, t1, t2);
+        }
+        if (FILL) a.out[o++] = q;
+        else ++n;
+      }
+    }
+  if (!FILL) a.cnt[i] = n;
+}
+
+}  // namespace b200ipc
+
+struct b200ipc_broad {
+  b200ipc::BroadBuf<int32_t> cnt;
+  b200ipc::BroadBuf<int64_t> off_bin, off_vt, off_ee;
+  b200ipc::BroadBuf<uint64_t> keys_a, keys_t, keys_e;   // scratch, sorted triangle bins, sorted edge bins
+  b200ipc::BroadBuf<uint32_t> ids_a, ids_t, ids_e;
+  b200ipc::BroadBuf<uint8_t> temp;
+  b200ipc::BroadBuf<int64_t> totals;
+  // state between count and fill
+  bool counted = false;
+  int64_t nverts = 0, n_sv = 0, n_tri = 0, n_edge = 0, nbin_t = 0, nbin_e = 0, n_vt = 0, n_ee = 0;
+  const double* pos = nullptr;
+  const int32_t *surf_verts = nullptr, *tris = nullptr, *edges = nullptr;
+  double d_hat = 0.0;
+  b200ipc::Grid grid{};
+};
+
+using namespace b200ipc;
+
+#define CK(expr)                            \
+  do {                                      \
+    cudaError_t _e = (expr);                \
+    if (_e != cudaSuccess) return -(int)_e; \
+  } while (0)
+#define RC(expr)       \
+  do {                 \
+    int _r = (expr);   \
+    if (_r) return _r; \
+  } while (0)
+
+static inline unsigned bblocks(int64_t n) { return (unsigned)((n + kBT - 1) / kBT); }
+
+// exclusive scan of int32 counts into int64 offsets (n + 1 entries: the last is the total)
+static int scan_counts(b200ipc_broad* h, const int32_t* cnt, int64_t* off, int64_t n, int64_t* total, cudaStream_t st) {
+  size_t tb = 0;
+  // scan n + 1 items (the extra trailing count is zeroed by the caller) so off[n] is the total
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, off, (int)(n + 1), st));
+  CK(h->temp.reserve(tb));
+  CK(cub::DeviceScan::ExclusiveSum(h->temp.ptr, tb, cnt, off, (int)(n + 1), st));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  CK(cudaMemcpyAsync(total, off + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+template <int KIND>
+static int bin_boxes(b200ipc_broad* h, const int32_t* elems, int64_t n, BroadBuf<uint64_t>& keys, BroadBuf<uint32_t>& ids,
+                     int64_t* nbins, cudaStream_t st) {
+  *nbins = 0;
+  if (n == 0) return 0;
+  CK(h->cnt.reserve(n + 1));
+  CK(h->off_bin.reserve(n + 1));
+  CK(cudaMemsetAsync(h->cnt.ptr + n, 0, sizeof(int32_t), st));
+  bin_count_kernel<KIND><<<bblocks(n), kBT, 0, st>>>(h->pos, elems, n, h->d_hat, h->grid, h->cnt.ptr);
+  RC(post_launch());
+  int64_t total = 0;
+  RC(scan_counts(h, h->cnt.ptr, h->off_bin.ptr, n, &total, st));
+  if (total >= (1ll << 31)) return B200IPC_EINVAL;  // cell size far too small for these boxes
+  CK(h->keys_a.reserve(total)); CK(h->ids_a.reserve(total)); CK(keys.reserve(total)); CK(ids.reserve(total));
+  bin_fill_kernel<KIND><<<bblocks(n), kBT, 0, st>>>(h->pos, elems, n, h->d_hat, h->grid, h->off_bin.ptr, h->keys_a.ptr,
+                                                    h->ids_a.ptr);
+  RC(post_launch());
+  size_t tb = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, h->keys_a.ptr, keys.ptr, h->ids_a.ptr, ids.ptr, (int)total, 0, 63, st));
+  CK(h->temp.reserve(tb));
+  CK(cub::DeviceRadixSort::SortPairs(h->temp.ptr, tb, h->keys_a.ptr, keys.ptr, h->ids_a.ptr, ids.ptr, (int)total, 0, 63,
+                                     st));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  *nbins = total;
+  return 0;
+}
+
+extern "C" int b200ipc_broad_create(b200ipc_broad** out) {
+  if (!out) return B200IPC_EINVAL;
+  *out = new (std::nothrow) b200ipc_broad();
+  return *out ? 0 : B200IPC_EINVAL;
+}
+
+extern "C" int b200ipc_broad_destroy(b200ipc_broad* h) {
+  if (!h) return 0;
+  h->cnt.release(); h->off_bin.release(); h->off_vt.release(); h->off_ee.release();
+  h->keys_a.release(); h->keys_t.release(); h->keys_e.release();
+  h->ids_a.release(); h->ids_t.release(); h->ids_e.release();
+  h->temp.release(); h->totals.release();
+  delete h;
+  return 0;
+}
+
+extern "C" int b200ipc_broad_phase_count(b200ipc_broad* h, int64_t nverts, const double* positions, int64_t n_sv,
+                                         const int32_t* surf_verts, int64_t n_tri, const int32_t* tris, int64_t n_edge,
+                                         const int32_t* edges, double d_hat, double cell, const double* origin,
+                                         int64_t* n_vt, int64_t* n_ee, void* stream) {
+  if (!h || nverts <= 0 || !positions || n_sv < 0 || n_tri < 0 || n_edge < 0 || !origin || !n_vt || !n_ee)
+    return B200IPC_EINVAL;
+  if ((n_sv && !surf_verts) || (n_tri && !tris) || (n_edge && !edges)) return B200IPC_EINVAL;
+  if (!(d_hat > 0.0) || !(cell > 0.0)) return B200IPC_EINVAL;
+  if (n_sv >= (1ll << 31) || n_tri >= (1ll << 31) || n_edge >= (1ll << 31)) return B200IPC_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  h->counted = false;
+  h->nverts = nverts; h->pos = positions; h->n_sv = n_sv; h->surf_verts = surf_verts; h->n_tri = n_tri; h->tris = tris;
+  h->n_edge = n_edge; h->edges = edges; h->d_hat = d_hat;
+  h->grid = Grid{origin[0], origin[1], origin[2], 1.0 / cell};
+  h->n_vt = h->n_ee = 0;
+
+  // ---- point-triangle: triangles binned, vertex boxes probe ----------------------------------------
+  if (n_sv && n_tri) {
+    RC(bin_boxes<1>(h, tris, n_tri, h->keys_t, h->ids_t, &h->nbin_t, st));
+    CK(h->cnt.reserve(n_sv + 1));
+    CK(h->off_vt.reserve(n_sv + 1));
+    CK(cudaMemsetAsync(h->cnt.ptr + n_sv, 0, sizeof(int32_t), st));
+    JoinArgs a{positions, surf_verts, tris, n_sv, h->nbin_t, d_hat, h->grid, h->keys_t.ptr, h->ids_t.ptr,
+               nullptr, h->cnt.ptr, nullptr};
+    join_kernel<false, false><<<bblocks(n_sv), kBT, 0, st>>>(a);
+    RC(post_launch());
+    RC(scan_counts(h, h->cnt.ptr, h->off_vt.ptr, n_sv, &h->n_vt, st));
+  }
+  // ---- edge-edge: edges binned, the same boxes probe --------------------------------------------------
+  if (n_edge > 1) {
+    RC(bin_boxes<2>(h, edges, n_edge, h->keys_e, h->ids_e, &h->nbin_e, st));
+    CK(h->cnt.reserve(n_edge + 1));
+    CK(h->off_ee.reserve(n_edge + 1));
+    CK(cudaMemsetAsync(h->cnt.ptr + n_edge, 0, sizeof(int32_t), st));
+    JoinArgs a{positions, edges, edges, n_edge, h->nbin_e, d_hat, h->grid, h->keys_e.ptr, h->ids_e.ptr,
+               nullptr, h->cnt.ptr, nullptr};
+    join_kernel<true, false><<<bblocks(n_edge), kBT, 0, st>>>(a);
+    RC(post_launch());
+    RC(scan_counts(h, h->cnt.ptr, h->off_ee.ptr, n_edge, &h->n_ee, st));
+  }
+  *n_vt = h->n_vt;
+  *n_ee = h->n_ee;
+  h->counted = true;
+  return 0;
+}
+
+extern "C" int b200ipc_broad_phase_fill(b200ipc_broad* h, int32_t* vt, int32_t* ee, void* stream) {
+  if (!h || !h->counted) return B200IPC_ESTATE;
+  if ((h->n_vt && !vt) || (h->n_ee && !ee)) return B200IPC_EINVAL;
+  if (((uintptr_t)vt | (uintptr_t)ee) & 15) return B200IPC_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (h->n_vt) {
+    JoinArgs a{h->pos, h->surf_verts, h->tris, h->n_sv, h->nbin_t, h->d_hat, h->grid, h->keys_t.ptr, h->ids_t.ptr,
+               h->off_vt.ptr, nullptr, reinterpret_cast<int4*>(vt)};
+    join_kernel<false, true><<<bblocks(h->n_sv), kBT, 0, st>>>(a);
+    RC(post_launch());
+  }
+  if (h->n_ee) {
+    JoinArgs a{h->pos, h->edges, h->edges, h->n_edge, h->nbin_e, h->d_hat, h->grid, h->keys_e.ptr, h->ids_e.ptr,
+               h->off_ee.ptr, nullptr, reinterpret_cast<int4*>(ee)};
+    join_kernel<true, true><<<bblocks(h->n_edge), kBT, 0, st>>>(a);
+    RC(post_launch());
+  }
+  return 0;
+}

@@ -182,12 +182,34 @@ __global__ void __launch_bounds__(kNT) narrow_gather_kernel(const GatherArgs a) 
 
 static inline unsigned nblocks(int64_t n) { return (unsigned)((n + kNT - 1) / kNT); }
 
+// Per-call scratch from the device's stream-ordered pool (cudaMallocAsync).  The pool's release
+// threshold is lifted once, so after the first call the buffers are recycled without touching the
+// driver: cudaMalloc / cudaFree per buffer cost ~30 ms per narrow phase.
+inline cudaError_t keep_pool_memory() {
+  static bool done = false;
+  if (done) return cudaSuccess;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  cudaMemPool_t pool;
+  e = cudaDeviceGetDefaultMemPool(&pool, dev);
+  if (e != cudaSuccess) return e;
+  uint64_t keep = ~0ull;
+  e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  done = e == cudaSuccess;
+  return e;
+}
+
 template <typename T>
 struct Scratch {
   T* p = nullptr;
-  cudaError_t alloc(size_t n) { return cudaMalloc(&p, (n ? n : 1) * sizeof(T)); }
+  cudaStream_t st = nullptr;
+  cudaError_t alloc(size_t n, cudaStream_t stream) {
+    st = stream;
+    return cudaMallocAsync(reinterpret_cast<void**>(&p), (n ? n : 1) * sizeof(T), stream);
+  }
   ~Scratch() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, st);
   }
 };
 
@@ -221,6 +243,7 @@ extern "C" int b200ipc_narrow_phase(int64_t nverts, const double* positions, con
   if (nq >= (1ll << 31) || nverts >= (1ll << 30)) return B200IPC_EINVAL;
   if (!kind || !verts || !sub || !eps_x) return B200IPC_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
+  CK(keep_pool_memory());
 
   Scratch<uint8_t> keep, kq, sq, temp;
   Scratch<int4> vq;
@@ -228,8 +251,8 @@ extern "C" int b200ipc_narrow_phase(int64_t nverts, const double* positions, con
   Scratch<uint32_t> iota, idx_a, idx_b;
   Scratch<uint64_t> key_a, key_b;
   Scratch<unsigned long long> counters;  // [0] = n_kept, [1..7] = histogram
-  CK(keep.alloc(nq)); CK(kq.alloc(nq)); CK(sq.alloc(nq)); CK(vq.alloc(nq)); CK(eq.alloc(nq));
-  CK(iota.alloc(nq)); CK(idx_a.alloc(nq)); CK(counters.alloc(8));
+  CK(keep.alloc(nq, st)); CK(kq.alloc(nq, st)); CK(sq.alloc(nq, st)); CK(vq.alloc(nq, st)); CK(eq.alloc(nq, st));
+  CK(iota.alloc(nq, st)); CK(idx_a.alloc(nq, st)); CK(counters.alloc(8, st));
   CK(cudaMemsetAsync(counters.p, 0, 8 * sizeof(unsigned long long), st));
 
   NarrowArgs na{positions, rest_positions, n_vt, n_ee, vt, ee, d_hat_sq, promote_parallel,
@@ -243,7 +266,7 @@ extern "C" int b200ipc_narrow_phase(int64_t nverts, const double* positions, con
   size_t tb = 0;
   int* d_nsel = reinterpret_cast<int*>(counters.p);
   CK(cub::DeviceSelect::Flagged(nullptr, tb, iota.p, keep.p, idx_a.p, d_nsel, (int)nq, st));
-  CK(temp.alloc(tb));
+  CK(temp.alloc(tb, st));
   CK(cub::DeviceSelect::Flagged(temp.p, tb, iota.p, keep.p, idx_a.p, d_nsel, (int)nq, st));
   g_launches.fetch_add(1, std::memory_order_relaxed);
   int nsel = 0;
@@ -257,11 +280,11 @@ extern "C" int b200ipc_narrow_phase(int64_t nverts, const double* positions, con
   // stable LSD sort, least significant word first
   int bits = 1;
   while (((int64_t)1 << bits) < nverts + 1) ++bits;
-  CK(idx_b.alloc(n)); CK(key_a.alloc(n)); CK(key_b.alloc(n));
+  CK(idx_b.alloc(n, st)); CK(key_a.alloc(n, st)); CK(key_b.alloc(n, st));
   size_t ts = 0;
   CK(cub::DeviceRadixSort::SortPairs(nullptr, ts, key_a.p, key_b.p, idx_a.p, idx_b.p, (int)n, 0, 64, st));
   Scratch<uint8_t> temp2;
-  CK(temp2.alloc(ts));
+  CK(temp2.alloc(ts, st));
   uint32_t* cur = idx_a.p;
   uint32_t* nxt = idx_b.p;
   for (int word = 0; word < 4; ++word) {

@@ -310,9 +310,48 @@ def golden_scene():
     save("scene", **out)
 
 
+def golden_broad():
+    """Candidate queries of the reference's broad phase: its own box construction
+    (proximity.py:276-281, :304-307) fed to its own ``_aabb_overlap_pairs`` (:232-248) and its own
+    incidence filters (:283-286, :310-317), on two poses of a small cloth stack."""
+    out = {}
+    for tag, (layers, n, seed, push) in {"a": (3, 6, 3, 0.0), "b": (2, 9, 11, 0.3)}.items():
+        cloth = wl.cloth_stack(layers=layers, n=n, seed=seed, twist_deg=5.0)
+        x = cloth.positions + push * cloth.d_hat * np.random.default_rng(seed).normal(size=cloth.positions.shape)
+        d_hat = cloth.d_hat
+        verts, tris, edges = np.unique(cloth.tris), cloth.tris, cloth.edges
+        p = x[verts]
+        tri_stack = np.stack([x[tris[:, 0]], x[tris[:, 1]], x[tris[:, 2]]], axis=1)
+        pairs = rp._aabb_overlap_pairs(p - d_hat, p + d_hat, tri_stack.min(axis=1), tri_stack.max(axis=1))
+        vid, tv = verts[pairs[:, 0]], tris[pairs[:, 1]]
+        keep = (vid != tv[:, 0]) & (vid != tv[:, 1]) & (vid != tv[:, 2])
+        vt = np.concatenate([vid[keep, None], tv[keep]], axis=1)
+        e1, e2 = x[edges[:, 0]], x[edges[:, 1]]
+        lo_e, hi_e = np.minimum(e1, e2) - d_hat * 0.5, np.maximum(e1, e2) + d_hat * 0.5
+        pairs = rp._aabb_overlap_pairs(lo_e, hi_e, lo_e, hi_e)
+        pairs = pairs[pairs[:, 0] < pairs[:, 1]]
+        ea, eb = edges[pairs[:, 0]], edges[pairs[:, 1]]
+        keep = (ea[:, 0] != eb[:, 0]) & (ea[:, 0] != eb[:, 1]) & (ea[:, 1] != eb[:, 0]) & (ea[:, 1] != eb[:, 1])
+        ee = np.concatenate([ea[keep], eb[keep]], axis=1)
+        # the list the reference builds from them
+        scene = _reference_scene(cloth)
+        stencils = rp.find_contact_pairs(scene, x, d_hat)
+        print(f"broad {tag}: {len(vt)} vt + {len(ee)} ee candidates -> {len(stencils)} contacts")
+        tab = table_of(stencils)
+        out.update({f"{tag}_positions": x, f"{tag}_rest_positions": cloth.rest_positions, f"{tag}_tris": tris,
+                    f"{tag}_edges": edges, f"{tag}_d_hat": d_hat, f"{tag}_vt": vt.astype(np.int32),
+                    f"{tag}_ee": ee.astype(np.int32)})
+        out.update({f"{tag}_list_{k}": v for k, v in tab.items()})
+    save("broad", **out)
+
+
 if __name__ == "__main__":
+    if "--broad-only" in sys.argv:
+        golden_broad()
+        sys.exit(0)
     golden_scalars()
     golden_classify()
     golden_plain_blocks()
     golden_parallel_blocks()
     golden_scene()
+    golden_broad()

@@ -88,3 +88,81 @@ def test_cloth_stack_grid_broad_phase_vs_all_pairs(Cn):
     got = Cn.contacts.narrow_phase(cloth.positions, cloth.rest_positions, vt, ee, cloth.d_hat)
     assert_same_table(got, ref)
     assert len(got) > 2000
+
+
+def _rows(a):
+    a = np.asarray(a, dtype=np.int64).reshape(-1, 4)
+    return a[np.lexsort(a.T[::-1])]
+
+
+@pytest.mark.parametrize("layers,n,seed", [(4, 10, 5), (3, 14, 2), (1, 9, 3)])
+def test_gpu_broad_phase_equals_reference_aabb_candidates(Cn, layers, n, seed):
+    """The grid join reports exactly the reference's AABB-overlap candidates, each once."""
+    from paper_2308_09400_b200 import device
+
+    cloth = Cn.workloads.cloth_stack(layers=layers, n=n, seed=seed)
+    surf = np.unique(cloth.tris)
+    ref_vt, ref_ee = o.aabb_candidates(cloth.positions, surf, cloth.tris, cloth.edges, cloth.d_hat)
+    for cell in (None, 0.37 * cloth.d_hat, 11.0 * cloth.d_hat):   # cell size is a speed knob only
+        bp = Cn.contacts.BroadPhase(surf, cloth.tris, cloth.edges, cloth.d_hat, cloth.positions, cell=cell)
+        vt, ee = bp.query(cloth.positions)
+        bp.close()
+        vt, ee = device.to_host(vt), device.to_host(ee)
+        assert vt.dtype == np.int32 and ee.dtype == np.int32
+        np.testing.assert_array_equal(_rows(vt), _rows(ref_vt))
+        np.testing.assert_array_equal(_rows(ee), _rows(ref_ee))
+    assert len(ref_vt) > 0 and (layers == 1 or len(ref_ee) > 100)
+
+
+def test_gpu_broad_phase_moving_scene_and_find_contact_pairs(Cn):
+    """One handle, several detects (positions change); find_contact_pairs end to end on the GPU."""
+    from types import SimpleNamespace
+
+    from paper_2308_09400_b200 import device
+
+    cloth = Cn.workloads.cloth_stack(layers=3, n=12, seed=9)
+    surf = np.unique(cloth.tris)
+    bp = Cn.contacts.BroadPhase(surf, cloth.tris, cloth.edges, cloth.d_hat, cloth.positions)
+    rng = np.random.default_rng(4)
+    for step in range(3):
+        x = cloth.positions + step * 0.1 * cloth.d_hat * rng.normal(size=cloth.positions.shape)
+        vt, ee = bp.query(device.to_device(x))
+        ref_vt, ref_ee = o.aabb_candidates(x, surf, cloth.tris, cloth.edges, cloth.d_hat)
+        np.testing.assert_array_equal(_rows(device.to_host(vt)), _rows(ref_vt))
+        np.testing.assert_array_equal(_rows(device.to_host(ee)), _rows(ref_ee))
+        got = Cn.contacts.narrow_phase(x, cloth.rest_positions, vt, ee, cloth.d_hat)
+        ref = o.narrow_phase(x, cloth.rest_positions, ref_vt, ref_ee, cloth.d_hat)
+        assert_same_table(got, ref)
+    bp.close()
+    scene = SimpleNamespace(surf_tris=cloth.tris, surf_edges=cloth.edges, surf_verts=surf,
+                            rest_positions=cloth.rest_positions)
+    stencils = Cn.contacts.find_contact_pairs(scene, cloth.positions, cloth.d_hat)
+    ref = o.narrow_phase(cloth.positions, cloth.rest_positions, *o.aabb_candidates(
+        cloth.positions, surf, cloth.tris, cloth.edges, cloth.d_hat), cloth.d_hat)
+    assert len(stencils) == len(ref["kind"]) > 1000
+    assert [tuple(v for v in s.verts) for s in stencils[:50]] == [
+        tuple(int(v) for v in row if v >= 0) for row in ref["verts"][:50]]
+
+
+def test_gpu_broad_phase_empty_inputs(Cn):
+    bp = Cn.contacts.BroadPhase(np.zeros(0, int), np.zeros((0, 3), int), np.zeros((0, 2), int), 0.1)
+    vt, ee = bp.query(np.zeros((4, 3)))
+    assert vt.shape == (0, 4) and ee.shape == (0, 4)
+    bp.close()
+
+
+@pytest.mark.parametrize("tag", ["a", "b"])
+def test_gpu_detect_matches_frozen_reference(Cn, tag):
+    """Broad + narrow phase on the GPU against the reference's frozen candidates and contact list."""
+    from paper_2308_09400_b200 import device
+
+    z = load_golden("broad")
+    x, tris, edges, d_hat = z[f"{tag}_positions"], z[f"{tag}_tris"], z[f"{tag}_edges"], float(z[f"{tag}_d_hat"])
+    bp = Cn.contacts.BroadPhase(np.unique(tris), tris, edges, d_hat, x)
+    vt, ee = bp.query(x)
+    np.testing.assert_array_equal(_rows(device.to_host(vt)), _rows(z[f"{tag}_vt"]))
+    np.testing.assert_array_equal(_rows(device.to_host(ee)), _rows(z[f"{tag}_ee"]))
+    got = Cn.contacts.narrow_phase(x, z[f"{tag}_rest_positions"], vt, ee, d_hat)
+    bp.close()
+    for key in KEYS:
+        np.testing.assert_array_equal(getattr(got, key), z[f"{tag}_list_{key}"], err_msg=key)

@@ -228,3 +228,18 @@ def test_scene_solver_golden():
     res = z["ref_dense"] @ d12 - rhs
     ref_res = z["ref_dense"] @ z["ref_pcg12_d"] - rhs
     assert np.linalg.norm(res) <= 10.0 * max(np.linalg.norm(ref_res), 1e-12 * np.linalg.norm(rhs))
+
+
+@pytest.mark.parametrize("tag", ["a", "b"])
+def test_broad_phase_candidates_golden(tag):
+    """oracle.aabb_candidates == the reference's own _aabb_overlap_pairs + incidence filters
+    (tests/golden/broad.npz, frozen by make_golden.py --broad-only), row for row, and the list the
+    oracle's narrow phase builds from them == the reference's find_contact_pairs output."""
+    z = load_golden("broad")
+    x, tris, edges, d_hat = z[f"{tag}_positions"], z[f"{tag}_tris"], z[f"{tag}_edges"], float(z[f"{tag}_d_hat"])
+    vt, ee = o.aabb_candidates(x, np.unique(tris), tris, edges, d_hat)
+    np.testing.assert_array_equal(vt, z[f"{tag}_vt"])
+    np.testing.assert_array_equal(ee, z[f"{tag}_ee"])
+    tab = o.narrow_phase(x, z[f"{tag}_rest_positions"], vt, ee, d_hat)
+    for key in ("kind", "verts", "sub", "eps_x", "origin_type", "origin"):
+        np.testing.assert_array_equal(tab[key], z[f"{tag}_list_{key}"], err_msg=key)
