@@ -265,6 +265,15 @@ def newton_section(torch, pkg, steps, warmup, peak, seed):
     t0 = time.perf_counter()
     d, it_full, ok_full, _, _ = sysm.pcg(rhs, 1e-4, 2000)
     ms_pcg_full = (time.perf_counter() - t0) * 1e3
+    # CCD step filter of the line search: swept-AABB candidates + ACCD bound, on the device
+    dirs = device.to_device(0.3 * cloth.d_hat * np.random.default_rng(3).normal(size=cloth.positions.shape))
+    alpha = bp.ccd_step_bound(pos, dirs)  # warm
+    s_vt, s_ee = bp.sweep(pos, dirs)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    alpha = bp.ccd_step_bound(pos, dirs)
+    torch.cuda.synchronize()
+    ms_ccd = (time.perf_counter() - t0) * 1e3
     n_c = table.n
     ent = sum(int(f.vids.shape[0]) * f.s * f.s for f in fams)
     num_bytes = sum(int(f.vids.shape[0]) * (72 * f.s * f.s) for f in fams) + 4 * ent + 72 * nnzb
@@ -279,6 +288,8 @@ def newton_section(torch, pkg, steps, warmup, peak, seed):
                   "note": "rank-1 path: the stencil kernel writes z (24 s bytes) instead of the dense block and the "
                           "assembly gathers from z; same matrix bit for bit"},
         "assembly_plus_spmv_ms": ms_numeric + ms_spmv, "gradient_scatter_ms": ms_grad,
+        "ccd": {"sweep_candidates": int(s_vt.shape[0]) + int(s_ee.shape[0]), "sweep_plus_filter_ms": ms_ccd,
+                "alpha": alpha, "note": "sweep_candidates + global_ccd_filter (proximity.py:388-432), random 0.3 d_hat step"},
         "pcg_ms_per_iter": ms_pcg_iter, "pcg_solve_ms": ms_pcg_full, "pcg_iters": it_full, "pcg_converged": ok_full,
         "roofline_assembly": {"bound": "hbm", "achieved": num_bytes / ms_numeric / 1e6, "peak": peak, "unit": "GB/s",
                               "frac": num_bytes / ms_numeric / 1e6 / peak},
@@ -304,6 +315,14 @@ def newton_section(torch, pkg, steps, warmup, peak, seed):
             fn(h, v, xv, acc)
             reps += 1
         el = (time.perf_counter() - t0) / reps
+        if core is not None:  # the reference's own compiled ACCD on a sample of the swept candidates
+            xs, ds = device.to_host(pos), device.to_host(dirs)
+            cand = device.to_host(s_vt[:20000]).astype(np.int64)
+            t0 = time.perf_counter()
+            for row in cand:
+                core.accd_max_step(xs[row], ds[row], 0, 0.9)
+            out["ccd"]["cpu_pairs_per_s"] = len(cand) / (time.perf_counter() - t0)
+            out["ccd"]["cpu_kind"] = "reference (tetipc.kernels._core.accd_max_step, 1 core, Python call per pair)"
         out["cpu_matvec_blocks"] = {"blocks_per_s": nb / el, "kind": "reference" if core is not None else "port",
                                     "cores": 1, "sample": f"{nb} 12x12 blocks, tetipc.kernels._core.matvec_blocks"
                                     if core is not None else f"{nb} 12x12 blocks, oracle_c port"}

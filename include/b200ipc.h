@@ -187,6 +187,40 @@ int b200ipc_broad_phase_count(b200ipc_broad* h, int64_t nverts, const double* po
                               int64_t* n_ee /* host */, void* stream);
 int b200ipc_broad_phase_fill(b200ipc_broad* h, int32_t* vt, int32_t* ee, void* stream);
 
+/* sweep_candidates (proximity.py:388-421): the same join on SWEPT boxes -- every element's AABB over
+ * its pose at `positions` and at positions + directions, grown by `margin` (the reference uses
+ * 1e-3 d_hat) -- with the same incidence filters.  Sizes the outputs; b200ipc_broad_phase_fill then
+ * writes vt (PAIR_PT candidates) and ee (PAIR_EE candidates). */
+int b200ipc_sweep_candidates_count(b200ipc_broad* h, int64_t nverts, const double* positions,
+                                   const double* directions, int64_t n_sv, const int32_t* surf_verts,
+                                   int64_t n_tri, const int32_t* tris, int64_t n_edge, const int32_t* edges,
+                                   double margin, double cell, const double* origin /* host[3] */,
+                                   int64_t* n_vt /* host */, int64_t* n_ee /* host */, void* stream);
+
+/* ---- additive CCD ------------------------------------------------------------------ */
+/* Pair kinds of tetipc.kernels (kernels/__init__.py:21-26). */
+#define B200IPC_PAIR_PT 0
+#define B200IPC_PAIR_EE 1
+#define B200IPC_PAIR_PE 2
+#define B200IPC_PAIR_PP 3
+/* accd_max_step (kernels/_core.pyx:272-325) for n pairs, one thread each: the largest step fraction
+ * t in [0,1] along `directions` that keeps the pair's distance >= (1 - slack) * (current distance),
+ * by conservative advancement with the reference's exits and iteration cap; bit-identical per pair.
+ * ids (n,4) i32 global vertex ids (16-byte aligned; unused entries ignored): PT (p,t1,t2,t3),
+ * EE (a1,a2,b1,b2), PE (p,e1,e2), PP (a,b).  pair_kind: u8 per pair, or NULL for `uniform_kind`.
+ * step (n) f64; status (n) u8, may be NULL: 0 ok, 2 = current distance not positive (the reference
+ * raises ValueError, :307-308; step is 0 there). */
+int b200ipc_accd_max_step(int64_t n, const int32_t* ids, const uint8_t* pair_kind, int32_t uniform_kind,
+                          const double* positions, const double* directions, double slack,
+                          int32_t max_iter, double* step, uint8_t* status, void* stream);
+/* global_ccd_filter (proximity.py:424-432) over the candidate lists of sweep_candidates: *alpha
+ * (device double) = min(1, min over pairs of their ACCD bound); *n_invalid (device int64, may be
+ * NULL) = pairs whose current distance is not positive (they do not enter the minimum; the
+ * reference raises).  The minimum is exact and order-free, so the result is deterministic. */
+int b200ipc_ccd_filter(int64_t n_vt, const int32_t* vt, int64_t n_ee, const int32_t* ee,
+                       const double* positions, const double* directions, double slack, int32_t max_iter,
+                       double* alpha /* device[1] */, int64_t* n_invalid /* device[1] */, void* stream);
+
 /* ---- narrow phase: candidate queries -> ordered contact list ------------------- */
 /* find_contact_pairs without its broad phase (proximity.py:284-358).  vt (n_vt,4) i32 =
  * (vertex, t1, t2, t3) and ee (n_ee,4) i32 = (a1, a2, b1, b2): any duplicate-free superset of

@@ -815,3 +815,134 @@ def narrow_phase(positions, rest_positions, vt_pairs, ee_pairs, d_hat, promote_p
                         verts[:, 3], verts[:, 2], verts[:, 1], verts[:, 0], kind))
     return {"kind": kind[order], "verts": verts[order].astype(np.int32), "sub": sub[order],
             "eps_x": eps_x[order], "origin_type": ot[order], "origin": origin[order].astype(np.int32)}
+
+
+# ---------------------------------------------------------------------------------------------
+# additive CCD: kernels/_core.pyx:250-325, proximity.py:388-432
+# ---------------------------------------------------------------------------------------------
+PAIR_PT, PAIR_EE, PAIR_PE, PAIR_PP = 0, 1, 2, 3
+_PAIR_SIZE = {PAIR_PT: 4, PAIR_EE: 4, PAIR_PE: 3, PAIR_PP: 2}
+
+
+def _pair_dist2(x, pair_kind):
+    """_pair_dist2_c (_core.pyx:250-269) on a batch: x (n,s,3) -> d2 (n,)."""
+    if pair_kind == PAIR_PT:
+        return pt_classify_batch(x[:, 0], x[:, 1], x[:, 2], x[:, 3])[1]
+    if pair_kind == PAIR_EE:
+        return ee_classify_batch(x[:, 0], x[:, 1], x[:, 2], x[:, 3])[1]
+    if pair_kind == PAIR_PE:
+        e = x[:, 2] - x[:, 1]
+        ee = _dot(e, e)
+        r = x[:, 0] - x[:, 1]
+        t = _clamp01(_dot(r, e) / ee)
+        r = r - t[:, None] * e
+        return _dot(r, r)
+    r = x[:, 0] - x[:, 1]
+    return _dot(r, r)
+
+
+def accd_max_step_batch(x, dx, pair_kind, slack, max_iter=512):
+    """accd_max_step (_core.pyx:272-325) for n pairs of one kind at once: x, dx (n,s,3).
+
+    Every pair runs the reference's scalar loop; pairs that left the loop are masked out, so each
+    row sees exactly the operations of a lone call.  Returns (step (n,), bad (n,) bool) where bad
+    marks a non-positive initial distance (the reference raises ValueError, :307-308).
+    """
+    x = np.asarray(x, dtype=np.float64)
+    dx = np.asarray(dx, dtype=np.float64)
+    n, s = x.shape[0], x.shape[1]
+    mean = np.zeros((n, 3))
+    for v in range(s):
+        mean = mean + dx[:, v]
+    mean = mean / s
+    q = dx - mean[:, None, :]
+    norms = np.sqrt(q[..., 0] * q[..., 0] + q[..., 1] * q[..., 1] + q[..., 2] * q[..., 2])
+    if pair_kind == PAIR_PT:
+        lp = norms[:, 0] + np.maximum(norms[:, 1], np.maximum(norms[:, 2], norms[:, 3]))
+    elif pair_kind == PAIR_EE:
+        lp = np.maximum(norms[:, 0], norms[:, 1]) + np.maximum(norms[:, 2], norms[:, 3])
+    elif pair_kind == PAIR_PE:
+        lp = norms[:, 0] + np.maximum(norms[:, 1], norms[:, 2])
+    else:
+        lp = norms[:, 0] + norms[:, 1]
+    out = np.ones(n)
+    live = lp != 0.0
+    d0 = np.zeros(n)
+    if live.any():
+        d0[live] = np.sqrt(_pair_dist2(x[live], pair_kind))
+    bad = live & ~(d0 > 0.0)
+    live &= ~bad
+    out[bad] = 0.0
+    gap = (1.0 - slack) * d0
+    t = np.zeros(n)
+    idx = np.flatnonzero(live)
+    for _ in range(max_iter):
+        if idx.size == 0:
+            break
+        xt = x[idx] + t[idx, None, None] * q[idx]
+        d = np.sqrt(_pair_dist2(xt, pair_kind))
+        step = (d - gap[idx]) / lp[idx]
+        stop = step <= 0.0                      # break: returns t
+        full = ~stop & (t[idx] + step >= 1.0)   # return 1.0
+        go = ~stop & ~full
+        out[idx[stop]] = t[idx[stop]]
+        out[idx[full]] = 1.0
+        t[idx[go]] = t[idx[go]] + step[go]
+        tiny = go & (step < 1e-14)              # break after the update
+        out[idx[tiny]] = t[idx[tiny]]
+        idx = idx[go & ~tiny]
+    out[idx] = t[idx]                           # iteration cap
+    return out, bad
+
+
+def sweep_candidates(positions, directions, surf_verts, tris, edges, d_hat):
+    """sweep_candidates (proximity.py:388-421), all pairs: (vt (m,4), ee (k,4)) in the reference's order."""
+    x0 = np.asarray(positions, dtype=np.float64)
+    x1 = x0 + np.asarray(directions, dtype=np.float64)
+    tris = np.asarray(tris, dtype=np.int64).reshape(-1, 3)
+    edges = np.asarray(edges, dtype=np.int64).reshape(-1, 2)
+    verts = np.asarray(surf_verts, dtype=np.int64)
+    margin = 1e-3 * d_hat
+
+    def overlap(lo_a, hi_a, lo_b, hi_b):
+        ok = np.ones((lo_a.shape[0], lo_b.shape[0]), dtype=bool)
+        for k in range(3):
+            ok &= lo_a[:, k:k + 1] <= hi_b[None, :, k]
+            ok &= lo_b[None, :, k] <= hi_a[:, k:k + 1]
+        return np.argwhere(ok)
+
+    vt = np.zeros((0, 4), np.int64)
+    if verts.size and tris.size:
+        lo_v = np.minimum(x0[verts], x1[verts]) - margin
+        hi_v = np.maximum(x0[verts], x1[verts]) + margin
+        lo_t = np.minimum(x0[tris].min(axis=1), x1[tris].min(axis=1)) - margin
+        hi_t = np.maximum(x0[tris].max(axis=1), x1[tris].max(axis=1)) + margin
+        pairs = overlap(lo_v, hi_v, lo_t, hi_t)
+        vid, tv = verts[pairs[:, 0]], tris[pairs[:, 1]]
+        keep = (vid != tv[:, 0]) & (vid != tv[:, 1]) & (vid != tv[:, 2])
+        vt = np.concatenate([vid[keep, None], tv[keep]], axis=1)
+    ee = np.zeros((0, 4), np.int64)
+    if edges.shape[0] > 1:
+        lo_e = np.minimum(x0[edges].min(axis=1), x1[edges].min(axis=1)) - margin
+        hi_e = np.maximum(x0[edges].max(axis=1), x1[edges].max(axis=1)) + margin
+        pairs = overlap(lo_e, hi_e, lo_e, hi_e)
+        pairs = pairs[pairs[:, 0] < pairs[:, 1]]
+        ea, eb = edges[pairs[:, 0]], edges[pairs[:, 1]]
+        keep = (ea[:, 0] != eb[:, 0]) & (ea[:, 0] != eb[:, 1]) & (ea[:, 1] != eb[:, 0]) & (ea[:, 1] != eb[:, 1])
+        ee = np.concatenate([ea[keep], eb[keep]], axis=1)
+    return vt, ee
+
+
+def global_ccd_filter(positions, directions, vt, ee, slack=0.9, max_iter=512):
+    """global_ccd_filter (proximity.py:424-432) over PT candidates vt and EE candidates ee."""
+    x = np.asarray(positions, dtype=np.float64)
+    d = np.asarray(directions, dtype=np.float64)
+    alpha = 1.0
+    for ids, kind in ((np.asarray(vt, dtype=np.int64).reshape(-1, 4), PAIR_PT),
+                      (np.asarray(ee, dtype=np.int64).reshape(-1, 4), PAIR_EE)):
+        if ids.shape[0]:
+            step, bad = accd_max_step_batch(x[ids], d[ids], kind, slack, max_iter)
+            if bad.any():
+                raise ValueError("additive CCD requires a strictly positive initial distance")
+            alpha = min(alpha, float(step.min()))
+    return alpha

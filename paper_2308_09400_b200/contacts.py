@@ -70,6 +70,102 @@ class BroadPhase:
                    "broad_phase_fill")
         return vt[:int(n_vt.value)], ee[:int(n_ee.value)]
 
+    def sweep(self, positions, directions, margin=None):
+        """sweep_candidates (proximity.py:388-421) on the device: pairs whose swept AABBs (pose at
+        ``positions`` and at ``positions + directions``, grown by 1e-3 d_hat) overlap ->
+        (vt (m,4) PAIR_PT ids, ee (k,4) PAIR_EE ids) int32 device tensors."""
+        pos = device.to_device(positions, np.float64)
+        dirs = device.to_device(directions, np.float64)
+        margin = 1e-3 * self.d_hat if margin is None else float(margin)
+        t = device.torch()
+        lo = t.minimum(pos, pos + dirs).amin(dim=0).cpu().numpy() - 2.0 * self.cell - margin
+        origin = (C.c_double * 3)(*[float(v) for v in lo])
+        n_vt, n_ee = C.c_int64(0), C.c_int64(0)
+        L = _lib.lib()
+        _lib.check(L.b200ipc_sweep_candidates_count(
+            self._h, pos.shape[0], device.ptr(pos), device.ptr(dirs), self.surf_verts.shape[0],
+            device.ptr(self.surf_verts), self.tris.shape[0], device.ptr(self.tris), self.edges.shape[0],
+            device.ptr(self.edges), margin, self.cell, origin, C.byref(n_vt), C.byref(n_ee), device.stream()),
+            "sweep_candidates_count")
+        vt = device.empty((max(int(n_vt.value), 1), 4), np.int32)
+        ee = device.empty((max(int(n_ee.value), 1), 4), np.int32)
+        _lib.check(L.b200ipc_broad_phase_fill(self._h, device.ptr(vt), device.ptr(ee), device.stream()),
+                   "broad_phase_fill")
+        return vt[:int(n_vt.value)], ee[:int(n_ee.value)]
+
+    def ccd_step_bound(self, positions, directions, slack=0.9, max_iter=512):
+        """sweep_candidates + global_ccd_filter (solver.py:337-340) without leaving the device:
+        the largest step fraction along ``directions`` every swept candidate pair verifies."""
+        pos = device.to_device(positions, np.float64)
+        dirs = device.to_device(directions, np.float64)
+        vt, ee = self.sweep(pos, dirs)
+        return ccd_filter_device(vt, ee, pos, dirs, slack, max_iter)
+
+
+def ccd_filter_device(vt, ee, positions, directions, slack=0.9, max_iter=512):
+    """min(1, min over candidate pairs of accd_max_step) -> float; raises like the reference when a
+    pair's current distance is not positive."""
+    if not 0.0 < slack < 1.0:
+        raise ValueError("slack must lie in (0, 1)")
+    out = device.empty((2,))  # [alpha, n_invalid (int64 bits)]
+    _lib.check(_lib.lib().b200ipc_ccd_filter(
+        int(vt.shape[0]), device.ptr(vt), int(ee.shape[0]), device.ptr(ee), device.ptr(positions),
+        device.ptr(directions), float(slack), int(max_iter), C.c_void_p(out.data_ptr()),
+        C.c_void_p(out.data_ptr() + 8), device.stream()), "ccd_filter")
+    host = device.to_host(out)
+    if int(host[1:2].view(np.int64)[0]) != 0:
+        raise ValueError("additive CCD requires a strictly positive initial distance")  # _core.pyx:307-308
+    return float(host[0])
+
+
+_PAIR_OF_KIND = {"point-triangle": 0, "edge-edge": 1, "edge-edge-parallel": 1, "point-edge-parallel": 1,
+                 "point-point-parallel": 1, "point-edge": 2, "point-point": 3}  # proximity.py:361-369
+
+
+def accd_step_bound(stencil, positions, directions, slack=0.9, max_iter=512):
+    """Twin of proximity.py:372-385: ACCD bound of one stencil along ``directions``."""
+    from . import kernels
+
+    if not 0.0 < slack < 1.0:
+        raise ValueError("slack must lie in (0, 1)")
+    ids = list(stencil.verts)
+    return kernels.accd_max_step(np.asarray(positions)[ids], np.asarray(directions)[ids],
+                                 _PAIR_OF_KIND[stencil.kind.value], slack, max_iter)
+
+
+def sweep_candidates(scene, positions, directions, d_hat):
+    """Twin of proximity.py:388-421: list of (pair_kind, (ids...)) whose swept AABBs overlap (the
+    reference's order: PT candidates by (vertex, triangle), then EE by (edge i, edge j))."""
+    from . import kernels
+
+    bp = BroadPhase(getattr(scene, "surf_verts", None), scene.surf_tris, scene.surf_edges, d_hat, positions)
+    try:
+        vt, ee = bp.sweep(positions, directions)
+        vt, ee = device.to_host(vt), device.to_host(ee)
+    finally:
+        bp.close()
+    return ([(kernels.PAIR_PT, tuple(int(v) for v in row)) for row in vt]
+            + [(kernels.PAIR_EE, tuple(int(v) for v in row)) for row in ee])
+
+
+def global_ccd_filter(scene, positions, directions, candidates, slack=0.9, max_iter=512):
+    """Twin of proximity.py:424-432: min of the per-pair ACCD bounds over ``candidates``."""
+    from . import kernels
+
+    if not candidates:
+        return 1.0
+    ids = np.zeros((len(candidates), 4), np.int32)
+    kinds = np.zeros(len(candidates), np.uint8)
+    for k, (pair, verts) in enumerate(candidates):
+        kinds[k] = pair
+        ids[k, :len(verts)] = verts
+    step, status = kernels.accd_max_step_device(device.to_device(ids), device.to_device(kinds),
+                                                device.to_device(positions, np.float64),
+                                                device.to_device(directions, np.float64), slack, max_iter)
+    if int(device.to_host(status).max()) != 0:
+        raise ValueError("additive CCD requires a strictly positive initial distance")
+    return float(min(1.0, device.to_host(step).min()))
+
 
 def narrow_phase_device(positions, rest_positions, vt, ee, d_hat, promote_parallel=True, want_origin=True):
     """Queries -> ``DeviceStencilTable`` (plus origin tensors when ``want_origin``).

@@ -15,6 +15,8 @@
 //          edge index i < j and no shared endpoint, :311-317);
 //      first to count, then -- after a scan -- to write (A, B) as global vertex ids.
 // Output order is deterministic (by A box, cell, B box) but irrelevant: the narrow phase sorts.
+// The same join with swept boxes (both ends of a step, margin 1e-3 d_hat) is sweep_candidates
+// (proximity.py:388-421), the candidate set of the CCD step filter (accd.cu).
 #include <cub/cub.cuh>
 
 #include "launch.cuh"
@@ -67,31 +69,52 @@ __device__ __forceinline__ void ld3(const double* p, int v, double& x, double& y
   z = p[3ll * v + 2];
 }
 
-// KIND 0: vertex box, 1: triangle AABB, 2: inflated edge AABB  (proximity.py:278-281, :305-307)
-template <int KIND>
-__device__ __forceinline__ Box make_box(const double* __restrict__ pos, const int32_t* __restrict__ elems, int64_t i,
-                                        double d_hat) {
-  Box b;
-  if (KIND == 0) {
-    double x, y, z;
-    ld3(pos, elems[i], x, y, z);
-    b.lx = x - d_hat; b.ly = y - d_hat; b.lz = z - d_hat;
-    b.hx = x + d_hat; b.hy = y + d_hat; b.hz = z + d_hat;
-  } else if (KIND == 1) {
-    double x0, y0, z0, x1, y1, z1, x2, y2, z2;
-    ld3(pos, elems[3 * i], x0, y0, z0);
-    ld3(pos, elems[3 * i + 1], x1, y1, z1);
-    ld3(pos, elems[3 * i + 2], x2, y2, z2);
-    b.lx = fmin(fmin(x0, x1), x2); b.ly = fmin(fmin(y0, y1), y2); b.lz = fmin(fmin(z0, z1), z2);
-    b.hx = fmax(fmax(x0, x1), x2); b.hy = fmax(fmax(y0, y1), y2); b.hz = fmax(fmax(z0, z1), z2);
+// Box of element i.  KIND 0: surface vertex, 1: triangle, 2: edge.  The box covers the element at
+// `pos` and -- when `dir` is given -- at pos + dir (the swept box of sweep_candidates,
+// proximity.py:393-401, :409-412), grown by `m` on every side.  Static detection uses dir = NULL and
+// m = d_hat / 0 / d_hat/2 (proximity.py:278-281, :305-307): min(p, p) - m = p - m and x - 0.0 = x, so
+// the corners are bit-identical to the reference's.
+struct Boxes {
+  const double* pos;
+  const double* dir;   // NULL: static
+  double m[3];         // margin per KIND
+};
+
+__device__ __forceinline__ void grow(Box& b, const Boxes& in, int v, bool first) {
+  double x, y, z;
+  ld3(in.pos, v, x, y, z);
+  if (first) {
+    b.lx = b.hx = x; b.ly = b.hy = y; b.lz = b.hz = z;
   } else {
-    double x0, y0, z0, x1, y1, z1;
-    ld3(pos, elems[2 * i], x0, y0, z0);
-    ld3(pos, elems[2 * i + 1], x1, y1, z1);
-    const double h = d_hat * 0.5;
-    b.lx = fmin(x0, x1) - h; b.ly = fmin(y0, y1) - h; b.lz = fmin(z0, z1) - h;
-    b.hx = fmax(x0, x1) + h; b.hy = fmax(y0, y1) + h; b.hz = fmax(z0, z1) + h;
+    b.lx = fmin(b.lx, x); b.ly = fmin(b.ly, y); b.lz = fmin(b.lz, z);
+    b.hx = fmax(b.hx, x); b.hy = fmax(b.hy, y); b.hz = fmax(b.hz, z);
   }
+}
+
+template <int KIND>
+__device__ __forceinline__ Box make_box(const Boxes& in, const int32_t* __restrict__ elems, int64_t i) {
+  constexpr int NV = KIND == 0 ? 1 : (KIND == 1 ? 3 : 2);
+  int v[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) v[k] = elems[NV * i + k];
+  Box b;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) grow(b, in, v[k], k == 0);
+  if (in.dir) {  // end-of-step positions pos + dir: min / max over both poses (the order of the
+                 // reference's nested minimum() calls does not matter: min and max are exact)
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      double x, y, z, dx, dy, dz;
+      ld3(in.pos, v[k], x, y, z);
+      ld3(in.dir, v[k], dx, dy, dz);
+      x = x + dx; y = y + dy; z = z + dz;
+      b.lx = fmin(b.lx, x); b.ly = fmin(b.ly, y); b.lz = fmin(b.lz, z);
+      b.hx = fmax(b.hx, x); b.hy = fmax(b.hy, y); b.hz = fmax(b.hz, z);
+    }
+  }
+  const double m = in.m[KIND];
+  b.lx -= m; b.ly -= m; b.lz -= m;
+  b.hx += m; b.hy += m; b.hz += m;
   return b;
 }
 
@@ -107,21 +130,21 @@ __device__ __forceinline__ Span span_of(const Box& b, const Grid& g) {
 }
 
 template <int KIND>
-__global__ void __launch_bounds__(kBT) bin_count_kernel(const double* __restrict__ pos, const int32_t* __restrict__ elems,
-                                                        int64_t n, double d_hat, Grid g, int32_t* __restrict__ cnt) {
+__global__ void __launch_bounds__(kBT) bin_count_kernel(const Boxes in, const int32_t* __restrict__ elems, int64_t n,
+                                                        Grid g, int32_t* __restrict__ cnt) {
   const int64_t i = (int64_t)blockIdx.x * kBT + threadIdx.x;
   if (i >= n) return;
-  const int64_t c = span_of(make_box<KIND>(pos, elems, i, d_hat), g).count();
+  const int64_t c = span_of(make_box<KIND>(in, elems, i), g).count();
   cnt[i] = (int32_t)(c > 0x7fffffff ? 0x7fffffff : c);
 }
 
 template <int KIND>
-__global__ void __launch_bounds__(kBT) bin_fill_kernel(const double* __restrict__ pos, const int32_t* __restrict__ elems,
-                                                       int64_t n, double d_hat, Grid g, const int64_t* __restrict__ off,
+__global__ void __launch_bounds__(kBT) bin_fill_kernel(const Boxes in, const int32_t* __restrict__ elems, int64_t n,
+                                                       Grid g, const int64_t* __restrict__ off,
                                                        uint64_t* __restrict__ keys, uint32_t* __restrict__ ids) {
   const int64_t i = (int64_t)blockIdx.x * kBT + threadIdx.x;
   if (i >= n) return;
-  const Span s = span_of(make_box<KIND>(pos, elems, i, d_hat), g);
+  const Span s = span_of(make_box<KIND>(in, elems, i), g);
   int64_t o = off[i];
   for (int cx = s.x0; cx <= s.x1; ++cx)
     for (int cy = s.y0; cy <= s.y1; ++cy)
@@ -143,11 +166,10 @@ __device__ __forceinline__ int64_t lower_bound_u64(const uint64_t* __restrict__ 
 }
 
 struct JoinArgs {
-  const double* pos;
+  Boxes in;
   const int32_t* a_elems;   // surf_verts (VT) or edges (EE)
   const int32_t* b_elems;   // tris (VT) or edges (EE)
   int64_t na, nbins;        // A boxes; sorted (cell, B box) incidences
-  double d_hat;
   Grid g;
   const uint64_t* keys;     // sorted
   const uint32_t* ids;
@@ -161,7 +183,7 @@ template <bool EE, bool FILL>
 __global__ void __launch_bounds__(kBT) join_kernel(const __grid_constant__ JoinArgs a) {
   const int64_t i = (int64_t)blockIdx.x * kBT + threadIdx.x;
   if (i >= a.na) return;
-  const Box A = EE ? make_box<2>(a.pos, a.a_elems, i, a.d_hat) : make_box<0>(a.pos, a.a_elems, i, a.d_hat);
+  const Box A = EE ? make_box<2>(a.in, a.a_elems, i) : make_box<0>(a.in, a.a_elems, i);
   const Span s = span_of(A, a.g);
   int av0, av1 = -1;
   if (EE) {
@@ -181,7 +203,7 @@ __global__ void __launch_bounds__(kBT) join_kernel(const __grid_constant__ JoinA
         if (key > k1) break;
         const int64_t j = a.ids[t];
         if (EE && j <= i) continue;  // each unordered pair once, lower edge index first (:310)
-        const Box B = EE ? make_box<2>(a.pos, a.b_elems, j, a.d_hat) : make_box<1>(a.pos, a.b_elems, j, a.d_hat);
+        const Box B = EE ? make_box<2>(a.in, a.b_elems, j) : make_box<1>(a.in, a.b_elems, j);
         if (!(A.lx <= B.hx && B.lx <= A.hx && A.ly <= B.hy && B.ly <= A.hy && A.lz <= B.hz && B.lz <= A.hz)) continue;
         // owner cell = cell of the lower corner of the intersection
         const int ox = cell_of(fmax(A.lx, B.lx), a.g.ox, a.g.inv), oy = cell_of(fmax(A.ly, B.ly), a.g.oy, a.g.inv),
@@ -216,9 +238,8 @@ struct b200ipc_broad {
   // state between count and fill
   bool counted = false;
   int64_t nverts = 0, n_sv = 0, n_tri = 0, n_edge = 0, nbin_t = 0, nbin_e = 0, n_vt = 0, n_ee = 0;
-  const double* pos = nullptr;
+  b200ipc::Boxes in{};
   const int32_t *surf_verts = nullptr, *tris = nullptr, *edges = nullptr;
-  double d_hat = 0.0;
   b200ipc::Grid grid{};
 };
 
@@ -258,14 +279,13 @@ static int bin_boxes(b200ipc_broad* h, const int32_t* elems, int64_t n, BroadBuf
   CK(h->cnt.reserve(n + 1));
   CK(h->off_bin.reserve(n + 1));
   CK(cudaMemsetAsync(h->cnt.ptr + n, 0, sizeof(int32_t), st));
-  bin_count_kernel<KIND><<<bblocks(n), kBT, 0, st>>>(h->pos, elems, n, h->d_hat, h->grid, h->cnt.ptr);
+  bin_count_kernel<KIND><<<bblocks(n), kBT, 0, st>>>(h->in, elems, n, h->grid, h->cnt.ptr);
   RC(post_launch());
   int64_t total = 0;
   RC(scan_counts(h, h->cnt.ptr, h->off_bin.ptr, n, &total, st));
   if (total >= (1ll << 31)) return B200IPC_EINVAL;  // cell size far too small for these boxes
   CK(h->keys_a.reserve(total)); CK(h->ids_a.reserve(total)); CK(keys.reserve(total)); CK(ids.reserve(total));
-  bin_fill_kernel<KIND><<<bblocks(n), kBT, 0, st>>>(h->pos, elems, n, h->d_hat, h->grid, h->off_bin.ptr, h->keys_a.ptr,
-                                                    h->ids_a.ptr);
+  bin_fill_kernel<KIND><<<bblocks(n), kBT, 0, st>>>(h->in, elems, n, h->grid, h->off_bin.ptr, h->keys_a.ptr, h->ids_a.ptr);
   RC(post_launch());
   size_t tb = 0;
   CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, h->keys_a.ptr, keys.ptr, h->ids_a.ptr, ids.ptr, (int)total, 0, 63, st));
@@ -293,19 +313,18 @@ extern "C" int b200ipc_broad_destroy(b200ipc_broad* h) {
   return 0;
 }
 
-extern "C" int b200ipc_broad_phase_count(b200ipc_broad* h, int64_t nverts, const double* positions, int64_t n_sv,
-                                         const int32_t* surf_verts, int64_t n_tri, const int32_t* tris, int64_t n_edge,
-                                         const int32_t* edges, double d_hat, double cell, const double* origin,
-                                         int64_t* n_vt, int64_t* n_ee, void* stream) {
-  if (!h || nverts <= 0 || !positions || n_sv < 0 || n_tri < 0 || n_edge < 0 || !origin || !n_vt || !n_ee)
+static int broad_count(b200ipc_broad* h, int64_t nverts, const Boxes& in, int64_t n_sv, const int32_t* surf_verts,
+                       int64_t n_tri, const int32_t* tris, int64_t n_edge, const int32_t* edges, double cell,
+                       const double* origin, int64_t* n_vt, int64_t* n_ee, void* stream) {
+  if (!h || nverts <= 0 || !in.pos || n_sv < 0 || n_tri < 0 || n_edge < 0 || !origin || !n_vt || !n_ee)
     return B200IPC_EINVAL;
   if ((n_sv && !surf_verts) || (n_tri && !tris) || (n_edge && !edges)) return B200IPC_EINVAL;
-  if (!(d_hat > 0.0) || !(cell > 0.0)) return B200IPC_EINVAL;
+  if (!(cell > 0.0)) return B200IPC_EINVAL;
   if (n_sv >= (1ll << 31) || n_tri >= (1ll << 31) || n_edge >= (1ll << 31)) return B200IPC_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
   h->counted = false;
-  h->nverts = nverts; h->pos = positions; h->n_sv = n_sv; h->surf_verts = surf_verts; h->n_tri = n_tri; h->tris = tris;
-  h->n_edge = n_edge; h->edges = edges; h->d_hat = d_hat;
+  h->nverts = nverts; h->in = in; h->n_sv = n_sv; h->surf_verts = surf_verts; h->n_tri = n_tri; h->tris = tris;
+  h->n_edge = n_edge; h->edges = edges;
   h->grid = Grid{origin[0], origin[1], origin[2], 1.0 / cell};
   h->n_vt = h->n_ee = 0;
 
@@ -315,8 +334,8 @@ extern "C" int b200ipc_broad_phase_count(b200ipc_broad* h, int64_t nverts, const
     CK(h->cnt.reserve(n_sv + 1));
     CK(h->off_vt.reserve(n_sv + 1));
     CK(cudaMemsetAsync(h->cnt.ptr + n_sv, 0, sizeof(int32_t), st));
-    JoinArgs a{positions, surf_verts, tris, n_sv, h->nbin_t, d_hat, h->grid, h->keys_t.ptr, h->ids_t.ptr,
-               nullptr, h->cnt.ptr, nullptr};
+    JoinArgs a{in, surf_verts, tris, n_sv, h->nbin_t, h->grid, h->keys_t.ptr, h->ids_t.ptr, nullptr, h->cnt.ptr,
+               nullptr};
     join_kernel<false, false><<<bblocks(n_sv), kBT, 0, st>>>(a);
     RC(post_launch());
     RC(scan_counts(h, h->cnt.ptr, h->off_vt.ptr, n_sv, &h->n_vt, st));
@@ -327,8 +346,8 @@ extern "C" int b200ipc_broad_phase_count(b200ipc_broad* h, int64_t nverts, const
     CK(h->cnt.reserve(n_edge + 1));
     CK(h->off_ee.reserve(n_edge + 1));
     CK(cudaMemsetAsync(h->cnt.ptr + n_edge, 0, sizeof(int32_t), st));
-    JoinArgs a{positions, edges, edges, n_edge, h->nbin_e, d_hat, h->grid, h->keys_e.ptr, h->ids_e.ptr,
-               nullptr, h->cnt.ptr, nullptr};
+    JoinArgs a{in, edges, edges, n_edge, h->nbin_e, h->grid, h->keys_e.ptr, h->ids_e.ptr, nullptr, h->cnt.ptr,
+               nullptr};
     join_kernel<true, false><<<bblocks(n_edge), kBT, 0, st>>>(a);
     RC(post_launch());
     RC(scan_counts(h, h->cnt.ptr, h->off_ee.ptr, n_edge, &h->n_ee, st));
@@ -339,19 +358,38 @@ extern "C" int b200ipc_broad_phase_count(b200ipc_broad* h, int64_t nverts, const
   return 0;
 }
 
+extern "C" int b200ipc_broad_phase_count(b200ipc_broad* h, int64_t nverts, const double* positions, int64_t n_sv,
+                                         const int32_t* surf_verts, int64_t n_tri, const int32_t* tris, int64_t n_edge,
+                                         const int32_t* edges, double d_hat, double cell, const double* origin,
+                                         int64_t* n_vt, int64_t* n_ee, void* stream) {
+  if (!(d_hat > 0.0)) return B200IPC_EINVAL;
+  const Boxes in{positions, nullptr, {d_hat, 0.0, d_hat * 0.5}};
+  return broad_count(h, nverts, in, n_sv, surf_verts, n_tri, tris, n_edge, edges, cell, origin, n_vt, n_ee, stream);
+}
+
+extern "C" int b200ipc_sweep_candidates_count(b200ipc_broad* h, int64_t nverts, const double* positions,
+                                              const double* directions, int64_t n_sv, const int32_t* surf_verts,
+                                              int64_t n_tri, const int32_t* tris, int64_t n_edge, const int32_t* edges,
+                                              double margin, double cell, const double* origin, int64_t* n_vt,
+                                              int64_t* n_ee, void* stream) {
+  if (!directions || !(margin >= 0.0)) return B200IPC_EINVAL;
+  const Boxes in{positions, directions, {margin, margin, margin}};
+  return broad_count(h, nverts, in, n_sv, surf_verts, n_tri, tris, n_edge, edges, cell, origin, n_vt, n_ee, stream);
+}
+
 extern "C" int b200ipc_broad_phase_fill(b200ipc_broad* h, int32_t* vt, int32_t* ee, void* stream) {
   if (!h || !h->counted) return B200IPC_ESTATE;
   if ((h->n_vt && !vt) || (h->n_ee && !ee)) return B200IPC_EINVAL;
   if (((uintptr_t)vt | (uintptr_t)ee) & 15) return B200IPC_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
   if (h->n_vt) {
-    JoinArgs a{h->pos, h->surf_verts, h->tris, h->n_sv, h->nbin_t, h->d_hat, h->grid, h->keys_t.ptr, h->ids_t.ptr,
+    JoinArgs a{h->in, h->surf_verts, h->tris, h->n_sv, h->nbin_t, h->grid, h->keys_t.ptr, h->ids_t.ptr,
                h->off_vt.ptr, nullptr, reinterpret_cast<int4*>(vt)};
     join_kernel<false, true><<<bblocks(h->n_sv), kBT, 0, st>>>(a);
     RC(post_launch());
   }
   if (h->n_ee) {
-    JoinArgs a{h->pos, h->edges, h->edges, h->n_edge, h->nbin_e, h->d_hat, h->grid, h->keys_e.ptr, h->ids_e.ptr,
+    JoinArgs a{h->in, h->edges, h->edges, h->n_edge, h->nbin_e, h->grid, h->keys_e.ptr, h->ids_e.ptr,
                h->off_ee.ptr, nullptr, reinterpret_cast<int4*>(ee)};
     join_kernel<true, true><<<bblocks(h->n_edge), kBT, 0, st>>>(a);
     RC(post_launch());

@@ -6,7 +6,8 @@ NumPy arrays out, ``matvec_blocks`` accumulating in place into ``out``.  Each ca
 its inputs to the GPU, runs the sm_100a kernel behind the C ABI (``include/b200ipc.h``) and
 copies the results back.  The ``*_device`` variants take and return device tensors.
 
-``accd_max_step`` is not on the hot path this package covers.
+``accd_max_step`` is the n = 1 shim of the batched
+``accd_max_step_device`` / ``contacts.global_ccd_filter``.
 """
 
 import numpy as np
@@ -90,8 +91,33 @@ def matvec_blocks(hess, vids, x, out):
     out[...] = device.to_host(d_out).reshape(out.shape)
 
 
+def accd_max_step_device(ids, pair_kind, positions, directions, slack, max_iter=512, want_status=True):
+    """Batched ACCD: ids (n,4) int32 device tensor, pair_kind an int (uniform) or a (n,) uint8 tensor,
+    positions / directions (N,3) device tensors -> (step (n,), status (n,) or None) device tensors."""
+    n = int(ids.shape[0])
+    step = device.empty((max(n, 1),))
+    status = device.empty((max(n, 1),), np.uint8) if want_status else None
+    uniform = isinstance(pair_kind, (int, np.integer))
+    kinds = None if uniform else pair_kind
+    _lib.check(_lib.lib().b200ipc_accd_max_step(n, device.ptr(ids), device.ptr(kinds), int(pair_kind) if uniform else 0,
+                                                device.ptr(positions), device.ptr(directions), float(slack),
+                                                int(max_iter), device.ptr(step), device.ptr(status), device.stream()),
+               "accd_max_step")
+    return step[:n], None if status is None else status[:n]
+
+
 def accd_max_step(x, dx, pair_kind, slack, max_iter=512):
-    raise NotImplementedError("accd_max_step is outside the accelerated hot path (SURVEY.md 8f N2)")
+    """Twin of kernels/_core.pyx:272-325: x, dx (s,3) of ONE pair -> step fraction (float)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    dx = np.ascontiguousarray(dx, dtype=np.float64)
+    s = x.shape[0]
+    ids = np.full((1, 4), 0, np.int32)
+    ids[0, :s] = np.arange(s)
+    step, status = accd_max_step_device(device.to_device(ids), int(pair_kind), device.to_device(x),
+                                        device.to_device(dx), slack, max_iter)
+    if int(device.to_host(status)[0]) != 0:
+        raise ValueError("additive CCD requires a strictly positive initial distance")  # _core.pyx:307-308
+    return float(device.to_host(step)[0])
 
 
 def get_backend(name):

@@ -345,9 +345,55 @@ def golden_broad():
     save("broad", **out)
 
 
+def golden_ccd():
+    """accd_max_step of the reference's compiled backend on seeded pairs of all four kinds (including
+    zero motion, head-on approach, iteration-cap and step<1e-14 exits), and sweep_candidates +
+    global_ccd_filter of the reference on a small cloth stack pushed along a random direction."""
+    rng = np.random.default_rng(20240819)
+    out = {}
+    n = 400
+    recipes = {
+        kernels.PAIR_PT: lambda d: wl.gen_point_triangle(rng, n, d),
+        kernels.PAIR_EE: lambda d: wl.gen_edge_edge(rng, n, d),
+        kernels.PAIR_PE: lambda d: wl.gen_point_edge(rng, n, d),
+        kernels.PAIR_PP: lambda d: wl.gen_point_point(rng, n, d),
+    }
+    for kind, gen in recipes.items():
+        dist = rng.uniform(0.05, 0.6, size=n)
+        x = gen(dist)
+        s = x.shape[1]
+        dx = rng.normal(size=x.shape) * rng.choice([0.02, 0.3, 2.0], size=(n, 1, 1))
+        dx[:10] = 0.0                                   # lp == 0 -> 1.0
+        dx[10:20] = dx[10:20, :1]                       # rigid translation: mean-free part is zero
+        # first vertex moves straight at the rest: forces contact-limited steps
+        dx[20:120, 0] = (x[20:120, 1:].mean(axis=1) - x[20:120, 0]) * rng.uniform(0.5, 3.0, size=(100, 1))
+        steps = np.array([kernels.accd_max_step(x[i], dx[i], kind, 0.9) for i in range(n)])
+        capped = np.array([kernels.accd_max_step(x[i], dx[i], kind, 0.5, 3) for i in range(n)])
+        out.update({f"k{kind}_x": x, f"k{kind}_dx": dx, f"k{kind}_step": steps, f"k{kind}_step_s05_it3": capped})
+        print(f"ccd kind {kind}: s={s}, full steps {np.mean(steps == 1.0):.2f}, min {steps.min():.3g}")
+    cloth = wl.cloth_stack(layers=3, n=7, seed=13, twist_deg=4.0)
+    scene = _reference_scene(cloth)
+    x = cloth.positions
+    d = rng.normal(size=x.shape) * 0.8 * cloth.d_hat
+    d[:, 2] -= 0.5 * cloth.d_hat * (x[:, 2] > x[:, 2].mean())   # push the upper sheets down
+    cands = rp.sweep_candidates(scene, x, d, cloth.d_hat)
+    alpha = rp.global_ccd_filter(scene, x, d, cands)
+    per_pair = np.array([kernels.accd_max_step(x[list(ids)], d[list(ids)], pair, 0.9) for pair, ids in cands])
+    print(f"ccd scene: {len(cands)} candidates, alpha = {alpha:.6g}")
+    out.update(scene_positions=x, scene_rest_positions=cloth.rest_positions, scene_directions=d, scene_tris=cloth.tris,
+               scene_edges=cloth.edges, scene_d_hat=cloth.d_hat,
+               scene_cand_kind=np.array([p for p, _ in cands], np.uint8),
+               scene_cand_ids=np.array([ids for _, ids in cands], np.int32), scene_cand_step=per_pair,
+               scene_alpha=alpha)
+    save("ccd", **out)
+
+
 if __name__ == "__main__":
     if "--broad-only" in sys.argv:
         golden_broad()
+        sys.exit(0)
+    if "--ccd-only" in sys.argv:
+        golden_ccd()
         sys.exit(0)
     golden_scalars()
     golden_classify()
@@ -355,3 +401,4 @@ if __name__ == "__main__":
     golden_parallel_blocks()
     golden_scene()
     golden_broad()
+    golden_ccd()

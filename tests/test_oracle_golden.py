@@ -243,3 +243,40 @@ def test_broad_phase_candidates_golden(tag):
     tab = o.narrow_phase(x, z[f"{tag}_rest_positions"], vt, ee, d_hat)
     for key in ("kind", "verts", "sub", "eps_x", "origin_type", "origin"):
         np.testing.assert_array_equal(tab[key], z[f"{tag}_list_{key}"], err_msg=key)
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2, 3])
+def test_accd_golden_bit_exact(kind):
+    """oracle.accd_max_step_batch == the reference's compiled accd_max_step (tests/golden/ccd.npz), bit for bit,
+    for PT / EE / PE / PP pairs, at the default cap and at a 3-iteration cap with slack 0.5."""
+    z = load_golden("ccd")
+    x, dx = z[f"k{kind}_x"], z[f"k{kind}_dx"]
+    step, bad = o.accd_max_step_batch(x, dx, kind, 0.9)
+    assert not bad.any()
+    np.testing.assert_array_equal(step, z[f"k{kind}_step"])
+    capped, _ = o.accd_max_step_batch(x, dx, kind, 0.5, 3)
+    np.testing.assert_array_equal(capped, z[f"k{kind}_step_s05_it3"])
+    assert (step[:20] == 1.0).all() and step.min() < 0.5
+
+
+def test_accd_rejects_touching_pair():
+    x = np.zeros((1, 2, 3))
+    dx = np.array([[[1.0, 0, 0], [-1.0, 0, 0]]])
+    step, bad = o.accd_max_step_batch(x, dx, o.PAIR_PP, 0.9)
+    assert bad[0]
+
+
+def test_sweep_and_ccd_filter_golden():
+    """sweep_candidates / global_ccd_filter restated == the reference's (ordered candidate list, per-pair
+    bounds and the global step bound)."""
+    z = load_golden("ccd")
+    x, d, tris, edges = z["scene_positions"], z["scene_directions"], z["scene_tris"], z["scene_edges"]
+    vt, ee = o.sweep_candidates(x, d, np.unique(tris), tris, edges, float(z["scene_d_hat"]))
+    kinds = z["scene_cand_kind"]
+    np.testing.assert_array_equal(vt, z["scene_cand_ids"][kinds == o.PAIR_PT])
+    np.testing.assert_array_equal(ee, z["scene_cand_ids"][kinds == o.PAIR_EE])
+    assert len(vt) + len(ee) == len(kinds)
+    s_vt, _ = o.accd_max_step_batch(x[vt], d[vt], o.PAIR_PT, 0.9)
+    s_ee, _ = o.accd_max_step_batch(x[ee], d[ee], o.PAIR_EE, 0.9)
+    np.testing.assert_array_equal(np.concatenate([s_vt, s_ee]), z["scene_cand_step"])
+    assert o.global_ccd_filter(x, d, vt, ee) == float(z["scene_alpha"]) < 1.0
