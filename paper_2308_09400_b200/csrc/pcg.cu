@@ -174,17 +174,17 @@ __global__ void __launch_bounds__(kPT) pcg_kernel(const PcgArgs a) {
 // the NEXT product as soon as a stage drains, so the first chunks of iteration k+1 arrive while the
 // vector updates and barriers of iteration k run.
 // The direction update c = s + beta c is folded into the product: vectors s and c live interleaved
-// per vertex in two ping-pong buffers B[2] of (n, 6); the product of iteration k+1 gathers (s_j, c_j)
-// from B[k], forms c'_j = s_j + beta c_j in registers (the same two roundings as a stored update),
-// and the lanes that finish row i store c'_i into B[k+1] -- so the separate update pass and its grid
-// barrier disappear.  x is read with coherent loads (it changes every iteration).
+// per component in two ping-pong buffers B[2] of (n, 3, 2) = (s_j, c_j) pairs; the product of
+// iteration k+1 gathers one pair with ONE 16-byte load from B[k], forms c'_j = s_j + beta c_j in
+// registers (the same two roundings as a stored update), and the lanes that finish row i store c'_i
+// into B[k+1] -- so the separate update pass and its grid barrier disappear.  x is read with coherent loads (it changes every iteration).
 struct PcgStreamArgs {
   int64_t n;
   const double* pinv;
   const uint8_t* fixed;
   const double* rhs;
   double* d;
-  double* buf[2];           // (n, 6): s (3), c (3)
+  double* buf[2];           // (n, 3, 2): (s_j, c_j) pairs
   double* rbuf[2];          // residual, ping-pong (the update reads all three entries of a vertex)
   double* q;
   double* part;             // 2 * kMaxParts partial sums (ping-pong)
@@ -220,8 +220,8 @@ __global__ void __launch_bounds__(kStreamThreads, 1) pcg_stream_kernel(const __g
     a.d[3 * v] = a.d[3 * v + 1] = a.d[3 * v + 2] = 0.0;
     a.rbuf[0][3 * v] = r0; a.rbuf[0][3 * v + 1] = r1; a.rbuf[0][3 * v + 2] = r2;
     double* w = a.buf[0] + 6 * v;
-    w[0] = s0; w[1] = s1; w[2] = s2;
-    w[3] = w[4] = w[5] = 0.0;
+    w[0] = s0; w[2] = s1; w[4] = s2;
+    w[1] = w[3] = w[5] = 0.0;
     acc += r0 * s0 + r1 * s1 + r2 * s2;
   }
   {
@@ -250,17 +250,17 @@ __global__ void __launch_bounds__(kStreamThreads, 1) pcg_stream_kernel(const __g
       double* bnew = a.buf[cur ^ 1];
       // ---- c = s + beta c (on the fly); q = A c; denom = c.q -----------------------------------------
       acc = 0.0;
-      const double* wj = bold + j;
+      const double2* wj = reinterpret_cast<const double2*>(bold) + j;
       stream_product(
           m, sm, st, unbounded,
           [&](int col) {
-            const double* w = wj + 6ll * col;
-            return w[0] + beta * w[3];
+            const double2 w = wj[3ll * col];
+            return w.x + beta * w.y;
           },
           [&](int64_t row, int i, double yi) {
-            const double* w = bold + 6 * row + i;
-            const double cn = w[0] + beta * w[3];
-            bnew[6 * row + 3 + i] = cn;
+            const double2 w = reinterpret_cast<const double2*>(bold)[3 * row + i];
+            const double cn = w.x + beta * w.y;
+            bnew[6 * row + 2 * i + 1] = cn;
             a.q[3 * row + i] = yi;
             acc += cn * yi;
           });
@@ -279,22 +279,24 @@ __global__ void __launch_bounds__(kStreamThreads, 1) pcg_stream_kernel(const __g
       // read P^-1 with a 72-byte stride).  Each thread forms the vertex's three new residual entries --
       // the same expressions in all three threads, so they agree bitwise -- and keeps row k of P^-1.
       acc = 0.0;
-      const double* rold = a.rbuf[cur];
-      double* rnew = a.rbuf[cur ^ 1];
+      const double* __restrict__ rold = a.rbuf[cur];
+      double* __restrict__ rnew = a.rbuf[cur ^ 1];
+      const double* __restrict__ qv = a.q;
+      const double* __restrict__ pinv = a.pinv;
+      double* __restrict__ dvec = a.d;
       for (int64_t t = tid; t < 3 * a.n; t += nthreads) {
         const int64_t v = t / 3;
         const int k = (int)(t - 3 * v);
-        const double rr0 = rold[3 * v] - alpha * a.q[3 * v];
-        const double rr1 = rold[3 * v + 1] - alpha * a.q[3 * v + 1];
-        const double rr2 = rold[3 * v + 2] - alpha * a.q[3 * v + 2];
-        const double* p = a.pinv + 9 * v + 3 * k;
+        const double rr0 = rold[3 * v] - alpha * qv[3 * v];
+        const double rr1 = rold[3 * v + 1] - alpha * qv[3 * v + 1];
+        const double rr2 = rold[3 * v + 2] - alpha * qv[3 * v + 2];
+        const double* p = pinv + 9 * v + 3 * k;
         const double sk = p[0] * rr0 + p[1] * rr1 + p[2] * rr2;
         const double rk = k == 0 ? rr0 : (k == 1 ? rr1 : rr2);
-        double* w = bnew + 6 * v;
-        a.d[t] += alpha * w[3 + k];
-        w[k] = sk;
-        acc += rk * sk;
+        dvec[t] += alpha * bnew[6 * v + 2 * k + 1];
+        bnew[6 * v + 2 * k] = sk;
         rnew[t] = rk;
+        acc += rk * sk;
       }
       {
         const double t = block_sum(acc, sh);

@@ -17,11 +17,11 @@
 // index, one x gather, one shared-memory value and one FMA per block per lane, no index arithmetic --
 // and two shuffles finish the three rows.  (One row per warp with cross-lane block partitioning costs
 // 3x the instructions per block plus a 5-shuffle tail; this kernel was issue-bound that way.)
-// The producer warp's lane 0 waits for a free stage (empty barrier) and issues three bulk copies per
-// chunk (row pointers, values, column indices); the block spans it needs for that are fetched 32
-// chunks at a time, one per lane -- a dependent row-pointer load per chunk capped the issue rate at
-// one chunk per global-memory round trip (25 us per product however the ring was configured).
-// Everything is coupled through full/empty mbarriers only.  (Prefetching the x rows a landed chunk will gather into L1 from the producer warp
+// The producer warp waits for a free stage (empty barrier), stores the chunk's row pointers (fetched
+// while the previous stage drained) next to it and lane 0 issues the two bulk copies.  Everything is
+// coupled through full/empty mbarriers only.  (Tried and dropped: row pointers by a third bulk copy
+// with the block spans fetched 32 chunks ahead -- 2.7 us slower per product; L1 prefetch of the
+// gathered x rows from the producer warp -- 3.8 us slower.)  (Prefetching the x rows a landed chunk will gather into L1 from the producer warp
 // was measured slower -- 28.8 vs 25.0 us -- and was removed.)
 //
 // A chunk whose span does not fit a stage (pathologically long rows) is reduced straight from
@@ -58,7 +58,7 @@ constexpr int kStageBlocks = B200IPC_STREAM_STAGE_BLOCKS;         // 3x3 blocks 
 // byte layout of one stage: values (16-byte aligned superset of the span), column indices, row pointers
 constexpr int kStageValBytes = (kStageBlocks * 72 + 32 + 15) / 16 * 16;
 constexpr int kStageColBytes = (kStageBlocks * 4 + 32 + 15) / 16 * 16;
-constexpr int kStageRowBytes = (kMaxChunkRows + 1 + 3 + 3) / 4 * 16;
+constexpr int kStageRowBytes = (kMaxChunkRows + 4 + 3) / 4 * 16;
 constexpr int kStageBytes = kStageValBytes + kStageColBytes + kStageRowBytes;
 constexpr int kStreamSmemBytes = kStreamStages * kStageBytes + 16 * kStreamStages;  // + full/empty mbarriers
 
@@ -137,7 +137,9 @@ struct StreamSmem {
   __device__ __forceinline__ int32_t* cols(int s) const {
     return reinterpret_cast<int32_t*>(base + (size_t)s * kStageBytes + kStageValBytes);
   }
-  // 16-byte aligned superset of rowptr[r0 .. r0 + nrows]
+  // rows(s)[0] = number of rows, rows(s)[1] = first block b0 of the chunk,
+  // rows(s)[2 + r] = rowptr[r0 + r] - b0 for r = 0..nrows (the last one = blocks of the chunk; a value
+  // above kStageBlocks marks a chunk that was not staged)
   __device__ __forceinline__ int32_t* rows(int s) const {
     return reinterpret_cast<int32_t*>(base + (size_t)s * kStageBytes + kStageValBytes + kStageColBytes);
   }
@@ -179,46 +181,33 @@ __device__ __forceinline__ int64_t stream_chunk_row(const StreamMatrix& m, const
 #endif
 }
 
-// Issue the loads of sequence number q: rows [r0, r0 + nrows), blocks [b0, b1) (one thread).  Three
-// bulk copies: the chunk's row pointers (always), its values and its column indices (unless the span
-// does not fit a stage: such a chunk is reduced straight from global memory).  Every copy moves a
-// 16-byte aligned superset of its span; only an array's very end may stick out of the allocation,
-// and there the last elements are patched with plain loads instead.
-__device__ __forceinline__ void stream_issue(const StreamMatrix& m, const StreamSmem& sm, uint32_t q, int64_t r0,
-                                             int nrows, int64_t b0, int64_t b1) {
+// Issue the loads of sequence number q, whose chunk covers blocks [b0, b1) (one thread).  Each copy
+// moves a 16-byte aligned superset of its span; only an array's very end may stick out of the
+// allocation, and there the last elements are patched with plain loads instead.
+__device__ __forceinline__ void stream_issue(const StreamMatrix& m, const StreamSmem& sm, uint32_t q, int64_t b0,
+                                             int64_t b1) {
   const int s = (int)(q % kStreamStages);
   uint64_t* bar = sm.full + s;
-  // row pointers: ints [r0, r0 + nrows] -> bytes [ra, re)
-  const int64_t ra = (4 * r0) & ~15ll;
-  int64_t re = (4 * (r0 + nrows + 1) + 15) & ~15ll;
-  int32_t* sr = sm.rows(s);
-  if (re > 4 * (m.n + 1)) {
-    re -= 16;
-    for (int64_t t = re / 4; t <= m.n; ++t) sr[t - ra / 4] = m.rowptr[t];
+  if (b1 - b0 > kStageBlocks || b1 == b0) {  // oversize (or empty) chunk: reduced from global memory
+    mbar_arrive(bar);
+    return;
   }
-  const uint32_t rbytes = (uint32_t)(re - ra);
-  uint32_t vbytes = 0, cbytes = 0;
-  int64_t va = 0, ca = 0;
+  const int64_t va = (72 * b0) & ~15ll;
+  int64_t ve = (72 * b1 + 15) & ~15ll;
   double* sv = sm.vals(s);
-  int32_t* sc = sm.cols(s);
-  if (b1 - b0 <= kStageBlocks && b1 > b0) {
-    va = (72 * b0) & ~15ll;
-    int64_t ve = (72 * b1 + 15) & ~15ll;
-    if (ve > 72 * m.nnzb) {
-      ve -= 16;
-      sv[(ve - va) / 8] = m.vals[ve / 8];
-    }
-    ca = (4 * b0) & ~15ll;
-    int64_t ce = (4 * b1 + 15) & ~15ll;
-    if (ce > 4 * m.nnzb) {
-      ce -= 16;
-      for (int64_t t = ce / 4; t < m.nnzb; ++t) sc[t - ca / 4] = m.colidx[t];
-    }
-    vbytes = (uint32_t)(ve - va);
-    cbytes = (uint32_t)(ce - ca);
+  if (ve > 72 * m.nnzb) {
+    ve -= 16;
+    sv[(ve - va) / 8] = m.vals[ve / 8];
   }
-  mbar_expect_tx(bar, rbytes + vbytes + cbytes);
-  if (rbytes) bulk_g2s(sr, reinterpret_cast<const char*>(m.rowptr) + ra, rbytes, bar);
+  const int64_t ca = (4 * b0) & ~15ll;
+  int64_t ce = (4 * b1 + 15) & ~15ll;
+  int32_t* sc = sm.cols(s);
+  if (ce > 4 * m.nnzb) {
+    ce -= 16;
+    for (int64_t t = ce / 4; t < m.nnzb; ++t) sc[t - ca / 4] = m.colidx[t];
+  }
+  const uint32_t vbytes = (uint32_t)(ve - va), cbytes = (uint32_t)(ce - ca);
+  mbar_expect_tx(bar, vbytes + cbytes);
   if (vbytes) bulk_g2s(sv, reinterpret_cast<const char*>(m.vals) + va, vbytes, bar);
   if (cbytes) bulk_g2s(sc, reinterpret_cast<const char*>(m.colidx) + ca, cbytes, bar);
 }
@@ -227,35 +216,34 @@ __device__ __forceinline__ void stream_issue(const StreamMatrix& m, const Stream
 // the lane's row (shared or global memory), len is its length (0 for an absent row or lane >= 27).
 // Returns, in lanes with j == 0, component i of row r.  x is read with plain (coherent) loads: the persistent PCG kernel rewrites it between
 // products.
-#ifndef B200IPC_STREAM_UNROLL
-#define B200IPC_STREAM_UNROLL 4
-#endif
-constexpr int kTrioUnroll = B200IPC_STREAM_UNROLL;
-
 template <typename GATHER>
 __device__ __forceinline__ double stream_trio_product(const double* __restrict__ v, const int32_t* __restrict__ ci,
-                                                      int len, int maxlen, GATHER xg) {
-  // Column indices and x gathers are unconditional (the block index is clamped to the row's last
-  // block, whose x row is already in cache); only the value is predicated, to zero, so an absent
-  // block adds v * x = 0.  Software pipeline: the gathers of trip t+1 are issued before the FMAs of
-  // trip t wait for their operands (in-order issue would otherwise serialise the gather latencies);
-  // values come from shared memory right before use.
-  const int last = len > 0 ? len - 1 : 0;
+                                                      int len, int minlen, int maxlen, GATHER xg) {
+  // Trips of four blocks.  While all three rows of the trio still have four blocks left (warp-uniform
+  // test) the body is branch- and predicate-free: four column indices, four gathers, four values, four
+  // FMAs.  The ragged end runs predicated: indices clamped to the row's last block (whose x row is in
+  // cache), values forced to zero, so an absent block adds v * x = 0.
   double acc = 0.0;
-  double xa[kTrioUnroll];
-#pragma unroll
-  for (int u = 0; u < kTrioUnroll; ++u) xa[u] = xg(ci[min(u, last)]);
-  for (int t = 0; t < maxlen; t += kTrioUnroll) {
-    double xb[kTrioUnroll];
-#pragma unroll
-    for (int u = 0; u < kTrioUnroll; ++u) xb[u] = xg(ci[min(t + kTrioUnroll + u, last)]);
-#pragma unroll
-    for (int u = 0; u < kTrioUnroll; ++u) {
-      const double vv = t + u < len ? v[9 * (t + u)] : 0.0;
-      acc = fma(vv, xa[u], acc);
-    }
-#pragma unroll
-    for (int u = 0; u < kTrioUnroll; ++u) xa[u] = xb[u];
+  int t = 0;
+  for (; t + 4 <= minlen; t += 4) {
+    const int c0 = ci[t], c1 = ci[t + 1], c2 = ci[t + 2], c3 = ci[t + 3];
+    const double x0 = xg(c0), x1 = xg(c1), x2 = xg(c2), x3 = xg(c3);
+    const double v0 = v[9 * t], v1 = v[9 * t + 9], v2 = v[9 * t + 18], v3 = v[9 * t + 27];
+    acc = fma(v0, x0, acc);
+    acc = fma(v1, x1, acc);
+    acc = fma(v2, x2, acc);
+    acc = fma(v3, x3, acc);
+  }
+  const int last = len > 0 ? len - 1 : 0;
+  for (; t < maxlen; t += 4) {
+    const int c0 = ci[min(t, last)], c1 = ci[min(t + 1, last)], c2 = ci[min(t + 2, last)], c3 = ci[min(t + 3, last)];
+    const double x0 = xg(c0), x1 = xg(c1), x2 = xg(c2), x3 = xg(c3);
+    const double v0 = t < len ? v[9 * t] : 0.0, v1 = t + 1 < len ? v[9 * t + 9] : 0.0;
+    const double v2 = t + 2 < len ? v[9 * t + 18] : 0.0, v3 = t + 3 < len ? v[9 * t + 27] : 0.0;
+    acc = fma(v0, x0, acc);
+    acc = fma(v1, x1, acc);
+    acc = fma(v2, x2, acc);
+    acc = fma(v3, x3, acc);
   }
   const double t1 = __shfl_down_sync(0xffffffffu, acc, 1);
   const double t2 = __shfl_down_sync(0xffffffffu, acc, 2);
@@ -277,40 +265,44 @@ __device__ __forceinline__ void stream_product(const StreamMatrix& m, const Stre
   if (issue_end > limit) issue_end = limit;
   if (st.nmine > 0) {
     if (warp == kConsumerWarps) {
-      // ---- producer warp -------------------------------------------------------------------------
-      // Lane l holds the block span of sequence number qbase + l: one round of (dependent) row-pointer
-      // loads per 32 chunks, so the issue rate is not tied to a global-memory round trip per chunk.
-      uint32_t q = st.issued, qbase = q;
-      int32_t sb0 = 0, sb1 = 0;
-      auto load_spans = [&]() {
-        const uint32_t qq = qbase + (uint32_t)lane;
-        if (qq < issue_end) {
-          const int64_t r0 = stream_chunk_row(m, st, qq);
-          sb0 = m.rowptr[r0];
-          sb1 = m.rowptr[min(m.n, r0 + m.rows_per_chunk)];
-        }
+      // ---- producer warp: waits for a drained stage, stores the chunk's row pointers, issues the copies;
+      // the row pointers of the following chunk are in flight meanwhile
+      uint32_t q = st.issued;
+      int64_t r0 = 0;
+      int nrows = 0;
+      int32_t rp[(kMaxChunkRows + 32) / 32];  // this lane's row pointers of chunk q
+      int32_t rb0 = 0, rb1 = 0;               // its block range
+      auto load_rows = [&](uint32_t qq) {
+        r0 = stream_chunk_row(m, st, qq);
+        nrows = (int)min((int64_t)m.rows_per_chunk, m.n - r0);
+#pragma unroll
+        for (int k = 0; k < (kMaxChunkRows + 32) / 32; ++k) rp[k] = m.rowptr[r0 + min(lane + 32 * k, nrows)];
+        rb0 = m.rowptr[r0];
+        rb1 = m.rowptr[r0 + nrows];
       };
-      load_spans();
-      for (; q < issue_end; ++q) {
-        if (q - qbase == 32u) {
-          qbase = q;
-          load_spans();
-        }
+      if (q < issue_end) load_rows(q);
+      for (; q < issue_end;) {
         const int s = (int)(q % kStreamStages);
-        const int32_t b0 = __shfl_sync(0xffffffffu, sb0, (int)(q - qbase));
-        const int32_t b1 = __shfl_sync(0xffffffffu, sb1, (int)(q - qbase));
+#ifdef B200IPC_PCG_TIMING
+        const long long t0 = clock64();
+#endif
+        if (q >= (uint32_t)kStreamStages) mbar_wait(sm.empty + s, ((q / kStreamStages) - 1u) & 1u);
+#ifdef B200IPC_PCG_TIMING
+        if (m.dbg && lane == 0) m.dbg[3 * blockIdx.x + 2] += (unsigned long long)(clock64() - t0);
+#endif
+        const int32_t b0 = rb0, b1 = rb1;
+        int32_t* hdr = sm.rows(s);
+#pragma unroll
+        for (int k = 0; k < (kMaxChunkRows + 32) / 32; ++k)
+          if (lane + 32 * k <= nrows) hdr[2 + lane + 32 * k] = rp[k] - b0;
         if (lane == 0) {
-#ifdef B200IPC_PCG_TIMING
-          const long long t0 = clock64();
-#endif
-          if (q >= (uint32_t)kStreamStages) mbar_wait(sm.empty + s, ((q / kStreamStages) - 1u) & 1u);
-#ifdef B200IPC_PCG_TIMING
-          if (m.dbg) m.dbg[3 * blockIdx.x + 2] += (unsigned long long)(clock64() - t0);
-#endif
-          const int64_t r0 = stream_chunk_row(m, st, q);
-          stream_issue(m, sm, q, r0, (int)min((int64_t)m.rows_per_chunk, m.n - r0), b0, b1);
+          hdr[0] = nrows;
+          hdr[1] = b0;
         }
-        __syncwarp();
+        __syncwarp();  // header stores happen before lane 0's releasing arrive
+        if (lane == 0) stream_issue(m, sm, q, b0, b1);
+        ++q;
+        if (q < issue_end) load_rows(q);  // in flight while the next stage drains
       }
     } else {
       // ---- consumer warps -------------------------------------------------------------------------
@@ -320,7 +312,6 @@ __device__ __forceinline__ void stream_product(const StreamMatrix& m, const Stre
       for (; q < end; q += kStreamGroups) {
         const int s = (int)(q % kStreamStages);
         const int64_t row0 = stream_chunk_row(m, st, q);
-        const int nrows = (int)min((int64_t)m.rows_per_chunk, m.n - row0);
 #ifdef B200IPC_PCG_TIMING
         const long long t0 = clock64();
 #endif
@@ -328,10 +319,10 @@ __device__ __forceinline__ void stream_product(const StreamMatrix& m, const Stre
 #ifdef B200IPC_PCG_TIMING
         const long long t1 = clock64();
 #endif
-        const int32_t* hdr = sm.rows(s) + (row0 & 3);    // 4 r0 mod 16 = 4 (r0 mod 4): alignment slack in ints
-        const int32_t cb0 = hdr[0];
-        const int32_t cblk = hdr[nrows] - cb0;
-        const bool staged = cblk <= kStageBlocks && cblk > 0;
+        const int32_t* hdr = sm.rows(s);
+        const int nrows = hdr[0];
+        const int32_t cb0 = hdr[1];
+        const bool staged = hdr[2 + nrows] <= kStageBlocks && hdr[2 + nrows] > 0;
         const double* sv = sm.vals(s) + (cb0 & 1) + e;   // 72 b0 mod 16 = 8 (b0 mod 2): alignment slack in doubles
         const int32_t* sc = sm.cols(s) + (cb0 & 3);      // 4 b0 mod 16 = 4 (b0 mod 4)
         for (int tr = 3 * gw; tr < nrows; tr += 3 * kGroupWarps) {
@@ -339,13 +330,14 @@ __device__ __forceinline__ void stream_product(const StreamMatrix& m, const Stre
           int o0 = 0, len = 0;
           const bool valid = r < 3 && row < nrows;
           if (valid) {
-            o0 = hdr[row] - cb0;
-            len = hdr[row + 1] - cb0 - o0;
+            o0 = hdr[2 + row];
+            len = hdr[3 + row] - o0;
           }
           const int maxlen = __reduce_max_sync(0xffffffffu, len);
+          const int minlen = __reduce_min_sync(0xffffffffu, valid ? len : 0x7fffffff);  // over the rows present
           double yi;
-          if (staged) yi = stream_trio_product(sv + 9 * o0, sc + o0, len, maxlen, xg);
-          else yi = stream_trio_product(m.vals + 9ll * ((int64_t)cb0 + o0) + e, m.colidx + (int64_t)cb0 + o0, len, maxlen, xg);
+          if (staged) yi = stream_trio_product(sv + 9 * o0, sc + o0, len, minlen, maxlen, xg);
+          else yi = stream_trio_product(m.vals + 9ll * ((int64_t)cb0 + o0) + e, m.colidx + (int64_t)cb0 + o0, len, minlen, maxlen, xg);
           if (j == 0 && valid) emit(row0 + row, e / 3, yi);
         }
         __syncwarp();
