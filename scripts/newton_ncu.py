@@ -6,19 +6,26 @@ import torch
 from paper_2308_09400_b200 import barrier, contacts, device, solver, stencils, workloads
 
 cloth = workloads.cloth_stack(layers=4, n=140, seed=1, d_hat_rel=0.2)
-vt, ee = workloads.broad_phase(cloth)
 params = barrier.BarrierParams(d_hat=cloth.d_hat, kappa=cloth.kappa)
 pos = device.to_device(cloth.positions)
-table, _ = contacts.narrow_phase_device(pos, cloth.rest_positions, vt, ee, cloth.d_hat, want_origin=False)
-batch = stencils.evaluate(table, pos, params, dt=cloth.dt)
+bp = contacts.BroadPhase(None, cloth.tris, cloth.edges, cloth.d_hat, cloth.positions)
+for _ in range(2):
+    vt, ee = bp.query(pos)
+    table, _ = contacts.narrow_phase_device(pos, cloth.rest_positions, vt, ee, cloth.d_hat, want_origin=False)
+dirs = device.to_device(0.3 * cloth.d_hat * np.random.default_rng(3).normal(size=cloth.positions.shape))
+for _ in range(2):
+    bp.ccd_step_bound(pos, dirs)
+batch = stencils.evaluate(table, pos, params, dt=cloth.dt, want_factors=True)
 fams = [batch.families[s] for s in sorted(batch.families)]
 sysm = solver.NewtonSystem(cloth.masses, cloth.fixed)
 sysm.set_pattern([(f.s, f.vids) for f in fams])
 hess = [f.hess for f in fams]
-for variant in (0, 1, 0):
+for variant in (0, 4, 0):
     sysm.set_numeric_variant(variant)
     for _ in range(2):
         sysm.assemble(hess)
+for _ in range(2):
+    sysm.assemble_from_factors([f.fac for f in fams])
 x = device.to_device(np.random.default_rng(0).normal(size=3 * sysm.n))
 for _ in range(3):
     y = sysm.spmv(x)
