@@ -261,7 +261,10 @@ def newton_section(torch, pkg, steps, warmup, peak, seed):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     d, iters, ok, _, _ = sysm.pcg(rhs, 1e-30, iters_cap)
-    ms_pcg_iter = (time.perf_counter() - t0) * 1e3 / max(iters, 1)
+    t1 = time.perf_counter()
+    d, iters2, ok, _, _ = sysm.pcg(rhs, 1e-30, 5 * iters_cap)
+    # slope between a 50- and a 250-iteration solve: launch, result copy and sync cancel
+    ms_pcg_iter = ((time.perf_counter() - t1) - (t1 - t0)) * 1e3 / max(iters2 - iters, 1)
     t0 = time.perf_counter()
     d, it_full, ok_full, _, _ = sysm.pcg(rhs, 1e-4, 2000)
     ms_pcg_full = (time.perf_counter() - t0) * 1e3
@@ -274,6 +277,31 @@ def newton_section(torch, pkg, steps, warmup, peak, seed):
     alpha = bp.ccd_step_bound(pos, dirs)
     torch.cuda.synchronize()
     ms_ccd = (time.perf_counter() - t0) * 1e3
+    # one whole Newton direction through the public device-resident API, host arrays in, host array out:
+    # H2D (x, x~) -> detect -> stencils (factors) -> symbolic + numeric assembly -> gradient -> PCG -> D2H d
+    x_host = np.ascontiguousarray(cloth.positions)
+    xt_host = np.ascontiguousarray(x_tilde)
+
+    def newton_direction():
+        px, pxt = device.to_device(x_host), device.to_device(xt_host)
+        cvt, cee = bp.query(px)
+        tab, _ = contacts.narrow_phase_device(px, d_rest, cvt, cee, cloth.d_hat, want_origin=False)
+        b = stencils.evaluate(tab, px, params, dt=cloth.dt, want_hess=False, want_factors=True)
+        fl = [b.families[s_] for s_ in sorted(b.families)]
+        sysm.set_pattern([(f.s, f.vids) for f in fl])
+        sysm.assemble_from_factors([f.fac for f in fl])
+        g = sysm.gradient(px, pxt, [f.grad for f in fl])
+        sysm.block_jacobi()
+        dd, its, okk, _, _ = sysm.pcg(-g, 1e-4, 2000)
+        return device.to_host(dd), its, okk, float(b.summary()[0])
+
+    newton_direction()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    reps_e2e = 3
+    for _ in range(reps_e2e):
+        d_host, its_e2e, ok_e2e, energy_e2e = newton_direction()
+    ms_newton_e2e = (time.perf_counter() - t0) * 1e3 / reps_e2e
     n_c = table.n
     ent = sum(int(f.vids.shape[0]) * f.s * f.s for f in fams)
     num_bytes = sum(int(f.vids.shape[0]) * (72 * f.s * f.s) for f in fams) + 4 * ent + 72 * nnzb
@@ -290,6 +318,10 @@ def newton_section(torch, pkg, steps, warmup, peak, seed):
         "assembly_plus_spmv_ms": ms_numeric + ms_spmv, "gradient_scatter_ms": ms_grad,
         "ccd": {"sweep_candidates": int(s_vt.shape[0]) + int(s_ee.shape[0]), "sweep_plus_filter_ms": ms_ccd,
                 "alpha": alpha, "note": "sweep_candidates + global_ccd_filter (proximity.py:388-432), random 0.3 d_hat step"},
+        "newton_direction_e2e": {"ms": ms_newton_e2e, "pcg_iters": its_e2e, "converged": ok_e2e,
+                                 "h2d_bytes": 2 * x_host.nbytes, "d2h_bytes": int(d_host.nbytes) + 8,
+                                 "note": "host x, x~ in -> detect, stencils (rank-1 factors), symbolic + numeric assembly, "
+                                         "gradient, block-Jacobi PCG to 1e-4 -> host direction + energy out; wall clock"},
         "pcg_ms_per_iter": ms_pcg_iter, "pcg_solve_ms": ms_pcg_full, "pcg_iters": it_full, "pcg_converged": ok_full,
         "roofline_assembly": {"bound": "hbm", "achieved": num_bytes / ms_numeric / 1e6, "peak": peak, "unit": "GB/s",
                               "frac": num_bytes / ms_numeric / 1e6 / peak},
