@@ -277,6 +277,21 @@ def newton_section(torch, pkg, steps, warmup, peak, seed):
     alpha = bp.ccd_step_bound(pos, dirs)
     torch.cuda.synchronize()
     ms_ccd = (time.perf_counter() - t0) * 1e3
+    # friction: lagged state once per time step, blocks once per Newton iteration
+    from paper_2308_09400_b200 import friction as friction_mod
+
+    raw = stencils.evaluate(table, pos, params, dt=1.0, want_energy=False, want_hess=False)
+    fstate = friction_mod.update_state(table, pos, 0.4, 1e-3, cloth.dt, barrier_batch=raw)  # warm
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    fstate = friction_mod.update_state(table, pos, 0.4, 1e-3, cloth.dt, barrier_batch=raw)
+    torch.cuda.synchronize()
+    ms_fstate = (time.perf_counter() - t0) * 1e3
+    x_moved = device.to_device(cloth.positions + 0.5 * cloth.dt * 1e-3 * np.random.default_rng(4).normal(size=cloth.positions.shape))
+    friction_mod.evaluate(fstate, x_moved, pos)
+    ms_fblocks = time_steps(torch, lambda: friction_mod.evaluate(fstate, x_moved, pos), 10, 2, noop) / 10
+    fr_bytes = sum(int(fstate.table.family_count(s_)) * (72 * s_ * s_ + 24 * s_ + 4 * s_ + 96) for s_ in (2, 3, 4))
+    del raw
     # one whole Newton direction through the public device-resident API, host arrays in, host array out:
     # H2D (x, x~) -> detect -> stencils (factors) -> symbolic + numeric assembly -> gradient -> PCG -> D2H d
     x_host = np.ascontiguousarray(cloth.positions)
@@ -322,6 +337,10 @@ def newton_section(torch, pkg, steps, warmup, peak, seed):
                                  "h2d_bytes": 2 * x_host.nbytes, "d2h_bytes": int(d_host.nbytes) + 8,
                                  "note": "host x, x~ in -> detect, stencils (rank-1 factors), symbolic + numeric assembly, "
                                          "gradient, block-Jacobi PCG to 1e-4 -> host direction + energy out; wall clock"},
+        "friction": {"data": int(fstate.n), "state_ms": ms_fstate, "blocks_ms": ms_fblocks,
+                     "blocks_GBps": fr_bytes / ms_fblocks / 1e6,
+                     "note": "update_friction_state (once per time step) and friction energy/grad/rank-2 PSD blocks "
+                             "(once per Newton iteration, incl. output allocation) on the same contact table"},
         "pcg_ms_per_iter": ms_pcg_iter, "pcg_solve_ms": ms_pcg_full, "pcg_iters": it_full, "pcg_converged": ok_full,
         "roofline_assembly": {"bound": "hbm", "achieved": num_bytes / ms_numeric / 1e6, "peak": peak, "unit": "GB/s",
                               "frac": num_bytes / ms_numeric / 1e6 / peak},

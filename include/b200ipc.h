@@ -237,6 +237,34 @@ int b200ipc_narrow_phase(int64_t nverts, const double* positions, const double* 
                          uint8_t* origin_type, int32_t* origin,
                          int64_t* n_out /* host */, int64_t* kind_off /* host[8] */, void* stream);
 
+/* ---- lagged smooth Coulomb friction (friction.py) ----------------------------------- */
+/* update_friction_state (friction.py:148-171) for a whole kind-sorted stencil table: per stencil the
+ * witness weights, contact normal, tangent frame (build_basis, :128-145) and lambda_n = |one side's
+ * summed RAW (not dt^2-scaled) barrier gradient|.  grad2/3/4: the barrier gradient families
+ * (nb,3s) in group_blocks order as written by b200ipc_barrier_stencils with dt2 = 1.  frame (n,12):
+ * cn[4] = coeffs/|coeffs|, t1[3], t2[3], lambda_n, 0 -- the sliding basis is T[3v:3v+3, k] = cn_v t_k.
+ * status (n) u8: 0 datum, 1 skipped (d2 <= 0 or lambda_n <= 0, as the reference skips them),
+ * 3 undefined contact normal (the reference raises ValueError, :138-139).  kind_off: host[8]. */
+int b200ipc_friction_state(int64_t n, const int64_t* kind_off /* host[8] */, const int32_t* verts,
+                           const uint8_t* sub, const double* positions, const double* grad2,
+                           const double* grad3, const double* grad4, double* frame, uint8_t* status,
+                           void* stream);
+/* The friction part of assemble_local_quadratics / _friction_energy (solver.py:147-152, :210-214) for a
+ * kind-sorted table of friction data (rows with status 0, compacted): u = T^T (x - x_start)
+ * (friction.py:174-178), energy (n, by table row, NOT dt^2-scaled) = mu lambda_n f0(|u|) (:49-52), gradient
+ * families = -dt^2 friction_force (:55-61), hess families = dt^2 friction_hessian_psd (:64-82): rank-2
+ * closed form w_p p p^T + w_q q q^T.  Families in group_blocks order; any output may be NULL. */
+int b200ipc_friction_blocks(int64_t n, const int64_t* kind_off /* host[8] */, const int32_t* verts,
+                            const double* frame, const double* x, const double* x_start, double mu,
+                            double eps_v, double dt, double* energy, double* grad2, double* hess2,
+                            double* grad3, double* hess3, double* grad4, double* hess4, void* stream);
+/* potential / friction_force / friction_hessian_psd (friction.py:49-82) with an explicit basis
+ * (n,3s,2) and tangential displacement u (n,2): potential (n), force (n,3s), hess (n,3s,3s) -- none of
+ * them dt^2-scaled, like the reference functions; any output may be NULL. */
+int b200ipc_friction_explicit(int64_t n, int32_t s, const double* basis, const double* u,
+                              const double* lambda_n, double mu, double eps_v, double dt,
+                              double* potential, double* force, double* hess, void* stream);
+
 /* ---- assembly into the 3x3-block sparse global matrix (BSR) -------------------- */
 /* The reference's production path is matrix-free; the assembled matrix is the one its tests
  * build densely (tests/test_solver.py:71-84): A = diag(m_i I3) + sum_b scatter(H_b), fixed

@@ -946,3 +946,157 @@ def global_ccd_filter(positions, directions, vt, ee, slack=0.9, max_iter=512):
                 raise ValueError("additive CCD requires a strictly positive initial distance")
             alpha = min(alpha, float(step.min()))
     return alpha
+
+
+# ---------------------------------------------------------------------------------------------
+# lagged smooth Coulomb friction: friction.py
+# ---------------------------------------------------------------------------------------------
+def stencil_witness_batch(kind, verts, sub, positions):
+    """Branch witness (n,2) of every table row as DistanceResult.witness holds it
+    (proximity.py:183-222): PT (w1,w2), EE (s,t), PE (t,-), PP (-,-); parallel kinds on x[sub]."""
+    kind = np.asarray(kind)
+    n = kind.shape[0]
+    x = _gather(np.asarray(positions, dtype=np.float64), np.asarray(verts))
+    wit = np.zeros((n, 2))
+    sub = np.asarray(sub)
+    loc = np.stack([(sub >> (2 * k)) & 3 for k in range(4)], axis=1).astype(np.int64)
+    i = np.flatnonzero(kind == PE)
+    if i.size:
+        wit[i, 0] = point_edge_batch(x[i, 0], x[i, 1], x[i, 2])[2]
+    i = np.flatnonzero(kind == PT)
+    if i.size:
+        wit[i] = pt_classify_batch(x[i, 0], x[i, 1], x[i, 2], x[i, 3])[3]
+    i = np.flatnonzero(kind == EE)
+    if i.size:
+        wit[i] = ee_classify_batch(x[i, 0], x[i, 1], x[i, 2], x[i, 3])[3]
+    i = np.flatnonzero(kind == EEP)
+    if i.size:
+        xs = np.take_along_axis(x[i], loc[i][:, :, None], axis=1)
+        wit[i] = ee_classify_batch(xs[:, 0], xs[:, 1], xs[:, 2], xs[:, 3])[3]
+    i = np.flatnonzero(kind == PEP)
+    if i.size:
+        xs = np.take_along_axis(x[i], loc[i][:, :, None], axis=1)
+        wit[i, 0] = point_edge_batch(xs[:, 0], xs[:, 1], xs[:, 2])[2]
+    return wit
+
+
+def friction_state(kind, verts, sub, positions, raw_grad):
+    """update_friction_state (friction.py:148-171) for every table row.
+
+    raw_grad (n,12): the raw (not dt^2-scaled) barrier gradient of each stencil, zero padded.
+    Returns dict(status (n,) u8: 0 datum / 1 skipped (d2 <= 0 or lambda_n <= 0) / 3 undefined normal,
+    lambda_n (n,), cn (n,4) = coeffs/|coeffs|, t1 (n,3), t2 (n,3)); the basis of row i is
+    T[3v:3v+3, k] = cn[i,v] * t_k[i] (build_basis, friction.py:128-145).
+    """
+    kind = np.asarray(kind)
+    n = kind.shape[0]
+    sub = np.asarray(sub)
+    d2, grad_d2 = stencil_distance_batch(kind, verts, sub, positions)
+    wit = stencil_witness_batch(kind, verts, sub, positions)
+    w0, w1 = wit[:, 0], wit[:, 1]
+    loc = np.stack([(sub >> (2 * k)) & 3 for k in range(4)], axis=1).astype(np.int64)
+    co = np.zeros((n, 4))
+    side = np.zeros((n, 4), dtype=bool)
+    # _witness_coefficients (friction.py:85-117)
+    i = kind == PP
+    co[i, 0], co[i, 1] = 1.0, -1.0
+    side[i, 0] = True
+    i = kind == PE
+    co[i, 0], co[i, 1], co[i, 2] = 1.0, -(1.0 - w0[i]), -w0[i]
+    side[i, 0] = True
+    i = kind == PT
+    co[i, 0], co[i, 1], co[i, 2], co[i, 3] = 1.0, -(1.0 - w0[i] - w1[i]), -w0[i], -w1[i]
+    side[i, 0] = True
+    i = kind == EE
+    co[i, 0], co[i, 1], co[i, 2], co[i, 3] = 1.0 - w0[i], w0[i], -(1.0 - w1[i]), -w1[i]
+    side[i, 0] = side[i, 1] = True
+    for k, nl in ((EEP, 4), (PEP, 3), (PPP, 2)):
+        rows = np.flatnonzero(kind == k)
+        if not rows.size:
+            continue
+        if k == EEP:
+            local = np.stack([1.0 - w0[rows], w0[rows], -(1.0 - w1[rows]), -w1[rows]], axis=1)
+        elif k == PEP:
+            local = np.stack([np.ones(rows.size), -(1.0 - w0[rows]), -w0[rows]], axis=1)
+        else:
+            local = np.stack([np.ones(rows.size), -np.ones(rows.size)], axis=1)
+        for r in range(nl):
+            co[rows, loc[rows, r]] = local[:, r]
+            pos = local[:, r] > 0.0
+            side[rows[pos], loc[rows[pos], r]] = True
+    status = np.zeros(n, np.uint8)
+    status[~(d2 > 0.0)] = 1
+    with np.errstate(divide="ignore", invalid="ignore"):
+        one = np.sum(np.where(side[:, :, None], grad_d2, 0.0), axis=1)
+        d = np.sqrt(d2)
+        normal = one / (2.0 * d)[:, None]
+        nn = np.sqrt(np.sum(normal * normal, axis=1))
+        status[(status == 0) & (nn == 0.0)] = 3
+        normal = normal / nn[:, None]
+        m = np.argmin(np.abs(normal), axis=1)          # first minimum on ties, like np.argmin in the reference
+        ref = np.zeros((n, 3))
+        ref[np.arange(n), m] = 1.0
+        t1 = np.cross(normal, ref)
+        t1 = t1 / np.sqrt(np.sum(t1 * t1, axis=1))[:, None]
+        t2 = np.cross(normal, t1)
+        gs = np.sum(np.where(side[:, :, None], np.asarray(raw_grad, dtype=np.float64).reshape(n, 4, 3), 0.0), axis=1)
+        lam = np.sqrt(np.sum(gs * gs, axis=1))
+        status[(status == 0) & ~(lam > 0.0)] = 1
+        cn = co / np.sqrt(np.sum(co * co, axis=1))[:, None]
+    ok = status == 0
+    return {"status": status, "lambda_n": np.where(ok, lam, 0.0), "cn": np.where(ok[:, None], cn, 0.0),
+            "t1": np.where(ok[:, None], t1, 0.0), "t2": np.where(ok[:, None], t2, 0.0)}
+
+
+def friction_basis(cn, t1, t2, s):
+    """basis_T (3s,2) of one datum from its frame."""
+    basis = np.zeros((3 * s, 2))
+    for v in range(s):
+        basis[3 * v:3 * v + 3, 0] = cn[v] * t1
+        basis[3 * v:3 * v + 3, 1] = cn[v] * t2
+    return basis
+
+
+def f0_f1(un, eps_v, dt):
+    """f0_f1 (friction.py:33-46), vectorised."""
+    un = np.asarray(un, dtype=np.float64)
+    h = dt * eps_v
+    f1 = -un * un / (h * h) + 2.0 * un / h
+    f1p = -2.0 * un / (h * h) + 2.0 / h
+    f0 = -un**3 / (3.0 * h * h) + un * un / h + h / 3.0
+    slide = un >= h
+    return np.where(slide, un, f0), np.where(slide, 1.0, f1), np.where(slide, 0.0, f1p)
+
+
+def friction_blocks(verts, size, lambda_n, cn, t1, t2, x, x_start, mu, eps_v, dt):
+    """Per datum: potential (not dt^2-scaled), grad = -dt^2 friction_force, hess = dt^2
+    friction_hessian_psd, padded to 12 (friction.py:49-82, :174-178; solver.py:147-152, :210-214)."""
+    verts = np.asarray(verts)
+    n = verts.shape[0]
+    rel = _gather(np.asarray(x, dtype=np.float64), verts) - _gather(np.asarray(x_start, dtype=np.float64), verts)
+    live = (np.arange(4)[None, :] < np.asarray(size)[:, None])
+    cnl = np.where(live, cn, 0.0)
+    u0 = np.sum(cnl * np.einsum("nvk,nk->nv", rel, t1), axis=1)
+    u1 = np.sum(cnl * np.einsum("nvk,nk->nv", rel, t2), axis=1)
+    un = np.sqrt(u0 * u0 + u1 * u1)
+    f0, f1, f1p = f0_f1(un, eps_v, dt)
+    ml = mu * lambda_n
+    energy = ml * f0
+    # T as (n,12,2)
+    T = np.zeros((n, 12, 2))
+    for v in range(4):
+        T[:, 3 * v:3 * v + 3, 0] = cnl[:, v:v + 1] * t1
+        T[:, 3 * v:3 * v + 3, 1] = cnl[:, v:v + 1] * t2
+    u = np.stack([u0, u1], axis=1)
+    zero = un == 0.0
+    safe = np.where(zero, 1.0, un)
+    force = -(ml * f1 / safe)[:, None] * np.einsum("nrk,nk->nr", T, u)
+    force[zero] = 0.0
+    uhat = u / safe[:, None]
+    outer = uhat[:, :, None] * uhat[:, None, :]
+    eye = np.eye(2)[None]
+    core = np.maximum(f1p, 0.0)[:, None, None] * outer + np.maximum(f1 / safe, 0.0)[:, None, None] * (eye - outer)
+    core[zero] = (2.0 / (eps_v * dt)) * np.eye(2)
+    hess = ml[:, None, None] * np.einsum("nrk,nkl,ncl->nrc", T, core, T)
+    dt2 = dt * dt
+    return {"energy": energy, "grad": -dt2 * force, "hess": dt2 * hess, "u": u}

@@ -388,7 +388,80 @@ def golden_ccd():
     save("ccd", **out)
 
 
+def _friction_case(rf, stencils, x0, x1, d_hat, kappa, mu, eps_v, dt, hess_stride):
+    st = fake_state(d_hat, kappa, dt, masses=np.ones(x0.shape[0]), fixed=np.zeros(x0.shape[0], bool))
+    grads = rs.SimState.barrier_gradient_blocks(st, x0, stencils)
+    data = rf.update_friction_state(stencils, grads, x0, mu, eps_v, dt)
+    index = {id(s): i for i, s in enumerate(stencils)}
+    rows = np.array([index[id(d.stencil)] for d in data])
+    n = len(data)
+    lam = np.array([d.lambda_n for d in data])
+    basis, u, pot = np.zeros((n, 12, 2)), np.zeros((n, 2)), np.zeros(n)
+    force, hess = np.zeros((n, 12)), np.zeros((n, 12, 12))
+    for i, d in enumerate(data):
+        s = len(d.stencil.verts)
+        basis[i, :3 * s] = d.basis_T
+        u[i] = rf.tangential_displacement(d, x1, x0)
+        pot[i] = rf.potential(d, u[i])
+        force[i, :3 * s] = rf.friction_force(d, u[i])
+        hess[i, :3 * s, :3 * s] = rf.friction_hessian_psd(d, u[i]).hess
+    raw = np.zeros((len(stencils), 12))
+    for i, g in enumerate(grads):
+        raw[i, :len(g)] = g
+    h = dt * eps_v
+    kinds = sorted({s.kind.value for s in stencils})
+    print(f"friction: {len(stencils)} stencils {kinds} -> {n} data, |u|/h up to {(np.linalg.norm(u, axis=1) / h).max():.3g}, "
+          f"zero-motion data {(np.linalg.norm(u, axis=1) == 0).sum()}")
+    return dict(table_of(stencils), x0=x0, x1=x1, raw_grad=raw, mu=mu, eps_v=eps_v, dt=dt, d_hat=d_hat, kappa=kappa,
+                rows=rows, lambda_n=lam, basis=basis, u=u, potential=pot, force=force,
+                hess_rows=np.arange(0, n, hess_stride), hess=hess[::hess_stride])
+
+
+def golden_friction():
+    """update_friction_state / tangential_displacement / potential / friction_force /
+    friction_hessian_psd of the reference, with the reference's own raw barrier gradients, at a displaced
+    pose with stick, slip and zero-motion data: (a) the golden cloth scene, (b) a nearly-parallel
+    edge-edge batch (edge-edge-parallel / point-edge-parallel / point-point-parallel stencils)."""
+    from tetipc import friction as rf
+
+    rng = np.random.default_rng(77)
+    cloth = wl.cloth_stack(layers=3, n=6, seed=3, twist_deg=5.0)
+    x0 = cloth.positions
+    stencils = rp.find_contact_pairs(_reference_scene(cloth), x0, cloth.d_hat)
+    mu, eps_v, dt = 0.4, 1e-2, cloth.dt
+    h = dt * eps_v
+    x1 = x0 + rng.normal(size=x0.shape) * h * rng.choice([0.05, 0.5, 5.0], size=(x0.shape[0], 1))
+    for st_ in stencils[::97]:                      # a few data with exactly zero tangential motion
+        x1[list(st_.verts)] = x0[list(st_.verts)]
+    out = {f"a_{k}": v for k, v in _friction_case(rf, stencils, x0, x1, cloth.d_hat, cloth.kappa, mu, eps_v, dt, 3).items()}
+
+    batch = wl.config2_batch(n=240, seed=20240820)
+    x0 = batch.positions
+    stencils = []
+    for q in batch.ee:
+        ea, eb = q[:2], q[2:]
+        eps = rp.edge_parallel_eps(batch.rest_positions, ea, eb)
+        kind, local, res, c = rp.classify_edge_edge(x0[q[0]], x0[q[1]], x0[q[2]], x0[q[3]], eps_x=eps)
+        if res.d2 >= batch.d_hat**2:
+            continue
+        gids = tuple(int(v) for v in q)
+        if kind in rp.PARALLEL_KINDS:
+            stencils.append(rp.ContactStencil(kind=kind, verts=gids, eps_x=eps, sub=local, origin=("ee",) + gids,
+                                              edge_pair=(gids[:2], gids[2:])))
+        else:
+            stencils.append(rp.ContactStencil(kind=kind, verts=tuple(gids[k] for k in local), origin=("ee",) + gids))
+    stencils.sort(key=lambda s: s.sort_key())
+    dt, eps_v = 0.01, 1.0
+    h = dt * eps_v
+    x1 = x0 + rng.normal(size=x0.shape) * h * rng.choice([0.05, 0.5, 5.0], size=(x0.shape[0], 1))
+    out.update({f"b_{k}": v for k, v in _friction_case(rf, stencils, x0, x1, batch.d_hat, batch.kappa, 0.3, eps_v, dt, 2).items()})
+    save("friction", **out)
+
+
 if __name__ == "__main__":
+    if "--friction-only" in sys.argv:
+        golden_friction()
+        sys.exit(0)
     if "--broad-only" in sys.argv:
         golden_broad()
         sys.exit(0)
@@ -402,3 +475,4 @@ if __name__ == "__main__":
     golden_scene()
     golden_broad()
     golden_ccd()
+    golden_friction()

@@ -1,0 +1,140 @@
+"""GPU friction against the reference's frozen outputs (tests/golden/friction.npz) and the oracle."""
+
+from types import SimpleNamespace
+
+import numpy as np
+import pytest
+
+from conftest import block_rel_err, load_golden, rel_err
+from oracle import tetipc_oracle as o
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-9
+
+
+@pytest.fixture(scope="module")
+def F():
+    from paper_2308_09400_b200 import barrier, device, friction, proximity, solver, stencils
+
+    return SimpleNamespace(barrier=barrier, device=device, friction=friction, proximity=proximity, solver=solver,
+                           stencils=stencils)
+
+
+@pytest.fixture(scope="module", params=["a", "b"])
+def z(request):
+    """(a) golden cloth scene, (b) nearly-parallel edge-edge batch (parallel kinds, skipped stencils)."""
+    full = load_golden("friction")
+    return {k[2:]: v for k, v in full.items() if k.startswith(request.param + "_")}
+
+
+def _state(F, z):
+    table = F.proximity.StencilTable(z["kind"], z["verts"], z["sub"], z["eps_x"])
+    params = F.barrier.BarrierParams(d_hat=float(z["d_hat"]), kappa=float(z["kappa"]))
+    return table, F.friction.update_state(table, z["x0"], float(z["mu"]), float(z["eps_v"]), float(z["dt"]), params=params)
+
+
+def test_friction_state_matches_reference(F, z):
+    table, state = _state(F, z)
+    assert np.array_equal(state.rows, z["rows"])                     # same data kept, same order
+    fr = F.device.to_host(state.frame)
+    assert rel_err(fr[:, 10], z["lambda_n"]) < TOL
+    size = F.proximity.KIND_SIZE[z["kind"]][state.rows]
+    worst = 0.0
+    for i in range(len(fr)):
+        s = int(size[i])
+        basis = np.zeros((3 * s, 2))
+        for v in range(s):
+            basis[3 * v:3 * v + 3, 0] = fr[i, v] * fr[i, 4:7]
+            basis[3 * v:3 * v + 3, 1] = fr[i, v] * fr[i, 7:10]
+        worst = max(worst, float(np.abs(basis - z["basis"][i, :3 * s]).max()))
+    assert worst < TOL                                                # basis columns are unit vectors
+    # the oracle agrees too (all seven kinds are present in the scene)
+    ref = o.friction_state(z["kind"], z["verts"], z["sub"], z["x0"], z["raw_grad"])
+    assert np.array_equal(np.flatnonzero(ref["status"] == 0), state.rows)
+    assert len(np.unique(z["kind"])) >= 5
+
+
+def test_friction_blocks_match_reference(F, z):
+    table, state = _state(F, z)
+    batch = F.friction.evaluate(state, z["x1"], z["x0"])
+    dt2 = float(z["dt"]) ** 2
+    assert rel_err(F.device.to_host(batch.energy), z["potential"]) < TOL
+    kinds = z["kind"][state.rows]
+    off = np.searchsorted(kinds, np.arange(8))
+    n_hess = 0
+    for s, fam in batch.families.items():
+        rows = np.concatenate([np.arange(off[k], off[k + 1]) for k in F.stencils.FAMILY_KINDS[s]])
+        grad, hess = F.device.to_host(fam.grad), F.device.to_host(fam.hess)
+        assert np.array_equal(F.device.to_host(fam.vids), z["verts"][state.rows][rows][:, :s])
+        assert block_rel_err(grad, -dt2 * z["force"][rows][:, :3 * s]) < TOL
+        pick = np.flatnonzero(np.isin(rows, z["hess_rows"]))
+        ref = dt2 * z["hess"][np.searchsorted(z["hess_rows"], rows[pick])][:, :3 * s, :3 * s]
+        assert block_rel_err(hess[pick], ref) < TOL
+        n_hess += len(pick)
+        # PSD, rank <= 2, symmetric
+        for blk in hess[:: max(1, len(hess) // 40)]:
+            assert np.array_equal(blk, blk.T)
+            ev = np.linalg.eigvalsh(blk)
+            assert ev.min() >= -1e-12 * max(ev.max(), 1e-300) and (ev > 1e-9 * ev.max()).sum() <= 2
+    assert n_hess == len(z["hess_rows"])
+    assert abs(batch.total_energy() - z["potential"].sum()) <= TOL * z["potential"].sum()
+
+
+def test_friction_blocks_flow_through_the_assembly(F, z):
+    """Friction families are ordinary (hess, vids) families: assembled next to nothing else here,
+    the matrix equals the dense sum of the reference's friction blocks."""
+    table, state = _state(F, z)
+    batch = F.friction.evaluate(state, z["x1"], z["x0"])
+    nv = z["x0"].shape[0]
+    masses, fixed = np.ones(nv), np.zeros(nv, bool)
+    grouped = [(F.device.to_host(h), F.device.to_host(v)) for h, v in batch.grouped()]
+    rowptr, colidx, vals = F.solver.assemble_bsr(grouped, masses, fixed)
+    dense = np.zeros((3 * nv, 3 * nv))
+    for r, (a, b) in enumerate(zip(rowptr[:-1], rowptr[1:])):
+        for c, blk in zip(colidx[a:b], vals[a:b]):
+            dense[3 * r:3 * r + 3, 3 * c:3 * c + 3] = blk
+    ref = np.eye(3 * nv)
+    dt2 = float(z["dt"]) ** 2
+    o_st = o.friction_state(z["kind"], z["verts"], z["sub"], z["x0"], z["raw_grad"])
+    rows = state.rows
+    size = o.KIND_SIZE[z["kind"]][rows]
+    blocks = o.friction_blocks(z["verts"][rows], size, o_st["lambda_n"][rows], o_st["cn"][rows], o_st["t1"][rows],
+                               o_st["t2"][rows], z["x1"], z["x0"], float(z["mu"]), float(z["eps_v"]), float(z["dt"]))
+    for i, r in enumerate(rows):
+        s = int(size[i])
+        idx = np.concatenate([[3 * v, 3 * v + 1, 3 * v + 2] for v in z["verts"][r, :s]])
+        ref[np.ix_(idx, idx)] += blocks["hess"][i, :3 * s, :3 * s]
+    assert np.abs(dense - ref).max() <= TOL * np.abs(ref).max()
+    assert dt2 > 0
+
+
+def test_reference_shaped_entry_points(F, z):
+    """update_friction_state / potential / friction_force / friction_hessian_psd / f0_f1 twins."""
+    table = F.proximity.StencilTable(z["kind"], z["verts"], z["sub"], z["eps_x"], z["origin_type"], z["origin"])
+    stencils = table.to_stencils()
+    size = F.proximity.KIND_SIZE[z["kind"]]
+    grads = [z["raw_grad"][i, :3 * int(size[i])] for i in range(len(stencils))]
+    data = F.friction.update_friction_state(stencils, grads, z["x0"], float(z["mu"]), float(z["eps_v"]), float(z["dt"]))
+    assert len(data) == len(z["rows"])
+    hess_at = {int(r): k for k, r in enumerate(z["hess_rows"])}
+    for i in list(range(0, len(data), 211)) + [len(data) - 1]:
+        d = data[i]
+        s = len(d.stencil.verts)
+        assert abs(d.lambda_n - z["lambda_n"][i]) <= TOL * z["lambda_n"][i]
+        assert np.abs(d.basis_T - z["basis"][i, :3 * s]).max() < TOL
+        u = F.friction.tangential_displacement(d, z["x1"], z["x0"])
+        assert np.abs(u - z["u"][i]).max() <= 1e-12 * max(np.abs(z["u"][i]).max(), 1e-300) + 1e-18
+        assert abs(F.friction.potential(d, u) - z["potential"][i]) <= TOL * z["potential"][i]
+        f = F.friction.friction_force(d, u)
+        assert np.abs(f - z["force"][i, :3 * s]).max() <= TOL * max(np.abs(z["force"][i]).max(), 1e-300)
+        if i in hess_at:
+            blk = F.friction.friction_hessian_psd(d, u)
+            ref = z["hess"][hess_at[i]][:3 * s, :3 * s]
+            assert np.abs(blk.hess - ref).max() <= TOL * np.abs(ref).max()
+            assert np.array_equal(blk.vert_ids, np.asarray(d.stencil.verts)) and not blk.grad.any()
+    h = float(z["dt"]) * float(z["eps_v"])
+    for un in (0.0, 0.3 * h, h, 2.5 * h):
+        f0, f1, f1p = F.friction.f0_f1(un, float(z["eps_v"]), float(z["dt"]))
+        r0, r1, r1p = o.f0_f1(un, float(z["eps_v"]), float(z["dt"]))
+        assert abs(f0 - r0) <= 1e-12 * abs(r0) and abs(f1 - r1) <= 1e-12 and abs(f1p - r1p) <= 1e-12 * max(abs(r1p), 1)
+    assert F.friction.update_friction_state(stencils, grads, z["x0"], 0.0, 1e-2, 0.01) == []

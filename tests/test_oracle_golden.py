@@ -280,3 +280,32 @@ def test_sweep_and_ccd_filter_golden():
     s_ee, _ = o.accd_max_step_batch(x[ee], d[ee], o.PAIR_EE, 0.9)
     np.testing.assert_array_equal(np.concatenate([s_vt, s_ee]), z["scene_cand_step"])
     assert o.global_ccd_filter(x, d, vt, ee) == float(z["scene_alpha"]) < 1.0
+
+
+@pytest.mark.parametrize("tag", ["a", "b"])
+def test_friction_golden(tag):
+    """oracle friction == the reference's update_friction_state / tangential_displacement / potential /
+    friction_force / friction_hessian_psd (tests/golden/friction.npz): (a) the golden cloth scene,
+    (b) a nearly-parallel edge-edge batch with all three parallel kinds and two skipped stencils."""
+    full = load_golden("friction")
+    z = {k[2:]: v for k, v in full.items() if k.startswith(tag + "_")}
+    st = o.friction_state(z["kind"], z["verts"], z["sub"], z["x0"], z["raw_grad"])
+    rows = z["rows"]
+    assert np.array_equal(np.flatnonzero(st["status"] == 0), rows)      # same data kept, same order
+    size = o.KIND_SIZE[z["kind"]][rows]
+    assert rel_err(st["lambda_n"][rows], z["lambda_n"]) < 1e-12
+    for i in range(0, len(rows), 7):
+        s = int(size[i])
+        b = o.friction_basis(st["cn"][rows[i]], st["t1"][rows[i]], st["t2"][rows[i]], s)
+        assert np.abs(b - z["basis"][i, :3 * s]).max() < 1e-12
+    out = o.friction_blocks(z["verts"][rows], size, st["lambda_n"][rows], st["cn"][rows], st["t1"][rows], st["t2"][rows],
+                            z["x1"], z["x0"], float(z["mu"]), float(z["eps_v"]), float(z["dt"]))
+    dt2 = float(z["dt"]) ** 2
+    assert np.abs(out["u"] - z["u"]).max() <= 1e-12 * np.abs(z["u"]).max()
+    assert rel_err(out["energy"], z["potential"]) < 1e-10
+    assert block_rel_err(out["grad"], -dt2 * z["force"]) < 1e-9
+    assert block_rel_err(out["hess"][z["hess_rows"]], dt2 * z["hess"]) < 1e-9
+    if tag == "a":
+        assert (np.linalg.norm(z["u"], axis=1) == 0.0).sum() > 0            # the isotropic u = 0 branch is covered
+    else:
+        assert len(rows) < len(z["kind"]) and {1, 3, 5} <= set(np.unique(z["kind"]))   # skips + parallel kinds
