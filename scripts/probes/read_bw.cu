@@ -30,6 +30,11 @@ __global__ void __launch_bounds__(256) plain_read_u4x4(const uint4* __restrict__
   if (acc == 0x12345678u) *sink = acc;
 }
 
+__global__ void __launch_bounds__(256) plain_write(uint4* __restrict__ p, size_t n) {
+  const uint4 v = make_uint4(1, 2, 3, 4);
+  for (size_t i = (size_t)blockIdx.x * 256 + threadIdx.x; i < n; i += (size_t)gridDim.x * 256) p[i] = v;
+}
+
 __global__ void __launch_bounds__(128, 1) bulk_read(const char* __restrict__ p, size_t bytes, int chunk, int stages,
                                                     unsigned* sink) {
   extern __shared__ __align__(128) unsigned char dyn[];
@@ -98,6 +103,15 @@ int main(int argc, char** argv) {
     cudaEventSynchronize(e1);
     cudaEventElapsedTime(&ms, e0, e1);
     printf("plain4 grid %5d : %.1f GB/s\n", grid, bytes * reps / ms / 1e6);
+  }
+  for (int grid : {148 * 4, 148 * 8, 148 * 16, 148 * 32}) {
+    plain_write<<<grid, 256>>>((uint4*)buf, bytes / 16);
+    cudaEventRecord(e0);
+    for (int r = 0; r < reps; ++r) plain_write<<<grid, 256>>>((uint4*)buf, bytes / 16);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+    printf("write  grid %5d : %.1f GB/s\n", grid, bytes * reps / ms / 1e6);
   }
   cudaFuncSetAttribute(bulk_read, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
   for (int chunkkb : {4, 8, 16, 32, 64}) {
