@@ -11,7 +11,7 @@ for spec in sys.argv[1:]:
     objs = []
     for src in _build.SOURCES:
         obj = os.path.join(_build.OBJ, src.replace(".cu", ".o"))
-        if src in ("spmv.cu", "pcg.cu"):
+        if src in os.environ.get("VARIANT_SOURCES", "spmv.cu,pcg.cu").split(","):
             obj = os.path.join(out, f"{tag}_{src.replace('.cu', '.o')}")
             subprocess.check_call([_build._nvcc()] + _build.NVCC_FLAGS + dflags + ["-c", os.path.join(_build.CSRC, src), "-o", obj])
         objs.append(obj)
