@@ -51,7 +51,10 @@ class BroadPhase:
             self._h = C.c_void_p()
 
     def __del__(self):
-        self.close()
+        try:
+            self.close()
+        except Exception:  # interpreter shutdown: module globals may already be gone
+            pass
 
     def query(self, positions):
         """positions (N,3) host array or device tensor -> (vt (m,4), ee (k,4)) int32 device tensors."""

@@ -52,7 +52,7 @@ struct Grid {
   double inv;         // 1 / cell
 };
 
-struct Box {
+struct __align__(16) Box {
   double lx, ly, lz, hx, hy, hz;
 };
 
@@ -129,6 +129,15 @@ __device__ __forceinline__ Span span_of(const Box& b, const Grid& g) {
   return s;
 }
 
+// Boxes of all elements of one kind, once per query: the join then tests 48 contiguous bytes per
+// candidate instead of rebuilding the box from two or three gathered vertices.
+template <int KIND>
+__global__ void __launch_bounds__(kBT) make_boxes_kernel(const Boxes in, const int32_t* __restrict__ elems, int64_t n,
+                                                         Box* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * kBT + threadIdx.x;
+  if (i < n) out[i] = make_box<KIND>(in, elems, i);
+}
+
 template <int KIND>
 __global__ void __launch_bounds__(kBT) bin_count_kernel(const Boxes in, const int32_t* __restrict__ elems, int64_t n,
                                                         Grid g, int32_t* __restrict__ cnt) {
@@ -173,6 +182,7 @@ struct JoinArgs {
   Grid g;
   const uint64_t* keys;     // sorted
   const uint32_t* ids;
+  const Box* bbox;          // boxes of the B elements
   const int64_t* off;       // per A box output offset (fill pass)
   int32_t* cnt;             // per A box pair count (count pass)
   int4* out;                // (pairs, 4) global vertex ids (fill pass)
@@ -183,7 +193,7 @@ template <bool EE, bool FILL>
 __global__ void __launch_bounds__(kBT) join_kernel(const __grid_constant__ JoinArgs a) {
   const int64_t i = (int64_t)blockIdx.x * kBT + threadIdx.x;
   if (i >= a.na) return;
-  const Box A = EE ? make_box<2>(a.in, a.a_elems, i) : make_box<0>(a.in, a.a_elems, i);
+  const Box A = EE ? a.bbox[i] : make_box<0>(a.in, a.a_elems, i);
   const Span s = span_of(A, a.g);
   int av0, av1 = -1;
   if (EE) {
@@ -203,7 +213,7 @@ __global__ void __launch_bounds__(kBT) join_kernel(const __grid_constant__ JoinA
         if (key > k1) break;
         const int64_t j = a.ids[t];
         if (EE && j <= i) continue;  // each unordered pair once, lower edge index first (:310)
-        const Box B = EE ? make_box<2>(a.in, a.b_elems, j) : make_box<1>(a.in, a.b_elems, j);
+        const Box B = a.bbox[j];
         if (!(A.lx <= B.hx && B.lx <= A.hx && A.ly <= B.hy && B.ly <= A.hy && A.lz <= B.hz && B.lz <= A.hz)) continue;
         // owner cell = cell of the lower corner of the intersection
         const int ox = cell_of(fmax(A.lx, B.lx), a.g.ox, a.g.inv), oy = cell_of(fmax(A.ly, B.ly), a.g.oy, a.g.inv),
@@ -235,6 +245,7 @@ struct b200ipc_broad {
   b200ipc::BroadBuf<uint32_t> ids_a, ids_t, ids_e;
   b200ipc::BroadBuf<uint8_t> temp;
   b200ipc::BroadBuf<int64_t> totals;
+  b200ipc::BroadBuf<b200ipc::Box> box_t, box_e;
   // state between count and fill
   bool counted = false;
   int64_t nverts = 0, n_sv = 0, n_tri = 0, n_edge = 0, nbin_t = 0, nbin_e = 0, n_vt = 0, n_ee = 0;
@@ -308,7 +319,7 @@ extern "C" int b200ipc_broad_destroy(b200ipc_broad* h) {
   h->cnt.release(); h->off_bin.release(); h->off_vt.release(); h->off_ee.release();
   h->keys_a.release(); h->keys_t.release(); h->keys_e.release();
   h->ids_a.release(); h->ids_t.release(); h->ids_e.release();
-  h->temp.release(); h->totals.release();
+  h->temp.release(); h->totals.release(); h->box_t.release(); h->box_e.release();
   delete h;
   return 0;
 }
@@ -330,24 +341,30 @@ static int broad_count(b200ipc_broad* h, int64_t nverts, const Boxes& in, int64_
 
   // ---- point-triangle: triangles binned, vertex boxes probe ----------------------------------------
   if (n_sv && n_tri) {
+    CK(h->box_t.reserve(n_tri));
+    make_boxes_kernel<1><<<bblocks(n_tri), kBT, 0, st>>>(in, tris, n_tri, h->box_t.ptr);
+    RC(post_launch());
     RC(bin_boxes<1>(h, tris, n_tri, h->keys_t, h->ids_t, &h->nbin_t, st));
     CK(h->cnt.reserve(n_sv + 1));
     CK(h->off_vt.reserve(n_sv + 1));
     CK(cudaMemsetAsync(h->cnt.ptr + n_sv, 0, sizeof(int32_t), st));
-    JoinArgs a{in, surf_verts, tris, n_sv, h->nbin_t, h->grid, h->keys_t.ptr, h->ids_t.ptr, nullptr, h->cnt.ptr,
-               nullptr};
+    JoinArgs a{in, surf_verts, tris, n_sv, h->nbin_t, h->grid, h->keys_t.ptr, h->ids_t.ptr, h->box_t.ptr, nullptr,
+               h->cnt.ptr, nullptr};
     join_kernel<false, false><<<bblocks(n_sv), kBT, 0, st>>>(a);
     RC(post_launch());
     RC(scan_counts(h, h->cnt.ptr, h->off_vt.ptr, n_sv, &h->n_vt, st));
   }
   // ---- edge-edge: edges binned, the same boxes probe --------------------------------------------------
   if (n_edge > 1) {
+    CK(h->box_e.reserve(n_edge));
+    make_boxes_kernel<2><<<bblocks(n_edge), kBT, 0, st>>>(in, edges, n_edge, h->box_e.ptr);
+    RC(post_launch());
     RC(bin_boxes<2>(h, edges, n_edge, h->keys_e, h->ids_e, &h->nbin_e, st));
     CK(h->cnt.reserve(n_edge + 1));
     CK(h->off_ee.reserve(n_edge + 1));
     CK(cudaMemsetAsync(h->cnt.ptr + n_edge, 0, sizeof(int32_t), st));
-    JoinArgs a{in, edges, edges, n_edge, h->nbin_e, h->grid, h->keys_e.ptr, h->ids_e.ptr, nullptr, h->cnt.ptr,
-               nullptr};
+    JoinArgs a{in, edges, edges, n_edge, h->nbin_e, h->grid, h->keys_e.ptr, h->ids_e.ptr, h->box_e.ptr, nullptr,
+               h->cnt.ptr, nullptr};
     join_kernel<true, false><<<bblocks(n_edge), kBT, 0, st>>>(a);
     RC(post_launch());
     RC(scan_counts(h, h->cnt.ptr, h->off_ee.ptr, n_edge, &h->n_ee, st));
@@ -383,13 +400,13 @@ extern "C" int b200ipc_broad_phase_fill(b200ipc_broad* h, int32_t* vt, int32_t* 
   if (((uintptr_t)vt | (uintptr_t)ee) & 15) return B200IPC_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
   if (h->n_vt) {
-    JoinArgs a{h->in, h->surf_verts, h->tris, h->n_sv, h->nbin_t, h->grid, h->keys_t.ptr, h->ids_t.ptr,
+    JoinArgs a{h->in, h->surf_verts, h->tris, h->n_sv, h->nbin_t, h->grid, h->keys_t.ptr, h->ids_t.ptr, h->box_t.ptr,
                h->off_vt.ptr, nullptr, reinterpret_cast<int4*>(vt)};
     join_kernel<false, true><<<bblocks(h->n_sv), kBT, 0, st>>>(a);
     RC(post_launch());
   }
   if (h->n_ee) {
-    JoinArgs a{h->in, h->edges, h->edges, h->n_edge, h->nbin_e, h->grid, h->keys_e.ptr, h->ids_e.ptr,
+    JoinArgs a{h->in, h->edges, h->edges, h->n_edge, h->nbin_e, h->grid, h->keys_e.ptr, h->ids_e.ptr, h->box_e.ptr,
                h->off_ee.ptr, nullptr, reinterpret_cast<int4*>(ee)};
     join_kernel<true, true><<<bblocks(h->n_edge), kBT, 0, st>>>(a);
     RC(post_launch());
