@@ -138,3 +138,40 @@ def test_reference_shaped_entry_points(F, z):
         r0, r1, r1p = o.f0_f1(un, float(z["eps_v"]), float(z["dt"]))
         assert abs(f0 - r0) <= 1e-12 * abs(r0) and abs(f1 - r1) <= 1e-12 and abs(f1p - r1p) <= 1e-12 * max(abs(r1p), 1)
     assert F.friction.update_friction_state(stencils, grads, z["x0"], 0.0, 1e-2, 0.01) == []
+
+
+def test_barrier_and_friction_families_assemble_together(F, z):
+    """Six families (barrier 6/9/12 + friction 6/9/12), as group_blocks would hand them to the solver:
+    pattern, values, SpMV and gradient scatter against the dense sum of the oracle's blocks."""
+    table, state = _state(F, z)
+    params = F.barrier.BarrierParams(d_hat=float(z["d_hat"]), kappa=float(z["kappa"]))
+    dt = float(z["dt"])
+    bar = F.stencils.evaluate(table, z["x1"], params, dt=dt)
+    st = F.device.to_host(bar.status)
+    if (st == 2).any():
+        pytest.skip("displaced pose penetrates")
+    fri = F.friction.evaluate(state, z["x1"], z["x0"])
+    fams = [bar.families[s] for s in sorted(bar.families)] + [fri.families[s] for s in sorted(fri.families)]
+    nv = z["x0"].shape[0]
+    rng = np.random.default_rng(3)
+    masses = rng.uniform(0.5, 2.0, size=nv)
+    fixed = rng.uniform(size=nv) < 0.05
+    sysm = F.solver.NewtonSystem(masses, fixed)
+    sysm.set_pattern([(f.s, f.vids) for f in fams])
+    vals = F.device.to_host(sysm.assemble([f.hess for f in fams]))
+    rowptr, colidx = F.device.to_host(sysm.rowptr), F.device.to_host(sysm.colidx)
+    grouped = [(F.device.to_host(f.hess), F.device.to_host(f.vids)) for f in fams]
+    ref = o.assemble_dense(grouped, masses, fixed)
+    dense = np.zeros_like(ref)
+    for r, (a, b) in enumerate(zip(rowptr[:-1], rowptr[1:])):
+        for c, blk in zip(colidx[a:b], vals[a:b]):
+            dense[3 * r:3 * r + 3, 3 * c:3 * c + 3] = blk
+    assert np.abs(dense - ref).max() <= TOL * np.abs(ref).max()
+    x = rng.normal(size=3 * nv)
+    y = F.device.to_host(sysm.spmv(x))
+    assert np.abs(y - ref @ x).max() <= 1e-11 * np.abs(ref @ x).max()
+    xt = z["x0"]
+    g = F.device.to_host(sysm.gradient(z["x1"], xt, [f.grad for f in fams]))
+    gref = o.scatter_gradient(masses, fixed, z["x1"], xt, [(f.s, None, F.device.to_host(f.vids), F.device.to_host(f.grad), None) for f in fams])
+    assert np.abs(g - gref).max() <= TOL * np.abs(gref).max()
+    sysm.close()
