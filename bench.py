@@ -292,6 +292,18 @@ def newton_section(torch, pkg, steps, warmup, peak, seed):
     ms_fblocks = time_steps(torch, lambda: friction_mod.evaluate(fstate, x_moved, pos), 10, 2, noop) / 10
     fr_bytes = sum(int(fstate.table.family_count(s_)) * (72 * s_ * s_ + 24 * s_ + 4 * s_ + 96) for s_ in (2, 3, 4))
     del raw
+    # elasticity: 400k random tets, energy + gradient + Jacobi-projected 12x12 block each
+    from paper_2308_09400_b200 import elasticity as elasticity_mod
+
+    rng_e = np.random.default_rng(11)
+    n_tet = 400_000
+    rest_t = rng_e.normal(size=(4 * n_tet, 3))
+    tets_t = np.arange(4 * n_tet).reshape(n_tet, 4)
+    mesh_t = elasticity_mod.TetMesh(rest_t, tets_t, 3.7e4, 8.6e4)
+    x_t = device.to_device(rest_t + 0.1 * rng_e.normal(size=rest_t.shape))
+    mesh_t.evaluate(x_t, dt=cloth.dt)
+    ms_elastic = time_steps(torch, lambda: mesh_t.evaluate(x_t, dt=cloth.dt), 5, 1, noop) / 5
+    del mesh_t, x_t
     # one whole Newton direction through the public device-resident API, host arrays in, host array out:
     # H2D (x, x~) -> detect -> stencils (factors) -> symbolic + numeric assembly -> gradient -> PCG -> D2H d
     x_host = np.ascontiguousarray(cloth.positions)
@@ -341,6 +353,8 @@ def newton_section(torch, pkg, steps, warmup, peak, seed):
                      "blocks_GBps": fr_bytes / ms_fblocks / 1e6,
                      "note": "update_friction_state (once per time step) and friction energy/grad/rank-2 PSD blocks "
                              "(once per Newton iteration, incl. output allocation) on the same contact table"},
+        "elastic": {"tets": n_tet, "blocks_ms": ms_elastic, "tets_per_s": n_tet / ms_elastic * 1e3,
+                    "note": "stable neo-Hookean energy + gradient + PSD 12x12 (9x9 Jacobi eigen-projection per thread)"},
         "pcg_ms_per_iter": ms_pcg_iter, "pcg_solve_ms": ms_pcg_full, "pcg_iters": it_full, "pcg_converged": ok_full,
         "roofline_assembly": {"bound": "hbm", "achieved": num_bytes / ms_numeric / 1e6, "peak": peak, "unit": "GB/s",
                               "frac": num_bytes / ms_numeric / 1e6 / peak},

@@ -265,6 +265,22 @@ int b200ipc_friction_explicit(int64_t n, int32_t s, const double* basis, const d
                               const double* lambda_n, double mu, double eps_v, double dt,
                               double* potential, double* force, double* hess, void* stream);
 
+/* ---- stable neo-Hookean tetrahedra (elasticity.py) ----------------------------------- */
+/* rest_data (elasticity.py:39-56): rest_inv (t,3,3) = inverse rest-shape matrices, vols (t) signed
+ * rest volumes, from tets (t,4) i32 (16-byte aligned) and rest positions.  The dvec(F)/dx maps are
+ * not stored: they are rest_inv rearranged. */
+int b200ipc_elastic_rest(int64_t ntets, const int32_t* tets, const double* rest_positions,
+                         double* rest_inv, double* vols, void* stream);
+/* batch_grad_hess (elasticity.py:128-137): per tet the volume-scaled energy (t), gradient (t,12) and
+ * 12x12 Hessian (t,12,12), the 9x9 dPsi/dF^2 projected PSD when `project` (the reference uses LAPACK
+ * eigh; here cyclic Jacobi per thread -- the projection is unique).  grad and hess are multiplied by
+ * `scale` (dt^2, solver.py:196-200), energy is not.  mu, lam: per-tet Lame parameters.  Any output
+ * may be NULL. */
+int b200ipc_elastic_blocks(int64_t ntets, const int32_t* tets, const double* positions,
+                           const double* rest_inv, const double* vols, const double* mu, const double* lam,
+                           double scale, int32_t project, double* energy, double* grad, double* hess,
+                           void* stream);
+
 /* ---- assembly into the 3x3-block sparse global matrix (BSR) -------------------- */
 /* The reference's production path is matrix-free; the assembled matrix is the one its tests
  * build densely (tests/test_solver.py:71-84): A = diag(m_i I3) + sum_b scatter(H_b), fixed

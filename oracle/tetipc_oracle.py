@@ -1100,3 +1100,56 @@ def friction_blocks(verts, size, lambda_n, cn, t1, t2, x, x_start, mu, eps_v, dt
     hess = ml[:, None, None] * np.einsum("nrk,nkl,ncl->nrc", T, core, T)
     dt2 = dt * dt
     return {"energy": energy, "grad": -dt2 * force, "hess": dt2 * hess, "u": u}
+
+
+# ---------------------------------------------------------------------------------------------
+# stable neo-Hookean tetrahedra: elasticity.py
+# ---------------------------------------------------------------------------------------------
+def elastic_rest(rest_positions, tets):
+    """rest_data (elasticity.py:39-56) without the explicit 9x12 maps: (rest_inv (t,3,3), vols (t,))."""
+    v = np.asarray(rest_positions, dtype=np.float64)
+    tets = np.asarray(tets, dtype=np.int64).reshape(-1, 4)
+    dm = np.stack([v[tets[:, 1]] - v[tets[:, 0]], v[tets[:, 2]] - v[tets[:, 0]], v[tets[:, 3]] - v[tets[:, 0]]], axis=2)
+    return np.linalg.inv(dm), np.linalg.det(dm) / 6.0
+
+
+def elastic_blocks(positions, tets, rest_inv, vols, mu, lam, project=True):
+    """batch_grad_hess (elasticity.py:128-137): (energy (t,), grad (t,12), hess (t,12,12)), volume-scaled."""
+    v = np.asarray(positions, dtype=np.float64)
+    tets = np.asarray(tets, dtype=np.int64).reshape(-1, 4)
+    t = tets.shape[0]
+    ds = np.stack([v[tets[:, 1]] - v[tets[:, 0]], v[tets[:, 2]] - v[tets[:, 0]], v[tets[:, 3]] - v[tets[:, 0]]], axis=2)
+    f = ds @ rest_inv
+    j = np.linalg.det(f)
+    alpha = 1.0 + mu / lam
+    f0, f1, f2 = f[:, :, 0], f[:, :, 1], f[:, :, 2]
+    gj_m = np.stack([np.cross(f1, f2), np.cross(f2, f0), np.cross(f0, f1)], axis=2)
+    vec = lambda m: np.swapaxes(m, -1, -2).reshape(t, 9)  # noqa: E731  column-major
+    energy = (0.5 * mu * (np.einsum("tij,tij->t", f, f) - 3.0) + 0.5 * lam * (j - alpha) ** 2) * vols
+    p = vec(mu[:, None, None] * f + (lam * (j - alpha))[:, None, None] * gj_m)
+    g = np.zeros((t, 9, 12))
+    for c in range(3):
+        for vtx in range(4):
+            w = -rest_inv[:, :, c].sum(axis=1) if vtx == 0 else rest_inv[:, vtx - 1, c]
+            for i in range(3):
+                g[:, 3 * c + i, 3 * vtx + i] = w
+    grad = vols[:, None] * np.einsum("tki,tk->ti", g, p)
+    gj = vec(gj_m)
+    h = mu[:, None, None] * np.eye(9)[None] + lam[:, None, None] * np.einsum("ti,tj->tij", gj, gj)
+
+    def skew(u):
+        s_ = np.zeros((t, 3, 3))
+        s_[:, 0, 1], s_[:, 0, 2], s_[:, 1, 0] = -u[:, 2], u[:, 1], u[:, 2]
+        s_[:, 1, 2], s_[:, 2, 0], s_[:, 2, 1] = -u[:, 0], -u[:, 1], u[:, 0]
+        return s_
+
+    hj = np.zeros((t, 9, 9))
+    hj[:, 0:3, 3:6], hj[:, 0:3, 6:9] = -skew(f2), skew(f1)
+    hj[:, 3:6, 0:3], hj[:, 3:6, 6:9] = skew(f2), -skew(f0)
+    hj[:, 6:9, 0:3], hj[:, 6:9, 3:6] = -skew(f1), skew(f0)
+    h = h + (lam * (j - alpha))[:, None, None] * hj
+    if project:
+        w_, q = np.linalg.eigh(h)
+        h = np.einsum("tik,tk,tjk->tij", q, np.maximum(w_, 0.0), q)
+    hess = vols[:, None, None] * np.einsum("tki,tkl,tlj->tij", g, h, g)
+    return energy, grad, hess

@@ -79,6 +79,8 @@ SIGNATURES = {
     "b200ipc_friction_blocks": [_i64, C.POINTER(_i64), _vp, _vp, _vp, _vp, _dbl, _dbl, _dbl, _vp, _vp, _vp, _vp, _vp,
                                 _vp, _vp, _vp],
     "b200ipc_friction_explicit": [_i64, _i32, _vp, _vp, _vp, _dbl, _dbl, _dbl, _vp, _vp, _vp, _vp],
+    "b200ipc_elastic_rest": [_i64, _vp, _vp, _vp, _vp, _vp],
+    "b200ipc_elastic_blocks": [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _dbl, _i32, _vp, _vp, _vp, _vp],
     "b200ipc_assembly_create": [C.POINTER(_vp)],
     "b200ipc_assembly_destroy": [_vp],
     "b200ipc_assembly_set_variant": [_vp, _i32],

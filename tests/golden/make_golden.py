@@ -458,7 +458,43 @@ def golden_friction():
     save("friction", **out)
 
 
+def golden_elastic():
+    """rest_data / batch_grad_hess of the reference on random tetrahedra: mildly deformed, strongly
+    compressed (indefinite dPsi/dF^2: the projection matters), inverted, and at rest."""
+    from tetipc import elasticity as re_
+
+    rng = np.random.default_rng(20240821)
+    t = 300
+    rest = rng.normal(size=(4 * t, 3))
+    tets = np.arange(4 * t).reshape(t, 4)
+    # make every rest tet positively oriented and not too flat
+    dm = np.stack([rest[tets[:, k]] - rest[tets[:, 0]] for k in (1, 2, 3)], axis=2)
+    flip = np.linalg.det(dm) < 0
+    tets[flip] = tets[flip][:, [0, 2, 1, 3]]
+    x = rest.copy()
+    amp = rng.choice([0.0, 0.05, 0.6], size=(t, 1, 1), p=[0.1, 0.5, 0.4])
+    a = np.eye(3)[None] + amp * rng.normal(size=(t, 3, 3))
+    a[20:40] = np.diag([1.0, 1.0, -0.7])[None] @ a[20:40]      # inverted elements
+    a[40:80] *= rng.uniform(0.2, 0.5, size=(40, 1, 1))         # strong compression
+    for k in range(t):
+        c = rest[tets[k]].mean(axis=0)
+        x[tets[k]] = (rest[tets[k]] - c) @ a[k].T + c
+    mat = re_.ElasticMaterial(youngs_E=2.0e5, poisson_nu=0.35)
+    mu = np.full(t, mat.lame_mu) * rng.uniform(0.5, 2.0, size=t)
+    lam = np.full(t, mat.lame_lambda) * rng.uniform(0.5, 2.0, size=t)
+    rest_inv, vols, g = re_.rest_data(rest, tets)
+    e, grad, hess = re_.batch_grad_hess(x, tets, rest_inv, vols, g, mu, lam)
+    _, _, hess_raw = re_.batch_grad_hess(x, tets, rest_inv, vols, g, mu, lam, project=False)
+    neg = (np.linalg.eigvalsh(hess_raw).min(axis=1) < -1e-9 * np.abs(hess_raw).max(axis=(1, 2))).sum()
+    print(f"elastic: {t} tets, {neg} with an indefinite raw Hessian, energy range [{e.min():.3g}, {e.max():.3g}]")
+    save("elastic", rest=rest, x=x, tets=tets, mu=mu, lam=lam, rest_inv=rest_inv, vols=vols, energy=e, grad=grad,
+         hess=hess, hess_raw=hess_raw[::5])
+
+
 if __name__ == "__main__":
+    if "--elastic-only" in sys.argv:
+        golden_elastic()
+        sys.exit(0)
     if "--friction-only" in sys.argv:
         golden_friction()
         sys.exit(0)
@@ -476,3 +512,4 @@ if __name__ == "__main__":
     golden_broad()
     golden_ccd()
     golden_friction()
+    golden_elastic()

@@ -309,3 +309,21 @@ def test_friction_golden(tag):
         assert (np.linalg.norm(z["u"], axis=1) == 0.0).sum() > 0            # the isotropic u = 0 branch is covered
     else:
         assert len(rows) < len(z["kind"]) and {1, 3, 5} <= set(np.unique(z["kind"]))   # skips + parallel kinds
+
+
+def test_elastic_golden():
+    """oracle.elastic_rest / elastic_blocks == the reference's rest_data / batch_grad_hess on 300 random
+    tets incl. inverted and strongly compressed ones (tests/golden/elastic.npz)."""
+    z = load_golden("elastic")
+    rest_inv, vols = o.elastic_rest(z["rest"], z["tets"])
+    assert np.array_equal(rest_inv, z["rest_inv"]) and np.array_equal(vols, z["vols"])
+    e, g, h = o.elastic_blocks(z["x"], z["tets"], rest_inv, vols, z["mu"], z["lam"])
+    assert rel_err(e, z["energy"]) < 1e-12
+    gscale = np.maximum(np.abs(z["grad"]).max(axis=1), 1e-6 * np.abs(z["grad"]).max())[:, None]
+    assert (np.abs(g - z["grad"]) / gscale).max() < 1e-12 and block_rel_err(h, z["hess"]) < 1e-10
+    _, _, hr = o.elastic_blocks(z["x"], z["tets"], rest_inv, vols, z["mu"], z["lam"], project=False)
+    assert block_rel_err(hr[::5], z["hess_raw"]) < 1e-12
+    # the projection is exercised: some raw Hessians are indefinite, all projected ones are PSD
+    assert (np.linalg.eigvalsh(hr).min(axis=1) < -1e-9 * np.abs(hr).max(axis=(1, 2))).sum() > 20
+    ev = np.linalg.eigvalsh(h)
+    assert (ev.min(axis=1) >= -1e-10 * ev.max(axis=1)).all()
