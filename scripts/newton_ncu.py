@@ -32,6 +32,15 @@ for _ in range(3):
 xt = device.to_device(cloth.positions + 1e-4 * np.random.default_rng(1).normal(size=cloth.positions.shape))
 for _ in range(2):
     g = sysm.gradient(pos, xt, [f.grad for f in fams])
+from paper_2308_09400_b200 import elasticity, friction
+raw = stencils.evaluate(table, pos, params, dt=1.0, want_energy=False, want_hess=False)
+fstate = friction.update_state(table, pos, 0.4, 1e-3, cloth.dt, barrier_batch=raw)
+xm = device.to_device(cloth.positions + 5e-6 * np.random.default_rng(4).normal(size=cloth.positions.shape))
+for _ in range(2):
+    friction.evaluate(fstate, xm, pos)
+rest_t = np.random.default_rng(11).normal(size=(400_000, 3))
+mesh_t = elasticity.TetMesh(rest_t, np.arange(400_000).reshape(-1, 4), 3.7e4, 8.6e4)
+mesh_t.evaluate(rest_t + 0.1 * np.random.default_rng(12).normal(size=rest_t.shape), dt=cloth.dt)
 sysm.block_jacobi()
 if "--pcg" in sys.argv:
     sysm.pcg(-g, 1e-30, 20)
