@@ -357,7 +357,7 @@ def newton_section(torch, pkg, steps, warmup, peak, seed):
                      "note": "update_friction_state (once per time step) and friction energy/grad/rank-2 PSD blocks "
                              "(once per Newton iteration, incl. output allocation) on the same contact table"},
         "elastic": {"tets": n_tet, "blocks_ms": ms_elastic, "tets_per_s": n_tet / ms_elastic * 1e3,
-                    "note": "stable neo-Hookean energy + gradient + PSD 12x12 (9x9 Jacobi eigen-projection per thread)"},
+                    "note": "stable neo-Hookean energy + gradient + analytically PSD-projected 12x12 per tet (incl. output allocation)"},
         "pcg_ms_per_iter": ms_pcg_iter, "pcg_solve_ms": ms_pcg_full, "pcg_iters": it_full, "pcg_converged": ok_full,
         "roofline_assembly": {"bound": "hbm", "achieved": num_bytes / ms_numeric / 1e6, "peak": peak, "unit": "GB/s",
                               "frac": num_bytes / ms_numeric / 1e6 / peak},

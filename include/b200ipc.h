@@ -273,7 +273,8 @@ int b200ipc_elastic_rest(int64_t ntets, const int32_t* tets, const double* rest_
                          double* rest_inv, double* vols, void* stream);
 /* batch_grad_hess (elasticity.py:128-137): per tet the volume-scaled energy (t), gradient (t,12) and
  * 12x12 Hessian (t,12,12), the 9x9 dPsi/dF^2 projected PSD when `project` (the reference uses LAPACK
- * eigh; here cyclic Jacobi per thread -- the projection is unique).  grad and hess are multiplied by
+ * eigh; here the closed-form twist / flip / scaling eigensystem from a 3x3 SVD of F -- the projection
+ * is unique).  grad and hess are multiplied by
  * `scale` (dt^2, solver.py:196-200), energy is not.  mu, lam: per-tet Lame parameters.  Any output
  * may be NULL. */
 int b200ipc_elastic_blocks(int64_t ntets, const int32_t* tets, const double* positions,

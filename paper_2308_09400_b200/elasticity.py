@@ -4,8 +4,8 @@ Mirror of ``/root/reference/pkg/src/tetipc/elasticity.py``: ``ElasticMaterial``,
 ``batch_grad_hess``, ``tet_energy_grad_hess``, ``tet_local_quadratic`` keep their names, arguments and
 results; ``TetMesh`` is the device-resident form (rest data uploaded once, one ``evaluate`` per Newton
 iteration) whose (hess, vids) family goes to ``solver.NewtonSystem`` next to the barrier families.
-The 9x9 dPsi/dF^2 is projected PSD by cyclic Jacobi rotations in registers/local memory per thread
-(the reference calls LAPACK ``eigh``; the projection is unique).
+The 9x9 dPsi/dF^2 is projected PSD analytically (closed-form twist / flip / scaling eigenpairs from a
+3x3 SVD of F, in registers; the reference calls LAPACK ``eigh`` -- the projection is unique).
 """
 
 from dataclasses import dataclass, field
@@ -17,21 +17,37 @@ from .barrier import LocalQuadratic
 from .stencils import Family
 
 
+def lame_parameters(youngs_E, poisson_nu):
+    """(mu, lambda) of an isotropic material; E > 0 and 0 < nu < 1/2 or ValueError (elasticity.py:24-30)."""
+    if not (youngs_E > 0.0 and 0.0 < poisson_nu < 0.5):
+        raise ValueError("need E > 0 and nu in (0, 0.5)")
+    shear = 0.5 * youngs_E / (1.0 + poisson_nu)
+    return shear, 2.0 * shear * poisson_nu / (1.0 - 2.0 * poisson_nu)
+
+
 @dataclass
 class ElasticMaterial:
-    """elasticity.py:18-30."""
+    """Field-compatible with the reference's material record (elasticity.py:18-30)."""
 
     youngs_E: float
     poisson_nu: float
-    lame_mu: float = field(init=False)
-    lame_lambda: float = field(init=False)
+    lame_mu: float = field(init=False, default=0.0)
+    lame_lambda: float = field(init=False, default=0.0)
 
     def __post_init__(self):
-        if self.youngs_E <= 0.0 or not 0.0 < self.poisson_nu < 0.5:
-            raise ValueError("need E > 0 and nu in (0, 0.5)")
-        e, nu = self.youngs_E, self.poisson_nu
-        self.lame_mu = e / (2.0 * (1.0 + nu))
-        self.lame_lambda = e * nu / ((1.0 + nu) * (1.0 - 2.0 * nu))
+        self.lame_mu, self.lame_lambda = lame_parameters(self.youngs_E, self.poisson_nu)
+
+
+def dvec_f_dx(rest_inv):
+    """(t,9,12) maps x -> vec(F) implied by rest_inv: row 3c+i, column 3v+i holds w_vc with
+    w_0c = -sum_r rest_inv[r,c] and w_vc = rest_inv[v-1,c]; pure indexing, kept for API parity."""
+    rest_inv = np.asarray(rest_inv, dtype=np.float64)
+    t = rest_inv.shape[0]
+    w = np.concatenate([-rest_inv.sum(axis=1, keepdims=True), rest_inv], axis=1)      # (t, 4 vertices, 3 columns c)
+    maps = np.zeros((t, 3, 3, 4, 3))                                                    # [t, c, i, v, i']
+    for i in range(3):
+        maps[:, :, i, :, i] = np.swapaxes(w, 1, 2)
+    return maps.reshape(t, 9, 12)
 
 
 class TetMesh:
@@ -70,14 +86,7 @@ def rest_data(rest_positions, tets):
     tets = np.asarray(tets).reshape(-1, 4)
     mesh = TetMesh(rest_positions, tets, 1.0, 1.0)
     rest_inv, vols = device.to_host(mesh.rest_inv), device.to_host(mesh.vols)
-    t = tets.shape[0]
-    g = np.zeros((t, 9, 12))   # the map is rest_inv rearranged: pure indexing, kept for API parity
-    for c in range(3):
-        for vtx in range(4):
-            w = -rest_inv[:, :, c].sum(axis=1) if vtx == 0 else rest_inv[:, vtx - 1, c]
-            for i in range(3):
-                g[:, 3 * c + i, 3 * vtx + i] = w
-    return rest_inv, vols, g
+    return rest_inv, vols, dvec_f_dx(rest_inv)
 
 
 def batch_grad_hess(positions, tets, rest_inv, vols, g_maps, mu, lam, project=True):
