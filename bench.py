@@ -213,18 +213,21 @@ def newton_section(torch, pkg, steps, warmup, peak, seed):
     bp = contacts.BroadPhase(None, cloth.tris, cloth.edges, cloth.d_hat, cloth.positions)
     d_vt, d_ee = bp.query(pos)  # warm (module load, workspace allocation)
     contacts.narrow_phase_device(pos, d_rest, d_vt, d_ee, cloth.d_hat, want_origin=False)
-    torch.cuda.synchronize()
-    reps_detect = 5
-    t0 = time.perf_counter()
-    for _ in range(reps_detect):
-        d_vt, d_ee = bp.query(pos)
-    torch.cuda.synchronize()
-    t_broad = (time.perf_counter() - t0) / reps_detect
-    t0 = time.perf_counter()
-    for _ in range(reps_detect):
-        table, _ = contacts.narrow_phase_device(pos, d_rest, d_vt, d_ee, cloth.d_hat, want_origin=False)
-    torch.cuda.synchronize()
-    t_narrow = (time.perf_counter() - t0) / reps_detect
+    def wall_ms(fn, reps=5):
+        """Best of `reps` wall-clock runs bracketed by synchronize (host-synchronising entry points)."""
+        best, out = float("inf"), None
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            out = fn()
+            torch.cuda.synchronize()
+            best = min(best, (time.perf_counter() - t0) * 1e3)
+        return best, out
+
+    ms_broad, (d_vt, d_ee) = wall_ms(lambda: bp.query(pos))
+    ms_narrow, (table, _) = wall_ms(lambda: contacts.narrow_phase_device(pos, d_rest, d_vt, d_ee, cloth.d_hat,
+                                                                         want_origin=False))
+    t_broad, t_narrow = ms_broad * 1e-3, ms_narrow * 1e-3
     n_queries = int(d_vt.shape[0]) + int(d_ee.shape[0])
     batch = stencils.evaluate(table, pos, params, dt=cloth.dt, want_factors=True)
     batch.raise_on_penetration()
@@ -233,11 +236,7 @@ def newton_section(torch, pkg, steps, warmup, peak, seed):
     noop = lambda: None  # noqa: E731
     ms_stencil = time_steps(torch, lambda: stencils.evaluate(table, pos, params, dt=cloth.dt, out=batch), steps, warmup, noop) / steps
     sysm.set_pattern([(f.s, f.vids) for f in fams])  # warm (module load, workspace allocation)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    nnzb = sysm.set_pattern([(f.s, f.vids) for f in fams])
-    torch.cuda.synchronize()
-    ms_symbolic = (time.perf_counter() - t0) * 1e3
+    ms_symbolic, nnzb = wall_ms(lambda: sysm.set_pattern([(f.s, f.vids) for f in fams]), reps=3)
     hess = [f.hess for f in fams]
     ms_numeric = time_steps(torch, lambda: sysm.assemble(hess), steps, warmup, noop) / steps
     sysm.set_numeric_variant(4)
@@ -275,27 +274,19 @@ def newton_section(torch, pkg, steps, warmup, peak, seed):
     dirs = device.to_device(0.3 * cloth.d_hat * np.random.default_rng(3).normal(size=cloth.positions.shape))
     alpha = bp.ccd_step_bound(pos, dirs)  # warm
     s_vt, s_ee = bp.sweep(pos, dirs)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    alpha = bp.ccd_step_bound(pos, dirs)
-    torch.cuda.synchronize()
-    ms_ccd = (time.perf_counter() - t0) * 1e3
+    ms_ccd, alpha = wall_ms(lambda: bp.ccd_step_bound(pos, dirs), reps=3)
     # friction: lagged state once per time step, blocks once per Newton iteration
     from paper_2308_09400_b200 import friction as friction_mod
 
     raw = stencils.evaluate(table, pos, params, dt=1.0, want_energy=False, want_hess=False)
     fstate = friction_mod.update_state(table, pos, 0.4, 1e-3, cloth.dt, barrier_batch=raw)  # warm
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    fstate = friction_mod.update_state(table, pos, 0.4, 1e-3, cloth.dt, barrier_batch=raw)
-    torch.cuda.synchronize()
-    ms_fstate = (time.perf_counter() - t0) * 1e3
+    ms_fstate, fstate = wall_ms(lambda: friction_mod.update_state(table, pos, 0.4, 1e-3, cloth.dt, barrier_batch=raw), reps=3)
     x_moved = device.to_device(cloth.positions + 0.5 * cloth.dt * 1e-3 * np.random.default_rng(4).normal(size=cloth.positions.shape))
     friction_mod.evaluate(fstate, x_moved, pos)
     ms_fblocks = time_steps(torch, lambda: friction_mod.evaluate(fstate, x_moved, pos), 10, 2, noop) / 10
     fr_bytes = sum(int(fstate.table.family_count(s_)) * (72 * s_ * s_ + 24 * s_ + 4 * s_ + 96) for s_ in (2, 3, 4))
     del raw
-    # elasticity: 400k random tets, energy + gradient + Jacobi-projected 12x12 block each
+    # elasticity: 400k random tets, energy + gradient + analytically projected 12x12 block each
     from paper_2308_09400_b200 import elasticity as elasticity_mod
 
     rng_e = np.random.default_rng(11)
