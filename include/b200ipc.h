@@ -298,8 +298,8 @@ int b200ipc_assembly_destroy(b200ipc_assembly* h);
  * output blocks, prefetches their source descriptors and gathers the 3x3 sub-blocks -- whenever the
  * 32-bit descriptors apply (<= 3 families, each below 24 GiB), else row-wise.  1 = per-block runs;
  * 4 = row-wise (one warp per block-row reads every dense block once as contiguous three-row runs,
- * accumulates in shared memory); 2, 3 = row-wise, family-specialised instantiations.  All are
- * atomic-free and deterministic; results agree to round-off. */
+ * accumulates in shared memory).  Both are atomic-free and deterministic; results agree to
+ * round-off.  Other values: B200IPC_EINVAL. */
 int b200ipc_assembly_set_variant(b200ipc_assembly* h, int32_t variant);
 /* Build the pattern and the source runs (sort by key).  fixed: device u8 (nverts).  Synchronises
  * `stream` and returns the number of 3x3 blocks in *nnzb_out (host).  The vids buffers must stay

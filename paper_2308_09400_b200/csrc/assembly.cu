@@ -65,7 +65,7 @@ struct b200ipc_assembly {
   int64_t nnzb = 0;
   int64_t ngslots = 0;     // sum nb*s
   bool ready = false;
-  int variant = 0;         // numeric kernel: 0 auto (per-block runs when applicable), 1 runs, 2/3 row-wise family, 4 row-wise
+  int variant = 0;         // numeric kernel: 0 auto (per-block runs when applicable), 1 runs, 4 row-wise
   b200ipc::FamDesc fam;
   b200ipc::DevBuf<uint8_t> fixed;
   b200ipc::DevBuf<uint64_t> keys_a, keys_b;
@@ -77,7 +77,6 @@ struct b200ipc_assembly {
   b200ipc::DevBuf<uint32_t> gkeys_a, gkeys_b, gslot_a, gslot_b;
   b200ipc::DevBuf<int32_t> gseg;              // (N+1) run starts per vertex
   b200ipc::DevBuf<uint64_t> rs_desc, rs_dst;  // per row-source: chunk offset|family, 4 x u16 destination block
-  b200ipc::DevBuf<int32_t> rseg;              // (N, nfam+1): row-source range of each family inside each row
   b200ipc::DevBuf<uint8_t> temp;
   b200ipc::DevBuf<int64_t> scalars;           // device scratch for counts
 };
@@ -494,138 +493,6 @@ __global__ void __launch_bounds__(32 * kRowWarps) assemble_rows_kernel(const __g
   }
 }
 
-// ---- row-wise numeric assembly, family-specialised (variants 2 and 3) ------------------------------
-// Same decomposition as assemble_rows_kernel, but the row-sources of one family are processed in a
-// loop specialised for that family's row length D (no per-source family lookup, lane-constant
-// element map) with PF sources per pipeline stage held in registers.
-__global__ void __launch_bounds__(kAT) row_family_split_kernel(FamDesc fd, int64_t nverts,
-                                                               const int32_t* __restrict__ gseg,
-                                                               const uint32_t* __restrict__ gperm,
-                                                               int32_t* __restrict__ rseg) {
-  const int64_t t = (int64_t)blockIdx.x * kAT + threadIdx.x;
-  const int nf1 = fd.nfam + 1;
-  if (t >= nverts * nf1) return;
-  const int64_t row = t / nf1;
-  const int f = (int)(t - row * nf1);
-  int32_t lo = gseg[row], hi = gseg[row + 1];
-  if (f == fd.nfam) {
-    rseg[t] = hi;
-    return;
-  }
-  const int64_t first_slot = fd.vert_off[f];
-  while (lo < hi) {
-    const int32_t mid = (lo + hi) >> 1;
-    if ((int64_t)gperm[mid] < first_slot) lo = mid + 1;
-    else hi = mid;
-  }
-  rseg[t] = lo;
-}
-
-struct RowFamArgs {
-  const double* base[kMaxFam];
-  int32_t fs[kMaxFam];
-  int32_t nfam;
-  int64_t nverts;
-  const uint8_t* fixed;
-  const double* masses;
-  const int32_t* rowptr;
-  const int32_t* colidx;
-  const int32_t* rseg;
-  const uint64_t* rs_desc;   // element offset of the run << 3 | family
-  const uint64_t* rs_dst;    // 4 x u16
-  double* vals;
-};
-
-template <int D, int PF>
-__device__ __forceinline__ void row_family_regs(double* acc, int lane, int win, int wlen,
-                                                const double* __restrict__ base,
-                                                const uint64_t* __restrict__ rs_desc,
-                                                const uint64_t* __restrict__ rs_dst, int32_t jb, int32_t je) {
-  constexpr int N = 3 * D;
-  const bool on0 = lane < N, on1 = lane + 32 < N;
-  const int t0 = on0 ? lane : 0, t1 = on1 ? lane + 32 : 0;
-  const int sh0 = 16 * ((t0 % D) / 3), k0 = 3 * (t0 / D) + t0 % 3;
-  const int sh1 = 16 * ((t1 % D) / 3), k1 = 3 * (t1 / D) + t1 % 3;
-  // batches of PF sources, no cross-iteration state: descriptors, then the PF dense runs (all
-  // independent loads), then the ordered adds; other warps of the SM cover the two latencies
-  for (int32_t j = jb; j < je; j += PF) {
-    uint64_t off[PF], dst[PF];
-    double v0[PF], v1[PF];
-#pragma unroll
-    for (int u = 0; u < PF; ++u) {
-      const int32_t jj = min(j + u, je - 1);
-      off[u] = rs_desc[jj] >> 3;
-      dst[u] = rs_dst[jj];
-    }
-#pragma unroll
-    for (int u = 0; u < PF; ++u) {
-      const double* p = base + off[u];
-      v0[u] = on0 ? __ldg(p + t0) : 0.0;
-      v1[u] = on1 ? __ldg(p + t1) : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < PF; ++u) {
-      if (j + u < je) {
-        const unsigned a0 = (unsigned)((dst[u] >> sh0) & 0xffff) - (unsigned)win;
-        if (on0 && a0 < (unsigned)wlen) acc[a0 * 9 + k0] += v0[u];
-        if (N > 32) {
-          const unsigned a1 = (unsigned)((dst[u] >> sh1) & 0xffff) - (unsigned)win;
-          if (on1 && a1 < (unsigned)wlen) acc[a1 * 9 + k1] += v1[u];
-        }
-      }
-      __syncwarp();
-    }
-  }
-}
-
-// PF sources per batch, WIN blocks of a row per shared-memory window, MINB resident CTAs per SM.
-// The gather is latency-bound: what buys bandwidth is resident warps (a 288-byte random-run probe
-// reaches 2.6 / 4.4 / 5.1 TB/s at 16 / 32 / 64 warps per SM, independent of per-warp prefetch depth),
-// so the production instantiation trades per-warp state for occupancy.
-template <int PF, int WIN, int MINB>
-__global__ void __launch_bounds__(32 * kRowWarps, MINB) assemble_rows_family_kernel(const __grid_constant__ RowFamArgs a) {
-  constexpr int kRowWin = WIN;
-  __shared__ double sm[kRowWarps][kRowWin * 9];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t row = (int64_t)blockIdx.x * kRowWarps + w;
-  if (row >= a.nverts) return;
-  double* acc = sm[w];
-  const int32_t r0 = a.rowptr[row], len = a.rowptr[row + 1] - r0;
-  double* out = a.vals + 9ll * r0;
-  if (a.fixed[row]) {
-    if (lane < 9) out[lane] = (lane == 0 || lane == 4 || lane == 8) ? 1.0 : 0.0;
-    return;
-  }
-  int32_t lo = 0, hi = len;
-  while (lo < hi) {
-    const int32_t mid = (lo + hi) >> 1;
-    if (a.colidx[r0 + mid] < row) lo = mid + 1;
-    else hi = mid;
-  }
-  const int drel = lo;
-  const double mass = a.masses[row];
-  const int32_t* seg = a.rseg + row * (a.nfam + 1);
-  for (int win = 0; win < len; win += kRowWin) {
-    const int wlen = min(kRowWin, len - win);
-    for (int t = lane; t < 9 * wlen; t += 32) acc[t] = 0.0;
-    __syncwarp();
-    if (lane < 3 && drel >= win && drel < win + wlen) acc[(drel - win) * 9 + 4 * lane] = mass;
-    __syncwarp();
-#pragma unroll
-    for (int f = 0; f < kMaxFam; ++f) {
-      if (f < a.nfam) {
-        const int32_t jb = seg[f], je = seg[f + 1];
-        const int sz = a.fs[f];
-        if (sz == 4) row_family_regs<12, PF>(acc, lane, win, wlen, a.base[f], a.rs_desc, a.rs_dst, jb, je);
-        else if (sz == 3) row_family_regs<9, PF>(acc, lane, win, wlen, a.base[f], a.rs_desc, a.rs_dst, jb, je);
-        else row_family_regs<6, PF>(acc, lane, win, wlen, a.base[f], a.rs_desc, a.rs_dst, jb, je);
-      }
-    }
-    for (int t = lane; t < 9 * wlen; t += 32) out[9 * win + t] = acc[t];
-    __syncwarp();
-  }
-}
-
 // ---- gradient ---------------------------------------------------------------------------------
 __global__ void __launch_bounds__(kAT) gradient_keys_kernel(FamDesc fd, int64_t ngslots, uint32_t* __restrict__ keys,
                                                             uint32_t* __restrict__ slots) {
@@ -705,7 +572,7 @@ extern "C" int b200ipc_assembly_create(b200ipc_assembly** out) {
 }
 
 extern "C" int b200ipc_assembly_set_variant(b200ipc_assembly* h, int32_t variant) {
-  if (!h || variant < 0 || variant > 4) return B200IPC_EINVAL;
+  if (!h || !(variant == 0 || variant == 1 || variant == 4)) return B200IPC_EINVAL;
   h->variant = variant;
   return 0;
 }
@@ -714,7 +581,7 @@ extern "C" int b200ipc_assembly_destroy(b200ipc_assembly* h) {
   if (!h) return 0;
   h->fixed.release(); h->keys_a.release(); h->keys_b.release(); h->slot_a.release(); h->slot_b.release();
   h->head.release(); h->useg.release(); h->desc.release(); h->fdesc.release(); h->rowptr.release(); h->colidx.release();
-  h->gkeys_a.release(); h->gkeys_b.release(); h->gslot_a.release(); h->gslot_b.release(); h->gseg.release(); h->rs_desc.release(); h->rs_dst.release(); h->rseg.release();
+  h->gkeys_a.release(); h->gkeys_b.release(); h->gslot_a.release(); h->gslot_b.release(); h->gseg.release(); h->rs_desc.release(); h->rs_dst.release();
   h->temp.release(); h->scalars.release();
   delete h;
   return 0;
@@ -831,10 +698,6 @@ extern "C" int b200ipc_assemble_symbolic(b200ipc_assembly* h, int64_t nverts, co
                                                      h->colidx.ptr, h->rs_desc.ptr, h->rs_dst.ptr);
     RC(post_launch());
   }
-  CK(h->rseg.reserve((size_t)nverts * (nfam + 1)));
-  row_family_split_kernel<<<blocks_for(nverts * (nfam + 1)), kAT, 0, st>>>(fd, nverts, h->gseg.ptr, h->gslot_b.ptr,
-                                                                          h->rseg.ptr);
-  RC(post_launch());
   h->ready = true;
   if (nnzb_out) *nnzb_out = h->nnzb;
   return 0;
@@ -867,20 +730,6 @@ extern "C" int b200ipc_assemble_numeric(b200ipc_assembly* h, const double* masse
   if ((h->variant == 0 || h->variant == 1) && packed_ok) {  // per-block runs (gather of 3x3 sub-blocks)
     const unsigned grid = (unsigned)((h->nnzb + kNumWarps * kBlocksPerWarp - 1) / (kNumWarps * kBlocksPerWarp));
     assemble_numeric_kernel<<<grid, 32 * kNumWarps, 0, (cudaStream_t)stream>>>(a);
-    return post_launch();
-  }
-  if (h->variant == 2 || h->variant == 3) {  // family-specialised row-wise kernels
-    RowFamArgs q;
-    for (int f = 0; f < kMaxFam; ++f) {
-      q.base[f] = f < h->fam.nfam ? fam_hess[f] : nullptr;
-      q.fs[f] = f < h->fam.nfam ? h->fam.s[f] : 0;
-    }
-    q.nfam = h->fam.nfam; q.nverts = h->nverts; q.fixed = h->fixed.ptr; q.masses = masses;
-    q.rowptr = h->rowptr.ptr; q.colidx = h->colidx.ptr; q.rseg = h->rseg.ptr; q.rs_desc = h->rs_desc.ptr;
-    q.rs_dst = h->rs_dst.ptr; q.vals = vals;
-    const unsigned grid = (unsigned)((h->nverts + kRowWarps - 1) / kRowWarps);
-    if (h->variant == 2) assemble_rows_family_kernel<1, 48, 8><<<grid, 32 * kRowWarps, 0, (cudaStream_t)stream>>>(q);
-    else assemble_rows_family_kernel<2, 48, 6><<<grid, 32 * kRowWarps, 0, (cudaStream_t)stream>>>(q);
     return post_launch();
   }
   RowArgs r;

@@ -38,7 +38,7 @@ class FrictionState:
 
     table: DeviceStencilTable
     frame: object          # (n,12) device
-    rows: np.ndarray       # rows of the source table that became data (host)
+    rows_dev: object       # rows of the source table that became data (device int64)
     mu: float
     eps_v: float
     dt: float
@@ -46,6 +46,11 @@ class FrictionState:
     @property
     def n(self):
         return self.table.n
+
+    @property
+    def rows(self):
+        """Rows of the source table that became data, as a host array."""
+        return device.to_host(self.rows_dev)
 
 
 @dataclass
@@ -81,7 +86,7 @@ def update_state(table, positions, mu, eps_v, dt, barrier_batch=None, params=Non
     if mu <= 0.0 or n == 0:
         empty = DeviceStencilTable(0, np.zeros(8, np.int64), device.empty((0, 4), np.int32), device.empty((0,), np.uint8),
                                    device.empty((0,)))
-        return FrictionState(empty, device.empty((0, 12)), np.zeros(0, np.int64), float(mu), float(eps_v), float(dt))
+        return FrictionState(empty, device.empty((0, 12)), device.empty((0,), np.int64), float(mu), float(eps_v), float(dt))
     if barrier_batch is None:
         barrier_batch = stencils.evaluate(table, pos, params, dt=1.0, want_energy=False, want_hess=False)
     if not isinstance(barrier_batch, BarrierBatch):
@@ -96,17 +101,19 @@ def update_state(table, positions, mu, eps_v, dt, barrier_batch=None, params=Non
     _lib.check(_lib.lib().b200ipc_friction_state(n, _koff(table.kind_off), device.ptr(table.verts), device.ptr(table.sub),
                                                  device.ptr(pos), g(2), g(3), g(4), device.ptr(frame),
                                                  device.ptr(status), device.stream()), "friction_state")
-    st = device.to_host(status)
-    if np.any(st == 3):
-        raise ValueError("undefined contact normal for friction basis")
-    keep = np.flatnonzero(st == 0)
+    # compaction of the kept rows on the device (the reference skips d2 <= 0 and lambda_n <= 0 stencils);
+    # only eight counters and one flag cross PCIe
     t = device.torch()
-    idx = t.from_numpy(keep).cuda()
-    kinds = np.repeat(np.arange(7), np.diff(table.kind_off))[keep]
-    koff = np.searchsorted(kinds, np.arange(8)).astype(np.int64)
-    sub = DeviceStencilTable(len(keep), koff, table.verts[idx].contiguous(), table.sub[idx].contiguous(),
-                             table.eps_x[idx].contiguous())
-    return FrictionState(sub, frame[idx].contiguous(), keep, float(mu), float(eps_v), float(dt))
+    kinds = t.repeat_interleave(t.arange(7, device="cuda"), t.as_tensor(np.diff(table.kind_off), device="cuda"))
+    keep = t.nonzero(status == 0).squeeze(1)
+    counts = t.bincount(kinds[keep], minlength=7)
+    host = t.cat([counts, (status == 3).any().to(counts.dtype).reshape(1)]).cpu().numpy()
+    if host[7]:
+        raise ValueError("undefined contact normal for friction basis")
+    koff = np.concatenate([[0], np.cumsum(host[:7])]).astype(np.int64)
+    sub = DeviceStencilTable(int(keep.shape[0]), koff, table.verts[keep].contiguous(), table.sub[keep].contiguous(),
+                             table.eps_x[keep].contiguous())
+    return FrictionState(sub, frame[keep].contiguous(), keep, float(mu), float(eps_v), float(dt))
 
 
 def evaluate(state, positions, positions_start, want_energy=True, want_grad=True, want_hess=True):

@@ -58,8 +58,8 @@ class NewtonSystem:
         self._pcg_ws = None
 
     def set_numeric_variant(self, variant):
-        """0 = automatic (default: per-block runs when applicable), 1 = per-block runs, 4 = row-wise,
-        2/3 = row-wise family-specialised (see include/b200ipc.h)."""
+        """0 = automatic (default: per-block runs when applicable), 1 = per-block runs, 4 = row-wise
+        (see include/b200ipc.h)."""
         _lib.check(_lib.lib().b200ipc_assembly_set_variant(self._h, int(variant)), "assembly_set_variant")
 
     def close(self):

@@ -17,7 +17,7 @@ sysm = solver.NewtonSystem(cloth.masses, cloth.fixed)
 nnzb = sysm.set_pattern([(f.s, f.vids) for f in fams])
 hess = [f.hess for f in fams]
 noop = lambda: None
-for variant in (0, 1, 2, 3):
+for variant in (0, 1, 4):
     sysm.set_numeric_variant(variant)
     ms = bench.time_steps(torch, lambda: sysm.assemble(hess), 20, 3, noop) / 20
     print("assemble variant", variant, "ms", ms, flush=True)

@@ -217,7 +217,7 @@ def test_random_blocks_assembly_vs_oracle(S, n, nb):
     assert rowptr[8] - rowptr[7] > 500
     assert block_rel_err(vals, o_vals) < 1e-12
     # the alternative numeric kernels give the same matrix
-    for variant in (1, 2, 3, 4):
+    for variant in (1, 4):
         alt = S.solver._system_from_grouped(grouped, masses, fixed, variant=variant)
         assert block_rel_err(S.device.to_host(alt.vals), o_vals) < 1e-12, variant
         alt.close()
