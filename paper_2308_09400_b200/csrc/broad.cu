@@ -3,18 +3,19 @@
 //
 // The reference tests every (surface vertex, triangle) and every (edge, edge) pair for AABB overlap --
 // O(n^2) boolean matrices.  Here both joins run on a uniform grid:
-//   1. every "B" box (triangle AABB; edge AABB inflated by d_hat/2) is binned into the cells it
-//      overlaps: count, scan, fill (cell key, box), stable radix sort by cell key;
-//   2. every "A" box (vertex box [p - d_hat, p + d_hat]; inflated edge AABB) walks its cells, finds
-//      each cell's run of B boxes by binary search, and keeps a pair when
+//   1. the boxes of the "B" elements (triangle AABB; edge AABB inflated by d_hat/2) are built once and
+//      each is filed under ONE cell, the cell of its lower corner (one radix sort of n keys; no
+//      multi-cell binning, so no pair can be found twice); the largest box extent per axis is reduced
+//      on the device alongside;
+//   2. every "A" box (vertex box [p - d_hat, p + d_hat]; inflated edge AABB) probes the cells that can
+//      hold the lower corner of an overlapping B box, [A.lo - max extent, A.hi], finds each cell
+//      column's run by binary search, and keeps a pair when
 //        - the boxes overlap (the reference's own predicate lo_a <= hi_b && lo_b <= hi_a on the same
 //          fp64 box corners, so the candidate SET equals the reference's),
-//        - this cell holds the lower corner of the boxes' intersection (a pair sharing several
-//          cells is reported exactly once: no de-duplication pass),
 //        - the reference's incidence filters pass (vertex not a corner of the triangle, :286;
 //          edge index i < j and no shared endpoint, :311-317);
 //      first to count, then -- after a scan -- to write (A, B) as global vertex ids.
-// Output order is deterministic (by A box, cell, B box) but irrelevant: the narrow phase sorts.
+// Output order is deterministic (by A box, probe slot, cell, B box) but irrelevant: the narrow phase sorts.
 // The same join with swept boxes (both ends of a step, margin 1e-3 d_hat) is sweep_candidates
 // (proximity.py:388-421), the candidate set of the CCD step filter (accd.cu).
 #include <cub/cub.cuh>
@@ -138,30 +139,30 @@ __global__ void __launch_bounds__(kBT) make_boxes_kernel(const Boxes in, const i
   if (i < n) out[i] = make_box<KIND>(in, elems, i);
 }
 
-template <int KIND>
-__global__ void __launch_bounds__(kBT) bin_count_kernel(const Boxes in, const int32_t* __restrict__ elems, int64_t n,
-                                                        Grid g, int32_t* __restrict__ cnt) {
+// Home cell (cell of the lower corner) of every B box, and the largest extent per axis (ordered-bits
+// atomicMax: extents are non-negative doubles).
+__global__ void __launch_bounds__(kBT) home_cell_kernel(const Box* __restrict__ box, int64_t n, Grid g,
+                                                        uint64_t* __restrict__ keys, uint32_t* __restrict__ ids,
+                                                        unsigned long long* __restrict__ ext) {
   const int64_t i = (int64_t)blockIdx.x * kBT + threadIdx.x;
-  if (i >= n) return;
-  const int64_t c = span_of(make_box<KIND>(in, elems, i), g).count();
-  cnt[i] = (int32_t)(c > 0x7fffffff ? 0x7fffffff : c);
-}
-
-template <int KIND>
-__global__ void __launch_bounds__(kBT) bin_fill_kernel(const Boxes in, const int32_t* __restrict__ elems, int64_t n,
-                                                       Grid g, const int64_t* __restrict__ off,
-                                                       uint64_t* __restrict__ keys, uint32_t* __restrict__ ids) {
-  const int64_t i = (int64_t)blockIdx.x * kBT + threadIdx.x;
-  if (i >= n) return;
-  const Span s = span_of(make_box<KIND>(in, elems, i), g);
-  int64_t o = off[i];
-  for (int cx = s.x0; cx <= s.x1; ++cx)
-    for (int cy = s.y0; cy <= s.y1; ++cy)
-      for (int cz = s.z0; cz <= s.z1; ++cz) {
-        keys[o] = cell_key(cx, cy, cz);
-        ids[o] = (uint32_t)i;
-        ++o;
-      }
+  double ex = 0.0, ey = 0.0, ez = 0.0;
+  if (i < n) {
+    const Box b = box[i];
+    keys[i] = cell_key(cell_of(b.lx, g.ox, g.inv), cell_of(b.ly, g.oy, g.inv), cell_of(b.lz, g.oz, g.inv));
+    ids[i] = (uint32_t)i;
+    ex = b.hx - b.lx; ey = b.hy - b.ly; ez = b.hz - b.lz;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ex = fmax(ex, __shfl_xor_sync(0xffffffffu, ex, o));
+    ey = fmax(ey, __shfl_xor_sync(0xffffffffu, ey, o));
+    ez = fmax(ez, __shfl_xor_sync(0xffffffffu, ez, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(ext, (unsigned long long)__double_as_longlong(ex));
+    atomicMax(ext + 1, (unsigned long long)__double_as_longlong(ey));
+    atomicMax(ext + 2, (unsigned long long)__double_as_longlong(ez));
+  }
 }
 
 __device__ __forceinline__ int64_t lower_bound_u64(const uint64_t* __restrict__ a, int64_t n, uint64_t key) {
@@ -178,23 +179,39 @@ struct JoinArgs {
   Boxes in;
   const int32_t* a_elems;   // surf_verts (VT) or edges (EE)
   const int32_t* b_elems;   // tris (VT) or edges (EE)
-  int64_t na, nbins;        // A boxes; sorted (cell, B box) incidences
+  int64_t na, nbins;        // A boxes; B boxes (one sorted (home cell, box) entry each)
   Grid g;
   const uint64_t* keys;     // sorted
   const uint32_t* ids;
   const Box* bbox;          // boxes of the B elements
-  const int64_t* off;       // per A box output offset (fill pass)
-  int32_t* cnt;             // per A box pair count (count pass)
+  const double* ext;        // largest B extent per axis (device, 3)
+  const int64_t* off;       // per (A box, slot) output offset (fill pass)
+  int32_t* cnt;             // per (A box, slot) pair count (count pass)
   int4* out;                // (pairs, 4) global vertex ids (fill pass)
 };
 
 // EE = false: A = vertex boxes, B = triangles.  EE = true: A = B = inflated edge boxes.
+// One thread per (A box, slot): slot (rx, ry) of kJoinSlots = 3 x 3 walks the cell columns
+// (x0 + rx + 3p, y0 + ry + 3q) of the box's span, so a box covering up to 3 x 3 columns is spread over
+// nine threads (4 - 8 x more threads and correspondingly shorter loops than one thread per box; larger
+// spans just loop).  Counts and offsets are per (box, slot): the output order stays deterministic.
+constexpr int kJoinSlots = 9;
+
 template <bool EE, bool FILL>
 __global__ void __launch_bounds__(kBT) join_kernel(const __grid_constant__ JoinArgs a) {
-  const int64_t i = (int64_t)blockIdx.x * kBT + threadIdx.x;
-  if (i >= a.na) return;
+  const int64_t T = (int64_t)blockIdx.x * kBT + threadIdx.x;
+  if (T >= a.na * kJoinSlots) return;
+  const int64_t i = T / kJoinSlots;
+  const int slot = (int)(T - i * kJoinSlots);
+  const int rx = slot / 3, ry = slot - 3 * rx;
   const Box A = EE ? a.bbox[i] : make_box<0>(a.in, a.a_elems, i);
-  const Span s = span_of(A, a.g);
+  // cells that can hold the lower corner of an overlapping B box: [A.lo - max extent, A.hi]; the extent
+  // is widened by 1e-9 relative so that the roundings of hi - lo and lo - extent cannot lose a cell
+  constexpr double kWiden = 1.000000001;
+  Span s;
+  s.x0 = cell_of(A.lx - kWiden * a.ext[0], a.g.ox, a.g.inv); s.x1 = cell_of(A.hx, a.g.ox, a.g.inv);
+  s.y0 = cell_of(A.ly - kWiden * a.ext[1], a.g.oy, a.g.inv); s.y1 = cell_of(A.hy, a.g.oy, a.g.inv);
+  s.z0 = cell_of(A.lz - kWiden * a.ext[2], a.g.oz, a.g.inv); s.z1 = cell_of(A.hz, a.g.oz, a.g.inv);
   int av0, av1 = -1;
   if (EE) {
     av0 = a.a_elems[2 * i];
@@ -203,9 +220,9 @@ __global__ void __launch_bounds__(kBT) join_kernel(const __grid_constant__ JoinA
     av0 = a.a_elems[i];
   }
   int32_t n = 0;
-  int64_t o = FILL ? a.off[i] : 0;
-  for (int cx = s.x0; cx <= s.x1; ++cx)
-    for (int cy = s.y0; cy <= s.y1; ++cy) {
+  int64_t o = FILL ? a.off[T] : 0;
+  for (int cx = s.x0 + rx; cx <= s.x1; cx += 3)
+    for (int cy = s.y0 + ry; cy <= s.y1; cy += 3) {
       // cells (cx, cy, z0..z1) are consecutive keys: one search, one walk
       const uint64_t k0 = cell_key(cx, cy, s.z0), k1 = cell_key(cx, cy, s.z1);
       for (int64_t t = lower_bound_u64(a.keys, a.nbins, k0); t < a.nbins; ++t) {
@@ -215,10 +232,6 @@ __global__ void __launch_bounds__(kBT) join_kernel(const __grid_constant__ JoinA
         if (EE && j <= i) continue;  // each unordered pair once, lower edge index first (:310)
         const Box B = a.bbox[j];
         if (!(A.lx <= B.hx && B.lx <= A.hx && A.ly <= B.hy && B.ly <= A.hy && A.lz <= B.hz && B.lz <= A.hz)) continue;
-        // owner cell = cell of the lower corner of the intersection
-        const int ox = cell_of(fmax(A.lx, B.lx), a.g.ox, a.g.inv), oy = cell_of(fmax(A.ly, B.ly), a.g.oy, a.g.inv),
-                  oz = cell_of(fmax(A.lz, B.lz), a.g.oz, a.g.inv);
-        if (cell_key(ox, oy, oz) != key) continue;
         int4 q;
         if (EE) {
           const int b0 = a.b_elems[2 * j], b1 = a.b_elems[2 * j + 1];
@@ -233,22 +246,23 @@ __global__ void __launch_bounds__(kBT) join_kernel(const __grid_constant__ JoinA
         else ++n;
       }
     }
-  if (!FILL) a.cnt[i] = n;
+  if (!FILL) a.cnt[T] = n;
 }
 
 }  // namespace b200ipc
 
 struct b200ipc_broad {
   b200ipc::BroadBuf<int32_t> cnt;
-  b200ipc::BroadBuf<int64_t> off_bin, off_vt, off_ee;
+  b200ipc::BroadBuf<int64_t> off_vt, off_ee;
   b200ipc::BroadBuf<uint64_t> keys_a, keys_t, keys_e;   // scratch, sorted triangle bins, sorted edge bins
   b200ipc::BroadBuf<uint32_t> ids_a, ids_t, ids_e;
   b200ipc::BroadBuf<uint8_t> temp;
   b200ipc::BroadBuf<int64_t> totals;
   b200ipc::BroadBuf<b200ipc::Box> box_t, box_e;
+  b200ipc::BroadBuf<double> ext;   // [0..2] triangles, [3..5] edges: largest box extent per axis
   // state between count and fill
   bool counted = false;
-  int64_t nverts = 0, n_sv = 0, n_tri = 0, n_edge = 0, nbin_t = 0, nbin_e = 0, n_vt = 0, n_ee = 0;
+  int64_t nverts = 0, n_sv = 0, n_tri = 0, n_edge = 0, n_vt = 0, n_ee = 0;
   b200ipc::Boxes in{};
   const int32_t *surf_verts = nullptr, *tris = nullptr, *edges = nullptr;
   b200ipc::Grid grid{};
@@ -282,29 +296,20 @@ static int scan_counts(b200ipc_broad* h, const int32_t* cnt, int64_t* off, int64
   return 0;
 }
 
-template <int KIND>
-static int bin_boxes(b200ipc_broad* h, const int32_t* elems, int64_t n, BroadBuf<uint64_t>& keys, BroadBuf<uint32_t>& ids,
-                     int64_t* nbins, cudaStream_t st) {
-  *nbins = 0;
+// File every B box under its home cell (sorted keys / ids) and reduce the largest extent per axis.
+static int bin_boxes(b200ipc_broad* h, const Box* box, int64_t n, BroadBuf<uint64_t>& keys, BroadBuf<uint32_t>& ids,
+                     double* ext, cudaStream_t st) {
+  CK(cudaMemsetAsync(ext, 0, 3 * sizeof(double), st));
   if (n == 0) return 0;
-  CK(h->cnt.reserve(n + 1));
-  CK(h->off_bin.reserve(n + 1));
-  CK(cudaMemsetAsync(h->cnt.ptr + n, 0, sizeof(int32_t), st));
-  bin_count_kernel<KIND><<<bblocks(n), kBT, 0, st>>>(h->in, elems, n, h->grid, h->cnt.ptr);
-  RC(post_launch());
-  int64_t total = 0;
-  RC(scan_counts(h, h->cnt.ptr, h->off_bin.ptr, n, &total, st));
-  if (total >= (1ll << 31)) return B200IPC_EINVAL;  // cell size far too small for these boxes
-  CK(h->keys_a.reserve(total)); CK(h->ids_a.reserve(total)); CK(keys.reserve(total)); CK(ids.reserve(total));
-  bin_fill_kernel<KIND><<<bblocks(n), kBT, 0, st>>>(h->in, elems, n, h->grid, h->off_bin.ptr, h->keys_a.ptr, h->ids_a.ptr);
+  CK(h->keys_a.reserve(n)); CK(h->ids_a.reserve(n)); CK(keys.reserve(n)); CK(ids.reserve(n));
+  home_cell_kernel<<<bblocks(n), kBT, 0, st>>>(box, n, h->grid, h->keys_a.ptr, h->ids_a.ptr,
+                                               reinterpret_cast<unsigned long long*>(ext));
   RC(post_launch());
   size_t tb = 0;
-  CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, h->keys_a.ptr, keys.ptr, h->ids_a.ptr, ids.ptr, (int)total, 0, 63, st));
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, h->keys_a.ptr, keys.ptr, h->ids_a.ptr, ids.ptr, (int)n, 0, 63, st));
   CK(h->temp.reserve(tb));
-  CK(cub::DeviceRadixSort::SortPairs(h->temp.ptr, tb, h->keys_a.ptr, keys.ptr, h->ids_a.ptr, ids.ptr, (int)total, 0, 63,
-                                     st));
+  CK(cub::DeviceRadixSort::SortPairs(h->temp.ptr, tb, h->keys_a.ptr, keys.ptr, h->ids_a.ptr, ids.ptr, (int)n, 0, 63, st));
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  *nbins = total;
   return 0;
 }
 
@@ -316,10 +321,10 @@ extern "C" int b200ipc_broad_create(b200ipc_broad** out) {
 
 extern "C" int b200ipc_broad_destroy(b200ipc_broad* h) {
   if (!h) return 0;
-  h->cnt.release(); h->off_bin.release(); h->off_vt.release(); h->off_ee.release();
+  h->cnt.release(); h->off_vt.release(); h->off_ee.release();
   h->keys_a.release(); h->keys_t.release(); h->keys_e.release();
   h->ids_a.release(); h->ids_t.release(); h->ids_e.release();
-  h->temp.release(); h->totals.release(); h->box_t.release(); h->box_e.release();
+  h->temp.release(); h->totals.release(); h->box_t.release(); h->box_e.release(); h->ext.release();
   delete h;
   return 0;
 }
@@ -331,43 +336,46 @@ static int broad_count(b200ipc_broad* h, int64_t nverts, const Boxes& in, int64_
     return B200IPC_EINVAL;
   if ((n_sv && !surf_verts) || (n_tri && !tris) || (n_edge && !edges)) return B200IPC_EINVAL;
   if (!(cell > 0.0)) return B200IPC_EINVAL;
-  if (n_sv >= (1ll << 31) || n_tri >= (1ll << 31) || n_edge >= (1ll << 31)) return B200IPC_EINVAL;
+  if (n_sv >= (1ll << 27) || n_tri >= (1ll << 31) || n_edge >= (1ll << 27)) return B200IPC_EINVAL;  // (box, slot) ids are int32-scanned
   cudaStream_t st = (cudaStream_t)stream;
   h->counted = false;
   h->nverts = nverts; h->in = in; h->n_sv = n_sv; h->surf_verts = surf_verts; h->n_tri = n_tri; h->tris = tris;
   h->n_edge = n_edge; h->edges = edges;
   h->grid = Grid{origin[0], origin[1], origin[2], 1.0 / cell};
   h->n_vt = h->n_ee = 0;
+  CK(h->ext.reserve(6));
 
   // ---- point-triangle: triangles binned, vertex boxes probe ----------------------------------------
   if (n_sv && n_tri) {
     CK(h->box_t.reserve(n_tri));
     make_boxes_kernel<1><<<bblocks(n_tri), kBT, 0, st>>>(in, tris, n_tri, h->box_t.ptr);
     RC(post_launch());
-    RC(bin_boxes<1>(h, tris, n_tri, h->keys_t, h->ids_t, &h->nbin_t, st));
-    CK(h->cnt.reserve(n_sv + 1));
-    CK(h->off_vt.reserve(n_sv + 1));
-    CK(cudaMemsetAsync(h->cnt.ptr + n_sv, 0, sizeof(int32_t), st));
-    JoinArgs a{in, surf_verts, tris, n_sv, h->nbin_t, h->grid, h->keys_t.ptr, h->ids_t.ptr, h->box_t.ptr, nullptr,
+    RC(bin_boxes(h, h->box_t.ptr, n_tri, h->keys_t, h->ids_t, h->ext.ptr, st));
+    const int64_t ns = n_sv * kJoinSlots;
+    CK(h->cnt.reserve(ns + 1));
+    CK(h->off_vt.reserve(ns + 1));
+    CK(cudaMemsetAsync(h->cnt.ptr + ns, 0, sizeof(int32_t), st));
+    JoinArgs a{in, surf_verts, tris, n_sv, n_tri, h->grid, h->keys_t.ptr, h->ids_t.ptr, h->box_t.ptr, h->ext.ptr, nullptr,
                h->cnt.ptr, nullptr};
-    join_kernel<false, false><<<bblocks(n_sv), kBT, 0, st>>>(a);
+    join_kernel<false, false><<<bblocks(ns), kBT, 0, st>>>(a);
     RC(post_launch());
-    RC(scan_counts(h, h->cnt.ptr, h->off_vt.ptr, n_sv, &h->n_vt, st));
+    RC(scan_counts(h, h->cnt.ptr, h->off_vt.ptr, ns, &h->n_vt, st));
   }
   // ---- edge-edge: edges binned, the same boxes probe --------------------------------------------------
   if (n_edge > 1) {
     CK(h->box_e.reserve(n_edge));
     make_boxes_kernel<2><<<bblocks(n_edge), kBT, 0, st>>>(in, edges, n_edge, h->box_e.ptr);
     RC(post_launch());
-    RC(bin_boxes<2>(h, edges, n_edge, h->keys_e, h->ids_e, &h->nbin_e, st));
-    CK(h->cnt.reserve(n_edge + 1));
-    CK(h->off_ee.reserve(n_edge + 1));
-    CK(cudaMemsetAsync(h->cnt.ptr + n_edge, 0, sizeof(int32_t), st));
-    JoinArgs a{in, edges, edges, n_edge, h->nbin_e, h->grid, h->keys_e.ptr, h->ids_e.ptr, h->box_e.ptr, nullptr,
+    RC(bin_boxes(h, h->box_e.ptr, n_edge, h->keys_e, h->ids_e, h->ext.ptr + 3, st));
+    const int64_t ns = n_edge * kJoinSlots;
+    CK(h->cnt.reserve(ns + 1));
+    CK(h->off_ee.reserve(ns + 1));
+    CK(cudaMemsetAsync(h->cnt.ptr + ns, 0, sizeof(int32_t), st));
+    JoinArgs a{in, edges, edges, n_edge, n_edge, h->grid, h->keys_e.ptr, h->ids_e.ptr, h->box_e.ptr, h->ext.ptr + 3, nullptr,
                h->cnt.ptr, nullptr};
-    join_kernel<true, false><<<bblocks(n_edge), kBT, 0, st>>>(a);
+    join_kernel<true, false><<<bblocks(ns), kBT, 0, st>>>(a);
     RC(post_launch());
-    RC(scan_counts(h, h->cnt.ptr, h->off_ee.ptr, n_edge, &h->n_ee, st));
+    RC(scan_counts(h, h->cnt.ptr, h->off_ee.ptr, ns, &h->n_ee, st));
   }
   *n_vt = h->n_vt;
   *n_ee = h->n_ee;
@@ -400,15 +408,15 @@ extern "C" int b200ipc_broad_phase_fill(b200ipc_broad* h, int32_t* vt, int32_t* 
   if (((uintptr_t)vt | (uintptr_t)ee) & 15) return B200IPC_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
   if (h->n_vt) {
-    JoinArgs a{h->in, h->surf_verts, h->tris, h->n_sv, h->nbin_t, h->grid, h->keys_t.ptr, h->ids_t.ptr, h->box_t.ptr,
+    JoinArgs a{h->in, h->surf_verts, h->tris, h->n_sv, h->n_tri, h->grid, h->keys_t.ptr, h->ids_t.ptr, h->box_t.ptr, h->ext.ptr,
                h->off_vt.ptr, nullptr, reinterpret_cast<int4*>(vt)};
-    join_kernel<false, true><<<bblocks(h->n_sv), kBT, 0, st>>>(a);
+    join_kernel<false, true><<<bblocks(h->n_sv * kJoinSlots), kBT, 0, st>>>(a);
     RC(post_launch());
   }
   if (h->n_ee) {
-    JoinArgs a{h->in, h->edges, h->edges, h->n_edge, h->nbin_e, h->grid, h->keys_e.ptr, h->ids_e.ptr, h->box_e.ptr,
+    JoinArgs a{h->in, h->edges, h->edges, h->n_edge, h->n_edge, h->grid, h->keys_e.ptr, h->ids_e.ptr, h->box_e.ptr, h->ext.ptr + 3,
                h->off_ee.ptr, nullptr, reinterpret_cast<int4*>(ee)};
-    join_kernel<true, true><<<bblocks(h->n_edge), kBT, 0, st>>>(a);
+    join_kernel<true, true><<<bblocks(h->n_edge * kJoinSlots), kBT, 0, st>>>(a);
     RC(post_launch());
   }
   return 0;
