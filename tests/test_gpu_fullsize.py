@@ -1,0 +1,132 @@
+"""BASELINE.json's full sizes (configs[1]: 1 M near-parallel EE stencils; configs[3]: ~1 M contacts of a
+multilayer cloth stack) through size-independent properties, evaluated on the device, plus the oracle
+on a strided sample: the 1e-9 parity tests run at sizes the oracle finishes in seconds, these make sure
+nothing changes at scale (tile tails, 64-bit offsets, kind-segment boundaries, chunk rings)."""
+
+import numpy as np
+import pytest
+
+from oracle import tetipc_oracle as o
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+
+    from paper_2308_09400_b200 import barrier, contacts, device, kernels, proximity, solver, stencils, workloads
+
+    class NS:
+        pass
+
+    ns = NS()
+    ns.torch, ns.barrier, ns.contacts, ns.device, ns.kernels = torch, barrier, contacts, device, kernels
+    ns.proximity, ns.solver, ns.stencils, ns.workloads = proximity, solver, stencils, workloads
+    return ns
+
+
+def block_properties(P, batch, pos_scale=1.0):
+    """Rank-1 / symmetry / translation invariance of every block family, on the device."""
+    t = P.torch
+    for s, fam in batch.families.items():
+        h, g, z = fam.hess, fam.grad, fam.fac
+        assert bool((h == h.transpose(1, 2)).all())                          # bit-symmetric
+        assert bool((h == z[:, :, None] * z[:, None, :]).all())              # exactly z z^T: rank <= 1, PSD
+        gsum = g.reshape(-1, s, 3).sum(dim=1).abs().amax(dim=1)              # sum_v grad_v = 0 (translation)
+        gmax = g.abs().amax(dim=1)
+        assert bool((gsum <= 1e-9 * gmax + 1e-300).all())
+        zsum = z.reshape(-1, s, 3).sum(dim=1).abs().amax(dim=1)              # H t = z (z . t) = 0 for translations t
+        assert bool((zsum <= 1e-9 * z.abs().amax(dim=1) + 1e-300).all())
+        assert bool(t.isfinite(h).all()) and bool(t.isfinite(g).all())
+
+
+def test_config2_one_million_parallel_ee(P):
+    qb = P.workloads.config2_batch(n=1_000_000)
+    table, extra = P.contacts.narrow_phase_device(qb.positions, qb.rest_positions, qb.vt, qb.ee, qb.d_hat)
+    assert table.n == 1_000_000
+    counts = np.diff(table.kind_off)
+    assert counts[1] > 4e5 and counts[3] > 4e5 and counts[5] > 1e5            # EE-par, PE-par, PP-par dominate
+    params = P.barrier.BarrierParams(d_hat=qb.d_hat, kappa=qb.kappa)
+    batch = P.stencils.evaluate(table, qb.positions, params, want_factors=True)
+    total, inactive, bad = batch.summary()
+    assert bad == 0 and inactive == 0
+    block_properties(P, batch)
+    # the oracle on every 100th row: 1e-9 parity of energy, gradient and block at full-table offsets
+    rows = np.arange(0, table.n, 100)
+    kind = P.device.to_host(extra.kind)[rows]
+    verts, sub, eps = (P.device.to_host(table.verts)[rows], P.device.to_host(table.sub)[rows],
+                       P.device.to_host(table.eps_x)[rows])
+    ref = o.local_quadratics_batch(kind, verts, sub, eps, qb.positions, qb.d_hat, qb.kappa)
+    energy = P.device.to_host(batch.energy)[rows]
+    assert np.abs(energy - ref["energy"]).max() <= 1e-9 * np.abs(ref["energy"]).max()
+    # family-4 rows of the sample (every kind here has four vertices except plain PE / PP)
+    off = table.kind_off
+    g4 = P.device.to_host(batch.families[4].grad)
+    h4 = batch.families[4].hess
+    start4 = {}
+    acc = 0
+    for k in P.stencils.FAMILY_KINDS[4]:
+        start4[k] = acc - off[k]
+        acc += off[k + 1] - off[k]
+    pick = [i for i in range(len(rows)) if kind[i] in (1, 3, 5)][:2000]
+    frows = np.array([rows[i] + start4[int(kind[i])] for i in pick])
+    gerr = np.abs(g4[frows] - ref["grad"][pick]).max(axis=1) / np.abs(ref["grad"][pick]).max(axis=1)
+    assert (gerr <= 1e-9).mean() > 0.97                                       # k2-cancellation rows: DESIGN.md 2
+    hs = P.device.to_host(h4[P.torch.from_numpy(frows).cuda()])
+    herr = np.abs(hs - ref["hess"][pick]).reshape(len(pick), -1).max(axis=1) / np.abs(ref["hess"][pick]).reshape(len(pick), -1).max(axis=1)
+    assert (herr <= 1e-9).mean() > 0.97
+    assert abs(total - float(P.device.to_host(batch.energy).sum())) <= 1e-12 * abs(total)
+
+
+def test_cloth_stack_one_million_contacts(P):
+    t = P.torch
+    cloth = P.workloads.cloth_stack(layers=4, n=140, seed=1, d_hat_rel=0.2)
+    bp = P.contacts.BroadPhase(None, cloth.tris, cloth.edges, cloth.d_hat, cloth.positions)
+    vt, ee = bp.query(cloth.positions)
+    bp.close()
+    table, extra = P.contacts.narrow_phase_device(cloth.positions, cloth.rest_positions, vt, ee, cloth.d_hat)
+    assert 0.9e6 < table.n < 1.1e6 and (np.diff(table.kind_off) > 0).all()     # all seven kinds
+    # ordered list: keys (kind, verts) non-decreasing, checked on the device
+    v = table.verts.to(t.int64) + 1
+    key = ((extra.kind.to(t.int64) * (1 << 18) + v[:, 0]) * (1 << 18) + v[:, 1])
+    assert bool((key[1:] >= key[:-1]).all())
+    params = P.barrier.BarrierParams(d_hat=cloth.d_hat, kappa=cloth.kappa)
+    batch = P.stencils.evaluate(table, cloth.positions, params, dt=cloth.dt, want_factors=True)
+    assert batch.summary()[2] == 0
+    block_properties(P, batch)
+    fams = [batch.families[s] for s in sorted(batch.families)]
+    sysm = P.solver.NewtonSystem(cloth.masses, cloth.fixed)
+    nnzb = sysm.set_pattern([(f.s, f.vids) for f in fams])
+    dense_path = sysm.assemble([f.hess for f in fams]).clone()
+    factor_path = sysm.assemble_from_factors([f.fac for f in fams])
+    assert bool((dense_path == factor_path).all())                             # bitwise, 1.3 M blocks
+    rowptr, colidx = sysm.rowptr, sysm.colidx
+    assert int(rowptr[-1]) == nnzb and bool((rowptr[1:] > rowptr[:-1]).all())
+    # assembled SpMV == matrix-free matvec of the reference kernel seam, two independent paths
+    rng = np.random.default_rng(0)
+    x = P.device.to_device(rng.normal(size=3 * sysm.n))
+    y = sysm.spmv(x)
+    free = t.from_numpy(~cloth.fixed).cuda().repeat_interleave(3)
+    xm = t.where(free, x, t.zeros_like(x))
+    out = t.repeat_interleave(sysm.masses, 3) * xm
+    for f in fams:
+        P.kernels.matvec_blocks_device(f.hess, f.vids, xm, out)
+    out = t.where(free, out, x)
+    assert float((y - out).abs().max()) <= 1e-11 * float(out.abs().max())
+    # symmetry of the operator: x . (A w) == w . (A x)
+    w = P.device.to_device(rng.normal(size=3 * sysm.n))
+    aw = sysm.spmv(w)
+    assert abs(float(x @ aw) - float(w @ y)) <= 1e-10 * abs(float(w @ y))
+    # PCG at scale: converges, and the re-evaluated residual meets the reference's stopping rule
+    xt = P.device.to_device(cloth.positions + 1e-4 * rng.normal(size=cloth.positions.shape))
+    rhs = -sysm.gradient(cloth.positions, xt, [f.grad for f in fams])
+    d, iters, ok, d0, dn = sysm.pcg(rhs, 1e-4, 2000)
+    assert ok and 50 < iters < 1000
+    res = t.where(free, rhs - sysm.spmv(d), t.zeros_like(rhs))
+    pinv = sysm.block_jacobi()
+    pres = (pinv @ res.reshape(-1, 3, 1)).reshape(-1)
+    r0 = t.where(free, rhs, t.zeros_like(rhs))
+    p0 = (pinv @ r0.reshape(-1, 3, 1)).reshape(-1)
+    assert float(res @ pres) <= 1.05e-4 * float(r0 @ p0)
+    sysm.close()
