@@ -303,7 +303,8 @@ int b200ipc_assembly_destroy(b200ipc_assembly* h);
 int b200ipc_assembly_set_variant(b200ipc_assembly* h, int32_t variant);
 /* Build the pattern and the source runs (sort by key).  fixed: device u8 (nverts).  Synchronises
  * `stream` and returns the number of 3x3 blocks in *nnzb_out (host).  The vids buffers must stay
- * valid until the next symbolic call (the numeric phase re-reads nothing from them). */
+ * valid until the next symbolic call: the descriptor tables of the numeric kernels are built from
+ * them on the first numeric call that needs them (a Newton iteration uses one numeric path). */
 int b200ipc_assemble_symbolic(b200ipc_assembly* h, int64_t nverts, const uint8_t* fixed, int32_t nfam,
                               const int32_t* fam_s /* host */, const int64_t* fam_nb /* host */,
                               const int64_t* const* fam_vids /* host array of device ptrs */,

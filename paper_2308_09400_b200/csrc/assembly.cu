@@ -65,6 +65,7 @@ struct b200ipc_assembly {
   int64_t nnzb = 0;
   int64_t ngslots = 0;     // sum nb*s
   bool ready = false;
+  bool have_desc = false, have_fdesc = false, have_rows = false;   // descriptor tables are built on first use
   int variant = 0;         // numeric kernel: 0 auto (per-block runs when applicable), 1 runs, 4 row-wise
   b200ipc::FamDesc fam;
   b200ipc::DevBuf<uint8_t> fixed;
@@ -667,13 +668,6 @@ extern "C" int b200ipc_assemble_symbolic(b200ipc_assembly* h, int64_t nverts, co
   }
   finish_pattern_kernel<<<1, 1, 0, st>>>(nverts, h->nnzb, h->nvalid, h->rowptr.ptr, h->useg.ptr);
   RC(post_launch());
-  CK(h->desc.reserve(h->nvalid));
-  source_desc_kernel<<<blocks_for(h->nvalid), kAT, 0, st>>>(fd, nverts, h->nvalid, h->slot_b.ptr, h->desc.ptr);
-  RC(post_launch());
-  CK(h->fdesc.reserve(h->nvalid));
-  factor_desc_kernel<<<blocks_for(h->nvalid), kAT, 0, st>>>(fd, nverts, h->nvalid, h->slot_b.ptr, h->fdesc.ptr);
-  RC(post_launch());
-
   // gradient runs: sort vertex slots by vertex id
   const int64_t ng = h->ngslots;
   CK(h->gseg.reserve(nverts + 1));
@@ -692,14 +686,42 @@ extern "C" int b200ipc_assemble_symbolic(b200ipc_assembly* h, int64_t nverts, co
   }
   lower_bound_kernel<<<blocks_for(nverts + 1), kAT, 0, st>>>(nverts, ng, h->gkeys_b.ptr, h->gseg.ptr);
   RC(post_launch());
+  h->have_desc = h->have_fdesc = h->have_rows = false;
+  h->ready = true;
+  if (nnzb_out) *nnzb_out = h->nnzb;
+  return 0;
+}
+
+// Descriptor tables of the numeric kernels, built on first use after a symbolic phase (a Newton
+// iteration uses one numeric path, so the other tables are never built).
+static int ensure_desc(b200ipc_assembly* h, cudaStream_t st) {
+  if (h->have_desc) return 0;
+  CK(h->desc.reserve(h->nvalid));
+  source_desc_kernel<<<blocks_for(h->nvalid), kAT, 0, st>>>(h->fam, h->nverts, h->nvalid, h->slot_b.ptr, h->desc.ptr);
+  RC(post_launch());
+  h->have_desc = true;
+  return 0;
+}
+
+static int ensure_fdesc(b200ipc_assembly* h, cudaStream_t st) {
+  if (h->have_fdesc) return 0;
+  CK(h->fdesc.reserve(h->nvalid));
+  factor_desc_kernel<<<blocks_for(h->nvalid), kAT, 0, st>>>(h->fam, h->nverts, h->nvalid, h->slot_b.ptr, h->fdesc.ptr);
+  RC(post_launch());
+  h->have_fdesc = true;
+  return 0;
+}
+
+static int ensure_rows(b200ipc_assembly* h, cudaStream_t st) {
+  if (h->have_rows) return 0;
+  const int64_t ng = h->ngslots;
   if (ng > 0) {
     CK(h->rs_desc.reserve(ng)); CK(h->rs_dst.reserve(ng));
-    row_source_kernel<<<blocks_for(ng), kAT, 0, st>>>(fd, nverts, ng, h->gslot_b.ptr, h->fixed.ptr, h->rowptr.ptr,
+    row_source_kernel<<<blocks_for(ng), kAT, 0, st>>>(h->fam, h->nverts, ng, h->gslot_b.ptr, h->fixed.ptr, h->rowptr.ptr,
                                                      h->colidx.ptr, h->rs_desc.ptr, h->rs_dst.ptr);
     RC(post_launch());
   }
-  h->ready = true;
-  if (nnzb_out) *nnzb_out = h->nnzb;
+  h->have_rows = true;
   return 0;
 }
 
@@ -728,10 +750,13 @@ extern "C" int b200ipc_assemble_numeric(b200ipc_assembly* h, const double* masse
   a.nnzb = h->nnzb; a.fixed = h->fixed.ptr; a.masses = masses;
   a.useg = h->useg.ptr; a.desc = h->desc.ptr; a.vals = vals;
   if ((h->variant == 0 || h->variant == 1) && packed_ok) {  // per-block runs (gather of 3x3 sub-blocks)
+    RC(ensure_desc(h, (cudaStream_t)stream));
+    a.desc = h->desc.ptr;
     const unsigned grid = (unsigned)((h->nnzb + kNumWarps * kBlocksPerWarp - 1) / (kNumWarps * kBlocksPerWarp));
     assemble_numeric_kernel<<<grid, 32 * kNumWarps, 0, (cudaStream_t)stream>>>(a);
     return post_launch();
   }
+  RC(ensure_rows(h, (cudaStream_t)stream));
   RowArgs r;
   r.hp = a.hp;
   for (int f = 0; f <= kMaxFam; ++f) r.fs[f] = f < h->fam.nfam ? h->fam.s[f] : 0;
@@ -754,6 +779,7 @@ extern "C" int b200ipc_assemble_numeric_factors(b200ipc_assembly* h, const doubl
     if (h->fam.nb[f] * 3 * h->fam.s[f] >= (1ll << 27)) return B200IPC_EINVAL;  // 27-bit element index
     a.fp.p[f] = fam_fac[f];
   }
+  RC(ensure_fdesc(h, (cudaStream_t)stream));
   a.nnzb = h->nnzb; a.fixed = h->fixed.ptr; a.masses = masses; a.useg = h->useg.ptr; a.fdesc = h->fdesc.ptr;
   a.vals = vals;
   const unsigned grid = (unsigned)((h->nnzb + kNumWarps * kBlocksPerWarp - 1) / (kNumWarps * kBlocksPerWarp));
