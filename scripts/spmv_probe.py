@@ -30,7 +30,7 @@ os.environ["B200IPC_SPMV_MODE"] = "legacy"
 sysm.spmv(x, out=y); ref = device.to_host(y).copy()
 print("legacy spmv ms", bench.time_steps(torch, lambda: sysm.spmv(x, out=y), 100, 5, noop) / 100, flush=True)
 os.environ["B200IPC_SPMV_MODE"] = "stream"
-for R, PF in (("24", "0"), ("27", "0"), ("27", "1")):
+for R, PF in (("12", "0"), ("18", "0"), ("24", "0"), ("30", "0")):
     os.environ["B200IPC_SPMV_ROWS_PER_CHUNK"] = R
     os.environ["B200IPC_SPMV_PREFETCH_X"] = PF
     y.zero_(); sysm.spmv(x, out=y); got = device.to_host(y)
