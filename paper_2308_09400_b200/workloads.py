@@ -273,6 +273,77 @@ def cloth_stack(layers=4, n=64, seed=1, h=0.01, gap_rel=0.6, d_hat_rel=0.5, jitt
                       d_hat, kappa, dt, f"cloth-stack-{layers}x{n}x{n}")
 
 
+def _icosphere(subdiv):
+    """Unit icosphere: (verts (V,3), tris (F,3)); V = 10*4^subdiv + 2."""
+    t = (1.0 + np.sqrt(5.0)) / 2.0
+    v = np.array([[-1, t, 0], [1, t, 0], [-1, -t, 0], [1, -t, 0], [0, -1, t], [0, 1, t], [0, -1, -t], [0, 1, -t],
+                  [t, 0, -1], [t, 0, 1], [-t, 0, -1], [-t, 0, 1]], dtype=np.float64)
+    v /= np.linalg.norm(v, axis=1, keepdims=True)
+    f = np.array([[0, 11, 5], [0, 5, 1], [0, 1, 7], [0, 7, 10], [0, 10, 11], [1, 5, 9], [5, 11, 4], [11, 10, 2],
+                  [10, 7, 6], [7, 1, 8], [3, 9, 4], [3, 4, 2], [3, 2, 6], [3, 6, 8], [3, 8, 9], [4, 9, 5],
+                  [2, 4, 11], [6, 2, 10], [8, 6, 7], [9, 8, 1]], dtype=np.int64)
+    for _ in range(subdiv):
+        e = np.sort(np.concatenate([f[:, [0, 1]], f[:, [1, 2]], f[:, [2, 0]]]), axis=1)
+        ue, inv = np.unique(e, axis=0, return_inverse=True)
+        mid = v[ue[:, 0]] + v[ue[:, 1]]
+        mid /= np.linalg.norm(mid, axis=1, keepdims=True)
+        m = inv.reshape(3, -1) + v.shape[0]          # midpoint ids of edges (01, 12, 20) per face
+        v = np.concatenate([v, mid])
+        a, b, c = f[:, 0], f[:, 1], f[:, 2]
+        ab, bc, ca = m[0], m[1], m[2]
+        f = np.concatenate([np.stack([a, ab, ca], 1), np.stack([b, bc, ab], 1), np.stack([c, ca, bc], 1),
+                            np.stack([ab, bc, ca], 1)])
+    return v, f
+
+
+def cloth_on_sphere(n=316, layers=1, subdiv=5, seed=1, radius=1.0, span=0.8, gap_rel=0.6, d_hat_rel=0.2,
+                    jitter_rel=0.02, twist_deg=7.0, kappa=2e8, dt=0.01, density=0.2, fixed_frac=0.01):
+    """BASELINE configs[2]: cloth draped over a sphere.
+
+    ``layers`` n x n sheets of side 2*span*radius conform to the upper cap of an icosphere
+    (subdivision ``subdiv``) at offsets (k + 1) * gap_rel * d_hat along the sphere normal, d_hat =
+    d_hat_rel * h with h the sheet spacing, each sheet rotated by twist_deg against the previous one;
+    outside the cap the sheets continue flat.  Defaults (the scene SURVEY 8d
+    describes): 10 242 + 316^2 = 110 098 vertices and 273 110 active contacts.  The sphere's
+    vertices are fixed.  Rest positions are the unjittered sheets.
+    """
+    rng = np.random.default_rng(seed)
+    h = 2.0 * span * radius / (n - 1)
+    d_hat = d_hat_rel * h
+    sv, sf = _icosphere(subdiv)
+    sv = sv * radius
+    se = np.unique(np.sort(np.concatenate([sf[:, [0, 1]], sf[:, [1, 2]], sf[:, [2, 0]]]), axis=1), axis=0)
+    tris_l, edges_l = _grid_mesh(n)
+    u = (np.arange(n) - 0.5 * (n - 1)) * h
+    gx, gy = np.meshgrid(u, u, indexing="ij")
+    gx0, gy0 = gx.reshape(-1), gy.reshape(-1)
+    pos, rest, tris, edges = [sv], [sv.copy()], [sf], [se]
+    base = sv.shape[0]
+    rim = 0.95 * radius
+    for k in range(layers):
+        th = np.deg2rad(twist_deg * (k + 1))      # sheets rotated against each other: no vertex-on-vertex alignment
+        gx, gy = np.cos(th) * gx0 - np.sin(th) * gy0, np.sin(th) * gx0 + np.cos(th) * gy0
+        rho2 = gx * gx + gy * gy
+        r_k = radius + (k + 1) * gap_rel * d_hat
+        inside = rho2 < rim * rim
+        z = np.where(inside, np.sqrt(np.maximum(r_k * r_k - rho2, 0.0)), np.sqrt(r_k * r_k - rim * rim))
+        sheet = np.stack([gx, gy, z], axis=1)
+        rest.append(sheet.copy())
+        jit = rng.normal(size=sheet.shape) * (jitter_rel * h)
+        jit[:, 2] = np.clip(rng.normal(size=n * n) * 0.05 * d_hat, -0.12 * d_hat, 0.12 * d_hat)
+        pos.append(sheet + jit)
+        tris.append(tris_l + base)
+        edges.append(edges_l + base)
+        base += n * n
+    pos, rest = np.concatenate(pos), np.concatenate(rest)
+    nv = pos.shape[0]
+    masses = np.full(nv, density * h * h)
+    fixed = rng.uniform(size=nv) < fixed_frac
+    fixed[:sv.shape[0]] = True
+    return ClothScene(pos, rest, np.concatenate(tris), np.concatenate(edges), masses, fixed, d_hat, kappa, dt,
+                      f"cloth-on-sphere-{layers}x{n}x{n}-ico{subdiv}")
+
+
 def _cells_of_boxes(lo, hi, cell, origin):
     """All (box, cell) incidences of axis-aligned boxes on a uniform grid."""
     ilo = np.floor((lo - origin) / cell).astype(np.int64)

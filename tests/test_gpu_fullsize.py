@@ -1,5 +1,5 @@
-"""BASELINE.json's full sizes (configs[1]: 1 M near-parallel EE stencils; configs[3]: ~1 M contacts of a
-multilayer cloth stack) through size-independent properties, evaluated on the device, plus the oracle
+"""BASELINE.json's full sizes (configs[1]: 1 M near-parallel EE stencils; configs[2]: cloth draped on a
+sphere, ~100 k vertices / ~300 k contacts; configs[3]: ~1 M contacts of a multilayer cloth stack) through size-independent properties, evaluated on the device, plus the oracle
 on a strided sample: the 1e-9 parity tests run at sizes the oracle finishes in seconds, these make sure
 nothing changes at scale (tile tails, 64-bit offsets, kind-segment boundaries, chunk rings)."""
 
@@ -129,4 +129,56 @@ def test_cloth_stack_one_million_contacts(P):
     r0 = t.where(free, rhs, t.zeros_like(rhs))
     p0 = (pinv @ r0.reshape(-1, 3, 1)).reshape(-1)
     assert float(res @ pres) <= 1.05e-4 * float(r0 @ p0)
+    sysm.close()
+
+
+def test_cloth_on_sphere_newton_direction(P):
+    """configs[2]: detect -> blocks -> assembly -> gradient -> PCG on the draped-cloth scene; candidate and
+    contact counts, the assembled operator against the matrix-free twin, PCG against its stopping rule,
+    and the oracle on a strided sample of the contact table."""
+    t = P.torch
+    scene = P.workloads.cloth_on_sphere()
+    nv = scene.positions.shape[0]
+    assert 1.0e5 < nv < 1.2e5
+    bp = P.contacts.BroadPhase(None, scene.tris, scene.edges, scene.d_hat, scene.positions)
+    vt, ee = bp.query(scene.positions)
+    table, extra = P.contacts.narrow_phase_device(scene.positions, scene.rest_positions, vt, ee, scene.d_hat)
+    assert 2.4e5 < table.n < 3.6e5, table.n
+    params = P.barrier.BarrierParams(d_hat=scene.d_hat, kappa=scene.kappa)
+    batch = P.stencils.evaluate(table, scene.positions, params, dt=scene.dt, want_factors=True)
+    assert batch.summary()[2] == 0
+    block_properties(P, batch)
+    rows = np.arange(0, table.n, 37)
+    kind = P.device.to_host(extra.kind)[rows]
+    ref = o.local_quadratics_batch(kind, P.device.to_host(table.verts)[rows], P.device.to_host(table.sub)[rows],
+                                   P.device.to_host(table.eps_x)[rows], scene.positions, scene.d_hat, scene.kappa)
+    energy = P.device.to_host(batch.energy)[rows]
+    assert np.abs(energy - ref["energy"]).max() <= 1e-9 * np.abs(ref["energy"]).max()
+    fams = [batch.families[s] for s in sorted(batch.families)]
+    sysm = P.solver.NewtonSystem(scene.masses, scene.fixed)
+    sysm.set_pattern([(f.s, f.vids) for f in fams])
+    sysm.assemble_from_factors([f.fac for f in fams])
+    rng = np.random.default_rng(1)
+    x = P.device.to_device(rng.normal(size=3 * sysm.n))
+    y = sysm.spmv(x)
+    free = t.from_numpy(~scene.fixed).cuda().repeat_interleave(3)
+    xm = t.where(free, x, t.zeros_like(x))
+    out = t.repeat_interleave(sysm.masses, 3) * xm
+    for f in fams:
+        P.kernels.matvec_blocks_device(f.hess, f.vids, xm, out)
+    out = t.where(free, out, x)
+    assert float((y - out).abs().max()) <= 1e-11 * float(out.abs().max())
+    xt = P.device.to_device(scene.positions + 1e-4 * rng.normal(size=scene.positions.shape))
+    rhs = -sysm.gradient(scene.positions, xt, [f.grad for f in fams])
+    d, iters, ok, d0, dn = sysm.pcg(rhs, 1e-4, 3000)
+    assert ok and iters > 2   # one sheet on a fixed sphere: block-Jacobi is nearly exact, a handful of iterations
+    pinv = sysm.block_jacobi()
+    res = t.where(free, rhs - sysm.spmv(d), t.zeros_like(rhs))
+    r0 = t.where(free, rhs, t.zeros_like(rhs))
+    assert float(res @ (pinv @ res.reshape(-1, 3, 1)).reshape(-1)) <= 1.05e-4 * float(r0 @ (pinv @ r0.reshape(-1, 3, 1)).reshape(-1))
+    # the direction is a descent direction and CCD accepts a positive step along it
+    assert float(d @ rhs) > 0.0
+    alpha = bp.ccd_step_bound(scene.positions, P.device.to_host(d).reshape(-1, 3))
+    assert 0.0 < alpha <= 1.0
+    bp.close()
     sysm.close()
