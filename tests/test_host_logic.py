@@ -114,3 +114,23 @@ def test_scene_batch_single_process():
     assert scene_batch.replica_seed(10, 3) == 13
     assert scene_batch.aggregate(5.0, 2.0) == (5.0, 2.0)
     assert scene_batch.throughput(8e6, 2.0, 4) == pytest.approx(1.6e10)
+
+
+def test_cloth_on_sphere_generator():
+    """configs[2] scene at a small size: closed icosphere, seeded, sheets outside the sphere, contacts of
+    several kinds and no penetration (oracle narrow phase on all-pairs candidates)."""
+    from oracle import tetipc_oracle as o
+    from paper_2308_09400_b200 import workloads
+
+    v, f = workloads._icosphere(2)
+    assert v.shape == (162, 3) and f.shape == (320, 3) and np.abs(np.linalg.norm(v, axis=1) - 1.0).max() < 1e-15
+    e = np.sort(np.concatenate([f[:, [0, 1]], f[:, [1, 2]], f[:, [2, 0]]]), axis=1)
+    assert (np.unique(e, axis=0, return_counts=True)[1] == 2).all()          # closed surface
+    a = workloads.cloth_on_sphere(n=36, layers=2, subdiv=2, seed=4)
+    b = workloads.cloth_on_sphere(n=36, layers=2, subdiv=2, seed=4)
+    assert np.array_equal(a.positions, b.positions) and a.positions.shape[0] == 162 + 2 * 36 * 36
+    assert a.fixed[:162].all() and (np.linalg.norm(a.positions[162:], axis=1) > 1.0).all()
+    vt, ee = o.aabb_candidates(a.positions, np.unique(a.tris), a.tris, a.edges, a.d_hat)
+    tab = o.narrow_phase(a.positions, a.rest_positions, vt, ee, a.d_hat)
+    out = o.local_quadratics_batch(tab["kind"], tab["verts"], tab["sub"], tab["eps_x"], a.positions, a.d_hat, a.kappa)
+    assert len(tab["kind"]) > 1000 and len(np.unique(tab["kind"])) >= 4 and not (out["status"] == 2).any()
