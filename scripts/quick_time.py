@@ -1,4 +1,4 @@
-"""Scratch timing of the stencil kernel (NOT bench.py): table built with the oracle on host."""
+"""Scratch timing of the stencil kernel (NOT bench.py): table built by the GPU narrow phase."""
 import json
 import sys
 import time
@@ -8,18 +8,16 @@ import numpy as np
 sys.path.insert(0, ".")
 import torch
 
-from oracle import tetipc_oracle as o
-from paper_2308_09400_b200 import barrier, proximity, stencils, workloads, device, _lib
+from paper_2308_09400_b200 import barrier, contacts, proximity, stencils, workloads, device, _lib
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000
 which = sys.argv[2] if len(sys.argv) > 2 else "c2"
 t0 = time.time()
 qb = workloads.config2_batch(n=n) if which == "c2" else workloads.config1_batch(n_pt=n // 2, n_ee=n // 2)
-tab = o.narrow_phase(qb.positions, qb.rest_positions, qb.vt, qb.ee, qb.d_hat)
-table = proximity.StencilTable(tab["kind"], tab["verts"], tab["sub"], tab["eps_x"])
-print("setup s", time.time() - t0, "rows", len(table), "kinds", np.bincount(tab["kind"], minlength=7).tolist(), flush=True)
+dt, extra = contacts.narrow_phase_device(qb.positions, qb.rest_positions, qb.vt, qb.ee, qb.d_hat, want_origin=False)
+tab = {"kind": device.to_host(extra.kind)}
+print("setup s", time.time() - t0, "rows", dt.n, "kinds", np.diff(dt.kind_off).tolist(), flush=True)
 params = barrier.BarrierParams(d_hat=qb.d_hat, kappa=qb.kappa)
-dt = stencils.DeviceStencilTable.from_host(table)
 pos = device.to_device(qb.positions)
 batch = stencils.evaluate(dt, pos, params)
 torch.cuda.synchronize()
@@ -37,5 +35,5 @@ for label, kw in (("all", {}), ("hess_only", dict(want_energy=False, want_grad=F
     torch.cuda.synchronize()
     ms = ev[0].elapsed_time(ev[1]) / reps
     nbytes = sum(1272 if s == 4 else (740 if s == 3 else 352) for s in proximity.KIND_SIZE[tab["kind"]])
-    print(json.dumps({"case": label, "ms": ms, "stencils_per_s": len(table) / ms * 1e3, "GBps_alg": nbytes / ms / 1e6}), flush=True)
+    print(json.dumps({"case": label, "ms": ms, "stencils_per_s": dt.n / ms * 1e3, "GBps_alg": nbytes / ms / 1e6}), flush=True)
 print("launches", _lib.lib().b200ipc_launch_count())
