@@ -205,7 +205,10 @@ struct ElasticArgs {
 
 constexpr int kEPad = 145;  // odd row stride: thread t writes row t, the copy-out reads consecutive entries
 
-__global__ void __launch_bounds__(kET) elastic_blocks_kernel(const __grid_constant__ ElasticArgs a) {
+#ifndef B200IPC_ELASTIC_MINB
+#define B200IPC_ELASTIC_MINB 1
+#endif
+__global__ void __launch_bounds__(kET, B200IPC_ELASTIC_MINB) elastic_blocks_kernel(const __grid_constant__ ElasticArgs a) {
   extern __shared__ double tile[];  // (kET, kEPad)
   const int64_t tile0 = (int64_t)blockIdx.x * kET;
   const int64_t t = tile0 + threadIdx.x;
