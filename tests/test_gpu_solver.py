@@ -247,3 +247,21 @@ def test_group_blocks_matches_reference_layout(S, scene):
     for (h, v), s in zip(grouped, (2, 3, 4)):
         np.testing.assert_array_equal(v, scene[f"fam{s}_vids"])
         assert block_rel_err(h, scene[f"fam{s}_hess"]) < TOL
+
+
+def test_direct_load_fallback_kernels_agree_with_the_streamed_ones(S, scene, monkeypatch):
+    """B200IPC_SPMV_MODE=legacy selects the direct-load SpMV / PCG kernels (the fallback for arrays that
+    are not 16-byte aligned): same operator, same solve."""
+    rhs = -scene["ref_gradient"]
+    d_s, it_s, ok_s = S.solver.pcg_solve(scene["grouped"], scene["masses"], scene["fixed"], rhs, 1e-12, 5000)
+    monkeypatch.setenv("B200IPC_SPMV_MODE", "legacy")
+    d_l, it_l, ok_l = S.solver.pcg_solve(scene["grouped"], scene["masses"], scene["fixed"], rhs, 1e-12, 5000)
+    assert ok_s and ok_l and abs(it_s - it_l) <= 0.05 * it_l
+    a = scene["ref_dense"]
+    diff = d_s - d_l
+    assert np.sqrt(diff @ a @ diff) <= 1e-5 * np.sqrt(d_l @ a @ d_l)
+    v = scene["v"]
+    mv_l = S.solver.matvec_matrix_free(scene["grouped"], scene["masses"], scene["fixed"], v)
+    monkeypatch.delenv("B200IPC_SPMV_MODE")
+    mv_s = S.solver.matvec_matrix_free(scene["grouped"], scene["masses"], scene["fixed"], v)
+    assert np.abs(mv_l - mv_s).max() <= 1e-12 * np.abs(mv_s).max()
