@@ -200,8 +200,14 @@ struct NumericArgs {
   double* vals;
 };
 
-constexpr int kNumWarps = 8;
-constexpr int kBlocksPerWarp = 8;   // consecutive output blocks per warp (one descriptor prefetch for all)
+#ifndef B200IPC_ASM_BLOCKS_PER_WARP
+#define B200IPC_ASM_BLOCKS_PER_WARP 8
+#endif
+#ifndef B200IPC_ASM_WARPS
+#define B200IPC_ASM_WARPS 8
+#endif
+constexpr int kNumWarps = B200IPC_ASM_WARPS;
+constexpr int kBlocksPerWarp = B200IPC_ASM_BLOCKS_PER_WARP;   // consecutive output blocks per warp (one descriptor prefetch for all)
 
 __device__ __forceinline__ double gather_entry(const NumericArgs& a, uint32_t d, int er, int ec) {
   const uint32_t f = d >> 30;

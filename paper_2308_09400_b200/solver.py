@@ -234,3 +234,17 @@ def pcg_solve(grouped, masses, fixed, rhs, rel_tol, max_iters):
         return device.to_host(d), iters, ok
     finally:
         sysm.close()
+
+
+_STEPPER_NAMES = ("SolverConfig", "StepStats", "SimState", "newton_step", "advance_time_step", "MODE_GIPC",
+                  "MODE_REFERENCE")
+
+
+def __getattr__(name):
+    """The reference keeps the time stepper in the same module (solver.py:32-235, :316-422); here it
+    lives in ``stepper`` and is reachable under the reference's import path as well."""
+    if name in _STEPPER_NAMES:
+        from . import stepper
+
+        return getattr(stepper, name)
+    raise AttributeError(f"module {__name__!r} has no attribute {name!r}")

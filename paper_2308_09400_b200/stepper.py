@@ -1,0 +1,317 @@
+"""Projected-Newton time stepper with every per-iteration stage on the GPU.
+
+Mirror of the reference's ``SolverConfig`` / ``StepStats`` / ``SimState`` / ``newton_step`` /
+``advance_time_step`` (``/root/reference/pkg/src/tetipc/solver.py:32-235, :316-422``): the same
+names, arguments, stopping rules and ``info`` / ``StepStats`` fields.  The state (x, v) and every
+intermediate (contact table, blocks, matrix, gradient, direction) stay in HBM; per Newton iteration the
+host sees a few scalars (contact counts, PCG result, CCD bound, one energy per line-search candidate).
+
+``scene`` is duck-typed on the reference ``Scene`` (mesh.py:76-141): ``positions``,
+``rest_positions``, ``masses``, ``fixed``, ``tets``, ``surf_tris``, ``surf_edges``, ``surf_verts``,
+``gravity``, ``bbox_diagonal`` and, when ``materials`` is per body, ``bodies[i].tets``.
+Only the GIPC mode is provided: the reference-IPC mode (finite-difference blocks + eigendecomposition)
+is the baseline the paper replaces and is not on this path.
+"""
+
+import ctypes as C
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib, contacts, device, elasticity, friction, stencils
+from .barrier import BarrierParams, c_params
+from .solver import NewtonSystem
+
+MODE_GIPC = "gipc"
+MODE_REFERENCE = "reference-ipc"
+
+
+@dataclass
+class SolverConfig:
+    """solver.py:32-51, field for field."""
+
+    dt: float
+    barrier: BarrierParams
+    eps_d: float = 1e-2
+    pcg_rel_tol: float = 1e-4
+    pcg_max_iters: int = 2000
+    newton_max_iters: int = 100
+    friction_mu: float = 0.0
+    friction_eps_v: float = 1e-3
+    mode: str = MODE_GIPC
+    accd_slack: float = 0.9
+    line_search_floor: float = 1e-12
+    mollify: bool = True
+
+    def __post_init__(self):
+        if self.dt <= 0.0 or self.eps_d <= 0.0 or self.pcg_rel_tol <= 0.0:
+            raise ValueError("dt and tolerances must be positive")
+        if self.mode not in (MODE_GIPC, MODE_REFERENCE):
+            raise ValueError(f"unknown mode {self.mode!r}")
+        if self.mode == MODE_REFERENCE:
+            raise NotImplementedError("the reference-IPC baseline mode is not part of the GPU path")
+
+
+@dataclass
+class StepStats:
+    """solver.py:54-64."""
+
+    step: int
+    newton_iters: int
+    pcg_iters: int
+    min_distance: float
+    energy: float
+    alpha_min: float
+    wall_ms: float
+    converged: bool
+    warning: str = ""
+
+
+def _tet_materials(scene, materials, nt):
+    """Per-tet Lame parameters: per-body materials like solver.py:83-97, or one material / a
+    (mu, lam) pair of arrays for scenes without a ``bodies`` list."""
+    mu, lam = np.zeros(nt), np.zeros(nt)
+    if hasattr(materials, "lame_mu"):
+        mu[:], lam[:] = materials.lame_mu, materials.lame_lambda
+    elif isinstance(materials, (list, tuple)) and hasattr(scene, "bodies") and len(materials) == len(scene.bodies):
+        cursor = 0
+        for i, body in enumerate(scene.bodies):
+            k = int(np.asarray(body.tets).reshape(-1, 4).shape[0])
+            if k == 0:
+                continue
+            if materials[i] is None:
+                raise ValueError(f"body {i} has tets but no material")
+            mu[cursor:cursor + k] = materials[i].lame_mu
+            lam[cursor:cursor + k] = materials[i].lame_lambda
+            cursor += k
+    elif isinstance(materials, (list, tuple)) and len(materials) == 2 and not hasattr(materials[0], "lame_mu"):
+        mu[:] = np.asarray(materials[0], dtype=np.float64)
+        lam[:] = np.asarray(materials[1], dtype=np.float64)
+    else:
+        raise ValueError("materials: one per body, a single ElasticMaterial, or (mu, lam) per tet")
+    return mu, lam
+
+
+class SimState:
+    """Device-resident simulation state (solver.py:67-235).  ``x`` and ``v`` are (N,3) device tensors;
+    ``positions()`` / ``velocities()`` give host copies."""
+
+    def __init__(self, scene, config, materials=None):
+        t = device.torch()
+        self.scene = scene
+        self.config = config
+        self.x = device.to_device(np.array(scene.positions, dtype=np.float64))
+        self.v = t.zeros_like(self.x)
+        self.n = int(self.x.shape[0])
+        masses = np.asarray(scene.masses, dtype=np.float64)
+        fixed = np.asarray(scene.fixed, dtype=bool)
+        if np.any(masses[~fixed] <= 0.0):
+            raise ValueError("free vertices need positive mass")
+        self.masses, self.fixed = masses.copy(), fixed.copy()
+        self.l = float(scene.bbox_diagonal)
+        self.step_index = 0
+        self.stats = []
+        self._fixed_dev = device.to_device(fixed.astype(np.uint8)).bool()
+        self._free_mass = device.to_device(np.where(fixed, 0.0, masses))[:, None]
+        self._gravity = device.to_device(np.asarray(scene.gravity, dtype=np.float64).reshape(1, 3))
+        self._rest = device.to_device(np.asarray(scene.rest_positions, dtype=np.float64))
+
+        tets = np.asarray(scene.tets).reshape(-1, 4)
+        self.tet_mesh = None
+        if tets.shape[0]:
+            mu, lam = _tet_materials(scene, materials, tets.shape[0])
+            self.tet_mesh = elasticity.TetMesh(scene.rest_positions, tets, mu, lam)
+
+        surf_verts = getattr(scene, "surf_verts", None)
+        self.broad = contacts.BroadPhase(surf_verts, scene.surf_tris, scene.surf_edges, config.barrier.d_hat,
+                                         np.asarray(scene.positions, dtype=np.float64))
+        self.system = NewtonSystem(masses, fixed)
+        self.friction_state = None
+        self._last_detect = None
+        if config.friction_mu > 0.0:
+            self._refresh_friction(self.x)
+
+    def close(self):
+        self.broad.close()
+        self.system.close()
+
+    def positions(self):
+        return device.to_host(self.x)
+
+    def velocities(self):
+        return device.to_host(self.v)
+
+    # -- contact set (solver.py:112-116) ----------------------------------------------------
+    def detect(self, x):
+        """``DeviceStencilTable`` of every stencil closer than d_hat, in the reference's list order.
+
+        The reference detects at the accepted line-search candidate and again, on the same positions, at
+        the top of the next Newton iteration and at the end of the step (solver.py:324, :343, :400); the
+        last result is kept and returned when the very same, unmodified tensor comes back."""
+        last = self._last_detect
+        if last is not None and last[0] is x and last[1] == x._version:
+            return last[2]
+        promote = self.config.mollify and self.config.mode == MODE_GIPC
+        vt, ee = self.broad.query(x)
+        table, extra = contacts.narrow_phase_device(x, self._rest, vt, ee, self.config.barrier.d_hat,
+                                                    promote_parallel=promote, want_origin=False)
+        table.kind_dev = extra.kind
+        self._last_detect = (x, x._version, table)
+        return table
+
+    # -- energies (solver.py:118-175) --------------------------------------------------------
+    def _inertia_target(self, x0):
+        cfg = self.config
+        x_tilde = x0 + cfg.dt * self.v + cfg.dt ** 2 * self._gravity
+        x_tilde[self._fixed_dev] = x0[self._fixed_dev]
+        return x_tilde
+
+    def _barrier_energy(self, x, table):
+        return stencils.barrier_energy(table, x, self.config.barrier) if table.n else 0.0
+
+    def _friction_energy(self, x, x_start):
+        if self.friction_state is None or self.friction_state.n == 0:
+            return 0.0
+        return friction.evaluate(self.friction_state, x, x_start, want_grad=False, want_hess=False).total_energy()
+
+    def _elastic_energy(self, x):
+        if self.tet_mesh is None:
+            return 0.0
+        energy, _ = self.tet_mesh.evaluate(x, want_grad=False, want_hess=False)
+        return float(energy.sum().item())
+
+    def evaluate_energy(self, x, x_tilde, x_start, stencils=None):
+        """Incremental potential at x; detects contacts unless a table is given."""
+        table = self.detect(x) if stencils is None else stencils
+        dx = x - x_tilde
+        inertia = 0.5 * float((self._free_mass * dx * dx).sum().item())
+        dt2 = self.config.dt ** 2
+        return inertia + dt2 * (self._elastic_energy(x) + self._barrier_energy(x, table)
+                                + self._friction_energy(x, x_start))
+
+    # -- gradient and PSD blocks (solver.py:177-235) -----------------------------------------
+    def assemble_local_quadratics(self, x, x_start, table):
+        """dt^2-scaled families in the reference's block order: elastic, barrier, friction.
+        Returns a list of ``stencils.Family`` (device tensors), at most seven."""
+        dt = self.config.dt
+        fams = []
+        if self.tet_mesh is not None:
+            fams.append(self.tet_mesh.evaluate(x, dt=dt, want_energy=False)[1])
+        if table.n:
+            batch = stencils.evaluate(table, x, self.config.barrier, dt=dt, want_energy=False)
+            fams += [batch.families[s] for s in sorted(batch.families)]
+        if self.friction_state is not None and self.friction_state.n:
+            fb = friction.evaluate(self.friction_state, x, x_start, want_energy=False)
+            fams += [fb.families[s] for s in sorted(fb.families)]
+        return fams
+
+    def gradient(self, x, x_tilde, fams):
+        return self.system.gradient(x, x_tilde, [f.grad for f in fams])
+
+    def _refresh_friction(self, x, table=None):
+        if table is None:
+            table = self.detect(x)
+        cfg = self.config
+        self.friction_state = friction.update_state(table, x, cfg.friction_mu, cfg.friction_eps_v, cfg.dt,
+                                                    params=cfg.barrier)
+
+    def min_distance(self, x, table):
+        """sqrt(min d2) over a contact table (advance_time_step's end-of-step report); NaN when empty."""
+        if table.n == 0:
+            return float("nan")
+        d2 = device.empty((table.n,))
+        prm = c_params(self.config.barrier)
+        null = C.c_void_p()
+        _lib.check(_lib.lib().b200ipc_diagonal_jacobian(
+            prm, self.n, device.ptr(x), table.n, device.ptr(table.kind_dev), device.ptr(table.verts),
+            device.ptr(table.sub), device.ptr(d2), null, null, null, null, null, null, null, null, null,
+            device.stream()), "diagonal_jacobian")
+        return float(np.sqrt(d2.min().item()))
+
+
+def newton_step(state, x, x_tilde, x_start, energy_prev):
+    """One projected-Newton iteration with CCD-bounded backtracking (solver.py:316-362).
+
+    Returns (x_new, energy_new, info); contacts are re-detected at every line-search candidate.
+    """
+    cfg = state.config
+    t = device.torch()
+    table = state.detect(x)
+    fams = state.assemble_local_quadratics(x, x_start, table)
+    sysm = state.system
+    sysm.set_pattern([(f.s, f.vids) for f in fams])
+    sysm.assemble([f.hess for f in fams])
+    grad = state.gradient(x, x_tilde, fams)
+
+    d, pcg_iters, pcg_ok, _, _ = sysm.pcg(-grad, cfg.pcg_rel_tol, cfg.pcg_max_iters)
+    dmat = d.reshape(-1, 3)
+    dmat[state._fixed_dev] = 0.0
+
+    alpha = min(1.0, state.broad.ccd_step_bound(x, dmat, slack=cfg.accd_slack))
+
+    accepted = False
+    x_new, energy_new = x, energy_prev
+    while alpha >= cfg.line_search_floor:
+        x_cand = x + alpha * dmat
+        energy_cand = state.evaluate_energy(x_cand, x_tilde, x_start)
+        if energy_cand <= energy_prev:
+            accepted = True
+            x_new, energy_new = x_cand, energy_cand
+            break
+        alpha *= 0.5
+
+    d_inf = float(t.max(t.abs(dmat)).item()) if dmat.numel() else 0.0
+    info = {
+        "pcg_iters": pcg_iters,
+        "pcg_converged": pcg_ok,
+        "alpha": alpha if accepted else 0.0,
+        "accepted": accepted,
+        "d_inf": d_inf,
+        "n_contacts": table.n,
+    }
+    return x_new, energy_new, info
+
+
+def advance_time_step(state):
+    """One time step: Newton iterations until |d|_inf / (l dt) <= eps_d (solver.py:365-422)."""
+    cfg = state.config
+    t0 = time.perf_counter()
+    x0 = state.x            # iterates are never modified in place, so no copies (and detect's cache applies)
+    x_tilde = state._inertia_target(x0)
+    x = x0
+    energy = state.evaluate_energy(x, x_tilde, x0)
+
+    newton_iters = 0
+    pcg_total = 0
+    alpha_min = 1.0
+    warning = ""
+    converged = False
+    while newton_iters < cfg.newton_max_iters:
+        x, energy, info = newton_step(state, x, x_tilde, x0, energy)
+        pcg_total += info["pcg_iters"]
+        newton_iters += 1
+        if not info["accepted"]:
+            warning = "line-search-collapse"
+            break
+        alpha_min = min(alpha_min, info["alpha"])
+        if info["d_inf"] / (state.l * cfg.dt) <= cfg.eps_d:
+            converged = True
+            break
+    if not converged and not warning:
+        warning = "newton-cap"
+
+    state.v = (x - x0) / cfg.dt
+    state.v[state._fixed_dev] = 0.0
+    state.x = x
+    state.step_index += 1
+
+    end_table = state.detect(x)
+    if cfg.friction_mu > 0.0:
+        state._refresh_friction(x, end_table)
+
+    stats = StepStats(step=state.step_index, newton_iters=newton_iters, pcg_iters=pcg_total,
+                      min_distance=state.min_distance(x, end_table), energy=energy, alpha_min=alpha_min,
+                      wall_ms=(time.perf_counter() - t0) * 1e3, converged=converged, warning=warning)
+    state.stats.append(stats)
+    return stats

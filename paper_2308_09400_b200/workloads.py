@@ -222,6 +222,17 @@ class ClothScene:
     dt: float
     name: str = ""
 
+    def as_scene(self, gravity=(0.0, 0.0, -9.81)):
+        """The reference ``Scene`` fields (mesh.py:76-141) ``stepper.SimState`` reads: a shell-only scene."""
+        from types import SimpleNamespace
+
+        lo, hi = self.positions.min(axis=0), self.positions.max(axis=0)
+        return SimpleNamespace(positions=self.positions, rest_positions=self.rest_positions, masses=self.masses,
+                               fixed=self.fixed, tets=np.zeros((0, 4), dtype=np.int64), surf_tris=self.tris,
+                               surf_edges=self.edges, surf_verts=np.unique(self.tris),
+                               gravity=np.asarray(gravity, dtype=np.float64),
+                               bbox_diagonal=float(np.linalg.norm(hi - lo)))
+
 
 def _grid_mesh(n):
     """n x n vertex grid: (tris (2(n-1)^2,3), edges) in local indices."""

@@ -491,7 +491,76 @@ def golden_elastic():
          hess=hess, hess_raw=hess_raw[::5])
 
 
+def golden_stepper():
+    """Trajectories of the reference's own ``advance_time_step`` on small drop scenes (the bodies of
+    tests/test_solver.py): per-step positions, velocities and StepStats, plus the scene arrays a
+    duck-typed scene needs.  One file per case: stepper_<name>.npz."""
+    import tempfile
+
+    from tetipc.elasticity import ElasticMaterial
+    from tetipc.mesh import compute_lumped_masses, load_obj_surface, load_tet_mesh
+    from tetipc.scenes import box_5tet, flat_tet, floor_quad, write_node_ele, write_obj
+
+    tmp = tempfile.mkdtemp(prefix="golden_stepper_")
+    mat = ElasticMaterial(youngs_E=1e5, poisson_nu=0.4)
+
+    def tet_mesh(name, verts_tets, translate, density=1000.0):
+        base = os.path.join(tmp, name)
+        write_node_ele(base, *verts_tets)
+        mesh = load_tet_mesh(base + ".node", base + ".ele").transformed(translate=translate)
+        mesh.vertex_mass = compute_lumped_masses(mesh, density)
+        return mesh
+
+    def floor(half=1.5):
+        path = os.path.join(tmp, "floor.obj")
+        write_obj(path, *floor_quad(half))
+        return load_obj_surface(path, fixed=True)
+
+    def run(name, bodies, materials, v0, steps, **cfg_kw):
+        scene = Scene.build(bodies)
+        params = rb.BarrierParams(d_hat=5e-3 * scene.bbox_diagonal, kappa=2e8)
+        cfg = rs.SolverConfig(dt=0.01, barrier=params, **cfg_kw)
+        state = rs.SimState(scene, cfg, materials)
+        state.v[:] = v0(scene)
+        xs, vs, stats = [state.x.copy()], [state.v.copy()], []
+        for _ in range(steps):
+            st = rs.advance_time_step(state)
+            xs.append(state.x.copy())
+            vs.append(state.v.copy())
+            stats.append([st.newton_iters, st.pcg_iters, st.min_distance, st.energy, st.alpha_min, float(st.converged)])
+        tet_mu = np.asarray(state.tet_mu)
+        tet_lam = np.asarray(state.tet_lam)
+        print(f"stepper {name}: {scene.positions.shape[0]} verts, {scene.tets.shape[0]} tets, newton iters "
+              f"{[int(s[0]) for s in stats]}, pcg iters {[int(s[1]) for s in stats]}")
+        save("stepper_" + name, positions=scene.positions, rest_positions=scene.rest_positions, masses=scene.masses,
+             fixed=scene.fixed, tets=scene.tets, surf_tris=scene.surf_tris, surf_edges=scene.surf_edges,
+             surf_verts=scene.surf_verts, gravity=scene.gravity, bbox_diagonal=scene.bbox_diagonal, tet_mu=tet_mu,
+             tet_lam=tet_lam, d_hat=params.d_hat, kappa=params.kappa, dt=cfg.dt, friction_mu=cfg.friction_mu,
+             friction_eps_v=cfg.friction_eps_v, v0=vs[0], xs=np.stack(xs), vs=np.stack(vs), stats=np.array(stats))
+
+    def down(vz, vx=0.0):
+        def f(scene):
+            v = np.zeros_like(scene.positions)
+            v[~scene.fixed] = [vx, 0.0, vz]
+            return v
+        return f
+
+    # the reference's drop_state with the initial velocity of test_pcg_vs_dense_per_step_positions
+    run("drop", [tet_mesh("tet", flat_tet(0.5), (0.0, 0.0, 0.004)), floor()], [mat, None], down(-0.3), 6)
+    # a sliding cube with lagged friction
+    run("slide", [tet_mesh("cube", box_5tet(0.4, 0.4, 0.4), (0.0, 0.0, 0.004)), floor()], [mat, None],
+        down(-0.2, 0.5), 6, friction_mu=0.5)
+    # two cubes stacked over the floor: body-body and body-floor contacts in the same system
+    run("stack", [tet_mesh("cube_a", box_5tet(0.4, 0.4, 0.4), (0.0, 0.0, 0.004)),
+                  tet_mesh("cube_b", box_5tet(0.3, 0.3, 0.3), (0.03, 0.02, 0.409)), floor()], [mat, mat, None],
+        down(-0.25), 5)
+    shutil.rmtree(tmp, ignore_errors=True)
+
+
 if __name__ == "__main__":
+    if "--stepper-only" in sys.argv:
+        golden_stepper()
+        sys.exit(0)
     if "--elastic-only" in sys.argv:
         golden_elastic()
         sys.exit(0)
@@ -513,3 +582,4 @@ if __name__ == "__main__":
     golden_ccd()
     golden_friction()
     golden_elastic()
+    golden_stepper()

@@ -134,3 +134,54 @@ def test_cloth_on_sphere_generator():
     tab = o.narrow_phase(a.positions, a.rest_positions, vt, ee, a.d_hat)
     out = o.local_quadratics_batch(tab["kind"], tab["verts"], tab["sub"], tab["eps_x"], a.positions, a.d_hat, a.kappa)
     assert len(tab["kind"]) > 1000 and len(np.unique(tab["kind"])) >= 4 and not (out["status"] == 2).any()
+
+
+def test_stepper_config_and_reexport():
+    """SolverConfig validation like solver.py:46-51; the stepper is reachable under the reference's
+    import path; the baseline mode is refused, not silently substituted."""
+    from paper_2308_09400_b200 import stepper
+
+    params = barrier.BarrierParams(d_hat=1e-2, kappa=1.0)
+    cfg = solver.SolverConfig(dt=0.01, barrier=params)
+    assert (cfg.eps_d, cfg.pcg_rel_tol, cfg.pcg_max_iters, cfg.newton_max_iters) == (1e-2, 1e-4, 2000, 100)
+    assert (cfg.accd_slack, cfg.line_search_floor, cfg.mollify, cfg.mode) == (0.9, 1e-12, True, "gipc")
+    assert solver.SimState is stepper.SimState and solver.advance_time_step is stepper.advance_time_step
+    for bad in (dict(dt=0.0), dict(dt=0.01, eps_d=0.0), dict(dt=0.01, pcg_rel_tol=-1.0)):
+        with pytest.raises(ValueError):
+            stepper.SolverConfig(barrier=params, **bad)
+    with pytest.raises(ValueError):
+        stepper.SolverConfig(dt=0.01, barrier=params, mode="nonsense")
+    with pytest.raises(NotImplementedError):
+        stepper.SolverConfig(dt=0.01, barrier=params, mode="reference-ipc")
+    with pytest.raises(AttributeError):
+        solver.no_such_name
+
+
+def test_stepper_materials_per_body_and_per_tet():
+    from types import SimpleNamespace
+
+    from paper_2308_09400_b200 import elasticity, stepper
+
+    soft, hard = elasticity.ElasticMaterial(1e4, 0.3), elasticity.ElasticMaterial(1e6, 0.45)
+    bodies = [SimpleNamespace(tets=np.zeros((2, 4), int)), SimpleNamespace(tets=np.zeros((0, 4), int)),
+              SimpleNamespace(tets=np.zeros((3, 4), int))]
+    scene = SimpleNamespace(bodies=bodies)
+    mu, lam = stepper._tet_materials(scene, [soft, None, hard], 5)
+    np.testing.assert_array_equal(mu, [soft.lame_mu] * 2 + [hard.lame_mu] * 3)
+    np.testing.assert_array_equal(lam, [soft.lame_lambda] * 2 + [hard.lame_lambda] * 3)
+    with pytest.raises(ValueError):
+        stepper._tet_materials(scene, [None, None, hard], 5)
+    mu, lam = stepper._tet_materials(SimpleNamespace(), soft, 4)
+    assert np.all(mu == soft.lame_mu) and np.all(lam == soft.lame_lambda)
+    mu, lam = stepper._tet_materials(SimpleNamespace(), (np.arange(4.0), 2 * np.arange(4.0)), 4)
+    np.testing.assert_array_equal(lam, 2 * mu)
+    with pytest.raises(ValueError):
+        stepper._tet_materials(SimpleNamespace(), None, 4)
+
+
+def test_cloth_scene_as_scene():
+    cloth = workloads.cloth_stack(layers=2, n=8, seed=3)
+    sc = cloth.as_scene()
+    assert sc.tets.shape == (0, 4) and sc.surf_tris is cloth.tris and sc.surf_edges is cloth.edges
+    np.testing.assert_array_equal(sc.surf_verts, np.arange(cloth.positions.shape[0]))
+    assert sc.bbox_diagonal == pytest.approx(np.linalg.norm(np.ptp(cloth.positions, axis=0)))
