@@ -57,7 +57,8 @@ class BroadPhase:
             pass
 
     def query(self, positions):
-        """positions (N,3) host array or device tensor -> (vt (m,4), ee (k,4)) int32 device tensors."""
+        """positions (N,3) host array or device tensor -> (vt (m,4), ee (k,4)) int32 device tensors.
+        The rows are a deterministic SET in no particular order (the narrow phase sorts its output)."""
         pos = device.to_device(positions, np.float64)
         lo = pos.amin(dim=0).cpu().numpy() - 2.0 * self.cell
         origin = (C.c_double * 3)(*[float(v) for v in lo])
@@ -137,8 +138,8 @@ def accd_step_bound(stencil, positions, directions, slack=0.9, max_iter=512):
 
 
 def sweep_candidates(scene, positions, directions, d_hat):
-    """Twin of proximity.py:388-421: list of (pair_kind, (ids...)) whose swept AABBs overlap (the
-    reference's order: PT candidates by (vertex, triangle), then EE by (edge i, edge j))."""
+    """Twin of proximity.py:388-421: list of (pair_kind, (ids...)) whose swept AABBs overlap: PT
+    candidates, then EE candidates, each sorted by vertex ids (the device list is an unordered set)."""
     from . import kernels
 
     bp = BroadPhase(getattr(scene, "surf_verts", None), scene.surf_tris, scene.surf_edges, d_hat, positions)
@@ -147,6 +148,7 @@ def sweep_candidates(scene, positions, directions, d_hat):
         vt, ee = device.to_host(vt), device.to_host(ee)
     finally:
         bp.close()
+    vt, ee = vt[np.lexsort(vt.T[::-1])], ee[np.lexsort(ee.T[::-1])]
     return ([(kernels.PAIR_PT, tuple(int(v) for v in row)) for row in vt]
             + [(kernels.PAIR_EE, tuple(int(v) for v in row)) for row in ee])
 

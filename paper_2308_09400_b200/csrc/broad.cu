@@ -14,8 +14,12 @@
 //          fp64 box corners, so the candidate SET equals the reference's),
 //        - the reference's incidence filters pass (vertex not a corner of the triangle, :286;
 //          edge index i < j and no shared endpoint, :311-317);
-//      first to count, then -- after a scan -- to write (A, B) as global vertex ids.
-// Output order is deterministic (by A box, probe slot, cell, B box) but irrelevant: the narrow phase sorts.
+//      and appends (A, B) as global vertex ids to a staging list in ONE pass: hits are buffered in
+//      registers and flushed with one atomic per warp; when the list is too small the pass only counts,
+//      the list is regrown with head-room and the pass repeated (first query of a scene, or a contact set
+//      that grew by more than the head-room).
+// The candidate SET is deterministic, its order is not -- and does not matter: the narrow phase sorts by
+// a total order over (kind, vertices, origin query), the CCD filter takes a minimum.
 // The same join with swept boxes (both ends of a step, margin 1e-3 d_hat) is sweep_candidates
 // (proximity.py:388-421), the candidate set of the CCD step filter (accd.cu).
 #include <cub/cub.cuh>
@@ -185,79 +189,121 @@ struct JoinArgs {
   const uint32_t* ids;
   const Box* bbox;          // boxes of the B elements
   const double* ext;        // largest B extent per axis (device, 3)
-  const int64_t* off;       // per (A box, slot) output offset (fill pass)
-  int32_t* cnt;             // per (A box, slot) pair count (count pass)
-  int4* out;                // (pairs, 4) global vertex ids (fill pass)
+  unsigned long long* total;  // pairs found (device counter)
+  int4* out;                // staging list of (pairs, 4) global vertex ids
+  unsigned long long cap;   // its capacity: pairs beyond it are counted, not stored
 };
 
 // EE = false: A = vertex boxes, B = triangles.  EE = true: A = B = inflated edge boxes.
 // One thread per (A box, slot): slot (rx, ry) of kJoinSlots = 3 x 3 walks the cell columns
 // (x0 + rx + 3p, y0 + ry + 3q) of the box's span, so a box covering up to 3 x 3 columns is spread over
 // nine threads (4 - 8 x more threads and correspondingly shorter loops than one thread per box; larger
-// spans just loop).  Counts and offsets are per (box, slot): the output order stays deterministic.
+// spans just loop).  A thread keeps up to kHold hit ids in registers; the warp reserves room for all of
+// them with one atomicAdd when its lanes have finished (a lane whose registers fill up mid-walk flushes
+// with the other lanes in the same state).
 constexpr int kJoinSlots = 9;
+constexpr int kHold = 4;
 
-template <bool EE, bool FILL>
+template <bool EE>
+__device__ __forceinline__ int4 pair_row(const JoinArgs& a, int av0, int av1, int64_t j) {
+  if (EE) return make_int4(av0, av1, a.b_elems[2 * j], a.b_elems[2 * j + 1]);
+  return make_int4(av0, a.b_elems[3 * j], a.b_elems[3 * j + 1], a.b_elems[3 * j + 2]);
+}
+
+template <bool EE>
 __global__ void __launch_bounds__(kBT) join_kernel(const __grid_constant__ JoinArgs a) {
   const int64_t T = (int64_t)blockIdx.x * kBT + threadIdx.x;
-  if (T >= a.na * kJoinSlots) return;
-  const int64_t i = T / kJoinSlots;
-  const int slot = (int)(T - i * kJoinSlots);
-  const int rx = slot / 3, ry = slot - 3 * rx;
-  const Box A = EE ? a.bbox[i] : make_box<0>(a.in, a.a_elems, i);
-  // cells that can hold the lower corner of an overlapping B box: [A.lo - max extent, A.hi]; the extent
-  // is widened by 1e-9 relative so that the roundings of hi - lo and lo - extent cannot lose a cell
-  constexpr double kWiden = 1.000000001;
-  Span s;
-  s.x0 = cell_of(A.lx - kWiden * a.ext[0], a.g.ox, a.g.inv); s.x1 = cell_of(A.hx, a.g.ox, a.g.inv);
-  s.y0 = cell_of(A.ly - kWiden * a.ext[1], a.g.oy, a.g.inv); s.y1 = cell_of(A.hy, a.g.oy, a.g.inv);
-  s.z0 = cell_of(A.lz - kWiden * a.ext[2], a.g.oz, a.g.inv); s.z1 = cell_of(A.hz, a.g.oz, a.g.inv);
-  int av0, av1 = -1;
-  if (EE) {
-    av0 = a.a_elems[2 * i];
-    av1 = a.a_elems[2 * i + 1];
-  } else {
-    av0 = a.a_elems[i];
-  }
+  const bool live = T < a.na * kJoinSlots;
   int32_t n = 0;
-  int64_t o = FILL ? a.off[T] : 0;
-  for (int cx = s.x0 + rx; cx <= s.x1; cx += 3)
-    for (int cy = s.y0 + ry; cy <= s.y1; cy += 3) {
-      // cells (cx, cy, z0..z1) are consecutive keys: one search, one walk
-      const uint64_t k0 = cell_key(cx, cy, s.z0), k1 = cell_key(cx, cy, s.z1);
-      for (int64_t t = lower_bound_u64(a.keys, a.nbins, k0); t < a.nbins; ++t) {
-        const uint64_t key = a.keys[t];
-        if (key > k1) break;
-        const int64_t j = a.ids[t];
-        if (EE && j <= i) continue;  // each unordered pair once, lower edge index first (:310)
-        const Box B = a.bbox[j];
-        if (!(A.lx <= B.hx && B.lx <= A.hx && A.ly <= B.hy && B.ly <= A.hy && A.lz <= B.hz && B.lz <= A.hz)) continue;
-        int4 q;
-        if (EE) {
-          const int b0 = a.b_elems[2 * j], b1 = a.b_elems[2 * j + 1];
-          if (av0 == b0 || av0 == b1 || av1 == b0 || av1 == b1) continue;
-          q = make_int4(av0, av1, b0, b1);
-        } else {
-          const int t0 = a.b_elems[3 * j], t1 = a.b_elems[3 * j + 1], t2 = a.b_elems[3 * j + 2];
-          if (av0 == t0 || av0 == t1 || av0 == t2) continue;
-          q = make_int4(av0, t0, t1, t2);
-        }
-        if (FILL) a.out[o++] = q;
-        else ++n;
-      }
+  int h0 = 0, h1 = 0, h2 = 0, h3 = 0;
+  int av0 = -1, av1 = -1;
+  if (live) {
+    const int64_t i = T / kJoinSlots;
+    const int slot = (int)(T - i * kJoinSlots);
+    const int rx = slot / 3, ry = slot - 3 * rx;
+    const Box A = EE ? a.bbox[i] : make_box<0>(a.in, a.a_elems, i);
+    // cells that can hold the lower corner of an overlapping B box: [A.lo - max extent, A.hi]; the extent
+    // is widened by 1e-9 relative so that the roundings of hi - lo and lo - extent cannot lose a cell
+    constexpr double kWiden = 1.000000001;
+    Span s;
+    s.x0 = cell_of(A.lx - kWiden * a.ext[0], a.g.ox, a.g.inv); s.x1 = cell_of(A.hx, a.g.ox, a.g.inv);
+    s.y0 = cell_of(A.ly - kWiden * a.ext[1], a.g.oy, a.g.inv); s.y1 = cell_of(A.hy, a.g.oy, a.g.inv);
+    s.z0 = cell_of(A.lz - kWiden * a.ext[2], a.g.oz, a.g.inv); s.z1 = cell_of(A.hz, a.g.oz, a.g.inv);
+    if (EE) {
+      av0 = a.a_elems[2 * i];
+      av1 = a.a_elems[2 * i + 1];
+    } else {
+      av0 = a.a_elems[i];
     }
-  if (!FILL) a.cnt[T] = n;
+    for (int cx = s.x0 + rx; cx <= s.x1; cx += 3)
+      for (int cy = s.y0 + ry; cy <= s.y1; cy += 3) {
+        // cells (cx, cy, z0..z1) are consecutive keys: one search, one walk
+        const uint64_t k0 = cell_key(cx, cy, s.z0), k1 = cell_key(cx, cy, s.z1);
+        for (int64_t t = lower_bound_u64(a.keys, a.nbins, k0); t < a.nbins; ++t) {
+          const uint64_t key = a.keys[t];
+          if (key > k1) break;
+          const int64_t j = a.ids[t];
+          if (EE && j <= i) continue;  // each unordered pair once, lower edge index first (:310)
+          const Box B = a.bbox[j];
+          if (!(A.lx <= B.hx && B.lx <= A.hx && A.ly <= B.hy && B.ly <= A.hy && A.lz <= B.hz && B.lz <= A.hz)) continue;
+          if (EE) {
+            const int b0 = a.b_elems[2 * j], b1 = a.b_elems[2 * j + 1];
+            if (av0 == b0 || av0 == b1 || av1 == b0 || av1 == b1) continue;
+          } else {
+            const int t0 = a.b_elems[3 * j], t1 = a.b_elems[3 * j + 1], t2 = a.b_elems[3 * j + 2];
+            if (av0 == t0 || av0 == t1 || av0 == t2) continue;
+          }
+          if (n == kHold) {  // registers full: flush with whichever lanes are here too
+            const unsigned m = __activemask();
+            const int lead = __ffs(m) - 1, rank = __popc(m & ((1u << (threadIdx.x & 31)) - 1));
+            unsigned long long base = 0;
+            if ((int)(threadIdx.x & 31) == lead) base = atomicAdd(a.total, (unsigned long long)kHold * __popc(m));
+            base = __shfl_sync(m, base, lead) + (unsigned long long)kHold * rank;
+            if (base + kHold <= a.cap) {
+              a.out[base] = pair_row<EE>(a, av0, av1, h0);
+              a.out[base + 1] = pair_row<EE>(a, av0, av1, h1);
+              a.out[base + 2] = pair_row<EE>(a, av0, av1, h2);
+              a.out[base + 3] = pair_row<EE>(a, av0, av1, h3);
+            }
+            n = 0;
+          }
+          if (n == 0) h0 = (int)j;
+          else if (n == 1) h1 = (int)j;
+          else if (n == 2) h2 = (int)j;
+          else h3 = (int)j;
+          ++n;
+        }
+      }
+  }
+  // the whole warp is here: exclusive prefix of the held counts, one reservation per warp
+  const int lane = threadIdx.x & 31;
+  int incl = n;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const int warp_total = __shfl_sync(0xffffffffu, incl, 31);
+  if (warp_total == 0) return;
+  unsigned long long base = 0;
+  if (lane == 0) base = atomicAdd(a.total, (unsigned long long)warp_total);
+  base = __shfl_sync(0xffffffffu, base, 0) + (unsigned long long)(incl - n);
+  if (base + n <= a.cap) {
+    if (n > 0) a.out[base] = pair_row<EE>(a, av0, av1, h0);
+    if (n > 1) a.out[base + 1] = pair_row<EE>(a, av0, av1, h1);
+    if (n > 2) a.out[base + 2] = pair_row<EE>(a, av0, av1, h2);
+    if (n > 3) a.out[base + 3] = pair_row<EE>(a, av0, av1, h3);
+  }
 }
 
 }  // namespace b200ipc
 
 struct b200ipc_broad {
-  b200ipc::BroadBuf<int32_t> cnt;
-  b200ipc::BroadBuf<int64_t> off_vt, off_ee;
+  b200ipc::BroadBuf<int4> stage_vt, stage_ee;            // candidate lists of the last query
+  b200ipc::BroadBuf<unsigned long long> counters;        // [0] point-triangle, [1] edge-edge pairs found
   b200ipc::BroadBuf<uint64_t> keys_a, keys_t, keys_e;   // scratch, sorted triangle bins, sorted edge bins
   b200ipc::BroadBuf<uint32_t> ids_a, ids_t, ids_e;
   b200ipc::BroadBuf<uint8_t> temp;
-  b200ipc::BroadBuf<int64_t> totals;
   b200ipc::BroadBuf<b200ipc::Box> box_t, box_e;
   b200ipc::BroadBuf<double> ext;   // [0..2] triangles, [3..5] edges: largest box extent per axis
   // state between count and fill
@@ -282,19 +328,6 @@ using namespace b200ipc;
   } while (0)
 
 static inline unsigned bblocks(int64_t n) { return (unsigned)((n + kBT - 1) / kBT); }
-
-// exclusive scan of int32 counts into int64 offsets (n + 1 entries: the last is the total)
-static int scan_counts(b200ipc_broad* h, const int32_t* cnt, int64_t* off, int64_t n, int64_t* total, cudaStream_t st) {
-  size_t tb = 0;
-  // scan n + 1 items (the extra trailing count is zeroed by the caller) so off[n] is the total
-  CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, off, (int)(n + 1), st));
-  CK(h->temp.reserve(tb));
-  CK(cub::DeviceScan::ExclusiveSum(h->temp.ptr, tb, cnt, off, (int)(n + 1), st));
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  CK(cudaMemcpyAsync(total, off + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  return 0;
-}
 
 // File every B box under its home cell (sorted keys / ids) and reduce the largest extent per axis.
 static int bin_boxes(b200ipc_broad* h, const Box* box, int64_t n, BroadBuf<uint64_t>& keys, BroadBuf<uint32_t>& ids,
@@ -321,10 +354,10 @@ extern "C" int b200ipc_broad_create(b200ipc_broad** out) {
 
 extern "C" int b200ipc_broad_destroy(b200ipc_broad* h) {
   if (!h) return 0;
-  h->cnt.release(); h->off_vt.release(); h->off_ee.release();
+  h->stage_vt.release(); h->stage_ee.release(); h->counters.release();
   h->keys_a.release(); h->keys_t.release(); h->keys_e.release();
   h->ids_a.release(); h->ids_t.release(); h->ids_e.release();
-  h->temp.release(); h->totals.release(); h->box_t.release(); h->box_e.release(); h->ext.release();
+  h->temp.release(); h->box_t.release(); h->box_e.release(); h->ext.release();
   delete h;
   return 0;
 }
@@ -345,38 +378,49 @@ static int broad_count(b200ipc_broad* h, int64_t nverts, const Boxes& in, int64_
   h->n_vt = h->n_ee = 0;
   CK(h->ext.reserve(6));
 
-  // ---- point-triangle: triangles binned, vertex boxes probe ----------------------------------------
-  if (n_sv && n_tri) {
+  // boxes and bins of both joins first, then the two passes, then ONE synchronisation for both counts
+  const bool do_vt = n_sv && n_tri, do_ee = n_edge > 1;
+  CK(h->counters.reserve(2));
+  if (do_vt) {
     CK(h->box_t.reserve(n_tri));
     make_boxes_kernel<1><<<bblocks(n_tri), kBT, 0, st>>>(in, tris, n_tri, h->box_t.ptr);
     RC(post_launch());
     RC(bin_boxes(h, h->box_t.ptr, n_tri, h->keys_t, h->ids_t, h->ext.ptr, st));
-    const int64_t ns = n_sv * kJoinSlots;
-    CK(h->cnt.reserve(ns + 1));
-    CK(h->off_vt.reserve(ns + 1));
-    CK(cudaMemsetAsync(h->cnt.ptr + ns, 0, sizeof(int32_t), st));
-    JoinArgs a{in, surf_verts, tris, n_sv, n_tri, h->grid, h->keys_t.ptr, h->ids_t.ptr, h->box_t.ptr, h->ext.ptr, nullptr,
-               h->cnt.ptr, nullptr};
-    join_kernel<false, false><<<bblocks(ns), kBT, 0, st>>>(a);
-    RC(post_launch());
-    RC(scan_counts(h, h->cnt.ptr, h->off_vt.ptr, ns, &h->n_vt, st));
   }
-  // ---- edge-edge: edges binned, the same boxes probe --------------------------------------------------
-  if (n_edge > 1) {
+  if (do_ee) {
     CK(h->box_e.reserve(n_edge));
     make_boxes_kernel<2><<<bblocks(n_edge), kBT, 0, st>>>(in, edges, n_edge, h->box_e.ptr);
     RC(post_launch());
     RC(bin_boxes(h, h->box_e.ptr, n_edge, h->keys_e, h->ids_e, h->ext.ptr + 3, st));
-    const int64_t ns = n_edge * kJoinSlots;
-    CK(h->cnt.reserve(ns + 1));
-    CK(h->off_ee.reserve(ns + 1));
-    CK(cudaMemsetAsync(h->cnt.ptr + ns, 0, sizeof(int32_t), st));
-    JoinArgs a{in, edges, edges, n_edge, n_edge, h->grid, h->keys_e.ptr, h->ids_e.ptr, h->box_e.ptr, h->ext.ptr + 3, nullptr,
-               h->cnt.ptr, nullptr};
-    join_kernel<true, false><<<bblocks(ns), kBT, 0, st>>>(a);
-    RC(post_launch());
-    RC(scan_counts(h, h->cnt.ptr, h->off_ee.ptr, ns, &h->n_ee, st));
   }
+  bool run_vt = do_vt, run_ee = do_ee;
+  for (int attempt = 0; attempt < 2 && (run_vt || run_ee); ++attempt) {
+    if (run_vt) {
+      CK(cudaMemsetAsync(h->counters.ptr, 0, sizeof(unsigned long long), st));
+      JoinArgs a{in, surf_verts, tris, n_sv, n_tri, h->grid, h->keys_t.ptr, h->ids_t.ptr, h->box_t.ptr, h->ext.ptr,
+                 h->counters.ptr, h->stage_vt.ptr, (unsigned long long)h->stage_vt.cap};
+      join_kernel<false><<<bblocks(n_sv * kJoinSlots), kBT, 0, st>>>(a);
+      RC(post_launch());
+    }
+    if (run_ee) {
+      CK(cudaMemsetAsync(h->counters.ptr + 1, 0, sizeof(unsigned long long), st));
+      JoinArgs a{in, edges, edges, n_edge, n_edge, h->grid, h->keys_e.ptr, h->ids_e.ptr, h->box_e.ptr, h->ext.ptr + 3,
+                 h->counters.ptr + 1, h->stage_ee.ptr, (unsigned long long)h->stage_ee.cap};
+      join_kernel<true><<<bblocks(n_edge * kJoinSlots), kBT, 0, st>>>(a);
+      RC(post_launch());
+    }
+    unsigned long long found[2] = {0, 0};
+    CK(cudaMemcpyAsync(found, h->counters.ptr, sizeof(found), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (do_vt) h->n_vt = (int64_t)found[0];
+    if (do_ee) h->n_ee = (int64_t)found[1];
+    // a list that was too small has only been counted: regrow it (with head-room) and repeat that pass
+    run_vt = do_vt && found[0] > h->stage_vt.cap;
+    run_ee = do_ee && found[1] > h->stage_ee.cap;
+    if (run_vt) CK(h->stage_vt.reserve(found[0] + found[0] / 4));
+    if (run_ee) CK(h->stage_ee.reserve(found[1] + found[1] / 4));
+  }
+  if (run_vt || run_ee) return B200IPC_ESTATE;  // the same pass cannot find more pairs the second time
   *n_vt = h->n_vt;
   *n_ee = h->n_ee;
   h->counted = true;
@@ -407,17 +451,7 @@ extern "C" int b200ipc_broad_phase_fill(b200ipc_broad* h, int32_t* vt, int32_t* 
   if ((h->n_vt && !vt) || (h->n_ee && !ee)) return B200IPC_EINVAL;
   if (((uintptr_t)vt | (uintptr_t)ee) & 15) return B200IPC_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
-  if (h->n_vt) {
-    JoinArgs a{h->in, h->surf_verts, h->tris, h->n_sv, h->n_tri, h->grid, h->keys_t.ptr, h->ids_t.ptr, h->box_t.ptr, h->ext.ptr,
-               h->off_vt.ptr, nullptr, reinterpret_cast<int4*>(vt)};
-    join_kernel<false, true><<<bblocks(h->n_sv * kJoinSlots), kBT, 0, st>>>(a);
-    RC(post_launch());
-  }
-  if (h->n_ee) {
-    JoinArgs a{h->in, h->edges, h->edges, h->n_edge, h->n_edge, h->grid, h->keys_e.ptr, h->ids_e.ptr, h->box_e.ptr, h->ext.ptr + 3,
-               h->off_ee.ptr, nullptr, reinterpret_cast<int4*>(ee)};
-    join_kernel<true, true><<<bblocks(h->n_edge * kJoinSlots), kBT, 0, st>>>(a);
-    RC(post_launch());
-  }
+  if (h->n_vt) CK(cudaMemcpyAsync(vt, h->stage_vt.ptr, (size_t)h->n_vt * sizeof(int4), cudaMemcpyDeviceToDevice, st));
+  if (h->n_ee) CK(cudaMemcpyAsync(ee, h->stage_ee.ptr, (size_t)h->n_ee * sizeof(int4), cudaMemcpyDeviceToDevice, st));
   return 0;
 }
