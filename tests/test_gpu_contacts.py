@@ -114,6 +114,33 @@ def test_gpu_broad_phase_equals_reference_aabb_candidates(Cn, layers, n, seed):
     assert len(ref_vt) > 0 and (layers == 1 or len(ref_ee) > 100)
 
 
+def test_gpu_broad_phase_list_regrows_and_shrinks(Cn):
+    """The appending join keeps its candidate list between queries: a sparse pose first (short list), then
+    a pose with many times more candidates (the pass only counts, the list is regrown, the pass repeats),
+    then the sparse pose again (long list, few rows) -- every answer is the reference's candidate set, and
+    sheets with many hits per probe (more than the four a thread holds in registers) flush correctly."""
+    from paper_2308_09400_b200 import device
+
+    cloth = Cn.workloads.cloth_stack(layers=4, n=12, seed=11)
+    surf = np.unique(cloth.tris)
+    sparse = cloth.positions.copy()
+    sparse[:, 2] *= 40.0                      # sheets far apart: only in-sheet neighbours overlap
+    dense = cloth.positions.copy()
+    dense[:, 2] *= 0.05                       # sheets almost coincident
+    # a d_hat of several cell widths makes every box overlap dozens of others
+    d_hat = 3.0 * cloth.d_hat
+    bp = Cn.contacts.BroadPhase(surf, cloth.tris, cloth.edges, d_hat, cloth.positions)
+    sizes = []
+    for x in (sparse, dense, sparse, dense):
+        vt, ee = bp.query(device.to_device(x))
+        ref_vt, ref_ee = o.aabb_candidates(x, surf, cloth.tris, cloth.edges, d_hat)
+        np.testing.assert_array_equal(_rows(device.to_host(vt)), _rows(ref_vt))
+        np.testing.assert_array_equal(_rows(device.to_host(ee)), _rows(ref_ee))
+        sizes.append(len(ref_ee))
+    bp.close()
+    assert sizes[1] > 3 * sizes[0] and sizes[1] > 9 * 4 * len(cloth.edges)   # > 4 hits per (box, slot) on average
+
+
 def test_gpu_broad_phase_moving_scene_and_find_contact_pairs(Cn):
     """One handle, several detects (positions change); find_contact_pairs end to end on the GPU."""
     from types import SimpleNamespace
