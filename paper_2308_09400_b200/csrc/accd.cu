@@ -44,8 +44,12 @@ __device__ __forceinline__ double pair_dist2(const V3 (&x)[4], int pair_kind) {
 
 // Returns the step fraction; *bad = true when the initial distance is not positive (the reference
 // raises ValueError there, _core.pyx:307-308).
+//
+// `bound` (step filter only): the running minimum over all pairs.  t only grows along the iteration and
+// the result is >= the current t, so a pair whose t has reached the running minimum cannot lower it and
+// stops (returning 1); the minimum itself -- the only thing the filter reports -- is unchanged, bit for bit.
 __device__ __forceinline__ double accd_one(const V3 (&x0)[4], const V3 (&dx)[4], int s, int pair_kind, double slack,
-                                           int max_iter, bool* bad) {
+                                           int max_iter, bool* bad, const unsigned long long* bound = nullptr) {
   *bad = false;
   V3 mean = vzero();
   for (int v = 0; v < s; ++v) mean = mean + dx[v];
@@ -82,6 +86,9 @@ __device__ __forceinline__ double accd_one(const V3 (&x0)[4], const V3 (&dx)[4],
     if (t + step >= 1.0) return 1.0;
     t += step;
     if (step < 1e-14) break;
+    if (bound && (it & 3) == 3 &&
+        t >= __longlong_as_double((long long)*reinterpret_cast<const volatile unsigned long long*>(bound)))
+      return 1.0;
   }
   return t;
 }
@@ -121,20 +128,19 @@ __global__ void __launch_bounds__(kCT) accd_kernel(const __grid_constant__ AccdA
       x0[k] = on ? load3(a.positions, v[k]) : vzero();
       dx[k] = on ? load3(a.directions, v[k]) : vzero();
     }
-    t = accd_one(x0, dx, s, kind, a.slack, a.max_iter, &bad);
+    t = accd_one(x0, dx, s, kind, a.slack, a.max_iter, &bad, a.step ? nullptr : a.alpha_bits);
     if (a.step) a.step[i] = t;
     if (a.status) a.status[i] = bad ? 2 : 0;
+    // non-negative doubles order like their bit patterns; a bad pair does not take part in the min.
+    // Published per lane as soon as it is known (and only when it lowers the minimum), so that the
+    // pairs still iterating can stop against it.
+    if (a.alpha_bits && !bad && t < 1.0 &&
+        t < __longlong_as_double((long long)*reinterpret_cast<const volatile unsigned long long*>(a.alpha_bits)))
+      atomicMin(a.alpha_bits, (unsigned long long)__double_as_longlong(t));
   }
-  if (a.alpha_bits) {
-    // non-negative doubles order like their bit patterns; a bad pair does not take part in the min
-    double m = bad ? 1.0 : t;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = fmin(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (a.alpha_bits && a.n_invalid) {
     const unsigned nbad = __popc(__ballot_sync(0xffffffffu, bad));
-    if ((threadIdx.x & 31) == 0) {
-      if (m < 1.0) atomicMin(a.alpha_bits, (unsigned long long)__double_as_longlong(m));
-      if (nbad && a.n_invalid) atomicAdd(a.n_invalid, (unsigned long long)nbad);
-    }
+    if ((threadIdx.x & 31) == 0 && nbad) atomicAdd(a.n_invalid, (unsigned long long)nbad);
   }
 }
 
