@@ -180,6 +180,11 @@ int b200ipc_reduce_energy(int64_t n, const double* energy, const uint8_t* status
 typedef struct b200ipc_broad b200ipc_broad;
 int b200ipc_broad_create(b200ipc_broad** out);
 int b200ipc_broad_destroy(b200ipc_broad* h);
+/* Optional speed hint for the next queries: the scene spans at most nx x ny x nz grid cells from `origin`
+ * (<= 0: the default 2^21 per axis).  Cell keys then take ceil(log2) bits per axis and the binning sort
+ * runs 3 radix passes instead of 8.  Coordinates beyond the hinted span fall into the boundary cells:
+ * slower there, the candidate set is unchanged. */
+int b200ipc_broad_set_grid_cells(b200ipc_broad* h, int32_t nx, int32_t ny, int32_t nz);
 int b200ipc_broad_phase_count(b200ipc_broad* h, int64_t nverts, const double* positions,
                               int64_t n_sv, const int32_t* surf_verts, int64_t n_tri, const int32_t* tris,
                               int64_t n_edge, const int32_t* edges, double d_hat, double cell,

@@ -56,12 +56,21 @@ class BroadPhase:
         except Exception:  # interpreter shutdown: module globals may already be gone
             pass
 
+    def _grid(self, span, margin):
+        """Grid origin (two cells below the lowest coordinate) and the cell-count hint for the key width."""
+        lo = span[0] - 2.0 * self.cell - margin
+        cells = np.ceil((span[1] - lo + margin + 2.0 * self.cell) / self.cell).astype(np.int64) + 1
+        cells = np.minimum(np.maximum(cells, 1), 1 << 21)
+        _lib.check(_lib.lib().b200ipc_broad_set_grid_cells(self._h, int(cells[0]), int(cells[1]), int(cells[2])),
+                   "broad_set_grid_cells")
+        return (C.c_double * 3)(*[float(v) for v in lo])
+
     def query(self, positions):
         """positions (N,3) host array or device tensor -> (vt (m,4), ee (k,4)) int32 device tensors.
         The rows are a deterministic SET in no particular order (the narrow phase sorts its output)."""
         pos = device.to_device(positions, np.float64)
-        lo = pos.amin(dim=0).cpu().numpy() - 2.0 * self.cell
-        origin = (C.c_double * 3)(*[float(v) for v in lo])
+        t = device.torch()
+        origin = self._grid(t.stack(t.aminmax(pos, dim=0)).cpu().numpy(), 0.0)
         n_vt, n_ee = C.c_int64(0), C.c_int64(0)
         L = _lib.lib()
         _lib.check(L.b200ipc_broad_phase_count(
@@ -82,8 +91,9 @@ class BroadPhase:
         dirs = device.to_device(directions, np.float64)
         margin = 1e-3 * self.d_hat if margin is None else float(margin)
         t = device.torch()
-        lo = t.minimum(pos, pos + dirs).amin(dim=0).cpu().numpy() - 2.0 * self.cell - margin
-        origin = (C.c_double * 3)(*[float(v) for v in lo])
+        end = pos + dirs
+        span = t.stack([t.minimum(pos, end).amin(dim=0), t.maximum(pos, end).amax(dim=0)]).cpu().numpy()
+        origin = self._grid(span, margin)
         n_vt, n_ee = C.c_int64(0), C.c_int64(0)
         L = _lib.lib()
         _lib.check(L.b200ipc_sweep_candidates_count(

@@ -55,18 +55,20 @@ struct BroadBuf {
 struct Grid {
   double ox, oy, oz;  // origin
   double inv;         // 1 / cell
+  int mx, my, mz;     // largest cell index per axis (coordinates beyond are clamped: cells merge, still exact)
+  int sy, sx;         // key = cx << sx | cy << sy | cz: as few key bits as the grid needs (fewer sort passes)
 };
 
 struct __align__(16) Box {
   double lx, ly, lz, hx, hy, hz;
 };
 
-__device__ __forceinline__ int cell_of(double x, double o, double inv) {
+__device__ __forceinline__ int cell_of(double x, double o, double inv, int maxc) {
   const double c = floor((x - o) * inv);
-  return c < 0.0 ? 0 : (c > 2097151.0 ? 2097151 : (int)c);  // 21 bits per axis
+  return c < 0.0 ? 0 : (c > (double)maxc ? maxc : (int)c);
 }
-__device__ __forceinline__ uint64_t cell_key(int cx, int cy, int cz) {
-  return ((uint64_t)cx << 42) | ((uint64_t)cy << 21) | (uint64_t)cz;
+__device__ __forceinline__ uint64_t cell_key(const Grid& g, int cx, int cy, int cz) {
+  return ((uint64_t)cx << g.sx) | ((uint64_t)cy << g.sy) | (uint64_t)cz;
 }
 __device__ __forceinline__ void ld3(const double* p, int v, double& x, double& y, double& z) {
   x = p[3ll * v];
@@ -129,8 +131,8 @@ struct Span {
 };
 __device__ __forceinline__ Span span_of(const Box& b, const Grid& g) {
   Span s;
-  s.x0 = cell_of(b.lx, g.ox, g.inv); s.y0 = cell_of(b.ly, g.oy, g.inv); s.z0 = cell_of(b.lz, g.oz, g.inv);
-  s.x1 = cell_of(b.hx, g.ox, g.inv); s.y1 = cell_of(b.hy, g.oy, g.inv); s.z1 = cell_of(b.hz, g.oz, g.inv);
+  s.x0 = cell_of(b.lx, g.ox, g.inv, g.mx); s.y0 = cell_of(b.ly, g.oy, g.inv, g.my); s.z0 = cell_of(b.lz, g.oz, g.inv, g.mz);
+  s.x1 = cell_of(b.hx, g.ox, g.inv, g.mx); s.y1 = cell_of(b.hy, g.oy, g.inv, g.my); s.z1 = cell_of(b.hz, g.oz, g.inv, g.mz);
   return s;
 }
 
@@ -152,7 +154,7 @@ __global__ void __launch_bounds__(kBT) home_cell_kernel(const Box* __restrict__ 
   double ex = 0.0, ey = 0.0, ez = 0.0;
   if (i < n) {
     const Box b = box[i];
-    keys[i] = cell_key(cell_of(b.lx, g.ox, g.inv), cell_of(b.ly, g.oy, g.inv), cell_of(b.lz, g.oz, g.inv));
+    keys[i] = cell_key(g, cell_of(b.lx, g.ox, g.inv, g.mx), cell_of(b.ly, g.oy, g.inv, g.my), cell_of(b.lz, g.oz, g.inv, g.mz));
     ids[i] = (uint32_t)i;
     ex = b.hx - b.lx; ey = b.hy - b.ly; ez = b.hz - b.lz;
   }
@@ -226,9 +228,9 @@ __global__ void __launch_bounds__(kBT) join_kernel(const __grid_constant__ JoinA
     // is widened by 1e-9 relative so that the roundings of hi - lo and lo - extent cannot lose a cell
     constexpr double kWiden = 1.000000001;
     Span s;
-    s.x0 = cell_of(A.lx - kWiden * a.ext[0], a.g.ox, a.g.inv); s.x1 = cell_of(A.hx, a.g.ox, a.g.inv);
-    s.y0 = cell_of(A.ly - kWiden * a.ext[1], a.g.oy, a.g.inv); s.y1 = cell_of(A.hy, a.g.oy, a.g.inv);
-    s.z0 = cell_of(A.lz - kWiden * a.ext[2], a.g.oz, a.g.inv); s.z1 = cell_of(A.hz, a.g.oz, a.g.inv);
+    s.x0 = cell_of(A.lx - kWiden * a.ext[0], a.g.ox, a.g.inv, a.g.mx); s.x1 = cell_of(A.hx, a.g.ox, a.g.inv, a.g.mx);
+    s.y0 = cell_of(A.ly - kWiden * a.ext[1], a.g.oy, a.g.inv, a.g.my); s.y1 = cell_of(A.hy, a.g.oy, a.g.inv, a.g.my);
+    s.z0 = cell_of(A.lz - kWiden * a.ext[2], a.g.oz, a.g.inv, a.g.mz); s.z1 = cell_of(A.hz, a.g.oz, a.g.inv, a.g.mz);
     if (EE) {
       av0 = a.a_elems[2 * i];
       av1 = a.a_elems[2 * i + 1];
@@ -238,7 +240,7 @@ __global__ void __launch_bounds__(kBT) join_kernel(const __grid_constant__ JoinA
     for (int cx = s.x0 + rx; cx <= s.x1; cx += 3)
       for (int cy = s.y0 + ry; cy <= s.y1; cy += 3) {
         // cells (cx, cy, z0..z1) are consecutive keys: one search, one walk
-        const uint64_t k0 = cell_key(cx, cy, s.z0), k1 = cell_key(cx, cy, s.z1);
+        const uint64_t k0 = cell_key(a.g, cx, cy, s.z0), k1 = cell_key(a.g, cx, cy, s.z1);
         for (int64_t t = lower_bound_u64(a.keys, a.nbins, k0); t < a.nbins; ++t) {
           const uint64_t key = a.keys[t];
           if (key > k1) break;
@@ -312,6 +314,8 @@ struct b200ipc_broad {
   b200ipc::Boxes in{};
   const int32_t *surf_verts = nullptr, *tris = nullptr, *edges = nullptr;
   b200ipc::Grid grid{};
+  int32_t cells[3] = {1 << 21, 1 << 21, 1 << 21};   // b200ipc_broad_set_grid_cells
+  int key_bits = 63;
 };
 
 using namespace b200ipc;
@@ -339,9 +343,9 @@ static int bin_boxes(b200ipc_broad* h, const Box* box, int64_t n, BroadBuf<uint6
                                                reinterpret_cast<unsigned long long*>(ext));
   RC(post_launch());
   size_t tb = 0;
-  CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, h->keys_a.ptr, keys.ptr, h->ids_a.ptr, ids.ptr, (int)n, 0, 63, st));
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, h->keys_a.ptr, keys.ptr, h->ids_a.ptr, ids.ptr, (int)n, 0, h->key_bits, st));
   CK(h->temp.reserve(tb));
-  CK(cub::DeviceRadixSort::SortPairs(h->temp.ptr, tb, h->keys_a.ptr, keys.ptr, h->ids_a.ptr, ids.ptr, (int)n, 0, 63, st));
+  CK(cub::DeviceRadixSort::SortPairs(h->temp.ptr, tb, h->keys_a.ptr, keys.ptr, h->ids_a.ptr, ids.ptr, (int)n, 0, h->key_bits, st));
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return 0;
 }
@@ -362,6 +366,13 @@ extern "C" int b200ipc_broad_destroy(b200ipc_broad* h) {
   return 0;
 }
 
+extern "C" int b200ipc_broad_set_grid_cells(b200ipc_broad* h, int32_t nx, int32_t ny, int32_t nz) {
+  if (!h) return B200IPC_EINVAL;
+  const int32_t want[3] = {nx, ny, nz};
+  for (int k = 0; k < 3; ++k) h->cells[k] = want[k] <= 0 ? (1 << 21) : (want[k] > (1 << 21) ? (1 << 21) : want[k]);
+  return 0;
+}
+
 static int broad_count(b200ipc_broad* h, int64_t nverts, const Boxes& in, int64_t n_sv, const int32_t* surf_verts,
                        int64_t n_tri, const int32_t* tris, int64_t n_edge, const int32_t* edges, double cell,
                        const double* origin, int64_t* n_vt, int64_t* n_ee, void* stream) {
@@ -374,7 +385,14 @@ static int broad_count(b200ipc_broad* h, int64_t nverts, const Boxes& in, int64_
   h->counted = false;
   h->nverts = nverts; h->in = in; h->n_sv = n_sv; h->surf_verts = surf_verts; h->n_tri = n_tri; h->tris = tris;
   h->n_edge = n_edge; h->edges = edges;
-  h->grid = Grid{origin[0], origin[1], origin[2], 1.0 / cell};
+  int nbits[3];
+  for (int k = 0; k < 3; ++k) {
+    nbits[k] = 1;
+    while ((1 << nbits[k]) < h->cells[k]) ++nbits[k];
+  }
+  h->grid = Grid{origin[0], origin[1], origin[2], 1.0 / cell, h->cells[0] - 1, h->cells[1] - 1, h->cells[2] - 1,
+                 nbits[2], nbits[1] + nbits[2]};
+  h->key_bits = nbits[0] + nbits[1] + nbits[2];
   h->n_vt = h->n_ee = 0;
   CK(h->ext.reserve(6));
 

@@ -50,6 +50,21 @@ def test_library_exports_every_declared_symbol():
     assert handle.b200ipc_launch_count() >= 0
 
 
+def test_broad_phase_handle_and_grid_hint_without_a_device():
+    """Handle life cycle and the grid-cell hint are host-only calls: valid handle -> 0, NULL -> EINVAL."""
+    import ctypes as C
+
+    from paper_2308_09400_b200 import _lib
+
+    L = _lib.lib()
+    h = C.c_void_p()
+    assert L.b200ipc_broad_create(C.byref(h)) == 0 and h
+    assert L.b200ipc_broad_set_grid_cells(h, 140, 140, 6) == 0
+    assert L.b200ipc_broad_set_grid_cells(h, 0, -5, 1 << 30) == 0      # out-of-range hints fall back / clamp
+    assert L.b200ipc_broad_set_grid_cells(None, 1, 1, 1) != 0
+    assert L.b200ipc_broad_destroy(h) == 0
+
+
 def test_struct_layouts_match_header():
     import ctypes as C
 

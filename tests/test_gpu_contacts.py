@@ -137,6 +137,21 @@ def test_gpu_broad_phase_list_regrows_and_shrinks(Cn):
         np.testing.assert_array_equal(_rows(device.to_host(vt)), _rows(ref_vt))
         np.testing.assert_array_equal(_rows(device.to_host(ee)), _rows(ref_ee))
         sizes.append(len(ref_ee))
+    # a cell-count hint far too small for the scene (coordinates clamp into the boundary cells, which
+    # merge): slower, same candidate set
+    from paper_2308_09400_b200 import _lib
+
+    grid = bp._grid
+
+    def tiny(span, margin):
+        origin = grid(span, margin)
+        _lib.check(_lib.lib().b200ipc_broad_set_grid_cells(bp._h, 3, 2, 1), "broad_set_grid_cells")
+        return origin
+
+    bp._grid = tiny
+    vt, ee = bp.query(device.to_device(dense))
+    np.testing.assert_array_equal(_rows(device.to_host(vt)), _rows(ref_vt))
+    np.testing.assert_array_equal(_rows(device.to_host(ee)), _rows(ref_ee))
     bp.close()
     assert sizes[1] > 3 * sizes[0] and sizes[1] > 9 * 4 * len(cloth.edges)   # > 4 hits per (box, slot) on average
 
