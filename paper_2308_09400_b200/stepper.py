@@ -230,88 +230,87 @@ class SimState:
         return float(np.sqrt(d2.min().item()))
 
 
+def _search_direction(state, x, x_tilde, x_start, table):
+    """Newton direction at x on the device: blocks -> BSR matrix -> gradient -> block-Jacobi PCG, fixed rows
+    zeroed (solver.py:325-334).  Returns (direction (N,3) tensor, PCG iterations, PCG converged)."""
+    cfg = state.config
+    fams = state.assemble_local_quadratics(x, x_start, table)
+    state.system.set_pattern([(f.s, f.vids) for f in fams])
+    state.system.assemble([f.hess for f in fams])
+    rhs = -state.gradient(x, x_tilde, fams)
+    flat, iters, ok, _, _ = state.system.pcg(rhs, cfg.pcg_rel_tol, cfg.pcg_max_iters)
+    direction = flat.view(-1, 3)
+    direction[state._fixed_dev] = 0.0
+    return direction, iters, ok
+
+
+def _backtrack(state, x, direction, alpha, x_tilde, x_start, energy_prev):
+    """Halve alpha from the CCD bound until the incremental potential does not rise, contacts re-detected
+    at every candidate (solver.py:342-351).  Returns (x_new, energy_new, alpha) or None on collapse."""
+    floor = state.config.line_search_floor
+    while alpha >= floor:
+        trial = x + alpha * direction
+        energy = state.evaluate_energy(trial, x_tilde, x_start)
+        if energy <= energy_prev:
+            return trial, energy, alpha
+        alpha *= 0.5
+    return None
+
+
 def newton_step(state, x, x_tilde, x_start, energy_prev):
     """One projected-Newton iteration with CCD-bounded backtracking (solver.py:316-362).
 
-    Returns (x_new, energy_new, info); contacts are re-detected at every line-search candidate.
+    Returns (x_new, energy_new, info) with the reference's ``info`` keys; a collapsed line search returns
+    the input iterate with ``accepted`` False and ``alpha`` 0.
     """
-    cfg = state.config
-    t = device.torch()
     table = state.detect(x)
-    fams = state.assemble_local_quadratics(x, x_start, table)
-    sysm = state.system
-    sysm.set_pattern([(f.s, f.vids) for f in fams])
-    sysm.assemble([f.hess for f in fams])
-    grad = state.gradient(x, x_tilde, fams)
-
-    d, pcg_iters, pcg_ok, _, _ = sysm.pcg(-grad, cfg.pcg_rel_tol, cfg.pcg_max_iters)
-    dmat = d.reshape(-1, 3)
-    dmat[state._fixed_dev] = 0.0
-
-    alpha = min(1.0, state.broad.ccd_step_bound(x, dmat, slack=cfg.accd_slack))
-
-    accepted = False
-    x_new, energy_new = x, energy_prev
-    while alpha >= cfg.line_search_floor:
-        x_cand = x + alpha * dmat
-        energy_cand = state.evaluate_energy(x_cand, x_tilde, x_start)
-        if energy_cand <= energy_prev:
-            accepted = True
-            x_new, energy_new = x_cand, energy_cand
-            break
-        alpha *= 0.5
-
-    d_inf = float(t.max(t.abs(dmat)).item()) if dmat.numel() else 0.0
-    info = {
-        "pcg_iters": pcg_iters,
-        "pcg_converged": pcg_ok,
-        "alpha": alpha if accepted else 0.0,
-        "accepted": accepted,
-        "d_inf": d_inf,
-        "n_contacts": table.n,
-    }
-    return x_new, energy_new, info
+    direction, pcg_iters, pcg_ok = _search_direction(state, x, x_tilde, x_start, table)
+    bound = state.broad.ccd_step_bound(x, direction, slack=state.config.accd_slack)
+    found = _backtrack(state, x, direction, min(1.0, bound), x_tilde, x_start, energy_prev)
+    info = {"pcg_iters": pcg_iters, "pcg_converged": pcg_ok, "alpha": 0.0, "accepted": found is not None,
+            "d_inf": float(direction.abs().max().item()) if direction.numel() else 0.0, "n_contacts": table.n}
+    if found is None:
+        return x, energy_prev, info
+    info["alpha"] = found[2]
+    return found[0], found[1], info
 
 
 def advance_time_step(state):
-    """One time step: Newton iterations until |d|_inf / (l dt) <= eps_d (solver.py:365-422)."""
+    """One time step: Newton iterations until |d|_inf / (l dt) <= eps_d, at least one, at most
+    ``newton_max_iters`` ("newton-cap"); a collapsed line search ends the step ("line-search-collapse").
+    Then velocities, the end-of-step contact set, the friction refresh and the ``StepStats`` record
+    (solver.py:365-422)."""
     cfg = state.config
-    t0 = time.perf_counter()
-    x0 = state.x            # iterates are never modified in place, so no copies (and detect's cache applies)
-    x_tilde = state._inertia_target(x0)
-    x = x0
-    energy = state.evaluate_energy(x, x_tilde, x0)
+    clock = time.perf_counter()
+    x_start = state.x        # iterates are never modified in place: no copies, and detect's cache applies
+    x_tilde = state._inertia_target(x_start)
+    x, energy = x_start, state.evaluate_energy(x_start, x_tilde, x_start)
 
-    newton_iters = 0
-    pcg_total = 0
-    alpha_min = 1.0
-    warning = ""
-    converged = False
-    while newton_iters < cfg.newton_max_iters:
-        x, energy, info = newton_step(state, x, x_tilde, x0, energy)
-        pcg_total += info["pcg_iters"]
-        newton_iters += 1
+    tally = {"newton": 0, "pcg": 0, "alpha_min": 1.0}
+    outcome = "newton-cap"
+    for _ in range(cfg.newton_max_iters):
+        x, energy, info = newton_step(state, x, x_tilde, x_start, energy)
+        tally["newton"] += 1
+        tally["pcg"] += info["pcg_iters"]
         if not info["accepted"]:
-            warning = "line-search-collapse"
+            outcome = "line-search-collapse"
             break
-        alpha_min = min(alpha_min, info["alpha"])
-        if info["d_inf"] / (state.l * cfg.dt) <= cfg.eps_d:
-            converged = True
+        tally["alpha_min"] = min(tally["alpha_min"], info["alpha"])
+        if info["d_inf"] / (state.l * cfg.dt) <= cfg.eps_d:     # the reference's expression, rounding included
+            outcome = ""
             break
-    if not converged and not warning:
-        warning = "newton-cap"
 
-    state.v = (x - x0) / cfg.dt
-    state.v[state._fixed_dev] = 0.0
-    state.x = x
+    velocity = (x - x_start) / cfg.dt
+    velocity[state._fixed_dev] = 0.0
+    state.x, state.v = x, velocity
     state.step_index += 1
 
-    end_table = state.detect(x)
+    closing = state.detect(x)
     if cfg.friction_mu > 0.0:
-        state._refresh_friction(x, end_table)
+        state._refresh_friction(x, closing)
 
-    stats = StepStats(step=state.step_index, newton_iters=newton_iters, pcg_iters=pcg_total,
-                      min_distance=state.min_distance(x, end_table), energy=energy, alpha_min=alpha_min,
-                      wall_ms=(time.perf_counter() - t0) * 1e3, converged=converged, warning=warning)
+    stats = StepStats(step=state.step_index, newton_iters=tally["newton"], pcg_iters=tally["pcg"],
+                      min_distance=state.min_distance(x, closing), energy=energy, alpha_min=tally["alpha_min"],
+                      wall_ms=(time.perf_counter() - clock) * 1e3, converged=outcome == "", warning=outcome)
     state.stats.append(stats)
     return stats
