@@ -6,8 +6,9 @@
 //      promote edge pairs with c < eps_x to the parallel kinds (:331-343), eps_x from rest lengths
 //      (edge_parallel_eps, :251-259);
 //   2. stream compaction of the kept queries (CUB select);
-//   3. stable LSD radix sort by the reference's key (kind.value, verts, origin)
-//      (ContactStencil.sort_key, :82-83) packed into four 64-bit words;
+//   3. the reference's order (ContactStencil.sort_key, :82-83: kind.value, verts, origin): LSD radix sort
+//      by (kind, verts) packed into two 64-bit words, then the few runs of equal (kind, verts) -- one
+//      stencil reached from several queries -- are ordered by origin in place;
 //   4. gather into the SoA stencil table.
 // The broad phase (any duplicate-free superset of the near queries, incident pairs removed) is the
 // caller's job; each query yields at most one stencil, so the reference's dedupe-by-origin is the
@@ -138,6 +139,54 @@ __global__ void __launch_bounds__(kNT) narrow_keys_kernel(const KeyArgs a) {
     else key = ((uint64_t)a.kind[q] << (2 * a.bits)) | ((uint64_t)(uint32_t)(v.x + 1) << a.bits) | (uint64_t)(uint32_t)(v.y + 1);
   }
   a.keys[i] = key;
+}
+
+// Ties of the (kind, vertices) sort: the same stencil reached from several queries (a point-point pair
+// is the closest feature of every incident edge pair, ...).  The reference orders those by origin
+// (type, then the query's vertex ids); runs are a handful of entries, so the head of each run orders
+// it in place by insertion -- instead of two more full radix sorts over every kept query.
+struct TieArgs {
+  int64_t n, n_vt;
+  uint32_t* idx;       // order after the (kind, vertices) sort; runs of equal keys are reordered in place
+  const uint8_t* kind;
+  const int4* verts;
+  const int32_t* vt;
+  const int32_t* ee;
+};
+
+__device__ __forceinline__ bool same_stencil(const TieArgs& a, uint32_t p, uint32_t q) {
+  const int4 u = a.verts[p], v = a.verts[q];
+  return a.kind[p] == a.kind[q] && u.x == v.x && u.y == v.y && u.z == v.z && u.w == v.w;
+}
+
+__device__ __forceinline__ bool origin_less(const TieArgs& a, uint32_t p, uint32_t q) {
+  const bool pv = p < a.n_vt, qv = q < a.n_vt;
+  if (pv != qv) return qv;  // origin type: edge-edge (1) before vertex-triangle (2)
+  const int4 u = pv ? reinterpret_cast<const int4*>(a.vt)[p] : reinterpret_cast<const int4*>(a.ee)[p - a.n_vt];
+  const int4 v = qv ? reinterpret_cast<const int4*>(a.vt)[q] : reinterpret_cast<const int4*>(a.ee)[q - a.n_vt];
+  if (u.x != v.x) return (uint32_t)u.x < (uint32_t)v.x;
+  if (u.y != v.y) return (uint32_t)u.y < (uint32_t)v.y;
+  if (u.z != v.z) return (uint32_t)u.z < (uint32_t)v.z;
+  return (uint32_t)u.w < (uint32_t)v.w;
+}
+
+__global__ void __launch_bounds__(kNT) narrow_ties_kernel(const TieArgs a) {
+  const int64_t i = (int64_t)blockIdx.x * kNT + threadIdx.x;
+  if (i >= a.n || i + 1 >= a.n) return;
+  const uint32_t q = a.idx[i];
+  if (i > 0 && same_stencil(a, a.idx[i - 1], q)) return;   // not the head of its run
+  if (!same_stencil(a, q, a.idx[i + 1])) return;           // a run of one
+  int64_t e = i + 2;
+  while (e < a.n && same_stencil(a, q, a.idx[e])) ++e;
+  for (int64_t k = i + 1; k < e; ++k) {                    // insertion sort of idx[i, e) by origin
+    const uint32_t cur = a.idx[k];
+    int64_t m = k;
+    while (m > i && origin_less(a, cur, a.idx[m - 1])) {
+      a.idx[m] = a.idx[m - 1];
+      --m;
+    }
+    a.idx[m] = cur;
+  }
 }
 
 struct GatherArgs {
@@ -277,7 +326,7 @@ extern "C" int b200ipc_narrow_phase(int64_t nverts, const double* positions, con
   *n_out = n;
   if (n == 0) return 0;
 
-  // stable LSD sort, least significant word first
+  // LSD sort by (kind, vertices), least significant word first; ties are ordered by origin afterwards
   int bits = 1;
   while (((int64_t)1 << bits) < nverts + 1) ++bits;
   CK(idx_b.alloc(n, st)); CK(key_a.alloc(n, st)); CK(key_b.alloc(n, st));
@@ -287,7 +336,7 @@ extern "C" int b200ipc_narrow_phase(int64_t nverts, const double* positions, con
   CK(temp2.alloc(ts, st));
   uint32_t* cur = idx_a.p;
   uint32_t* nxt = idx_b.p;
-  for (int word = 0; word < 4; ++word) {
+  for (int word = 2; word < 4; ++word) {
     KeyArgs ka{n, n_vt, bits, cur, kq.p, vq.p, vt, ee, word, key_a.p};
     narrow_keys_kernel<<<nblocks(n), kNT, 0, st>>>(ka);
     RC(post_launch());
@@ -298,6 +347,9 @@ extern "C" int b200ipc_narrow_phase(int64_t nverts, const double* positions, con
     cur = nxt;
     nxt = t;
   }
+  TieArgs ta{n, n_vt, cur, kq.p, vq.p, vt, ee};
+  narrow_ties_kernel<<<nblocks(n), kNT, 0, st>>>(ta);
+  RC(post_launch());
 
   GatherArgs ga{n, n_vt, cur, kq.p, vq.p, sq.p, eq.p, vt, ee, kind, reinterpret_cast<int4*>(verts), sub, eps_x,
                 origin_type, reinterpret_cast<int4*>(origin), counters.p + 1};
