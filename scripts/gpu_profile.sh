@@ -14,7 +14,7 @@ ncu --set full --clock-control none --import-source on -k regex:barrier_stencil_
     > gpurun_out/prof_stencil_${TAG}.log 2>&1
 # 3. Newton-step kernels at bench scale
 ncu --set full --clock-control none \
-    -k regex:"bsr_spmv_stream_kernel|assemble_rows_kernel|assemble_numeric_kernel|assemble_factors_kernel|scatter_gradient_kernel|block_jacobi_kernel|pcg_stream_kernel|join_kernel|narrow_classify_kernel|accd_kernel|friction_blocks_kernel|friction_state_kernel|elastic_blocks_kernel" \
+    -k regex:"bsr_spmv_stream_kernel|assemble_rows_kernel|assemble_numeric_kernel|assemble_factors_kernel|scatter_gradient_kernel|block_jacobi_kernel|pcg_stream_kernel|join_kernel|narrow_classify_kernel|narrow_ties_kernel|accd_kernel|friction_blocks_kernel|friction_state_kernel|elastic_blocks_kernel" \
     -c 60 -o gpurun_out/prof_newton_${TAG} -f python scripts/newton_ncu.py --pcg > gpurun_out/prof_newton_${TAG}.log 2>&1
 python bench.py --impl reference --steps 20 --warmup 3 > gpurun_out/bench_${TAG}_ref.json 2>/dev/null
 # 4. summarise on the box (the raw reports exceed what gpurun brings back) and ship the summaries
