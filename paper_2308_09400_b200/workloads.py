@@ -442,3 +442,64 @@ def broad_phase(scene, positions=None, surf_verts=None):
     ee = np.concatenate([ea[ok], eb[ok]], axis=1)
     ee = ee[np.lexsort((pairs[ok, 1], pairs[ok, 0]))]
     return vt, ee
+
+
+# ---- volumetric scene: a grid of elastic cubes over a tessellated floor -------------------------------
+
+_CUBE_CORNERS = np.array([[0, 0, 0], [1, 0, 0], [1, 1, 0], [0, 1, 0], [0, 0, 1], [1, 0, 1], [1, 1, 1], [0, 1, 1]],
+                         dtype=np.float64)
+# five-tet split of the unit cube (four corner tets around one central tet), positively oriented
+_CUBE_TETS = np.array([[0, 1, 3, 4], [1, 2, 3, 6], [1, 5, 6, 4], [3, 6, 7, 4], [1, 6, 3, 4]], dtype=np.int64)
+
+
+def tet_boundary(tets):
+    """Boundary triangles (faces that belong to one tet) and their unique edges, global vertex ids."""
+    tets = np.asarray(tets, dtype=np.int64).reshape(-1, 4)
+    faces = np.concatenate([tets[:, [1, 2, 3]], tets[:, [0, 3, 2]], tets[:, [0, 1, 3]], tets[:, [0, 2, 1]]])
+    key = np.sort(faces, axis=1)
+    _, first, count = np.unique(key, axis=0, return_index=True, return_counts=True)
+    tris = faces[np.sort(first[count == 1])]
+    e = np.sort(np.concatenate([tris[:, [0, 1]], tris[:, [1, 2]], tris[:, [2, 0]]]), axis=1)
+    return tris, np.unique(e, axis=0)
+
+
+def cube_drop(k=12, size=0.4, pitch=0.6, z0=0.004, d_hat=0.02, kappa=2e8, dt=0.01, density=1000.0, seed=1,
+              tilt=0.0):
+    """k x k elastic cubes (five tets each) hovering ``z0`` above a fixed tessellated floor, as a
+    reference-``Scene``-shaped namespace (tets, surface arrays, lumped masses, gravity) plus ``d_hat``,
+    ``kappa``, ``dt`` and ``v0`` (free vertices moving down).  ``tilt`` jitters the cube heights (relative
+    to z0) so that contacts do not all switch on in the same iteration."""
+    from types import SimpleNamespace
+
+    rng = np.random.default_rng(seed)
+    verts, tets = [], []
+    for i in range(k):
+        for j in range(k):
+            base = np.array([i * pitch, j * pitch, z0 * (1.0 + tilt * rng.uniform(-0.5, 0.5))])
+            tets.append(_CUBE_TETS + 8 * (i * k + j))
+            verts.append(base + size * _CUBE_CORNERS)
+    verts, tets = np.concatenate(verts), np.concatenate(tets)
+    nb = verts.shape[0]
+    g = k + 2
+    ax = (np.arange(g) - 1.0) * pitch + 0.5 * (size - pitch)      # floor vertices between the cubes
+    fx, fy = np.meshgrid(ax, ax, indexing="ij")
+    floor = np.stack([fx.ravel(), fy.ravel(), np.zeros(g * g)], axis=1)
+    ftris, fedges = _grid_mesh(g)
+    positions = np.concatenate([verts, floor])
+    btris, bedges = tet_boundary(tets)
+    tris = np.concatenate([btris, ftris + nb])
+    edges = np.concatenate([bedges, fedges + nb])
+    # lumped masses: a quarter of each tet's mass to each of its vertices (mesh.py:295-305)
+    p = positions[tets]
+    vol = np.abs(np.einsum("ij,ij->i", np.cross(p[:, 1] - p[:, 0], p[:, 2] - p[:, 0]), p[:, 3] - p[:, 0])) / 6.0
+    masses = np.zeros(positions.shape[0])
+    np.add.at(masses, tets.ravel(), np.repeat(0.25 * density * vol, 4))
+    fixed = np.zeros(positions.shape[0], dtype=bool)
+    fixed[nb:] = True
+    lo, hi = positions.min(axis=0), positions.max(axis=0)
+    v0 = np.zeros_like(positions)
+    v0[:nb, 2] = -0.25
+    return SimpleNamespace(positions=positions, rest_positions=positions.copy(), masses=masses, fixed=fixed, tets=tets,
+                           surf_tris=tris, surf_edges=edges, surf_verts=np.unique(tris),
+                           gravity=np.array([0.0, 0.0, -9.81]), bbox_diagonal=float(np.linalg.norm(hi - lo)),
+                           d_hat=d_hat, kappa=kappa, dt=dt, v0=v0, name=f"cube-drop-{k}x{k}")

@@ -149,3 +149,69 @@ def test_time_step_at_bench_scale(S):
     np.testing.assert_array_equal(state.positions()[fixed], cloth.positions[fixed])
     assert np.all(state.velocities()[fixed] == 0.0)
     state.close()
+
+
+def _cube_state(S, k, friction_mu):
+    from paper_2308_09400_b200 import elasticity, workloads
+
+    sc = workloads.cube_drop(k=k, tilt=0.5)
+    cfg = S.stepper.SolverConfig(dt=sc.dt, barrier=S.barrier.BarrierParams(sc.d_hat, sc.kappa), friction_mu=friction_mu)
+    state = S.stepper.SimState(sc, cfg, elasticity.ElasticMaterial(1e5, 0.4))
+    state.v = S.device.to_device(sc.v0.copy())
+    return sc, state
+
+
+def test_all_seven_families_in_one_newton_matrix(S):
+    """Elastic tets + barrier 6/9/12 + friction 6/9/12 blocks of a cube-drop scene through one pattern:
+    the assembled SpMV equals mass + the sum of the families' block products (an independent kernel)."""
+    from paper_2308_09400_b200 import kernels
+
+    t = S.device.torch()
+    sc, state = _cube_state(S, 6, 0.3)
+    rng = np.random.default_rng(5)
+    x0 = state.x
+    x = x0 + S.device.to_device(np.where(sc.fixed[:, None], 0.0, 2e-4 * rng.normal(size=sc.positions.shape)))
+    table = state.detect(x)
+    fams = state.assemble_local_quadratics(x, x0, table)
+    sizes = sorted(f.s for f in fams)
+    assert sizes.count(4) >= 3 and len(fams) >= 4, sizes          # elastic, barrier and friction 12x12 at least
+    assert state.friction_state.n > 0 and table.n > 0
+    sysm = state.system
+    sysm.set_pattern([(f.s, f.vids) for f in fams])
+    sysm.assemble([f.hess for f in fams])
+    v = S.device.to_device(rng.normal(size=3 * state.n))
+    y = sysm.spmv(v)
+    free = (~state._fixed_dev).repeat_interleave(3)
+    vm = t.where(free, v, t.zeros_like(v))
+    ref = t.repeat_interleave(sysm.masses, 3) * vm
+    for f in fams:
+        kernels.matvec_blocks_device(f.hess, f.vids, vm, ref)
+    ref = t.where(free, ref, v)
+    assert float((y - ref).abs().max()) <= 1e-11 * float(ref.abs().max())
+    # and the gradient: M (x - x~) + scattered family gradients, fixed rows zero
+    x_tilde = state._inertia_target(x0)
+    g = state.gradient(x, x_tilde, fams).reshape(-1, 3)
+    want = sysm.masses[:, None] * (x - x_tilde)
+    for f in fams:
+        want.index_add_(0, f.vids.reshape(-1), f.grad.reshape(-1, 3))
+    want[state._fixed_dev] = 0.0
+    assert float((g - want).abs().max()) <= 1e-11 * float(want.abs().max())
+    state.close()
+
+
+def test_cube_drop_with_friction_bounces_without_interpenetration(S):
+    """144 elastic cubes dropping on a floor with friction 0.3, eight steps: every step converges, contacts
+    switch on and off, nothing crosses the floor, fixed vertices stay put."""
+    sc, state = _cube_state(S, 12, 0.3)
+    seen_contact = seen_free = False
+    for _ in range(8):
+        stats = S.stepper.advance_time_step(state)
+        assert stats.converged and stats.warning == ""
+        assert np.isnan(stats.min_distance) or stats.min_distance > 0.0
+        seen_contact |= not np.isnan(stats.min_distance)
+        seen_free |= bool(np.isnan(stats.min_distance))
+    x = state.positions()
+    assert seen_contact and seen_free
+    assert x[~sc.fixed, 2].min() > 0.0
+    np.testing.assert_array_equal(x[sc.fixed], sc.positions[sc.fixed])
+    state.close()

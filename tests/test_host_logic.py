@@ -185,3 +185,15 @@ def test_cloth_scene_as_scene():
     assert sc.tets.shape == (0, 4) and sc.surf_tris is cloth.tris and sc.surf_edges is cloth.edges
     np.testing.assert_array_equal(sc.surf_verts, np.arange(cloth.positions.shape[0]))
     assert sc.bbox_diagonal == pytest.approx(np.linalg.norm(np.ptp(cloth.positions, axis=0)))
+
+
+def test_cube_drop_workload_is_well_formed():
+    sc = workloads.cube_drop(k=3)
+    p = sc.positions[sc.tets]
+    det = np.einsum("ij,ij->i", np.cross(p[:, 1] - p[:, 0], p[:, 2] - p[:, 0]), p[:, 3] - p[:, 0])
+    assert det.min() > 0.0                                                     # positively oriented tets
+    np.testing.assert_allclose(det.reshape(-1, 5).sum(axis=1) / 6.0, 0.4 ** 3)  # five tets fill each cube
+    tris, edges = workloads.tet_boundary(sc.tets[:5])
+    assert tris.shape == (12, 3) and edges.shape == (18, 2)                    # a cube's surface
+    np.testing.assert_allclose(sc.masses[:8].sum(), 1000.0 * 0.4 ** 3)
+    assert sc.fixed[72:].all() and not sc.fixed[:72].any() and sc.surf_verts.size == sc.positions.shape[0]
