@@ -68,6 +68,11 @@ class StepStats:
     warning: str = ""
 
 
+def _dev(a):
+    """Device fp64 tensor of a host array; a device tensor passes through as the same object."""
+    return device.to_device(a, np.float64)
+
+
 def _tet_materials(scene, materials, nt):
     """Per-tet Lame parameters: per-body materials like solver.py:83-97, or one material / a
     (mu, lam) pair of arrays for scenes without a ``bodies`` list."""
@@ -163,7 +168,8 @@ class SimState:
     # -- energies (solver.py:118-175) --------------------------------------------------------
     def _inertia_target(self, x0):
         cfg = self.config
-        x_tilde = x0 + cfg.dt * self.v + cfg.dt ** 2 * self._gravity
+        x0 = _dev(x0)
+        x_tilde = x0 + cfg.dt * _dev(self.v) + cfg.dt ** 2 * self._gravity
         x_tilde[self._fixed_dev] = x0[self._fixed_dev]
         return x_tilde
 
@@ -183,6 +189,7 @@ class SimState:
 
     def evaluate_energy(self, x, x_tilde, x_start, stencils=None):
         """Incremental potential at x; detects contacts unless a table is given."""
+        x, x_tilde, x_start = _dev(x), _dev(x_tilde), _dev(x_start)
         table = self.detect(x) if stencils is None else stencils
         dx = x - x_tilde
         inertia = 0.5 * float((self._free_mass * dx * dx).sum().item())
@@ -263,6 +270,7 @@ def newton_step(state, x, x_tilde, x_start, energy_prev):
     Returns (x_new, energy_new, info) with the reference's ``info`` keys; a collapsed line search returns
     the input iterate with ``accepted`` False and ``alpha`` 0.
     """
+    x, x_tilde, x_start = _dev(x), _dev(x_tilde), _dev(x_start)
     table = state.detect(x)
     direction, pcg_iters, pcg_ok = _search_direction(state, x, x_tilde, x_start, table)
     bound = state.broad.ccd_step_bound(x, direction, slack=state.config.accd_slack)
@@ -282,6 +290,7 @@ def advance_time_step(state):
     (solver.py:365-422)."""
     cfg = state.config
     clock = time.perf_counter()
+    state.x, state.v = _dev(state.x), _dev(state.v)      # host arrays assigned by the caller are welcome
     x_start = state.x        # iterates are never modified in place: no copies, and detect's cache applies
     x_tilde = state._inertia_target(x_start)
     x, energy = x_start, state.evaluate_energy(x_start, x_tilde, x_start)

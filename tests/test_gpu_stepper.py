@@ -109,6 +109,21 @@ def test_newton_step_decreases_energy_and_stays_feasible(S):
     assert state.min_distance(x1, table) > 0.0
 
 
+def test_host_arrays_are_accepted_like_the_reference(S):
+    """The reference passes NumPy arrays around; the device path takes them at its entry points."""
+    z = load_golden("stepper_drop")
+    state = state_of(S, z)
+    x0 = z["positions"].copy()
+    state.v = z["v0"].copy()                                  # a host array, as reference code would assign
+    x_tilde = state._inertia_target(x0)
+    e0 = state.evaluate_energy(x0, S.device.to_host(x_tilde), x0)
+    x1, e1, info = S.stepper.newton_step(state, x0, S.device.to_host(x_tilde), x0, e0)
+    assert info["accepted"] and e1 <= e0
+    state.x = x0
+    stats = S.stepper.advance_time_step(state)
+    assert abs(np.abs(state.positions() - z["xs"][1]).max()) < POS_TOL * state.l and stats.converged
+
+
 def test_drop_lands_without_interpenetration(S):
     """tests/test_solver.py:194-204 on the stacked cubes: 40 steps, every end-of-step distance positive,
     nothing falls through, no line-search collapse."""
