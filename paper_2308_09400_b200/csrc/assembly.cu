@@ -655,26 +655,8 @@ extern "C" int b200ipc_assemble_symbolic(b200ipc_assembly* h, int64_t nverts, co
   RC(post_launch());
   CK(cub::DeviceScan::InclusiveSum(h->temp.ptr, tb2, h->head.ptr, h->head.ptr, (int)n, st));
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  // nnzb = scan[n-1]
-  int32_t nnzb32 = 0;
-  CK(cudaMemcpyAsync(&nnzb32, h->head.ptr + (n - 1), sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  h->nnzb = nnzb32;
-  CK(h->colidx.reserve(h->nnzb)); CK(h->useg.reserve(h->nnzb + 1));
-  emit_pattern_kernel<<<blocks_for(n), kAT, 0, st>>>(n, nverts, h->keys_b.ptr, h->head.ptr, h->colidx.ptr,
-                                                     h->useg.ptr, h->rowptr.ptr);
-  RC(post_launch());
-  {
-    first_sentinel_kernel<<<1, 1, 0, st>>>(n, sentinel, h->keys_b.ptr, h->scalars.ptr);
-    RC(post_launch());
-    int64_t nvalid = 0;
-    CK(cudaMemcpyAsync(&nvalid, h->scalars.ptr, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    h->nvalid = nvalid;
-  }
-  finish_pattern_kernel<<<1, 1, 0, st>>>(nverts, h->nnzb, h->nvalid, h->rowptr.ptr, h->useg.ptr);
-  RC(post_launch());
-  // gradient runs: sort vertex slots by vertex id
+  // gradient runs (sort vertex slots by vertex id): queued before the host reads nnzb, so the device keeps
+  // working through that round trip
   const int64_t ng = h->ngslots;
   CK(h->gseg.reserve(nverts + 1));
   if (ng > 0) {
@@ -691,6 +673,22 @@ extern "C" int b200ipc_assemble_symbolic(b200ipc_assembly* h, int64_t nverts, co
     g_launches.fetch_add(1, std::memory_order_relaxed);
   }
   lower_bound_kernel<<<blocks_for(nverts + 1), kAT, 0, st>>>(nverts, ng, h->gkeys_b.ptr, h->gseg.ptr);
+  RC(post_launch());
+  // nnzb = scan[n-1] and the number of kept slots, both with one synchronisation
+  first_sentinel_kernel<<<1, 1, 0, st>>>(n, sentinel, h->keys_b.ptr, h->scalars.ptr);
+  RC(post_launch());
+  int32_t nnzb32 = 0;
+  int64_t nvalid = 0;
+  CK(cudaMemcpyAsync(&nnzb32, h->head.ptr + (n - 1), sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&nvalid, h->scalars.ptr, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  h->nnzb = nnzb32;
+  h->nvalid = nvalid;
+  CK(h->colidx.reserve(h->nnzb)); CK(h->useg.reserve(h->nnzb + 1));
+  emit_pattern_kernel<<<blocks_for(n), kAT, 0, st>>>(n, nverts, h->keys_b.ptr, h->head.ptr, h->colidx.ptr,
+                                                     h->useg.ptr, h->rowptr.ptr);
+  RC(post_launch());
+  finish_pattern_kernel<<<1, 1, 0, st>>>(nverts, h->nnzb, h->nvalid, h->rowptr.ptr, h->useg.ptr);
   RC(post_launch());
   h->have_desc = h->have_fdesc = h->have_rows = false;
   h->ready = true;
