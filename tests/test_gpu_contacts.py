@@ -208,3 +208,28 @@ def test_gpu_detect_matches_frozen_reference(Cn, tag):
     bp.close()
     for key in KEYS:
         np.testing.assert_array_equal(getattr(got, key), z[f"{tag}_list_{key}"], err_msg=key)
+
+
+def test_long_tie_runs_are_ordered_by_origin(Cn):
+    """Two cones whose apexes almost touch: every (upper spoke, lower spoke) edge query and every
+    apex-triangle query reduces to the same point-point stencil, a run of ~m*m + 2m equal (kind, vertices)
+    keys that the narrow phase must order by origin exactly as the reference's sort_key does -- in random
+    candidate order, as the broad phase delivers them."""
+    m = 14
+    ang = 2.0 * np.pi * np.arange(m) / m
+    rng = np.random.default_rng(12)
+    up = np.stack([np.cos(ang), np.sin(ang), np.full(m, 1.0)], axis=1) + 0.01 * rng.normal(size=(m, 3))
+    dn = np.stack([np.cos(ang + 0.2), np.sin(ang + 0.2), np.full(m, -1.0)], axis=1) + 0.01 * rng.normal(size=(m, 3))
+    pos = np.concatenate([[[0.0, 0.0, 0.004]], up, [[0.001, -0.002, -0.004]], dn])   # apex A = 0, apex B = m + 1
+    a, b = 0, m + 1
+    tris = np.array([[a, 1 + i, 1 + (i + 1) % m] for i in range(m)] + [[b, b + 1 + i, b + 1 + (i + 1) % m] for i in range(m)])
+    edges = np.unique(np.sort(np.concatenate([tris[:, [0, 1]], tris[:, [1, 2]], tris[:, [2, 0]]]), axis=1), axis=0)
+    d_hat = 0.05
+    vt, ee = all_pairs(tris, edges)
+    ref = o.narrow_phase(pos, pos, vt, ee, d_hat)
+    key = np.concatenate([ref["kind"][:, None].astype(np.int64), ref["verts"]], axis=1)
+    _, counts = np.unique(key, axis=0, return_counts=True)
+    assert counts.max() >= 200                                              # one very long run of ties (210 of the 224 queries)
+    vt_s, ee_s = vt[rng.permutation(len(vt))], ee[rng.permutation(len(ee))]  # unordered candidate sets
+    got = Cn.contacts.narrow_phase(pos, pos, vt_s, ee_s, d_hat)
+    assert_same_table(got, ref)
