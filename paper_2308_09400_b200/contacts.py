@@ -91,8 +91,7 @@ class BroadPhase:
         dirs = device.to_device(directions, np.float64)
         margin = 1e-3 * self.d_hat if margin is None else float(margin)
         t = device.torch()
-        end = pos + dirs
-        span = t.stack([t.minimum(pos, end).amin(dim=0), t.maximum(pos, end).amax(dim=0)]).cpu().numpy()
+        span = t.stack(t.aminmax(t.cat([pos, pos + dirs]), dim=0)).cpu().numpy()   # over both poses
         origin = self._grid(span, margin)
         n_vt, n_ee = C.c_int64(0), C.c_int64(0)
         L = _lib.lib()
