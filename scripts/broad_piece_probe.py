@@ -4,7 +4,11 @@ import numpy as np, torch
 from paper_2308_09400_b200 import workloads, contacts, device, _lib
 gap = float(sys.argv[1]) if len(sys.argv) > 1 else 3.0
 cloth = workloads.cloth_stack(layers=4, n=140, seed=1, d_hat_rel=0.2, jitter_rel=0.01, gap_rel=gap)
+cf = float(sys.argv[2]) if len(sys.argv) > 2 else 0.0
 bp = contacts.BroadPhase(np.unique(cloth.tris), cloth.tris, cloth.edges, cloth.d_hat, cloth.positions)
+if cf:
+    bp.cell *= cf
+print('cell', bp.cell)
 pos = device.to_device(cloth.positions)
 def t(fn, reps=50):
     fn(); torch.cuda.synchronize(); t0 = time.perf_counter()
