@@ -104,12 +104,15 @@ def update_state(table, positions, mu, eps_v, dt, barrier_batch=None, params=Non
     # compaction of the kept rows on the device (the reference skips d2 <= 0 and lambda_n <= 0 stencils);
     # only eight counters and one flag cross PCIe
     t = device.torch()
-    kinds = t.repeat_interleave(t.arange(7, device="cuda"), t.as_tensor(np.diff(table.kind_off), device="cuda"))
-    keep = t.nonzero(status == 0).squeeze(1)
-    counts = t.bincount(kinds[keep], minlength=7)
-    host = t.cat([counts, (status == 3).any().to(counts.dtype).reshape(1)]).cpu().numpy()
+    ok = status == 0
+    # kept rows per kind = differences of the running count of kept rows at the kind boundaries (the table is
+    # kind-sorted and the compaction keeps its order)
+    running = t.cat([t.zeros(1, dtype=t.int64, device=ok.device), t.cumsum(ok, 0, dtype=t.int64)])
+    at = running[t.as_tensor(np.asarray(table.kind_off, dtype=np.int64), device=ok.device)]
+    host = t.cat([at[1:] - at[:-1], (status == 3).any().to(t.int64).reshape(1)]).cpu().numpy()
     if host[7]:
         raise ValueError("undefined contact normal for friction basis")
+    keep = t.nonzero(ok).squeeze(1)
     koff = np.concatenate([[0], np.cumsum(host[:7])]).astype(np.int64)
     sub = DeviceStencilTable(int(keep.shape[0]), koff, table.verts[keep].contiguous(), table.sub[keep].contiguous(),
                              table.eps_x[keep].contiguous())
