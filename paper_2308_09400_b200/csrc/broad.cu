@@ -29,7 +29,10 @@
 
 namespace b200ipc {
 
-constexpr int kBT = 256;
+#ifndef B200IPC_BROAD_THREADS
+#define B200IPC_BROAD_THREADS 256
+#endif
+constexpr int kBT = B200IPC_BROAD_THREADS;
 
 template <typename T>
 struct BroadBuf {
