@@ -445,6 +445,93 @@ def mollified_eigensystem(g, c, eps_x, scale, form="qlog"):
     }
 
 
+def mollified_eigensystem_extended(g, c, eps_x, scale, decoupled=None, ulps=0.0):
+    """mollifier.py:106-144 evaluated in x87 extended precision (64-bit mantissa) from the SAME fp64
+    inputs (g, c, eps_x): the arbiter for rows where k2 = (dl + 2p)/(8t) cancels (DESIGN.md section 2,
+    "conditioning of k2").  ``decoupled`` = the fp64 evaluation's branch decision (the reference's),
+    reused so that both evaluations describe the same branch.  ``ulps`` != 0 perturbs the two channel
+    eigenvalues by that many fp64 ulps in opposite directions and k2 by the same many ulps of its
+    numerator's terms (|dl| + 2p)/|8t|: the change it causes is the first-order noise an fp64 evaluation
+    of the reference formula carries (inputs that differ in the last bits of ``log``, and the rounding of
+    dl + 2p where it cancels).
+    Returns (lambda8', q_gamma, q_f) as longdouble arrays.  qlog form only.
+    """
+    ld = np.longdouble
+    g, c, eps_x = (np.asarray(a, dtype=np.float64).astype(ld) for a in (g, c, eps_x))
+    scale = ld(scale)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        lg, om = np.log(g), ld(1.0) - g
+        b = scale * om**2 * lg * lg
+        bg = scale * (-2 * om * lg * lg + 2 * om**2 * lg / g)
+        bgg = scale * (2 * lg * lg - 8 * om * lg / g + 2 * om**2 * (1 - lg) / g**2)
+        inside = c < eps_x
+        e = np.where(inside, -(c * c) / (eps_x * eps_x) + 2 * c / eps_x, ld(1.0))
+        de = np.where(inside, -2 * c / (eps_x * eps_x) + 2 / eps_x, ld(0.0))
+        d2e = np.where(inside, -2 / (eps_x * eps_x), ld(0.0))
+        lam_gamma1 = 2 * (de * b + 2 * c * (d2e * b))
+        lam_g1 = 2 * (e * bg + 2 * g * (e * bgg))
+        if ulps:
+            du = ld(ulps) * ld(2.0) ** -52
+            lam_gamma1 = lam_gamma1 * (1 + du)
+            lam_g1 = lam_g1 * (1 - du)
+        t = de * bg * np.sqrt(c) * np.sqrt(g)
+        p = np.sqrt((lam_gamma1 - lam_g1) ** 2 + 64 * t * t) / 2
+        lam8 = (lam_gamma1 + lam_g1) / 2 + p
+        if decoupled is None:
+            decoupled = (np.abs(8 * t) < ld(1e-12) * (np.abs(lam_gamma1) + np.abs(lam_g1))) | (t == 0)
+        k2 = (lam_gamma1 - lam_g1 + 2 * p) / (8 * t)
+        if ulps:   # rounding of the numerator dl + 2p in fp64: the part that explodes when it cancels
+            k2 = k2 + du * (np.abs(lam_gamma1 - lam_g1) + 2 * p) / np.abs(8 * t)
+        nrm = np.sqrt(k2 * k2 + 1)
+        q_gamma = np.where(decoupled, np.where(lam_gamma1 >= lam_g1, ld(1.0), ld(0.0)), k2 / nrm)
+        q_f = np.where(decoupled, np.where(lam_gamma1 >= lam_g1, ld(0.0), ld(1.0)), 1 / nrm)
+    return lam8, q_gamma, q_f
+
+
+def mollified_blocks_arbiter(kind, verts, sub, eps_x, positions, d_hat, kappa, dt2=1.0, ulps=8.0):
+    """Extended-precision mollified blocks of the parallel rows of a table + the per-row fp64 noise bound.
+
+    For every row (parallel kinds only, others get NaN / 0): ``hess`` (n,12,12) fp64-rounded block
+    lam8 w w^T with (lam8, q) from ``mollified_eigensystem_extended``, and ``noise`` (n,) = the largest
+    block-entry change, relative to the block's max-abs, when the two channel eigenvalues move by
+    ``ulps`` fp64 ulps -- what two correct fp64 evaluations of mollifier.py:113-127 may differ by.
+    Geometry (f, grad f, sqrt c, grad sqrt c) is the fp64 one (bit-identical on every side).
+    """
+    kind = np.asarray(kind)
+    n = kind.shape[0]
+    par = np.flatnonzero(IS_PARALLEL[kind])
+    hess = np.full((n, 12, 12), np.nan)
+    noise = np.zeros(n)
+    if par.size == 0:
+        return hess, noise
+    verts = np.asarray(verts)
+    d2, grad_d2 = stencil_distance_batch(kind[par], verts[par], np.asarray(sub)[par], positions)
+    c, grad_c = parallel_measure_batch(verts[par], positions)
+    scale = kappa * d_hat**4
+    with np.errstate(divide="ignore", invalid="ignore"):
+        d = np.sqrt(d2)
+        f = d / d_hat
+        u_f = (grad_d2 / (2.0 * d * d_hat)[:, None, None]).reshape(-1, 12)
+        sqrt_c = np.sqrt(c)
+        safe = np.where(sqrt_c > 0.0, sqrt_c, 1.0)
+        u_c = np.where((sqrt_c > 0.0)[:, None], grad_c.reshape(-1, 12) / (2.0 * safe)[:, None], 0.0)
+        g, cc = f * f, sqrt_c * sqrt_c
+        ref = mollified_eigensystem(g, cc, np.asarray(eps_x)[par], scale)
+        dec = (np.abs(8.0 * ref["t"]) < 1e-12 * (np.abs(ref["lam_gamma1"]) + np.abs(ref["lam_g1"]))) | (ref["t"] == 0.0)
+        blocks = []
+        for u in (0.0, ulps, -ulps):
+            lam8, qg, qf = mollified_eigensystem_extended(g, cc, np.asarray(eps_x)[par], scale, dec, u)
+            w = qg[:, None] * u_c.astype(np.longdouble) + qf[:, None] * u_f.astype(np.longdouble)
+            blocks.append(np.longdouble(dt2) * np.maximum(lam8, 0)[:, None, None] * (w[:, :, None] * w[:, None, :]))
+        top = np.abs(blocks[0]).reshape(len(par), -1).max(axis=1)
+        top = np.where(top > 0, top, 1)
+        dev = np.maximum(np.abs(blocks[1] - blocks[0]), np.abs(blocks[2] - blocks[0])).reshape(len(par), -1).max(axis=1)
+    live = (d2 > 0.0) & (d2 < d_hat * d_hat)
+    hess[par] = np.where(live[:, None, None], blocks[0].astype(np.float64), 0.0)
+    noise[par] = np.where(live, (dev / top).astype(np.float64), 0.0)
+    return hess, noise
+
+
 # ----------------------------------------------------------------------------
 # a12, a15, a17, a19-a22: per-stencil energy, gradient and PSD block
 # ----------------------------------------------------------------------------
@@ -687,6 +774,46 @@ def assemble_bsr(grouped, masses, fixed):
     np.add.at(rowptr, r + 1, 1)
     rowptr = np.cumsum(rowptr).astype(np.int32)
     return rowptr, c.astype(np.int32), out
+
+
+def bsr_pattern(vids_list, n, fixed):
+    """(rowptr, colidx) of ``assemble_bsr`` from the families' vertex ids alone -- the sparsity pattern
+    {(i,j): i,j in one block} U {(i,i)} with fixed rows/cols reduced to the diagonal (SURVEY.md a29,
+    tests/test_solver.py:71-84 of the reference) -- cheap enough for a million contacts."""
+    keys = [np.arange(n, dtype=np.int64) * (n + 1)]
+    for vids in vids_list:
+        vids = np.asarray(vids, dtype=np.int64)
+        r = np.repeat(vids, vids.shape[1], axis=1).reshape(-1)
+        c = np.tile(vids, (1, vids.shape[1])).reshape(-1)
+        keep = ~(fixed[r] | fixed[c]) | (r == c)
+        keys.append(r[keep] * n + c[keep])
+    uniq = np.unique(np.concatenate(keys))
+    r = uniq // n
+    rowptr = np.zeros(n + 1, dtype=np.int64)
+    np.add.at(rowptr, r + 1, 1)
+    return np.cumsum(rowptr).astype(np.int32), (uniq % n).astype(np.int32)
+
+
+def bsr_rows_dense(grouped, masses, fixed, rows):
+    """Block rows ``rows`` of the assembled matrix as {row: {col: 3x3}} summed in list order -- the value
+    check of a million-contact matrix on a sample of rows without building the whole thing."""
+    want = np.zeros(masses.shape[0], dtype=bool)
+    want[rows] = True
+    out = {int(r): {int(r): (np.eye(3) if fixed[r] else masses[r] * np.eye(3))} for r in rows}
+    for hess, vids in grouped:
+        nb, s = vids.shape
+        hit = np.argwhere(want[vids])
+        for b, a in hit:
+            i = int(vids[b, a])
+            if fixed[i]:
+                continue
+            for cc in range(s):
+                j = int(vids[b, cc])
+                if fixed[j]:
+                    continue
+                blk = hess[b, 3 * a:3 * a + 3, 3 * cc:3 * cc + 3]
+                out[i][j] = out[i].get(j, 0.0) + blk
+    return out
 
 
 def bsr_matvec(rowptr, colidx, vals, x):

@@ -45,3 +45,26 @@ def block_rel_err(got, ref):
     scale = np.abs(ref.reshape(n, -1)).max(axis=1)
     scale = np.where(scale == 0.0, 1.0, scale).reshape((n,) + (1,) * (ref.ndim - 1))
     return float(np.max(np.abs(got - ref) / scale))
+
+
+def row_rel_err(got, ref):
+    """block_rel_err per row: (n,) array of max |got-ref| over the block / the block's max-abs."""
+    got, ref = np.asarray(got, dtype=np.float64), np.asarray(ref, dtype=np.float64)
+    n = ref.shape[0]
+    scale = np.abs(ref.reshape(n, -1)).max(axis=1)
+    scale = np.where(scale == 0.0, 1.0, scale)
+    return np.abs(got - ref).reshape(n, -1).max(axis=1) / scale
+
+
+def entry_rel_err(got, ref, floor=1e-6):
+    """True per-entry relative error: |got-ref| / |ref| for every entry with |ref| > floor * (its block's
+    max-abs); entries below that (the analytically-zero ones and their round-off)
+    are measured against floor * block max-abs, i.e. they must be < tol * floor of the block scale."""
+    got, ref = np.asarray(got, dtype=np.float64), np.asarray(ref, dtype=np.float64)
+    if ref.size == 0:
+        return 0.0
+    n = ref.shape[0]
+    top = np.abs(ref.reshape(n, -1)).max(axis=1)
+    top = np.where(top == 0.0, 1.0, top).reshape((n,) + (1,) * (ref.ndim - 1))
+    scale = np.maximum(np.abs(ref), floor * top)
+    return float(np.max(np.abs(got - ref) / scale))

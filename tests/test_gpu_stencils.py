@@ -8,7 +8,7 @@ projected blocks PSD (min eigenvalue >= -1e-12 * lambda_max) and symmetric.
 import numpy as np
 import pytest
 
-from conftest import block_rel_err, load_golden
+from conftest import block_rel_err, entry_rel_err, load_golden, row_rel_err
 from oracle import tetipc_oracle as o
 
 pytestmark = pytest.mark.gpu
@@ -71,6 +71,8 @@ def test_plain_blocks_vs_reference_golden(P, pset):
     np.testing.assert_allclose(energy, z[f"{pset}_ref_energy"], rtol=TOL, atol=0.0)
     assert block_rel_err(grad, z[f"{pset}_ref_grad"]) < TOL
     assert block_rel_err(hess, z[f"{pset}_ref_hess"]) < TOL
+    assert entry_rel_err(grad, z[f"{pset}_ref_grad"]) < TOL      # true per-entry, not only against the block scale
+    assert entry_rel_err(hess, z[f"{pset}_ref_hess"]) < TOL
     check_psd_symmetric(hess)
     nf = P.stencils.evaluate(table_from(P, z), x, P.barrier.BarrierParams(d_hat=d_hat, kappa=kappa, use_filter=False), dt=dt)
     assert block_rel_err(padded(P, nf)[3], z[f"{pset}_nofilter_ref_hess"]) < TOL
@@ -85,6 +87,8 @@ def test_parallel_blocks_vs_reference_golden(P):
     np.testing.assert_allclose(energy, z["unit_ref_energy"], rtol=TOL, atol=0.0)
     assert block_rel_err(grad, z["unit_ref_grad"]) < TOL
     assert block_rel_err(hess, z["unit_ref_hess"]) < TOL
+    assert entry_rel_err(grad, z["unit_ref_grad"]) < TOL
+    assert entry_rel_err(hess, z["unit_ref_hess"]) < TOL
     check_psd_symmetric(hess)
     total, n_inactive, n_pen = batch.summary()
     assert total == pytest.approx(float(z["unit_ref_energy"].sum()), rel=1e-12)
@@ -111,6 +115,8 @@ def test_config1_10k_pt_ee_vs_oracle(P, d_hat, kappa, dt):
     np.testing.assert_allclose(energy, ref["energy"], rtol=TOL, atol=0.0)
     assert block_rel_err(grad, ref["grad"]) < TOL
     assert block_rel_err(hess, ref["hess"]) < TOL
+    assert entry_rel_err(grad, ref["grad"]) < TOL
+    assert entry_rel_err(hess, ref["hess"]) < TOL
     check_psd_symmetric(hess)
 
 
@@ -126,22 +132,63 @@ def test_config2_parallel_subset_vs_oracle(P):
     np.testing.assert_array_equal(status, ref["status"])
     np.testing.assert_allclose(energy, ref["energy"], rtol=TOL, atol=1e-300)
     assert block_rel_err(grad, ref["grad"]) < TOL
-    # the reference's k2 = (dl + 2p)/(8t) cancels catastrophically when lam_gamma1 < lam_g1 and
-    # |t| << |dl|: there the two correctly-rounded evaluations
-    # differ by ulp(dl)/(8|t|); compare those rows through that bound and all others at 1e-9
-    par = np.flatnonzero(o.IS_PARALLEL[tab["kind"]])
-    c, _ = o.parallel_measure_batch(tab["verts"][par], qb.positions)
-    sc = np.sqrt(c)
-    sysm = o.mollified_eigensystem(ref["f"][par] ** 2, sc * sc, tab["eps_x"][par], qb.kappa * qb.d_hat**4)
-    dl = sysm["lam_gamma1"] - sysm["lam_g1"]
-    with np.errstate(divide="ignore", invalid="ignore"):
-        amp_par = np.where(dl < 0, 4e-16 * np.abs(dl) / np.abs(8.0 * sysm["t"]), 0.0)
-    amp = np.zeros(len(table))
-    amp[par] = np.nan_to_num(amp_par, nan=0.0, posinf=0.0)
-    easy = amp < 1e-11
-    assert easy.mean() > 0.97
-    assert block_rel_err(hess[easy], ref["hess"][easy]) < TOL
+    assert entry_rel_err(grad, ref["grad"]) < TOL
+    assert_mollified_rows(tab, qb, hess, ref["hess"])
     check_psd_symmetric(hess)
+
+
+def assert_mollified_rows(tab, qb, hess, ref_hess, dt2=1.0):
+    """EVERY row at 1e-9, no carve-out.  The reference's k2 = (dl + 2p)/(8t) cancels when lam_gamma1 <
+    lam_g1 and |t| << |dl|, so a row is held to max(1e-9, its own fp64
+    noise) where the noise is what an 8-ulp change of the two channel eigenvalues does to the block in an
+    extended-precision evaluation of mollifier.py:113-127 (oracle.mollified_blocks_arbiter); the fp64
+    oracle is held to the same bound, and both are compared with the extended-precision block itself."""
+    arb, noise = o.mollified_blocks_arbiter(tab["kind"], tab["verts"], tab["sub"], tab["eps_x"], qb.positions,
+                                            qb.d_hat, qb.kappa, dt2=dt2)
+    bound = np.maximum(TOL, noise)
+    err = row_rel_err(hess, ref_hess)
+    assert np.all(err <= bound), f"{(err > bound).sum()} rows beyond max(1e-9, noise): worst {err.max():.3e}"
+    par = np.flatnonzero(o.IS_PARALLEL[tab["kind"]])
+    assert np.all(row_rel_err(hess[par], arb[par]) <= bound[par])          # GPU vs extended precision
+    assert np.all(row_rel_err(ref_hess[par], arb[par]) <= bound[par])      # fp64 oracle vs extended precision
+    easy = noise < 1e-11
+    assert entry_rel_err(hess[easy], ref_hess[easy]) < TOL
+    return float((~easy).mean())
+
+
+def test_k2_cancellation_regime_vs_extended_precision(P):
+    """The regime the config-2 recipe hardly reaches: c -> eps_x (e' -> 0, so |t| << |dl| with
+    lam_gamma1 < lam_g1) through ``b200ipc_mollified_eigensystem``.  The GPU takes the reference's branch on
+    every row, and its eigenvector is as close to the extended-precision one as the fp64 reference formula
+    allows: within max(1e-12, the 8-ulp noise of the row)."""
+    rng = np.random.default_rng(7)
+    n = 200_000
+    g = rng.uniform(0.04, 0.95, n)
+    eps = np.full(n, 1e-3)
+    c = eps * (1.0 - 10.0 ** rng.uniform(-14, -0.01, n))
+    prm = P.barrier.BarrierParams(d_hat=1.0, kappa=1.0)
+    got = P.mollifier.mollified_eigensystem_batch(g, c, eps, prm)
+    ref = o.mollified_eigensystem(g, c, eps, 1.0)
+    dec = (np.abs(8.0 * ref["t"]) < 1e-12 * (np.abs(ref["lam_gamma1"]) + np.abs(ref["lam_g1"]))) | (ref["t"] == 0.0)
+    assert 0.05 < dec.mean() < 0.5                                         # both branches well populated
+    # ``log`` differs by an ulp between libm and CUDA, so |8t| may straddle the 1e-12 threshold on a handful of
+    # rows: those (and only those) may take the other branch
+    thr = 1e-12 * (np.abs(ref["lam_gamma1"]) + np.abs(ref["lam_g1"]))
+    same = np.abs(np.abs(8.0 * ref["t"]) / thr - 1.0) > 1e-6
+    assert (~same).sum() <= 20
+    for col, key in ((0, "lam_gamma1"), (1, "lam_g1"), (2, "t"), (3, "p"), (5, "lambda8p")):
+        np.testing.assert_allclose(got[:, col], ref[key], rtol=1e-12, atol=1e-300)
+    _, qg, qf = o.mollified_eigensystem_extended(g, c, eps, 1.0, dec)
+    dev = np.zeros(n)
+    for u in (8.0, -8.0):
+        _, qgu, qfu = o.mollified_eigensystem_extended(g, c, eps, 1.0, dec, u)
+        dev = np.maximum(dev, np.maximum(np.abs(qgu - qg), np.abs(qfu - qf)).astype(np.float64))
+    bound = np.maximum(1e-12, dev)
+    err_gpu = np.maximum(np.abs(got[:, 6] - qg), np.abs(got[:, 7] - qf)).astype(np.float64)
+    err_ref = np.maximum(np.abs(ref["q_gamma"] - qg), np.abs(ref["q_f"] - qf)).astype(np.float64)
+    assert np.all(err_gpu[same] <= bound[same]) and np.all(err_ref <= bound)
+    assert (err_ref > 1e-9).sum() > 1000                                   # the regime IS noisy in fp64 ...
+    assert np.median(err_gpu[same & (err_ref > 1e-9)]) <= 4.0 * np.median(err_ref[same & (err_ref > 1e-9)])   # ... equally on both sides
 
 
 def test_inactive_and_penetrating_rows(P):
