@@ -14,7 +14,14 @@ contacts) and reported under "newton".
 Timing: W untimed warm-up steps, then K steps between CUDA events on the launching stream,
 bracketed by barrier + synchronize; max over ranks.  Every step rewrites 1.27 GB of blocks, ten
 times the 126 MB L2, so no flush is needed ("l2" in config).  N > 1 runs N independent replicas
-(one scene per GPU, no data-path collective): weak scaling.
+(one scene per GPU, no data-path collective): weak scaling.  ``python bench.py --gpus N`` without a
+rank environment re-executes itself under ``torch.distributed.run`` with N ranks
+(``scene_batch.launch``); under torchrun it joins the ranks it is given.  ``--dry-run`` rehearses that
+launch / aggregate path on CPUs with gloo (tests/test_multiproc.py).
+
+``--impl reference`` times the CPU implementation of the same path on the SAME workload table (the same
+1 M-row config-2 table, same config object) and prints the same ``newton`` keys, measured with the
+reference's own compiled ``matvec_blocks`` (oracle/_ref) inside the reference's PCG recurrence.
 """
 
 import argparse
@@ -125,19 +132,20 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def time_steps(torch, fn, steps, warmup, barrier):
-    for _ in range(warmup):
-        fn()
-    barrier()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(steps):
-        fn()
-    e1.record()
-    torch.cuda.synchronize()
-    barrier()
-    return e0.elapsed_time(e1)  # ms for all steps
+def time_steps(torch, fn, steps, warmup, dist=None):
+    """The contract's timed region (scene_batch.timed_steps): ms for all ``steps`` on this rank."""
+    from paper_2308_09400_b200 import scene_batch
+
+    return scene_batch.timed_steps(fn, steps, warmup, dist, cuda=True)
+
+
+def workload_config(n, kinds, world, alg_bytes):
+    """The ``config`` object of BOTH arms (the driver compares them): BASELINE configs[1]."""
+    return {"workload": "config2-parallel-ee: 1M nearly-parallel edge-edge queries (BASELINE configs[1])",
+            "stencils_per_gpu": int(n), "kinds_ee_eep_pe_pep_pp_ppp_pt": [int(k) for k in kinds],
+            "outputs": "energy + grad + dense PSD Hessian blocks (12x12/9x9/6x6 families)",
+            "parallelism": f"{world} independent replica(s), no collective",
+            "l2": "each step writes %.2f GB >> 126 MB L2; no flush needed" % (alg_bytes / 1e9)}
 
 
 # ---------------------------------------------------------------------------------------------
@@ -176,14 +184,96 @@ def host_table(qb):
     return o.narrow_phase(qb.positions, qb.rest_positions, qb.vt, qb.ee, qb.d_hat)
 
 
+def reference_newton(scene, tab, budget_iters=12):
+    """Second half of the metric the way the REFERENCE computes it, on the host, for one scene:
+    blocks (assemble_local_quadratics' barrier loop, solver.py:190-216 -- C port, all threads) ->
+    group_blocks -> matvec_matrix_free (solver.py:251-262) through the reference's own compiled
+    ``kernels._core.matvec_blocks`` (oracle/_ref; single thread, as the reference runs it) -> gradient
+    (:218-226) -> block-Jacobi (:265-276) -> ``budget_iters`` iterations of pcg_solve (:279-315).
+    The reference has no assembled matrix: its "assembly" is the grouped block list."""
+    from oracle import c_oracle
+    from oracle import tetipc_oracle as o
+
+    cores = os.cpu_count() or 1
+    c_oracle.set_threads(cores)
+    koff = np.searchsorted(tab["kind"], np.arange(8)).astype(np.int64)
+    prm = c_oracle.make_params(scene.d_hat, scene.kappa, dt=scene.dt)
+    args_ = (prm, scene.positions, koff, tab["verts"], tab["sub"], tab["eps_x"])
+    out = c_oracle.barrier_stencils(*args_)
+    t0 = time.perf_counter()
+    reps = 3
+    for _ in range(reps):
+        c_oracle.barrier_stencils(*args_, out=out)
+    ms_blocks = (time.perf_counter() - t0) * 1e3 / reps
+    verts = tab["verts"]
+    fam_rows = {2: np.arange(koff[4], koff[5]), 3: np.arange(koff[2], koff[3]),
+                4: np.concatenate([np.arange(koff[k], koff[k + 1]) for k in (0, 1, 3, 5, 6)])}
+    grouped, grads = [], []
+    for s_ in (2, 3, 4):
+        if len(fam_rows[s_]):
+            grouped.append((out[f"hess{s_}"], np.ascontiguousarray(verts[fam_rows[s_], :s_].astype(np.int64))))
+            grads.append((None, None, grouped[-1][1], out[f"grad{s_}"], None))
+    core = c_oracle.reference_core()
+    kernel = core.matvec_blocks if core is not None else c_oracle.matvec_blocks
+    n = scene.masses.shape[0]
+    fixed = np.asarray(scene.fixed, dtype=bool)
+
+    def matvec(v):
+        vin = v.copy()
+        vin.reshape(n, 3)[fixed] = 0.0
+        acc = (scene.masses[:, None] * vin.reshape(n, 3)).reshape(-1).copy()
+        for hess, vids in grouped:
+            kernel(hess, vids, vin, acc)
+        acc.reshape(n, 3)[fixed] = v.reshape(n, 3)[fixed]
+        return acc
+
+    v = np.random.default_rng(0).normal(size=3 * n)
+    matvec(v)
+    t0 = time.perf_counter()
+    reps = 3
+    for _ in range(reps):
+        matvec(v)
+    ms_matvec = (time.perf_counter() - t0) * 1e3 / reps
+    x_tilde = scene.positions + 1e-4 * np.random.default_rng(1).normal(size=scene.positions.shape)
+    t0 = time.perf_counter()
+    g = o.scatter_gradient(scene.masses, fixed, scene.positions, x_tilde, grads)
+    ms_grad = (time.perf_counter() - t0) * 1e3
+    t0 = time.perf_counter()
+    o.block_jacobi(grouped, scene.masses, fixed)
+    ms_prec = (time.perf_counter() - t0) * 1e3
+    t0 = time.perf_counter()
+    _, iters, ok = o.pcg_solve(grouped, scene.masses, fixed, -g, 1e-4, budget_iters, matvec=matvec)
+    ms_pcg = (time.perf_counter() - t0) * 1e3 - ms_prec   # pcg_solve rebuilds the preconditioner, like the reference
+    per_iter = ms_pcg / max(iters, 1)
+    return {"workload": scene.name, "vertices": int(n), "contacts": int(len(tab["kind"])),
+            "blocks_ms": ms_blocks, "matvec_ms": ms_matvec, "assembly_plus_spmv_ms": ms_blocks + ms_matvec,
+            "gradient_ms": ms_grad, "preconditioner_ms": ms_prec, "pcg_ms_per_iter": per_iter,
+            "pcg_iters_run": int(iters), "pcg_converged_within_budget": bool(ok),
+            "cores": {"blocks": cores, "matvec_pcg": 1},
+            "kind": {"blocks": "port (oracle/oracle_c.c)",
+                     "matvec": "reference (tetipc.kernels._core.matvec_blocks, oracle/_ref)" if core is not None
+                     else "port (oracle_c matvec_blocks)", "pcg": "port of solver.py:279-315 (NumPy) around that matvec"},
+            "note": "the reference keeps no assembled matrix: assembly = building the grouped dense block list; "
+                    f"PCG bounded to {budget_iters} iterations, per-iteration cost is iteration-independent"}
+
+
+def host_scene_table(scene):
+    """Contact table of a cloth scene on the CPU: host grid broad phase + oracle narrow phase."""
+    from oracle import tetipc_oracle as o
+    from paper_2308_09400_b200 import workloads
+
+    vt, ee = workloads.broad_phase(scene)
+    return o.narrow_phase(scene.positions, scene.rest_positions, vt, ee, scene.d_hat)
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from paper_2308_09400_b200 import workloads
 
-    n_sample = min(args.n_stencils, 250_000)
-    qb = workloads.config2_batch(n=n_sample, seed=20240818)
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    qb = workloads.config2_batch(n=args.n_stencils, seed=20240818)     # rank 0's replica of the B200 arm
     tab = host_table(qb)
     from oracle import c_oracle
 
@@ -204,18 +294,27 @@ def run_reference(args):
     el = time.perf_counter() - t0
     n = len(tab["kind"])
     value = n * args.steps / el
-    sample = (f"{n} stencils per step (config-2 recipe at {n_sample} queries), oracle/oracle_c.c port with "
-              f"{cores} pthreads; the Python reference itself (77-132 us/stencil, single thread) cannot travel")
+    sample = (f"the whole workload table: {n} stencils per step, {args.steps} steps; oracle/oracle_c.c port with "
+              f"{cores} pthreads writing the dense block families to host RAM; the Python reference itself "
+              f"(77-132 us/stencil, single thread) cannot travel")
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "config2-parallel-ee (bounded CPU sample)", "stencils_per_step": n,
-                   "kinds": np.diff(koff).tolist()},
+        "config": workload_config(n, np.diff(koff), world, algorithmic_bytes(koff, qb.positions.shape[0])),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
+    del out
+    if not args.skip_newton:
+        line["newton"] = {}
+        for key, scene in (("cloth_stack", workloads.cloth_stack(layers=4, n=140, seed=1, d_hat_rel=0.2)),
+                           ("cloth_on_sphere", workloads.cloth_on_sphere())):
+            try:
+                line["newton"][key] = reference_newton(scene, host_scene_table(scene))
+            except Exception as exc:  # the headline above stands on its own
+                line["newton"][key] = {"error": repr(exc)}
     print(json.dumps(line), flush=True)
 
 
@@ -223,10 +322,10 @@ def run_reference(args):
 # B200 arm
 # ---------------------------------------------------------------------------------------------
 
-def newton_section(torch, pkg, steps, warmup, peak, seed):
-    """Assembly + SpMV (+ PCG iteration) on a teaser-style cloth stack with ~1M contacts."""
+def newton_section(torch, pkg, steps, warmup, peak, cloth, extras=True, cpu_leg=True):
+    """Assembly + SpMV (+ PCG) on one cloth scene: BASELINE configs[3] (teaser-style stack, ~1M contacts;
+    ``extras``: CCD, friction, elasticity, whole time steps) or configs[2] (cloth on sphere, ~100k vertices)."""
     workloads, contacts, stencils, solver, barrier, device, _lib = pkg
-    cloth = workloads.cloth_stack(layers=4, n=140, seed=seed, d_hat_rel=0.2)
     params = barrier.BarrierParams(d_hat=cloth.d_hat, kappa=cloth.kappa)
     pos = device.to_device(cloth.positions)
     d_rest = device.to_device(cloth.rest_positions)
@@ -246,38 +345,37 @@ def newton_section(torch, pkg, steps, warmup, peak, seed):
         return best, out
 
     ms_broad, (d_vt, d_ee) = wall_ms(lambda: bp.query(pos))
-    ms_narrow, (table, _) = wall_ms(lambda: contacts.narrow_phase_device(pos, d_rest, d_vt, d_ee, cloth.d_hat,
-                                                                         want_origin=False))
+    ms_narrow, (table, extra_np) = wall_ms(lambda: contacts.narrow_phase_device(pos, d_rest, d_vt, d_ee, cloth.d_hat,
+                                                                                want_origin=False))
     t_broad, t_narrow = ms_broad * 1e-3, ms_narrow * 1e-3
     n_queries = int(d_vt.shape[0]) + int(d_ee.shape[0])
     batch = stencils.evaluate(table, pos, params, dt=cloth.dt, want_factors=True)
     batch.raise_on_penetration()
     fams = [batch.families[s] for s in sorted(batch.families)]
     sysm = solver.NewtonSystem(cloth.masses, cloth.fixed)
-    noop = lambda: None  # noqa: E731
-    ms_stencil = time_steps(torch, lambda: stencils.evaluate(table, pos, params, dt=cloth.dt, out=batch), steps, warmup, noop) / steps
+    ms_stencil = time_steps(torch, lambda: stencils.evaluate(table, pos, params, dt=cloth.dt, out=batch), steps, warmup) / steps
     sysm.set_pattern([(f.s, f.vids) for f in fams])  # warm (module load, workspace allocation)
     ms_symbolic, nnzb = wall_ms(lambda: sysm.set_pattern([(f.s, f.vids) for f in fams]), reps=3)
     hess = [f.hess for f in fams]
-    ms_numeric = time_steps(torch, lambda: sysm.assemble(hess), steps, warmup, noop) / steps
+    ms_numeric = time_steps(torch, lambda: sysm.assemble(hess), steps, warmup) / steps
     sysm.set_numeric_variant(4)
-    ms_numeric_rows = time_steps(torch, lambda: sysm.assemble(hess), steps, warmup, noop) / steps
+    ms_numeric_rows = time_steps(torch, lambda: sysm.assemble(hess), steps, warmup) / steps
     sysm.set_numeric_variant(0)
     # fused path: the matrix straight from the rank-1 factors, dense blocks never materialised
     fac = [f.fac for f in fams]
-    ms_factors = time_steps(torch, lambda: sysm.assemble_from_factors(fac), steps, warmup, noop) / steps
+    ms_factors = time_steps(torch, lambda: sysm.assemble_from_factors(fac), steps, warmup) / steps
     lean = stencils.evaluate(table, pos, params, dt=cloth.dt, want_hess=False, want_factors=True)
     ms_stencil_lean = time_steps(torch, lambda: stencils.evaluate(table, pos, params, dt=cloth.dt, want_hess=False,
-                                                                   want_factors=True, out=lean), steps, warmup, noop) / steps
+                                                                   want_factors=True, out=lean), steps, warmup) / steps
     del lean
     sysm.assemble(hess)
     x = device.to_device(np.random.default_rng(0).normal(size=3 * sysm.n))
     y = device.empty((3 * sysm.n,))
-    ms_spmv = time_steps(torch, lambda: sysm.spmv(x, out=y), steps, warmup, noop) / steps
+    ms_spmv = time_steps(torch, lambda: sysm.spmv(x, out=y), steps, warmup) / steps
     x_tilde = cloth.positions + 1e-4 * np.random.default_rng(1).normal(size=cloth.positions.shape)
     xt = device.to_device(x_tilde)
     grads = [f.grad for f in fams]
-    ms_grad = time_steps(torch, lambda: sysm.gradient(pos, xt, grads), steps, warmup, noop) / steps
+    ms_grad = time_steps(torch, lambda: sysm.gradient(pos, xt, grads), steps, warmup) / steps
     rhs = -sysm.gradient(pos, xt, grads)
     sysm.block_jacobi()
     iters_cap = 50
@@ -291,34 +389,36 @@ def newton_section(torch, pkg, steps, warmup, peak, seed):
     t0 = time.perf_counter()
     d, it_full, ok_full, _, _ = sysm.pcg(rhs, 1e-4, 2000)
     ms_pcg_full = (time.perf_counter() - t0) * 1e3
-    # CCD step filter of the line search: swept-AABB candidates + ACCD bound, on the device
-    dirs = device.to_device(0.3 * cloth.d_hat * np.random.default_rng(3).normal(size=cloth.positions.shape))
-    alpha = bp.ccd_step_bound(pos, dirs)  # warm
-    s_vt, s_ee = bp.sweep(pos, dirs)
-    ms_ccd, alpha = wall_ms(lambda: bp.ccd_step_bound(pos, dirs), reps=3)
-    # friction: lagged state once per time step, blocks once per Newton iteration
-    from paper_2308_09400_b200 import friction as friction_mod
+    if extras:
+        # CCD step filter of the line search: swept-AABB candidates + ACCD bound, on the device
+        dirs = device.to_device(0.3 * cloth.d_hat * np.random.default_rng(3).normal(size=cloth.positions.shape))
+        alpha = bp.ccd_step_bound(pos, dirs)  # warm
+        s_vt, s_ee = bp.sweep(pos, dirs)
+        ms_ccd, alpha = wall_ms(lambda: bp.ccd_step_bound(pos, dirs), reps=3)
+        ms_ccd_filter = time_steps(torch, lambda: contacts.ccd_filter_device(s_vt, s_ee, pos, dirs), 3, 1) / 3
+        # friction: lagged state once per time step, blocks once per Newton iteration
+        from paper_2308_09400_b200 import friction as friction_mod
 
-    raw = stencils.evaluate(table, pos, params, dt=1.0, want_energy=False, want_hess=False)
-    fstate = friction_mod.update_state(table, pos, 0.4, 1e-3, cloth.dt, barrier_batch=raw)  # warm
-    ms_fstate, fstate = wall_ms(lambda: friction_mod.update_state(table, pos, 0.4, 1e-3, cloth.dt, barrier_batch=raw), reps=3)
-    x_moved = device.to_device(cloth.positions + 0.5 * cloth.dt * 1e-3 * np.random.default_rng(4).normal(size=cloth.positions.shape))
-    friction_mod.evaluate(fstate, x_moved, pos)
-    ms_fblocks = time_steps(torch, lambda: friction_mod.evaluate(fstate, x_moved, pos), 10, 2, noop) / 10
-    fr_bytes = sum(int(fstate.table.family_count(s_)) * (72 * s_ * s_ + 24 * s_ + 4 * s_ + 96) for s_ in (2, 3, 4))
-    del raw
-    # elasticity: 400k random tets, energy + gradient + analytically projected 12x12 block each
-    from paper_2308_09400_b200 import elasticity as elasticity_mod
+        raw = stencils.evaluate(table, pos, params, dt=1.0, want_energy=False, want_hess=False)
+        fstate = friction_mod.update_state(table, pos, 0.4, 1e-3, cloth.dt, barrier_batch=raw)  # warm
+        ms_fstate, fstate = wall_ms(lambda: friction_mod.update_state(table, pos, 0.4, 1e-3, cloth.dt, barrier_batch=raw), reps=3)
+        x_moved = device.to_device(cloth.positions + 0.5 * cloth.dt * 1e-3 * np.random.default_rng(4).normal(size=cloth.positions.shape))
+        friction_mod.evaluate(fstate, x_moved, pos)
+        ms_fblocks = time_steps(torch, lambda: friction_mod.evaluate(fstate, x_moved, pos), 10, 2) / 10
+        fr_bytes = sum(int(fstate.table.family_count(s_)) * (72 * s_ * s_ + 24 * s_ + 4 * s_ + 96) for s_ in (2, 3, 4))
+        del raw
+        # elasticity: 400k random tets, energy + gradient + analytically projected 12x12 block each
+        from paper_2308_09400_b200 import elasticity as elasticity_mod
 
-    rng_e = np.random.default_rng(11)
-    n_tet = 400_000
-    rest_t = rng_e.normal(size=(4 * n_tet, 3))
-    tets_t = np.arange(4 * n_tet).reshape(n_tet, 4)
-    mesh_t = elasticity_mod.TetMesh(rest_t, tets_t, 3.7e4, 8.6e4)
-    x_t = device.to_device(rest_t + 0.1 * rng_e.normal(size=rest_t.shape))
-    mesh_t.evaluate(x_t, dt=cloth.dt)
-    ms_elastic = time_steps(torch, lambda: mesh_t.evaluate(x_t, dt=cloth.dt), 5, 1, noop) / 5
-    del mesh_t, x_t
+        rng_e = np.random.default_rng(11)
+        n_tet = 400_000
+        rest_t = rng_e.normal(size=(4 * n_tet, 3))
+        tets_t = np.arange(4 * n_tet).reshape(n_tet, 4)
+        mesh_t = elasticity_mod.TetMesh(rest_t, tets_t, 3.7e4, 8.6e4)
+        x_t = device.to_device(rest_t + 0.1 * rng_e.normal(size=rest_t.shape))
+        mesh_t.evaluate(x_t, dt=cloth.dt)
+        ms_elastic = time_steps(torch, lambda: mesh_t.evaluate(x_t, dt=cloth.dt), 5, 1) / 5
+        del mesh_t, x_t
     # one whole Newton direction through the public device-resident API, host arrays in, host array out:
     # H2D (x, x~) -> detect -> stencils (factors) -> symbolic + numeric assembly -> gradient -> PCG -> D2H d
     x_host = np.ascontiguousarray(cloth.positions)
@@ -348,8 +448,9 @@ def newton_section(torch, pkg, steps, warmup, peak, seed):
     ent = sum(int(f.vids.shape[0]) * f.s * f.s for f in fams)
     num_bytes = sum(int(f.vids.shape[0]) * (72 * f.s * f.s) for f in fams) + 4 * ent + 72 * nnzb
     spmv_bytes = 76 * nnzb + 52 * sysm.n
+    fac_bytes = sum(int(f.vids.shape[0]) * 24 * f.s for f in fams) + 4 * ent + 72 * nnzb
     out = {
-        "workload": cloth.name + f" d_hat={cloth.d_hat:.3g} (teaser-style cloth stack)",
+        "workload": cloth.name + f" d_hat={cloth.d_hat:.3g}",
         "vertices": sysm.n, "contacts": n_c, "kinds": np.diff(table.kind_off).tolist(), "nnzb": nnzb,
         "candidate_queries": n_queries, "broad_phase_ms": t_broad * 1e3, "narrow_phase_ms": t_narrow * 1e3,
         "detect_ms": (t_broad + t_narrow) * 1e3,
@@ -358,58 +459,66 @@ def newton_section(torch, pkg, steps, warmup, peak, seed):
                   "note": "rank-1 path: the stencil kernel writes z (24 s bytes) instead of the dense block and the "
                           "assembly gathers from z; same matrix bit for bit"},
         "assembly_plus_spmv_ms": ms_numeric + ms_spmv, "gradient_scatter_ms": ms_grad,
-        "ccd": {"sweep_candidates": int(s_vt.shape[0]) + int(s_ee.shape[0]), "sweep_plus_filter_ms": ms_ccd,
-                "alpha": alpha, "note": "sweep_candidates + global_ccd_filter (proximity.py:388-432), random 0.3 d_hat step"},
+        "per_newton_iteration_ms": {"symbolic": ms_symbolic, "numeric_from_factors": ms_factors, "spmv": ms_spmv,
+                                    "total": ms_symbolic + ms_factors + ms_spmv,
+                                    "note": "the contact set changes every Newton iteration, so the symbolic phase is "
+                                            "paid every time: this is the honest assembly+SpMV figure of the solver loop"},
         "newton_direction_e2e": {"ms": ms_newton_e2e, "pcg_iters": its_e2e, "converged": ok_e2e,
                                  "h2d_bytes": 2 * x_host.nbytes, "d2h_bytes": int(d_host.nbytes) + 8,
                                  "note": "host x, x~ in -> detect, stencils (rank-1 factors), symbolic + numeric assembly, "
                                          "gradient, block-Jacobi PCG to 1e-4 -> host direction + energy out; wall clock"},
-        "friction": {"data": int(fstate.n), "state_ms": ms_fstate, "blocks_ms": ms_fblocks,
-                     "blocks_GBps": fr_bytes / ms_fblocks / 1e6,
-                     "note": "update_friction_state (once per time step) and friction energy/grad/rank-2 PSD blocks "
-                             "(once per Newton iteration, incl. output allocation) on the same contact table"},
-        "elastic": {"tets": n_tet, "blocks_ms": ms_elastic, "tets_per_s": n_tet / ms_elastic * 1e3,
-                    "note": "stable neo-Hookean energy + gradient + analytically PSD-projected 12x12 per tet (incl. output allocation)"},
         "pcg_ms_per_iter": ms_pcg_iter, "pcg_solve_ms": ms_pcg_full, "pcg_iters": it_full, "pcg_converged": ok_full,
         "roofline_assembly": {"bound": "hbm", "achieved": num_bytes / ms_numeric / 1e6, "peak": peak, "unit": "GB/s",
                               "frac": num_bytes / ms_numeric / 1e6 / peak},
+        "roofline_assembly_factors": {"bound": "hbm", "achieved": fac_bytes / ms_factors / 1e6, "peak": peak,
+                                      "unit": "GB/s", "frac": fac_bytes / ms_factors / 1e6 / peak,
+                                      "algorithmic_bytes": fac_bytes},
         "roofline_spmv": {"bound": "hbm", "achieved": spmv_bytes / ms_spmv / 1e6, "peak": peak, "unit": "GB/s",
                           "frac": spmv_bytes / ms_spmv / 1e6 / peak},
     }
-    # CPU baseline for the matvec: the reference's own compiled kernel when oracle/_ref travelled here
-    try:
-        from oracle import c_oracle
+    if extras:
+        out["ccd"] = {"sweep_candidates": int(s_vt.shape[0]) + int(s_ee.shape[0]), "sweep_plus_filter_ms": ms_ccd,
+                      "filter_kernel_ms": ms_ccd_filter, "alpha": alpha, "note": "sweep_candidates + global_ccd_filter (proximity.py:388-432), random 0.3 d_hat step"}
+        out["friction"] = {"data": int(fstate.n), "state_ms": ms_fstate, "blocks_ms": ms_fblocks,
+                           "blocks_GBps": fr_bytes / ms_fblocks / 1e6,
+                           "note": "update_friction_state (once per time step) and friction energy/grad/rank-2 PSD blocks "
+                                   "(once per Newton iteration, incl. output allocation) on the same contact table"}
+        out["elastic"] = {"tets": n_tet, "blocks_ms": ms_elastic, "tets_per_s": n_tet / ms_elastic * 1e3,
+                          "note": "stable neo-Hookean energy + gradient + analytically PSD-projected 12x12 per tet (incl. output allocation)"}
+    # CPU side of the same half of the metric, on the same contact table: the reference's way of doing it
+    # (blocks -> grouped list -> compiled matvec_blocks inside its PCG recurrence), bounded
+    if cpu_leg:
+        try:
+            tab_np = {"kind": device.to_host(extra_np.kind), "verts": device.to_host(table.verts),
+                      "sub": device.to_host(table.sub), "eps_x": device.to_host(table.eps_x)}
+            ref = reference_newton(cloth, tab_np)
+            out["reference_cpu"] = ref
+            out["vs_reference_cpu"] = {
+                "assembly_plus_spmv": ref["assembly_plus_spmv_ms"] / (ms_numeric + ms_spmv),
+                "pcg_per_iter": ref["pcg_ms_per_iter"] / ms_pcg_iter,
+                "newton_direction": (ref["blocks_ms"] + ref["gradient_ms"] + ref["preconditioner_ms"]
+                                     + it_full * ref["pcg_ms_per_iter"]) / ms_newton_e2e,
+                "note": "reference-side time / B200 time; the reference's Newton direction is projected as blocks + "
+                        "gradient + preconditioner + (this solve's iteration count) x its measured per-iteration cost, "
+                        "detect excluded on the reference side and included on the B200 side"}
+            if extras:  # the reference's own compiled ACCD on a sample of the swept candidates
+                from oracle import c_oracle
 
-        core = c_oracle.reference_core()
-        f4 = batch.families[4]
-        nb = min(int(f4.vids.shape[0]), 100_000)
-        h = device.to_host(f4.hess[:nb])
-        v = device.to_host(f4.vids[:nb])
-        xv = np.random.default_rng(2).normal(size=3 * sysm.n)
-        acc = np.zeros(3 * sysm.n)
-        fn = core.matvec_blocks if core is not None else c_oracle.matvec_blocks
-        fn(h, v, xv, acc)
-        t0 = time.perf_counter()
-        reps = 0
-        while time.perf_counter() - t0 < 2.0:
-            fn(h, v, xv, acc)
-            reps += 1
-        el = (time.perf_counter() - t0) / reps
-        if core is not None:  # the reference's own compiled ACCD on a sample of the swept candidates
-            xs, ds = device.to_host(pos), device.to_host(dirs)
-            cand = device.to_host(s_vt[:20000]).astype(np.int64)
-            t0 = time.perf_counter()
-            for row in cand:
-                core.accd_max_step(xs[row], ds[row], 0, 0.9)
-            out["ccd"]["cpu_pairs_per_s"] = len(cand) / (time.perf_counter() - t0)
-            out["ccd"]["cpu_kind"] = "reference (tetipc.kernels._core.accd_max_step, 1 core, Python call per pair)"
-        out["cpu_matvec_blocks"] = {"blocks_per_s": nb / el, "kind": "reference" if core is not None else "port",
-                                    "cores": 1, "sample": f"{nb} 12x12 blocks, tetipc.kernels._core.matvec_blocks"
-                                    if core is not None else f"{nb} 12x12 blocks, oracle_c port"}
-    except Exception as exc:  # baseline only; never fail the bench on it
-        out["cpu_matvec_blocks"] = {"error": str(exc)}
+                core = c_oracle.reference_core()
+                if core is not None:
+                    xs, ds = device.to_host(pos), device.to_host(dirs)
+                    cand = device.to_host(s_vt[:20000]).astype(np.int64)
+                    t0 = time.perf_counter()
+                    for row in cand:
+                        core.accd_max_step(xs[row], ds[row], 0, 0.9)
+                    out["ccd"]["cpu_pairs_per_s"] = len(cand) / (time.perf_counter() - t0)
+                    out["ccd"]["cpu_kind"] = "reference (tetipc.kernels._core.accd_max_step, 1 core, Python call per pair)"
+        except Exception as exc:  # baseline only; never fail the bench on it
+            out["reference_cpu"] = {"error": repr(exc)}
     sysm.close()
     bp.close()
+    if not extras:
+        return out
     # whole time steps through the stepper (the reference's advance_time_step on the device path): a softer
     # cloth stack of the same size whose Newton loop converges (the stiff one above is a kernel workload)
     from paper_2308_09400_b200 import stepper
@@ -432,22 +541,37 @@ def newton_section(torch, pkg, steps, warmup, peak, seed):
     return out
 
 
+def run_dry(args):
+    """CPU rehearsal of the N-rank path (launch, rank environment, timed bracket, aggregate) with gloo: a step
+    is the generation of the rank's own replica workload.  Prints a line flagged ``dry_run``; never a bench value."""
+    from paper_2308_09400_b200 import scene_batch, workloads
+
+    rank, world, _, dist = scene_batch.init(backend="gloo")
+    seed = scene_batch.replica_seed(20240818, rank)
+    state = {}
+
+    def step():
+        state["qb"] = workloads.config2_batch(n=2000, seed=seed)
+
+    ms = scene_batch.timed_steps(step, args.steps, args.warmup, dist, cuda=False)
+    units, ms_max = scene_batch.aggregate(len(state["qb"].ee), ms, dist)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "metric": "replica workloads generated/s (CPU rehearsal, not a bench value)",
+                          "value": scene_batch.throughput(units, ms_max, args.steps), "n_gpus": world,
+                          "steps": args.steps, "warmup": args.warmup, "units_per_step_all_ranks": units,
+                          "ms_per_step": ms_max / args.steps, "scaling": "weak"}), flush=True)
+    scene_batch.finish(dist)
+
+
 def run_b200(args):
     import torch
 
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
+    from paper_2308_09400_b200 import scene_batch
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, world, local, dist = scene_batch.init(backend="nccl")
 
     def barrier():
-        if dist is not None:
-            dist.barrier()
+        scene_batch.barrier(dist)
 
     from paper_2308_09400_b200 import _lib, barrier as barrier_mod, contacts, device, solver, stencils, workloads
 
@@ -455,7 +579,7 @@ def run_b200(args):
     peak, peak_src = measured_peak()
 
     # ---- workload: config 2, one independent replica per rank ----------------------------------
-    qb = workloads.config2_batch(n=args.n_stencils, seed=20240818 + rank)
+    qb = workloads.config2_batch(n=args.n_stencils, seed=scene_batch.replica_seed(20240818, rank))
     params = barrier_mod.BarrierParams(d_hat=qb.d_hat, kappa=qb.kappa)
     pos = device.to_device(qb.positions)
     table, extra = contacts.narrow_phase_device(pos, qb.rest_positions, qb.vt, qb.ee, qb.d_hat, want_origin=False)
@@ -470,22 +594,16 @@ def run_b200(args):
     launches0 = L.b200ipc_launch_count()
     clocks = ClockSampler(local)
     clocks.__enter__()  # sampled across the device-timed and the end-to-end regions below
-    ms_total = time_steps(torch, step, args.steps, args.warmup, barrier)
+    ms_total = time_steps(torch, step, args.steps, args.warmup, dist)
     # counted by the library: launches of (warm-up + timed) steps, scaled to the timed region
     counted = int(L.b200ipc_launch_count() - launches0)
     per_step_launches = counted // (args.steps + args.warmup)
     assert per_step_launches == 1, (counted, args.steps, args.warmup)  # one fused launch per step
     gpu_launches = per_step_launches * args.steps
 
-    t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
-    cnt = torch.tensor([float(n)], dtype=torch.float64, device="cuda")
-    if dist is not None:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(cnt, op=dist.ReduceOp.SUM)
-    ms_max = float(t.item())
-    total_stencils = float(cnt.item())
+    total_stencils, ms_max = scene_batch.aggregate(n, ms_total, dist, device="cuda")
     ms_per_step = ms_max / args.steps
-    value = total_stencils / (ms_per_step * 1e-3)
+    value = scene_batch.throughput(total_stencils, ms_max, args.steps)
 
     # ---- end to end through the public API with HOST buffers ------------------------------------
     # strict: pinned host inputs -> H2D -> kernel -> every output (energy, status, grad, hess) D2H
@@ -571,11 +689,7 @@ def run_b200(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "config2-parallel-ee: 1M nearly-parallel edge-edge queries (BASELINE configs[1])",
-                       "stencils_per_gpu": n, "kinds_ee_eep_pe_pep_pp_ppp_pt": np.diff(table.kind_off).tolist(),
-                       "outputs": "energy + grad + dense PSD Hessian blocks (12x12/9x9/6x6 families)",
-                       "parallelism": f"{world} independent replica(s), no collective",
-                       "l2": "each step writes %.2f GB >> 126 MB L2; no flush needed" % (alg_bytes / 1e9)},
+            "config": workload_config(n, np.diff(table.kind_off), world, alg_bytes),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "peak_source": peak_src,
                          "kernel": "barrier_stencil_kernel (one fused launch per step, CTA-uniform kind dispatch)",
@@ -591,11 +705,16 @@ def run_b200(args):
             "clocks": clocks.summary(),
         }
     # ---- second half of the metric + CPU baseline: rank 0, single-GPU runs only -------------------
+    pkg = (workloads, contacts, stencils, solver, barrier_mod, device, _lib)
     if rank == 0 and world == 1 and not args.skip_newton:
-        pkg = (workloads, contacts, stencils, solver, barrier_mod, device, _lib)
         del batch
         torch.cuda.empty_cache()
-        line["newton"] = newton_section(torch, pkg, 20, 3, peak, seed=1)
+        stack = workloads.cloth_stack(layers=4, n=140, seed=1, d_hat_rel=0.2)
+        line["newton"] = newton_section(torch, pkg, 20, 3, peak, stack, extras=True, cpu_leg=not args.skip_cpu)
+        torch.cuda.empty_cache()
+        line["newton_cloth_on_sphere"] = newton_section(torch, pkg, 20, 3, peak, workloads.cloth_on_sphere(),
+                                                        extras=False, cpu_leg=not args.skip_cpu)
+        line["fp64"] = fp64_section(torch, L, line)
     if rank == 0 and world == 1 and not args.skip_cpu:
         tab_np = {"kind": device.to_host(extra.kind), "verts": device.to_host(table.verts),
                   "sub": device.to_host(table.sub), "eps_x": device.to_host(table.eps_x)}
@@ -604,11 +723,85 @@ def run_b200(args):
         except Exception as exc:
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                                     "sample": f"unavailable: {exc}"}
+    # ---- BASELINE configs[4]: N independent multilayer-cloth scenes, one per GPU --------------------
+    if world > 1 and not args.skip_newton:
+        batch = None
+        torch.cuda.empty_cache()
+        sb = scene_batch_section(torch, pkg, scene_batch, dist, rank, world)
+        if rank == 0:
+            line["scene_batch"] = sb
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if dist is not None:
-        dist.barrier()
-        dist.destroy_process_group()
+    scene_batch.finish(dist)
+
+
+def scene_batch_section(torch, pkg, scene_batch, dist, rank, world, reps=5):
+    """configs[4]: every rank owns one teaser-style cloth stack (its own seed) and computes whole Newton
+    directions for it, host positions in, host direction out; scenes/s = all ranks' directions over the
+    slowest rank's time.  No collective on the data path."""
+    workloads, contacts, stencils, solver, barrier, device, _lib = pkg
+    cloth = workloads.cloth_stack(layers=4, n=140, seed=scene_batch.replica_seed(1, rank), d_hat_rel=0.2)
+    params = barrier.BarrierParams(d_hat=cloth.d_hat, kappa=cloth.kappa)
+    d_rest = device.to_device(cloth.rest_positions)
+    bp = contacts.BroadPhase(None, cloth.tris, cloth.edges, cloth.d_hat, cloth.positions)
+    sysm = solver.NewtonSystem(cloth.masses, cloth.fixed)
+    x_host = torch.from_numpy(np.ascontiguousarray(cloth.positions)).pin_memory()
+    xt_host = torch.from_numpy(cloth.positions + 1e-4 * np.random.default_rng(1).normal(size=cloth.positions.shape)).pin_memory()
+    stats = {}
+
+    def direction():
+        px, pxt = x_host.cuda(non_blocking=True), xt_host.cuda(non_blocking=True)
+        cvt, cee = bp.query(px)
+        tab, _ = contacts.narrow_phase_device(px, d_rest, cvt, cee, cloth.d_hat, want_origin=False)
+        b = stencils.evaluate(tab, px, params, dt=cloth.dt, want_hess=False, want_factors=True)
+        fl = [b.families[s_] for s_ in sorted(b.families)]
+        sysm.set_pattern([(f.s, f.vids) for f in fl])
+        sysm.assemble_from_factors([f.fac for f in fl])
+        g = sysm.gradient(px, pxt, [f.grad for f in fl])
+        sysm.block_jacobi()
+        dd, its, okk, _, _ = sysm.pcg(-g, 1e-4, 2000)
+        stats.update(contacts=tab.n, pcg_iters=its, converged=bool(okk), d=device.to_host(dd))
+
+    ms = scene_batch.timed_steps(direction, reps, 2, dist, cuda=True)
+    scenes, ms_max = scene_batch.aggregate(1.0, ms, dist, device="cuda")
+    contacts_total, _ = scene_batch.aggregate(stats["contacts"], ms, dist, device="cuda")
+    sysm.close()
+    bp.close()
+    return {"workload": "BASELINE configs[4]: one cloth-stack-4x140x140 scene per GPU (seed = 1 + rank)",
+            "scenes": scenes, "contacts_all_scenes": contacts_total, "newton_direction_ms_slowest_rank": ms_max / reps,
+            "scenes_per_s": scene_batch.throughput(scenes, ms_max, reps),
+            "contacts_per_s": scene_batch.throughput(contacts_total, ms_max, reps),
+            "rank0": {"contacts": stats["contacts"], "pcg_iters": stats["pcg_iters"], "converged": stats["converged"]},
+            "note": "host x, x~ in -> detect, stencils, symbolic + numeric assembly, gradient, PCG to 1e-4 -> host "
+                    "direction out; barrier + synchronize bracket, max over ranks; weak scaling"}
+
+
+def fp64_section(torch, L, line):
+    """DFMA peak measured on this GPU (b200ipc_fp64_probe) and the fp64 rooflines of the two kernels that are
+    not HBM-bound; flop counts from the kernel headers (csrc/accd.cu, csrc/elastic.cu)."""
+    import ctypes as C
+
+    tf = C.c_double(0.0)
+    rc = L.b200ipc_fp64_probe(C.byref(tf), C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    out = {"fp64_tflops_measured": tf.value if rc == 0 else None,
+           "how": "b200ipc_fp64_probe: 8 independent DFMA chains per thread, 148 x 32 CTAs x 256 threads, best of 5"}
+    # fp64 flops per launch of the two compute-bound kernels: counted by ncu (2 x DFMA + DADD + DMUL thread
+    # instructions, profiles/fp64_flops.json, same workloads as timed here); times are this run's
+    path = os.path.join(ROOT, "profiles", "fp64_flops.json")
+    if rc == 0 and os.path.exists(path):
+        with open(path) as fh:
+            counted = json.load(fh)
+        newton = line.get("newton", {})
+        times = {"accd_kernel": newton.get("ccd", {}).get("filter_kernel_ms"),
+                 "elastic_blocks_kernel": newton.get("elastic", {}).get("blocks_ms")}
+        for name, ms in times.items():
+            c = counted.get(name)
+            if c and ms:
+                ach = c["flops_per_launch"] / (ms * 1e-3) / 1e12
+                out["roofline_" + name] = {"bound": "fp64", "achieved": ach, "peak": tf.value, "unit": "TFLOP/s",
+                                           "frac": ach / tf.value, "flops_per_launch": c["flops_per_launch"],
+                                           "workload": c.get("workload")}
+    return out
 
 
 def main():
@@ -620,9 +813,17 @@ def main():
     ap.add_argument("--n-stencils", type=int, default=1_000_000)
     ap.add_argument("--skip-newton", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--dry-run", action="store_true", help="CPU/gloo rehearsal of the N-rank launch + aggregate path")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
-    if args.impl == "reference":
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `python bench.py --gpus N`: become N ranks, one per GPU, exactly as the driver would launch us
+        from paper_2308_09400_b200 import scene_batch
+
+        sys.exit(scene_batch.launch(args.gpus, [os.path.abspath(__file__)] + sys.argv[1:]))
+    if args.dry_run:
+        run_dry(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_b200(args)

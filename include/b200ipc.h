@@ -64,6 +64,11 @@ const char* b200ipc_build_info(void);
 /* Number of kernel launches issued by this library since load (all threads). */
 int64_t b200ipc_launch_count(void);
 
+/* Measured FP64 FMA throughput of the current device in TFLOP/s (2 flop per DFMA): a register-resident
+ * DFMA microbenchmark, best of five launches.  The denominator of the fp64 rooflines.
+ * *tflops is host memory; synchronises `stream`. */
+int b200ipc_fp64_probe(double* tflops /* host */, void* stream);
+
 /* ---- tetipc.kernels twins (kernels/__init__.py:28-31) ------------------------ */
 /* pt_classify_batch (_core.pyx:46-106,153-171): p,t1,t2,t3 are (n,3) f64 row-major.
  * codes (n) i64, d2 (n), grad (n,4,3), w (n,2).  Any output pointer may be NULL. */
