@@ -96,18 +96,23 @@ class BarrierBatch:
         """``[(hess, vids)]`` by ascending stencil size, as ``group_blocks`` returns (device tensors)."""
         return [(self.families[s].hess, self.families[s].vids) for s in sorted(self.families)]
 
-    def to_local_quadratics(self):
+    def to_local_quadratics(self, keep_inactive=False):
         """Host ``LocalQuadratic`` list in the reference's block order, inactive rows dropped
-        (solver.py:202-209)."""
+        (solver.py:202-209) unless ``keep_inactive`` (then one entry per table row, zeros for inactive rows:
+        the positional list ``barrier_gradient_blocks`` returns, solver.py:186-188).  Outputs that were not
+        requested from ``evaluate`` come back as ``None`` fields."""
         status = device.to_host(self.status)
         out = [None] * self.table.n
         off = self.table.kind_off
         for s, fam in self.families.items():
             rows = np.concatenate([np.arange(off[k], off[k + 1]) for k in FAMILY_KINDS[s]])
-            vids, grad, hess = (device.to_host(fam.vids), device.to_host(fam.grad), device.to_host(fam.hess))
+            vids = device.to_host(fam.vids)
+            grad = device.to_host(fam.grad) if fam.grad is not None else None
+            hess = device.to_host(fam.hess) if fam.hess is not None else None
             for j, r in enumerate(rows):
-                if status[r] == 0:
-                    out[r] = LocalQuadratic(vert_ids=vids[j].copy(), grad=grad[j].copy(), hess=hess[j].copy())
+                if status[r] == 0 or keep_inactive:
+                    out[r] = LocalQuadratic(vert_ids=vids[j].copy(), grad=None if grad is None else grad[j].copy(),
+                                            hess=None if hess is None else hess[j].copy())
         return [b for b in out if b is not None]
 
 
