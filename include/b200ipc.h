@@ -311,10 +311,20 @@ int b200ipc_assembly_destroy(b200ipc_assembly* h);
  * accumulates in shared memory).  Both are atomic-free and deterministic; results agree to
  * round-off.  Other values: B200IPC_EINVAL. */
 int b200ipc_assembly_set_variant(b200ipc_assembly* h, int32_t variant);
-/* Build the pattern and the source runs (sort by key).  fixed: device u8 (nverts).  Synchronises
- * `stream` and returns the number of 3x3 blocks in *nnzb_out (host).  The vids buffers must stay
- * valid until the next symbolic call: the descriptor tables of the numeric kernels are built from
- * them on the first numeric call that needs them (a Newton iteration uses one numeric path). */
+/* Symbolic phase choice.  0 (default) = row-wise: one warp per block-row builds the row's column set and
+ * source runs from the vertex-incidence runs (shared-memory hash set, ranks, stable placement; no global
+ * sort of the 16 n_c slots), falling back to 1 when a row has more than 256 distinct columns.  1 = sort by
+ * key (stable radix sort of every (row, col) slot).  Identical pattern, run order and matrices. */
+int b200ipc_assembly_set_symbolic(b200ipc_assembly* h, int32_t mode);
+/* out[4] (host) = {symbolic path that built the current pattern (1 sort, 2 row-wise), longest block row
+ * (-1: not measured), nnzb, kept source slots}.  B200IPC_ESTATE before the first symbolic call. */
+int b200ipc_assembly_stats(b200ipc_assembly* h, int64_t* out);
+/* Build the pattern and the source runs.   fixed: device u8 (nverts).  Synchronises
+ * `stream` once and returns the number of 3x3 blocks in *nnzb_out (host).  The vids buffers must stay
+ * valid until the next symbolic call (the sort path builds the descriptor tables of the numeric kernels
+ * from them on the first numeric call that needs them).  The row-wise numeric kernel (variant 4, or more
+ * than three families) addresses a row's blocks with 16 bits: it returns B200IPC_EINVAL for a pattern
+ * with a block row of 65535 or more entries; the per-block-run kernels have no such limit. */
 int b200ipc_assemble_symbolic(b200ipc_assembly* h, int64_t nverts, const uint8_t* fixed, int32_t nfam,
                               const int32_t* fam_s /* host */, const int64_t* fam_nb /* host */,
                               const int64_t* const* fam_vids /* host array of device ptrs */,

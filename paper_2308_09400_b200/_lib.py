@@ -86,6 +86,8 @@ SIGNATURES = {
     "b200ipc_assembly_create": [C.POINTER(_vp)],
     "b200ipc_assembly_destroy": [_vp],
     "b200ipc_assembly_set_variant": [_vp, _i32],
+    "b200ipc_assembly_set_symbolic": [_vp, _i32],
+    "b200ipc_assembly_stats": [_vp, C.POINTER(_i64)],
     "b200ipc_assemble_symbolic": [_vp, _i64, _vp, _i32, C.POINTER(_i32), C.POINTER(_i64), C.POINTER(_vp),
                                   C.POINTER(_i64), _vp],
     "b200ipc_assembly_pattern": [_vp, _vp, _vp, _vp],

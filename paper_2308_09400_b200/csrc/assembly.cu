@@ -18,69 +18,7 @@
 #include "launch.cuh"
 #include "../../include/b200ipc.h"
 
-namespace b200ipc {
-
-constexpr int kMaxFam = 7;  // family ids 0..6; 7 tags the diagonal mass slot in source descriptors
-constexpr int kAT = 256;
-
-struct FamDesc {
-  int32_t s[kMaxFam];
-  int64_t nb[kMaxFam];
-  int64_t ent_off[kMaxFam + 1];   // prefix of nb*s*s  (matrix slots, after the N diagonal slots)
-  int64_t vert_off[kMaxFam + 1];  // prefix of nb*s    (gradient slots)
-  const int64_t* vids[kMaxFam];
-  int32_t nfam;
-};
-
-struct HessPtrs {
-  const double* p[kMaxFam + 1];  // slot 7 = "no source" (null)
-};
-
-template <typename T>
-struct DevBuf {
-  T* ptr = nullptr;
-  size_t cap = 0;
-  cudaError_t reserve(size_t n) {
-    if (n <= cap) return cudaSuccess;
-    if (ptr) cudaFree(ptr);
-    ptr = nullptr;
-    cap = 0;
-    cudaError_t e = cudaMalloc(&ptr, n * sizeof(T));
-    if (e == cudaSuccess) cap = n;
-    return e;
-  }
-  void release() {
-    if (ptr) cudaFree(ptr);
-    ptr = nullptr;
-    cap = 0;
-  }
-};
-
-}  // namespace b200ipc
-
-struct b200ipc_assembly {
-  int64_t nverts = 0;
-  int64_t nslots = 0;      // N + sum nb*s*s
-  int64_t nvalid = 0;      // slots that survive the fixed-vertex filter
-  int64_t nnzb = 0;
-  int64_t ngslots = 0;     // sum nb*s
-  bool ready = false;
-  bool have_desc = false, have_fdesc = false, have_rows = false;   // descriptor tables are built on first use
-  int variant = 0;         // numeric kernel: 0 auto (per-block runs when applicable), 1 runs, 4 row-wise
-  b200ipc::FamDesc fam;
-  b200ipc::DevBuf<uint8_t> fixed;
-  b200ipc::DevBuf<uint64_t> keys_a, keys_b;
-  b200ipc::DevBuf<uint32_t> slot_a, slot_b;   // slot_b ends up as the sorted permutation
-  b200ipc::DevBuf<int32_t> head, useg;        // head flags / scan, run starts (nnzb+1)
-  b200ipc::DevBuf<uint32_t> desc;             // per sorted source: family << 30 | element offset / 3 (3 = mass slot)
-  b200ipc::DevBuf<uint32_t> fdesc;            // per sorted source, factor form: family | c-a+3 | b*D+3a
-  b200ipc::DevBuf<int32_t> rowptr, colidx;
-  b200ipc::DevBuf<uint32_t> gkeys_a, gkeys_b, gslot_a, gslot_b;
-  b200ipc::DevBuf<int32_t> gseg;              // (N+1) run starts per vertex
-  b200ipc::DevBuf<uint64_t> rs_desc, rs_dst;  // per row-source: chunk offset|family, 4 x u16 destination block
-  b200ipc::DevBuf<uint8_t> temp;
-  b200ipc::DevBuf<int64_t> scalars;           // device scratch for counts
-};
+#include "assembly.cuh"
 
 namespace b200ipc {
 
@@ -560,6 +498,13 @@ __global__ void __launch_bounds__(kAT) scatter_gradient_kernel(const __grid_cons
   a.out[t] = acc;
 }
 
+__global__ void __launch_bounds__(kAT) max_row_kernel(int64_t nverts, const int32_t* __restrict__ rowptr, int64_t* out) {
+  const int64_t v = (int64_t)blockIdx.x * kAT + threadIdx.x;
+  int len = v < nverts ? rowptr[v + 1] - rowptr[v] : 0;
+  len = __reduce_max_sync(0xffffffffu, len);
+  if ((threadIdx.x & 31) == 0 && len > 0) atomicMax(reinterpret_cast<unsigned long long*>(out), (unsigned long long)len);
+}
+
 static inline unsigned blocks_for(int64_t n) { return (unsigned)((n + kAT - 1) / kAT); }
 
 static int bits_for(uint64_t maxval) {
@@ -589,7 +534,7 @@ extern "C" int b200ipc_assembly_destroy(b200ipc_assembly* h) {
   h->fixed.release(); h->keys_a.release(); h->keys_b.release(); h->slot_a.release(); h->slot_b.release();
   h->head.release(); h->useg.release(); h->desc.release(); h->fdesc.release(); h->rowptr.release(); h->colidx.release();
   h->gkeys_a.release(); h->gkeys_b.release(); h->gslot_a.release(); h->gslot_b.release(); h->gseg.release(); h->rs_desc.release(); h->rs_dst.release();
-  h->temp.release(); h->scalars.release();
+  h->temp.release(); h->scalars.release(); h->row_counts.release(); h->row_base.release();
   delete h;
   return 0;
 }
@@ -604,6 +549,90 @@ extern "C" int b200ipc_assembly_destroy(b200ipc_assembly* h) {
     int _r = (expr);        \
     if (_r) return _r;      \
   } while (0)
+
+namespace b200ipc {
+int symbolic_by_rows(b200ipc_assembly* h, bool want_desc, bool want_fdesc, bool* overflow, cudaStream_t st);  // symbolic_rows.cu
+
+// Sort-based symbolic phase: every sub-block slot keyed by row*N+col, one stable LSD radix sort, run heads
+// -> colidx / rowptr / run starts.  Handles rows of any length; the row-wise phase falls back to it.
+static int symbolic_by_sort(b200ipc_assembly* h, cudaStream_t st) {
+  const FamDesc& fd = h->fam;
+  const int64_t nverts = h->nverts, n = h->nslots;
+  CK(h->keys_a.reserve(n)); CK(h->keys_b.reserve(n)); CK(h->slot_a.reserve(n)); CK(h->slot_b.reserve(n));
+  CK(h->head.reserve(n)); CK(h->rowptr.reserve(nverts + 1)); CK(h->scalars.reserve(4));
+
+  matrix_keys_kernel<<<blocks_for(n), kAT, 0, st>>>(fd, nverts, n, h->fixed.ptr, h->keys_a.ptr, h->slot_a.ptr);
+  RC(post_launch());
+
+  // stable LSD radix sort over the significant bits only; the sentinel N*N is the largest key
+  const uint64_t sentinel = (uint64_t)nverts * (uint64_t)nverts;
+  const int end_bit = bits_for(sentinel);
+  size_t tb = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, h->keys_a.ptr, h->keys_b.ptr, h->slot_a.ptr, h->slot_b.ptr, (int)n,
+                                     0, end_bit, st));
+  size_t tb2 = 0;
+  CK(cub::DeviceScan::InclusiveSum(nullptr, tb2, h->head.ptr, h->head.ptr, (int)n, st));
+  CK(h->temp.reserve(tb > tb2 ? tb : tb2));
+  CK(cub::DeviceRadixSort::SortPairs(h->temp.ptr, tb, h->keys_a.ptr, h->keys_b.ptr, h->slot_a.ptr, h->slot_b.ptr,
+                                     (int)n, 0, end_bit, st));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+
+  head_flags_kernel<<<blocks_for(n), kAT, 0, st>>>(n, sentinel, h->keys_b.ptr, h->head.ptr);
+  RC(post_launch());
+  CK(cub::DeviceScan::InclusiveSum(h->temp.ptr, tb2, h->head.ptr, h->head.ptr, (int)n, st));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  // nnzb = scan[n-1] and the number of kept slots, both with one synchronisation
+  first_sentinel_kernel<<<1, 1, 0, st>>>(n, sentinel, h->keys_b.ptr, h->scalars.ptr);
+  RC(post_launch());
+  int32_t nnzb32 = 0;
+  int64_t nvalid = 0;
+  CK(cudaMemcpyAsync(&nnzb32, h->head.ptr + (n - 1), sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&nvalid, h->scalars.ptr, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  h->nnzb = nnzb32;
+  h->nvalid = nvalid;
+  CK(h->colidx.reserve(h->nnzb)); CK(h->useg.reserve(h->nnzb + 1));
+  emit_pattern_kernel<<<blocks_for(n), kAT, 0, st>>>(n, nverts, h->keys_b.ptr, h->head.ptr, h->colidx.ptr,
+                                                     h->useg.ptr, h->rowptr.ptr);
+  RC(post_launch());
+  finish_pattern_kernel<<<1, 1, 0, st>>>(nverts, h->nnzb, h->nvalid, h->rowptr.ptr, h->useg.ptr);
+  RC(post_launch());
+  h->have_desc = h->have_fdesc = false;   // built from the slot permutation on first use
+  h->max_row = -1;
+  return 0;
+}
+
+// 32-bit source descriptors apply: <= 3 families (2-bit family field), element offsets inside the fields
+static bool dense_desc_fits(const FamDesc& fd) {
+  if (fd.nfam > 3) return false;
+  for (int f = 0; f < fd.nfam; ++f)
+    if (fd.nb[f] * 9 * fd.s[f] * fd.s[f] >= (3ll << 30)) return false;
+  return true;
+}
+static bool factor_desc_fits(const FamDesc& fd) {
+  if (fd.nfam > 3) return false;
+  for (int f = 0; f < fd.nfam; ++f)
+    if (fd.nb[f] * 3 * fd.s[f] >= (1ll << 27)) return false;
+  return true;
+}
+
+}  // namespace b200ipc
+
+extern "C" int b200ipc_assembly_set_symbolic(b200ipc_assembly* h, int32_t mode) {
+  if (!h || !(mode == 0 || mode == 1)) return B200IPC_EINVAL;
+  h->symbolic_mode = mode;
+  return 0;
+}
+
+extern "C" int b200ipc_assembly_stats(b200ipc_assembly* h, int64_t* out) {
+  if (!h || !out) return B200IPC_EINVAL;
+  if (!h->ready) return B200IPC_ESTATE;
+  out[0] = h->symbolic_used;
+  out[1] = h->max_row;
+  out[2] = h->nnzb;
+  out[3] = h->nvalid;
+  return 0;
+}
 
 extern "C" int b200ipc_assemble_symbolic(b200ipc_assembly* h, int64_t nverts, const uint8_t* fixed, int32_t nfam,
                                          const int32_t* fam_s, const int64_t* fam_nb, const int64_t* const* fam_vids,
@@ -628,35 +657,12 @@ extern "C" int b200ipc_assemble_symbolic(b200ipc_assembly* h, int64_t nverts, co
   h->nslots = nverts + fd.ent_off[nfam];
   h->ngslots = fd.vert_off[nfam];
   if (h->nslots >= (1ll << 31)) return B200IPC_EINVAL;  // int32 run offsets
-  const int64_t n = h->nslots;
 
   CK(h->fixed.reserve(nverts));
   CK(cudaMemcpyAsync(h->fixed.ptr, fixed, nverts, cudaMemcpyDeviceToDevice, st));
-  CK(h->keys_a.reserve(n)); CK(h->keys_b.reserve(n)); CK(h->slot_a.reserve(n)); CK(h->slot_b.reserve(n));
-  CK(h->head.reserve(n)); CK(h->rowptr.reserve(nverts + 1)); CK(h->scalars.reserve(4));
 
-  matrix_keys_kernel<<<blocks_for(n), kAT, 0, st>>>(fd, nverts, n, h->fixed.ptr, h->keys_a.ptr, h->slot_a.ptr);
-  RC(post_launch());
-
-  // stable LSD radix sort over the significant bits only; the sentinel N*N is the largest key
-  const uint64_t sentinel = (uint64_t)nverts * (uint64_t)nverts;
-  const int end_bit = bits_for(sentinel);
-  size_t tb = 0;
-  CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, h->keys_a.ptr, h->keys_b.ptr, h->slot_a.ptr, h->slot_b.ptr, (int)n,
-                                     0, end_bit, st));
-  size_t tb2 = 0;
-  CK(cub::DeviceScan::InclusiveSum(nullptr, tb2, h->head.ptr, h->head.ptr, (int)n, st));
-  CK(h->temp.reserve(tb > tb2 ? tb : tb2));
-  CK(cub::DeviceRadixSort::SortPairs(h->temp.ptr, tb, h->keys_a.ptr, h->keys_b.ptr, h->slot_a.ptr, h->slot_b.ptr,
-                                     (int)n, 0, end_bit, st));
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-
-  head_flags_kernel<<<blocks_for(n), kAT, 0, st>>>(n, sentinel, h->keys_b.ptr, h->head.ptr);
-  RC(post_launch());
-  CK(cub::DeviceScan::InclusiveSum(h->temp.ptr, tb2, h->head.ptr, h->head.ptr, (int)n, st));
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  // gradient runs (sort vertex slots by vertex id): queued before the host reads nnzb, so the device keeps
-  // working through that round trip
+  // incidence runs: the (block, local vertex) slots sorted by vertex, in list order inside a vertex.  The
+  // gradient scatter, the row-wise numeric kernel and the row-wise symbolic phase all walk them.
   const int64_t ng = h->ngslots;
   CK(h->gseg.reserve(nverts + 1));
   if (ng > 0) {
@@ -674,23 +680,16 @@ extern "C" int b200ipc_assemble_symbolic(b200ipc_assembly* h, int64_t nverts, co
   }
   lower_bound_kernel<<<blocks_for(nverts + 1), kAT, 0, st>>>(nverts, ng, h->gkeys_b.ptr, h->gseg.ptr);
   RC(post_launch());
-  // nnzb = scan[n-1] and the number of kept slots, both with one synchronisation
-  first_sentinel_kernel<<<1, 1, 0, st>>>(n, sentinel, h->keys_b.ptr, h->scalars.ptr);
-  RC(post_launch());
-  int32_t nnzb32 = 0;
-  int64_t nvalid = 0;
-  CK(cudaMemcpyAsync(&nnzb32, h->head.ptr + (n - 1), sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(&nvalid, h->scalars.ptr, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  h->nnzb = nnzb32;
-  h->nvalid = nvalid;
-  CK(h->colidx.reserve(h->nnzb)); CK(h->useg.reserve(h->nnzb + 1));
-  emit_pattern_kernel<<<blocks_for(n), kAT, 0, st>>>(n, nverts, h->keys_b.ptr, h->head.ptr, h->colidx.ptr,
-                                                     h->useg.ptr, h->rowptr.ptr);
-  RC(post_launch());
-  finish_pattern_kernel<<<1, 1, 0, st>>>(nverts, h->nnzb, h->nvalid, h->rowptr.ptr, h->useg.ptr);
-  RC(post_launch());
-  h->have_desc = h->have_fdesc = h->have_rows = false;
+
+  bool by_rows = h->symbolic_mode == 0;
+  if (by_rows) {
+    bool overflow = false;
+    RC(symbolic_by_rows(h, dense_desc_fits(fd), factor_desc_fits(fd), &overflow, st));
+    if (overflow) by_rows = false;   // some row has more distinct columns than the per-warp set holds
+  }
+  if (!by_rows) RC(symbolic_by_sort(h, st));
+  h->symbolic_used = by_rows ? 2 : 1;
+  h->have_rows = false;
   h->ready = true;
   if (nnzb_out) *nnzb_out = h->nnzb;
   return 0;
@@ -718,6 +717,18 @@ static int ensure_fdesc(b200ipc_assembly* h, cudaStream_t st) {
 
 static int ensure_rows(b200ipc_assembly* h, cudaStream_t st) {
   if (h->have_rows) return 0;
+  if (h->max_row < 0) {   // pattern from the sort path: measure the longest row once
+    CK(h->scalars.reserve(4));
+    CK(cudaMemsetAsync(h->scalars.ptr, 0, sizeof(int64_t), st));
+    max_row_kernel<<<blocks_for(h->nverts), kAT, 0, st>>>(h->nverts, h->rowptr.ptr, h->scalars.ptr);
+    RC(post_launch());
+    int64_t m = 0;
+    CK(cudaMemcpyAsync(&m, h->scalars.ptr, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    h->max_row = m;
+  }
+  // rs_dst packs the position of a destination block inside its row into 16 bits (0xffff = dropped)
+  if (h->max_row >= 0xffff) return B200IPC_EINVAL;
   const int64_t ng = h->ngslots;
   if (ng > 0) {
     CK(h->rs_desc.reserve(ng)); CK(h->rs_dst.reserve(ng));

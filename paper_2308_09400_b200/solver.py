@@ -62,6 +62,17 @@ class NewtonSystem:
         (see include/b200ipc.h)."""
         _lib.check(_lib.lib().b200ipc_assembly_set_variant(self._h, int(variant)), "assembly_set_variant")
 
+    def set_symbolic_mode(self, mode):
+        """0 = row-wise symbolic phase (default; sort path when a row has > 256 columns), 1 = sort by key."""
+        _lib.check(_lib.lib().b200ipc_assembly_set_symbolic(self._h, int(mode)), "assembly_set_symbolic")
+
+    def stats(self):
+        """{'symbolic': 'rows' | 'sort', 'max_row': longest block row (-1 = not measured), 'nnzb', 'sources'}."""
+        out = (C.c_int64 * 4)()
+        _lib.check(_lib.lib().b200ipc_assembly_stats(self._h, out), "assembly_stats")
+        return {"symbolic": {1: "sort", 2: "rows"}.get(int(out[0]), "?"), "max_row": int(out[1]),
+                "nnzb": int(out[2]), "sources": int(out[3])}
+
     def close(self):
         if getattr(self, "_h", None) is not None and self._h:
             _lib.lib().b200ipc_assembly_destroy(self._h)
