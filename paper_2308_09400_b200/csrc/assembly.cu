@@ -104,6 +104,12 @@ __global__ void finish_pattern_kernel(int64_t nverts, int64_t nnzb, int64_t nval
   useg[nnzb] = (int32_t)nvalid;
 }
 
+// sorted sources are contiguous: run u ends where run u+1 starts
+__global__ void __launch_bounds__(kAT) run_ends_kernel(int64_t nnzb, const int32_t* __restrict__ useg, int32_t* __restrict__ uend) {
+  const int64_t u = (int64_t)blockIdx.x * kAT + threadIdx.x;
+  if (u < nnzb) uend[u] = useg[u + 1];
+}
+
 // Source descriptors, written once per pattern in sorted order, 32 bits each: the numeric phase then
 // needs no integer division, no family search and a single address computation per source.
 //   block source : family (2 bits) << 30 | (element offset of the 3x3 sub-block) / 3
@@ -133,7 +139,8 @@ struct NumericArgs {
   int64_t nnzb;
   const uint8_t* fixed;
   const double* masses;
-  const int32_t* useg;
+  const int32_t* useg;      // run u = sources [useg[u], uend[u])
+  const int32_t* uend;
   const uint32_t* desc;
   double* vals;
 };
@@ -172,14 +179,14 @@ __device__ __forceinline__ void walk_runs(const ARGS& a, const uint32_t* __restr
   if (u0 >= a.nnzb) return;
   const int lane = threadIdx.x & 31;
   const int nb = (int)min((int64_t)kBlocksPerWarp, a.nnzb - u0);
-  const int32_t mine = a.useg[u0 + min(lane, nb)];
-  const int32_t span0 = __shfl_sync(0xffffffffu, mine, 0), span1 = __shfl_sync(0xffffffffu, mine, nb);
+  const int32_t mine = a.useg[u0 + min(lane, nb - 1)], mine_end = a.uend[u0 + min(lane, nb - 1)];
+  const int32_t span0 = __shfl_sync(0xffffffffu, mine, 0), span1 = __shfl_sync(0xffffffffu, mine_end, nb - 1);
   for (int32_t t = span0 + lane; t < span1; t += 32) touch_l1(desc + t);  // 128-byte lines, fire and forget
   const int g = lane / 9, e = lane - 9 * g;
   const int er = e / 3, ec = e - 3 * er;
   for (int i = 0; i < nb; ++i) {
     int32_t j0 = __shfl_sync(0xffffffffu, mine, i);
-    const int32_t j1 = __shfl_sync(0xffffffffu, mine, i + 1);
+    const int32_t j1 = __shfl_sync(0xffffffffu, mine_end, i);
     const int64_t u = u0 + i;
     double acc = 0.0;
     const uint32_t first = desc[j0];
@@ -244,6 +251,7 @@ struct FactorArgs {
   const uint8_t* fixed;
   const double* masses;
   const int32_t* useg;
+  const int32_t* uend;
   const uint32_t* fdesc;
   double* vals;
 };
@@ -534,7 +542,7 @@ extern "C" int b200ipc_assembly_destroy(b200ipc_assembly* h) {
   h->fixed.release(); h->keys_a.release(); h->keys_b.release(); h->slot_a.release(); h->slot_b.release();
   h->head.release(); h->useg.release(); h->desc.release(); h->fdesc.release(); h->rowptr.release(); h->colidx.release();
   h->gkeys_a.release(); h->gkeys_b.release(); h->gslot_a.release(); h->gslot_b.release(); h->gseg.release(); h->rs_desc.release(); h->rs_dst.release();
-  h->temp.release(); h->scalars.release(); h->row_counts.release(); h->row_base.release();
+  h->temp.release(); h->scalars.release(); h->uend.release(); h->row_len.release(); h->slab_col.release(); h->slab_beg.release(); h->slab_end.release();
   delete h;
   return 0;
 }
@@ -596,6 +604,9 @@ static int symbolic_by_sort(b200ipc_assembly* h, cudaStream_t st) {
                                                      h->useg.ptr, h->rowptr.ptr);
   RC(post_launch());
   finish_pattern_kernel<<<1, 1, 0, st>>>(nverts, h->nnzb, h->nvalid, h->rowptr.ptr, h->useg.ptr);
+  RC(post_launch());
+  CK(h->uend.reserve(h->nnzb + 1));
+  run_ends_kernel<<<blocks_for(h->nnzb), kAT, 0, st>>>(h->nnzb, h->useg.ptr, h->uend.ptr);
   RC(post_launch());
   h->have_desc = h->have_fdesc = false;   // built from the slot permutation on first use
   h->max_row = -1;
@@ -763,7 +774,7 @@ extern "C" int b200ipc_assemble_numeric(b200ipc_assembly* h, const double* masse
     if (h->fam.nb[f] * 9 * h->fam.s[f] * h->fam.s[f] >= (3ll << 30)) packed_ok = false;
   }
   a.nnzb = h->nnzb; a.fixed = h->fixed.ptr; a.masses = masses;
-  a.useg = h->useg.ptr; a.desc = h->desc.ptr; a.vals = vals;
+  a.useg = h->useg.ptr; a.uend = h->uend.ptr; a.desc = h->desc.ptr; a.vals = vals;
   if ((h->variant == 0 || h->variant == 1) && packed_ok) {  // per-block runs (gather of 3x3 sub-blocks)
     RC(ensure_desc(h, (cudaStream_t)stream));
     a.desc = h->desc.ptr;
@@ -795,7 +806,7 @@ extern "C" int b200ipc_assemble_numeric_factors(b200ipc_assembly* h, const doubl
     a.fp.p[f] = fam_fac[f];
   }
   RC(ensure_fdesc(h, (cudaStream_t)stream));
-  a.nnzb = h->nnzb; a.fixed = h->fixed.ptr; a.masses = masses; a.useg = h->useg.ptr; a.fdesc = h->fdesc.ptr;
+  a.nnzb = h->nnzb; a.fixed = h->fixed.ptr; a.masses = masses; a.useg = h->useg.ptr; a.uend = h->uend.ptr; a.fdesc = h->fdesc.ptr;
   a.vals = vals;
   const unsigned grid = (unsigned)((h->nnzb + kNumWarps * kBlocksPerWarp - 1) / (kNumWarps * kBlocksPerWarp));
   assemble_factors_kernel<<<grid, 32 * kNumWarps, 0, (cudaStream_t)stream>>>(a);

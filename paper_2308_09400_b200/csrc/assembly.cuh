@@ -70,6 +70,7 @@ struct b200ipc_assembly {
   b200ipc::DevBuf<uint64_t> rs_desc, rs_dst;  // per row-source: chunk offset|family, 4 x u16 destination block
   b200ipc::DevBuf<uint8_t> temp;
   b200ipc::DevBuf<int64_t> scalars;           // device scratch for counts
-  b200ipc::DevBuf<unsigned long long> row_counts, row_base;   // row-wise symbolic: (blocks << 32 | sources) per row, scan
+  b200ipc::DevBuf<int32_t> uend;                // run ends (a run is [useg[u], uend[u]); slab-spaced after the row-wise phase)
+  b200ipc::DevBuf<int32_t> row_len, slab_col, slab_beg, slab_end;   // row-wise symbolic phase: per-row slabs
 };
 
