@@ -369,6 +369,38 @@ int b200ipc_pcg(int64_t nverts, int64_t nnzb, const int32_t* rowptr, const int32
                 double* d, double rel_tol, int32_t max_iters, void* workspace, int64_t workspace_bytes,
                 b200ipc_pcg_result* result /* host */, void* stream);
 
+/* ---- multilevel additive Schwarz preconditioner -------------
+ * The reference package has only block_jacobi_preconditioner (solver.py:265-276); the paper's GPU solver adds
+ * the MAS preconditioner of Wu et al. 2022 and picks per simulation whichever is faster.  Same choice here:
+ * b200ipc_pcg stays the parity default, b200ipc_pcg_mas is the alternative.  One handle per scene/GPU.
+ *   order : Morton order of `positions` ((nverts,3) device f64; isotropic 10-bit cells over the largest
+ *           extent); NULL = index order.  Domains are runs of 32 vertices in that order.
+ *   setup : per level the 96x96 domain matrices (Galerkin, piecewise-constant prolongation) gathered from the
+ *           assembled BSR matrix, inverted (fp64 Gauss-Jordan in shared memory), stored symmetrised in fp32.
+ *           levels in {1, 2}.  Dirichlet vertices (`fixed`, u8 device, must stay valid while the handle is
+ *           used) are kept out of the coarse spaces, so corrections leave them exactly at rest.  Needs
+ *           b200ipc_mas_order first; call again whenever vals change.
+ *   apply : z = sum_l P_l D_l^-1 P_l^T r, (3 nverts) device vectors.
+ *   get_order : rank (nverts) i32 device = position of each vertex in the domain order. */
+typedef struct b200ipc_mas b200ipc_mas;
+int b200ipc_mas_create(b200ipc_mas** out);
+int b200ipc_mas_destroy(b200ipc_mas* h);
+int b200ipc_mas_order(b200ipc_mas* h, int64_t nverts, const double* positions, void* stream);
+int b200ipc_mas_get_order(b200ipc_mas* h, int32_t* rank, void* stream);
+int b200ipc_mas_setup(b200ipc_mas* h, int64_t nverts, int64_t nnzb, const int32_t* rowptr,
+                      const int32_t* colidx, const double* vals, const uint8_t* fixed, int32_t levels,
+                      void* stream);
+int b200ipc_mas_apply(b200ipc_mas* h, const double* r, double* z, void* stream);
+int64_t b200ipc_pcg_mas_workspace_bytes(int64_t nverts);
+/* pcg_solve (solver.py:279-315) driven by the MAS operator of `h`, one persistent cooperative kernel.  The
+ * loop STOPS ON THE REFERENCE'S RULE, measured with the block-Jacobi inverses `pinv`:
+ * r . P_bj r <= rel_tol * (r0 . P_bj r0); result->delta0 / delta_new are those two quantities.  rowptr,
+ * colidx, vals must be 16-byte aligned.  Synchronises `stream`; *result is host memory. */
+int b200ipc_pcg_mas(b200ipc_mas* h, int64_t nverts, int64_t nnzb, const int32_t* rowptr,
+                    const int32_t* colidx, const double* vals, const double* pinv, const uint8_t* fixed,
+                    const double* rhs, double* d, double rel_tol, int32_t max_iters, void* workspace,
+                    int64_t workspace_bytes, b200ipc_pcg_result* result /* host */, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -16,7 +16,7 @@ OBJ = os.path.join(CSRC, "_obj")
 LIB = os.path.join(HERE, "libb200ipc.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
-SOURCES = ["capi.cu", "classify.cu", "stencil.cu", "diag.cu", "matvec.cu", "assembly.cu", "symbolic_rows.cu", "spmv.cu", "pcg.cu", "narrow.cu", "broad.cu", "accd.cu", "friction.cu", "elastic.cu", "probe.cu"]
+SOURCES = ["capi.cu", "classify.cu", "stencil.cu", "diag.cu", "matvec.cu", "assembly.cu", "symbolic_rows.cu", "spmv.cu", "pcg.cu", "mas.cu", "narrow.cu", "broad.cu", "accd.cu", "friction.cu", "elastic.cu", "probe.cu"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -99,9 +99,18 @@ SIGNATURES = {
     "b200ipc_pcg_workspace_bytes": [_i64],
     "b200ipc_pcg": [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _dbl, _i32, _vp, _i64, C.POINTER(PcgResult),
                     _vp],
+    "b200ipc_mas_create": [C.POINTER(_vp)],
+    "b200ipc_mas_destroy": [_vp],
+    "b200ipc_mas_order": [_vp, _i64, _vp, _vp],
+    "b200ipc_mas_get_order": [_vp, _vp, _vp],
+    "b200ipc_mas_setup": [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _i32, _vp],
+    "b200ipc_mas_apply": [_vp, _vp, _vp, _vp],
+    "b200ipc_pcg_mas_workspace_bytes": [_i64],
+    "b200ipc_pcg_mas": [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _dbl, _i32, _vp, _i64,
+                        C.POINTER(PcgResult), _vp],
 }
 _RESTYPE = {"b200ipc_build_info": C.c_char_p, "b200ipc_launch_count": _i64,
-            "b200ipc_pcg_workspace_bytes": _i64}
+            "b200ipc_pcg_workspace_bytes": _i64, "b200ipc_pcg_mas_workspace_bytes": _i64}
 
 _lib = None
 

@@ -24,6 +24,7 @@ namespace b200ipc {
 
 constexpr int kPT = 256;
 constexpr int kMaxParts = 4096;
+constexpr double kPcgPinMb = 0.0;   // matrix bytes kept L2-resident across iterations (see spmv_stream.cuh)
 
 struct PcgArgs {
   int64_t n;
@@ -327,6 +328,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) pcg_stream_kernel(const __g
 
 int pick_lpr(int64_t n, int64_t nnzb);  // spmv.cu
 int stream_rows_per_chunk(int64_t n, int64_t nnzb);  // spmv.cu
+int64_t stream_pin_rows(int64_t n, int64_t nnzb, double budget_mb);  // spmv.cu
 
 }  // namespace b200ipc
 
@@ -361,7 +363,7 @@ extern "C" int b200ipc_pcg(int64_t n, int64_t nnzb, const int32_t* rowptr, const
   const char* mode = getenv("B200IPC_SPMV_MODE");
   const bool aligned = (((uintptr_t)vals | (uintptr_t)colidx | (uintptr_t)rowptr) & 15) == 0;
   if (aligned && !(mode && mode[0] == 'l')) {
-    StreamMatrix m{n, nnzb, stream_rows_per_chunk(n, nnzb), 0, rowptr, colidx, vals, nullptr};
+    StreamMatrix m{n, nnzb, stream_rows_per_chunk(n, nnzb), 0, rowptr, colidx, vals, nullptr, stream_pin_rows(n, nnzb, kPcgPinMb)};
 #ifdef B200IPC_PCG_TIMING
     m.dbg = reinterpret_cast<unsigned long long*>(w + 21 * n + 3072);  // inside the partial-sum scratch
     cudaMemsetAsync(m.dbg, 0, 3 * 148 * 8, st);

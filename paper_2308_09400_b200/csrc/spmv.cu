@@ -54,6 +54,16 @@ int stream_rows_per_chunk(int64_t n, int64_t nnzb) {
   return r < 3 ? 3 : (r > kMaxChunkRows ? kMaxChunkRows : r);
 }
 
+// Rows of the matrix to keep L2-resident across the iterations of a persistent solver loop: `budget_mb` MB of
+// (values + column indices), from row 0.  B200IPC_L2_PIN_MB overrides the budget (0 = no hints).
+int64_t stream_pin_rows(int64_t n, int64_t nnzb, double budget_mb) {
+  if (const char* env = getenv("B200IPC_L2_PIN_MB")) budget_mb = atof(env);
+  if (budget_mb <= 0.0 || n <= 0) return 0;
+  const double per_row = 76.0 * (double)nnzb / (double)n;
+  const double rows = budget_mb * 1e6 / per_row;
+  return rows >= (double)n ? n : (rows < 1.0 ? 1 : (int64_t)rows);
+}
+
 // Inverse of the diagonal 3x3 block of every row (closed-form adjugate / determinant).
 __global__ void __launch_bounds__(kST) block_jacobi_kernel(int64_t n, const int32_t* __restrict__ rowptr,
                                                            const int32_t* __restrict__ colidx,

@@ -107,6 +107,16 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                : "memory");
 }
 
+// global -> shared bulk copy with an L2 eviction-priority hint (pre-encoded createpolicy values)
+constexpr uint64_t kL2EvictFirst = 0x12F0000000000000ull, kL2EvictLast = 0x14F0000000000000ull;
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
 struct StreamMatrix {
   int64_t n;            // block rows
   int64_t nnzb;
@@ -116,6 +126,10 @@ struct StreamMatrix {
   const int32_t* colidx;   // 16-byte aligned
   const double* vals;      // 16-byte aligned
   unsigned long long* dbg; // timing builds only: per-CTA [full-wait, compute, empty-wait] clock sums
+  // L2 residency across the products of a persistent solver loop: chunks of rows below pin_rows are fetched
+  // with evict-last priority (they stay in the 126 MB L2 from one iteration to the next), the others with
+  // evict-first (they stream through without displacing them).  0 = no hints (single products).
+  int64_t pin_rows;
 };
 
 // Per-CTA streaming state; lives in registers (identical in every thread) and survives across the
@@ -185,7 +199,7 @@ __device__ __forceinline__ int64_t stream_chunk_row(const StreamMatrix& m, const
 // moves a 16-byte aligned superset of its span; only an array's very end may stick out of the
 // allocation, and there the last elements are patched with plain loads instead.
 __device__ __forceinline__ void stream_issue(const StreamMatrix& m, const StreamSmem& sm, uint32_t q, int64_t b0,
-                                             int64_t b1) {
+                                             int64_t b1, int64_t r0) {
   const int s = (int)(q % kStreamStages);
   uint64_t* bar = sm.full + s;
   if (b1 - b0 > kStageBlocks || b1 == b0) {  // oversize (or empty) chunk: reduced from global memory
@@ -208,8 +222,14 @@ __device__ __forceinline__ void stream_issue(const StreamMatrix& m, const Stream
   }
   const uint32_t vbytes = (uint32_t)(ve - va), cbytes = (uint32_t)(ce - ca);
   mbar_expect_tx(bar, vbytes + cbytes);
-  if (vbytes) bulk_g2s(sv, reinterpret_cast<const char*>(m.vals) + va, vbytes, bar);
-  if (cbytes) bulk_g2s(sc, reinterpret_cast<const char*>(m.colidx) + ca, cbytes, bar);
+  if (m.pin_rows > 0) {
+    const uint64_t policy = r0 < m.pin_rows ? kL2EvictLast : kL2EvictFirst;
+    if (vbytes) bulk_g2s_hint(sv, reinterpret_cast<const char*>(m.vals) + va, vbytes, bar, policy);
+    if (cbytes) bulk_g2s_hint(sc, reinterpret_cast<const char*>(m.colidx) + ca, cbytes, bar, policy);
+  } else {
+    if (vbytes) bulk_g2s(sv, reinterpret_cast<const char*>(m.vals) + va, vbytes, bar);
+    if (cbytes) bulk_g2s(sc, reinterpret_cast<const char*>(m.colidx) + ca, cbytes, bar);
+  }
 }
 
 // Three rows per warp trip: lane = 9 r + 3 i + j (r < 3) walks the blocks of row r; v / ci point at
@@ -300,7 +320,7 @@ __device__ __forceinline__ void stream_product(const StreamMatrix& m, const Stre
           hdr[1] = b0;
         }
         __syncwarp();  // header stores happen before lane 0's releasing arrive
-        if (lane == 0) stream_issue(m, sm, q, b0, b1);
+        if (lane == 0) stream_issue(m, sm, q, b0, b1, r0);
         ++q;
         if (q < issue_end) load_rows(q);  // in flight while the next stage drains
       }
