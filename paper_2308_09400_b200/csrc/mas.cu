@@ -47,6 +47,10 @@ constexpr int kLd = kDim + 1;       // shared-memory row stride of the matrix be
 constexpr int kInvThreads = 256;
 constexpr int kMaxLevels = 2;
 constexpr int kMaxParts = 4096;
+// Matrix bytes fetched with evict-last priority in the PCG loop; everything else streams evict-first, which is what
+// keeps the stored inverses (48 MB at 78 k vertices, evict-last loads) L2-resident from one iteration to the next:
+// measured 56.0 -> 47.7 us per iteration, DRAM reads 162 -> 102 MB per iteration.
+constexpr double kMasPinMb = 1.0;
 constexpr int kOffsets = kDom / 2 + 1;   // stored node-block diagonals: block (k, (k + o) mod 32), o = 0..16
 constexpr int64_t kInvFloats = (int64_t)kOffsets * 9 * kDom;   // fp32 entries of one stored inverse (symmetric half)
 
@@ -84,6 +88,7 @@ struct b200ipc_mas {
   b200ipc::mas::Buf<int32_t> rank;    // (nverts): rank of each vertex
   b200ipc::mas::Buf<float> inv[b200ipc::mas::kMaxLevels];   // stored inverses, (ndom, 17, 9, 32)
   b200ipc::mas::Buf<double> coarse;   // level-1 node residuals and corrections: 2 x 3 x nnode1
+  b200ipc::mas::Buf<int32_t> colrank;  // column indices renamed to ranks (the PCG loop's vectors are in domain order)
   b200ipc::mas::Buf<uint32_t> keys_a, keys_b, val_a, val_b;
   b200ipc::mas::Buf<unsigned long long> box;   // 6 order-preserving encodings: min xyz, max xyz
   b200ipc::mas::Buf<uint8_t> temp;
@@ -284,7 +289,7 @@ __device__ __forceinline__ void invert_in_place(double* A, double* Rp, double* C
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(kInvThreads) mas_setup_kernel(const __grid_constant__ SetupArgs a) {
+__global__ void __launch_bounds__(kInvThreads, 2) mas_setup_kernel(const __grid_constant__ SetupArgs a) {
   extern __shared__ __align__(16) double sm[];
   double* A = sm;                       // kDim x kLd
   double* Rp = sm + kDim * kLd;         // 3 x kDim
@@ -502,9 +507,14 @@ struct PcgMasArgs {
   const uint8_t* fixed;
   const double* rhs;
   double* d;
+  // every working vector lives in DOMAIN ORDER (position p = rank of the vertex), so that the update phase of a
+  // domain touches 32 consecutive vertices; the product reaches them through the renamed column indices
   double* buf[2];           // (n, 3, 2): (s_j, c_j) pairs, as in pcg_stream_kernel
   double* rbuf[2];
   double* q;
+  double* dm;               // the solution in domain order (scattered to d at the end)
+  double* pinvm;            // block-Jacobi inverses in domain order
+  uint8_t* fixedm;          // Dirichlet flags in domain order
   double* part;             // 4 * kMaxParts partial sums
   double rel_tol;
   int32_t max_iters;
@@ -561,36 +571,45 @@ __global__ void __launch_bounds__(kStreamThreads, 1) pcg_mas_kernel(const __grid
   // d += alpha c, s = level-0 correction of r', partial sums of r'.s and of the block-Jacobi norm r'.P_bj r'.
   auto update = [&](bool first, double alpha, const double* rold, double* rnew, double* bnew) {
     double acc_mas = 0.0, acc_bj = 0.0;
-    for (int64_t D = gwarp; D < h.ndom0; D += nwarps) {
-      const int32_t v = h.perm[kDom * D + lane];
+    // domains dealt round-robin over the CTAs first: every SM streams its share of the stored inverses
+    for (int64_t D = (int64_t)(threadIdx.x >> 5) * gridDim.x + blockIdx.x; D < h.ndom0; D += nwarps) {
+      const int64_t p = kDom * D + lane;
+      const bool in = p < a.n;
       double r0 = 0.0, r1 = 0.0, r2 = 0.0;
-      if (v >= 0) {
-        if (first) {
-          const bool fx = a.fixed[v];
+      bool fx = false;
+      if (in) {
+        double* pm = a.pinvm + 9 * p;
+        if (first) {   // bring the caller's arrays into domain order
+          const int32_t v = h.perm[p];
+          fx = a.fixed[v];
+          a.fixedm[p] = fx;
           r0 = fx ? 0.0 : a.rhs[3 * v]; r1 = fx ? 0.0 : a.rhs[3 * v + 1]; r2 = fx ? 0.0 : a.rhs[3 * v + 2];
-          a.d[3 * v] = a.d[3 * v + 1] = a.d[3 * v + 2] = 0.0;
+          a.dm[3 * p] = a.dm[3 * p + 1] = a.dm[3 * p + 2] = 0.0;
+#pragma unroll
+          for (int e = 0; e < 9; ++e) pm[e] = a.pinv[9 * v + e];
         } else {
-          r0 = rold[3 * v] - alpha * a.q[3 * v];
-          r1 = rold[3 * v + 1] - alpha * a.q[3 * v + 1];
-          r2 = rold[3 * v + 2] - alpha * a.q[3 * v + 2];
-          a.d[3 * v] += alpha * bnew[6 * v + 1];
-          a.d[3 * v + 1] += alpha * bnew[6 * v + 3];
-          a.d[3 * v + 2] += alpha * bnew[6 * v + 5];
+          fx = a.fixedm[p];
+          r0 = rold[3 * p] - alpha * a.q[3 * p];
+          r1 = rold[3 * p + 1] - alpha * a.q[3 * p + 1];
+          r2 = rold[3 * p + 2] - alpha * a.q[3 * p + 2];
+          a.dm[3 * p] += alpha * bnew[6 * p + 1];
+          a.dm[3 * p + 1] += alpha * bnew[6 * p + 3];
+          a.dm[3 * p + 2] += alpha * bnew[6 * p + 5];
         }
-        rnew[3 * v] = r0; rnew[3 * v + 1] = r1; rnew[3 * v + 2] = r2;
-        const double* p = a.pinv + 9 * v;
-        acc_bj += r0 * (p[0] * r0 + p[1] * r1 + p[2] * r2) + r1 * (p[3] * r0 + p[4] * r1 + p[5] * r2) +
-                  r2 * (p[6] * r0 + p[7] * r1 + p[8] * r2);
+        rnew[3 * p] = r0; rnew[3 * p + 1] = r1; rnew[3 * p + 2] = r2;
+        acc_bj += r0 * (pm[0] * r0 + pm[1] * r1 + pm[2] * r2) + r1 * (pm[3] * r0 + pm[4] * r1 + pm[5] * r2) +
+                  r2 * (pm[6] * r0 + pm[7] * r1 + pm[8] * r2);
       }
       double z0 = r0, z1 = r1, z2 = r2;
       if (h.debug != 1) domain_apply(h.inv0 + D * kInvFloats, lane, r0, r1, r2, z0, z1, z2);
-      if (v >= 0) {
-        bnew[6 * v] = z0; bnew[6 * v + 2] = z1; bnew[6 * v + 4] = z2;
-        if (first) bnew[6 * v + 1] = bnew[6 * v + 3] = bnew[6 * v + 5] = 0.0;   // beta = 0 makes the first direction s
+      if (in) {
+        bnew[6 * p] = z0; bnew[6 * p + 2] = z1; bnew[6 * p + 4] = z2;
+        if (first) bnew[6 * p + 1] = bnew[6 * p + 3] = bnew[6 * p + 5] = 0.0;   // beta = 0 makes the first direction s
         acc_mas += r0 * z0 + r1 * z1 + r2 * z2;
       }
       if (h.levels > 1) {
-        const double s0 = warp_sum(r0), s1 = warp_sum(r1), s2 = warp_sum(r2);
+        const bool use = in && !fx;
+        const double s0 = warp_sum(use ? r0 : 0.0), s1 = warp_sum(use ? r1 : 0.0), s2 = warp_sum(use ? r2 : 0.0);
         if (lane == 0) {
           h.r1[3 * D] = s0; h.r1[3 * D + 1] = s1; h.r1[3 * D + 2] = s2;
         }
@@ -622,9 +641,9 @@ __global__ void __launch_bounds__(kStreamThreads, 1) pcg_mas_kernel(const __grid
     if (threadIdx.x == 0) part_co[blockIdx.x] = t;
     grid.sync();
     for (int64_t t3 = tid; t3 < 3 * a.n; t3 += nthreads) {
-      const int64_t v = t3 / 3;
-      const int k = (int)(t3 - 3 * v);
-      if (!a.fixed[v]) bnew[6 * v + 2 * k] += h.y1[3 * (int64_t)(h.rank[v] >> 5) + k];
+      const int64_t p = t3 / 3;
+      const int k = (int)(t3 - 3 * p);
+      if (!a.fixedm[p]) bnew[6 * p + 2 * k] += h.y1[3 * (p >> 5) + k];
     }
     const double co = sum_parts(part_co, nparts, sh, &bc);
     grid.sync();
@@ -640,6 +659,16 @@ __global__ void __launch_bounds__(kStreamThreads, 1) pcg_mas_kernel(const __grid
   double beta = 0.0;
   int iters = 0, cur = 0;
 
+#ifdef B200IPC_PCG_TIMING
+  unsigned long long tm[4] = {0, 0, 0, 0}, t0, t1;
+#define MAS_TICK(k)                                            \
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));     \
+  tm[k] += t1 - t0;                                            \
+  t0 = t1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+#else
+#define MAS_TICK(k)
+#endif
   if (bj0 > 0.0 && delta0 > 0.0) {
     while (iters < a.max_iters && bj_new > a.rel_tol * bj0) {
       const double* bold = a.buf[cur];
@@ -654,21 +683,25 @@ __global__ void __launch_bounds__(kStreamThreads, 1) pcg_mas_kernel(const __grid
             return w.x + beta * w.y;
           },
           [&](int64_t row, int i, double yi) {
-            const double2 w = reinterpret_cast<const double2*>(bold)[3 * row + i];
+            const int64_t p = h.rank[row];   // rows stream in matrix order; their vector entries sit at the rank
+            const double2 w = reinterpret_cast<const double2*>(bold)[3 * p + i];
             const double cn = w.x + beta * w.y;
-            bnew[6 * row + 2 * i + 1] = cn;
-            a.q[3 * row + i] = yi;
+            bnew[6 * p + 2 * i + 1] = cn;
+            a.q[3 * p + i] = yi;
             acc += cn * yi;
           });
       {
         const double t = block_sum(acc, sh);
         if (threadIdx.x == 0) part_cq[blockIdx.x] = t;
       }
+      MAS_TICK(0)
       grid.sync();
       const double denom = sum_parts(part_cq, nparts, sh, &bc);
       if (denom <= 0.0) break;  // solver.py:305-306
       const double alpha = delta_new / denom;
+      MAS_TICK(1)
       update(false, alpha, a.rbuf[cur], a.rbuf[cur ^ 1], bnew);
+      MAS_TICK(2)
       grid.sync();
       const double delta_old = delta_new;
       delta_new = sum_parts(part_mas, nparts, sh, &bc);
@@ -677,9 +710,18 @@ __global__ void __launch_bounds__(kStreamThreads, 1) pcg_mas_kernel(const __grid
       beta = delta_new / delta_old;
       cur ^= 1;
       ++iters;
+      MAS_TICK(3)
     }
   }
   stream_drain(sm, st);
+#ifdef B200IPC_PCG_TIMING
+  if (threadIdx.x == 0 && blockIdx.x < 512)   // [product, barrier 1 + sums, update, barrier 2 + sums] ns per CTA
+    for (int k = 0; k < 4; ++k) part_co[512 * k + blockIdx.x] = (double)tm[k];
+#endif
+  for (int64_t t3 = tid; t3 < 3 * a.n; t3 += nthreads) {   // back to the caller's order
+    const int64_t p = t3 / 3;
+    a.d[3 * (int64_t)h.perm[p] + (t3 - 3 * p)] = a.dm[t3];
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     a.result->iters = iters;
     a.result->converged = (bj0 <= 0.0) || (bj_new <= a.rel_tol * bj0);
@@ -720,7 +762,7 @@ extern "C" int b200ipc_mas_create(b200ipc_mas** out) {
 extern "C" int b200ipc_mas_destroy(b200ipc_mas* h) {
   if (!h) return 0;
   h->perm.release(); h->rank.release(); h->inv[0].release(); h->inv[1].release(); h->coarse.release();
-  h->keys_a.release(); h->keys_b.release(); h->val_a.release(); h->val_b.release(); h->box.release(); h->temp.release();
+  h->colrank.release(); h->keys_a.release(); h->keys_b.release(); h->val_a.release(); h->val_b.release(); h->box.release(); h->temp.release();
   delete h;
   return 0;
 }
@@ -831,8 +873,19 @@ extern "C" int b200ipc_mas_apply(b200ipc_mas* h, const double* r, double* z, voi
 
 extern "C" int64_t b200ipc_pcg_mas_workspace_bytes(int64_t n) {
   if (n < 0) return 0;
-  return (int64_t)sizeof(double) * (7 * 3 * n + 4 * kMaxParts) + 256;
+  // 2 x (n,6) pairs, 2 r, q, d and the 3x3 inverses in domain order, the flags, the partial sums
+  return (int64_t)sizeof(double) * (8 * 3 * n + 9 * n + 4 * kMaxParts) + ((n + 255) & ~255ll) + 256;
 }
+
+namespace b200ipc {
+namespace mas {
+__global__ void __launch_bounds__(256) rename_columns_kernel(int64_t nnzb, const int32_t* __restrict__ colidx,
+                                                             const int32_t* __restrict__ rank, int32_t* __restrict__ out) {
+  const int64_t b = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (b < nnzb) out[b] = rank[colidx[b]];
+}
+}  // namespace mas
+}  // namespace b200ipc
 
 extern "C" int b200ipc_pcg_mas(b200ipc_mas* h, int64_t n, int64_t nnzb, const int32_t* rowptr, const int32_t* colidx,
                                const double* vals, const double* pinv, const uint8_t* fixed, const double* rhs, double* d,
@@ -847,8 +900,12 @@ extern "C" int b200ipc_pcg_mas(b200ipc_mas* h, int64_t n, int64_t nnzb, const in
   int dev = 0, sms = 0;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  StreamMatrix m{n, nnzb, b200ipc::stream_rows_per_chunk(n, nnzb), 0, rowptr, colidx, vals, nullptr,
-                 b200ipc::stream_pin_rows(n, nnzb, 0.0)};
+  // the product gathers from vectors kept in domain order: stream the column indices renamed to ranks
+  CK(h->colrank.reserve((size_t)nnzb));
+  rename_columns_kernel<<<nblk(nnzb), 256, 0, st>>>(nnzb, colidx, h->rank.ptr, h->colrank.ptr);
+  RC(post_launch());
+  StreamMatrix m{n, nnzb, b200ipc::stream_rows_per_chunk(n, nnzb), 0, rowptr, h->colrank.ptr, vals, nullptr,
+                 b200ipc::stream_pin_rows(n, nnzb, kMasPinMb)};
   CK(cudaFuncSetAttribute(pcg_mas_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kStreamSmemBytes));
   const int64_t nchunks = (n + m.rows_per_chunk - 1) / m.rows_per_chunk;
   int64_t grid = nchunks < sms ? nchunks : sms;
@@ -857,8 +914,10 @@ extern "C" int b200ipc_pcg_mas(b200ipc_mas* h, int64_t n, int64_t nnzb, const in
   PcgMasArgs a;
   a.n = n; a.pinv = pinv; a.fixed = fixed; a.rhs = rhs; a.d = d;
   a.buf[0] = w; a.buf[1] = w + 6 * n; a.rbuf[0] = w + 12 * n; a.rbuf[1] = w + 15 * n; a.q = w + 18 * n;
-  a.part = w + 21 * n;
+  a.dm = w + 21 * n; a.pinvm = w + 24 * n;
+  a.part = w + 33 * n;
   a.result = reinterpret_cast<b200ipc_pcg_result*>(a.part + 4 * kMaxParts);
+  a.fixedm = reinterpret_cast<uint8_t*>(a.part + 4 * kMaxParts) + 64;
   a.rel_tol = rel_tol; a.max_iters = max_iters;
   Hierarchy y = hierarchy_of(h);
   void* args[] = {(void*)&a, (void*)&m, (void*)&y};
