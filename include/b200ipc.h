@@ -304,12 +304,15 @@ int b200ipc_elastic_blocks(int64_t ntets, const int32_t* tets, const double* pos
 typedef struct b200ipc_assembly b200ipc_assembly;
 int b200ipc_assembly_create(b200ipc_assembly** out);
 int b200ipc_assembly_destroy(b200ipc_assembly* h);
-/* Numeric kernel choice.  0 (default) = automatic: per-block runs -- one warp owns eight consecutive
- * output blocks, prefetches their source descriptors and gathers the 3x3 sub-blocks -- whenever the
- * 32-bit descriptors apply (<= 3 families, each below 24 GiB), else row-wise.  1 = per-block runs;
- * 4 = row-wise (one warp per block-row reads every dense block once as contiguous three-row runs,
- * accumulates in shared memory).  Both are atomic-free and deterministic; results agree to
- * round-off.  Other values: B200IPC_EINVAL. */
+/* Numeric kernel choice.  0 (default) = automatic: per-block runs whenever the 32-bit descriptors apply
+ * (<= 3 families, each below 24 GiB) -- walker 2 while runs are short (fewer than 4 sources per block on
+ * average), else walker 1 -- and row-wise otherwise.  1 = per-block runs, three-group walker: one warp owns
+ * eight consecutive output blocks, prefetches their source descriptors, lanes (g, e) sum entry e of every
+ * third source.  2 = per-block runs, trio walker: three blocks per warp trip, nine lanes per block walk the
+ * whole run.  4 = row-wise (one warp per block-row reads every dense block once as contiguous three-row
+ * runs, accumulates in shared memory).  All are atomic-free and deterministic; results agree to round-off;
+ * b200ipc_assemble_numeric_factors follows the same choice and is bitwise equal to the dense path of the
+ * same walker.  Other values: B200IPC_EINVAL. */
 int b200ipc_assembly_set_variant(b200ipc_assembly* h, int32_t variant);
 /* Symbolic phase choice.  0 (default) = row-wise: one warp per block-row builds the row's column set and
  * source runs from the vertex-incidence runs (shared-memory hash set, ranks, stable placement; no global
@@ -338,7 +341,7 @@ int b200ipc_assemble_numeric(b200ipc_assembly* h, const double* masses,
                              double* vals, void* stream);
 /* Numeric assembly straight from the rank-1 factors of b200ipc_barrier_stencils_ex (barrier
  * families only; fam_fac[f]: device (nb,3s)); at most 3 families.  Bitwise identical to
- * b200ipc_assemble_numeric variant 1 on the dense blocks of the same factors. */
+ * b200ipc_assemble_numeric (walkers 1 / 2, same variant setting) on the dense blocks of the same factors. */
 int b200ipc_assemble_numeric_factors(b200ipc_assembly* h, const double* masses,
                                      const double* const* fam_fac /* host array of device ptrs */,
                                      double* vals, void* stream);

@@ -218,6 +218,61 @@ __device__ __forceinline__ void walk_runs(const ARGS& a, const uint32_t* __restr
   }
 }
 
+// Second walker: THREE output blocks per warp trip, nine lanes per block (lane = 9 r + e), each lane walking its
+// block's whole run, four sources per step.  The per-block overhead of walk_runs (run bounds by shuffle, head
+// test, two-shuffle tail: ~100 warp instructions against ~36 for an average run of nine sources) is shared by
+// three blocks and the three-group split disappears; the price is that a trio runs as long as its longest run.
+#ifndef B200IPC_ASM_TRIOS
+#define B200IPC_ASM_TRIOS 4
+#endif
+constexpr int kTriosPerWarp = B200IPC_ASM_TRIOS;
+
+template <typename ARGS, typename ENTRY>
+__device__ __forceinline__ void walk_trios(const ARGS& a, const uint32_t* __restrict__ desc, ENTRY entry) {
+  const int lane = threadIdx.x & 31;
+  const int r = lane / 9, e = lane - 9 * r;
+  const int er = e / 3, ec = e - 3 * er;
+  const int64_t first_trio = ((int64_t)blockIdx.x * kNumWarps + (threadIdx.x >> 5)) * kTriosPerWarp;
+#pragma unroll 1
+  for (int t = 0; t < kTriosPerWarp; ++t) {
+    const int64_t u = (first_trio + t) * 3 + r;
+    const bool valid = r < 3 && u < a.nnzb;
+    if (!__any_sync(0xffffffffu, valid)) return;
+    int32_t j0 = 0, j1 = 0;
+    double acc = 0.0;
+    bool unit = false;
+    if (valid) {
+      j0 = a.useg[u];
+      j1 = a.uend[u];
+      const uint32_t head = desc[j0];
+      if (head >= 0xC0000000u) {  // diagonal block: mass slot first
+        const uint32_t v = head & 0x3fffffffu;
+        unit = a.fixed[v];        // Dirichlet vertex: unit diagonal, nothing else
+        if (er == ec) acc = unit ? 1.0 : a.masses[v];
+        ++j0;
+        if (unit) j1 = j0;
+      }
+    }
+    const int len = j1 - j0;
+    const int maxlen = __reduce_max_sync(0xffffffffu, len);
+    const uint32_t* dj = desc + j0;
+    int k = 0;
+    for (; k + 4 <= maxlen; k += 4) {
+      const bool p0 = k < len, p1 = k + 1 < len, p2 = k + 2 < len, p3 = k + 3 < len;
+      const uint32_t d0 = p0 ? dj[k] : 0u, d1 = p1 ? dj[k + 1] : 0u, d2 = p2 ? dj[k + 2] : 0u, d3 = p3 ? dj[k + 3] : 0u;
+      const double v0 = p0 ? entry(d0, er, ec) : 0.0, v1 = p1 ? entry(d1, er, ec) : 0.0;
+      const double v2 = p2 ? entry(d2, er, ec) : 0.0, v3 = p3 ? entry(d3, er, ec) : 0.0;
+      if (p0) acc += v0;
+      if (p1) acc += v1;
+      if (p2) acc += v2;
+      if (p3) acc += v3;
+    }
+    for (; k < maxlen; ++k)
+      if (k < len) acc += entry(dj[k], er, ec);
+    if (valid) a.vals[9 * u + e] = acc;
+  }
+}
+
 __global__ void __launch_bounds__(32 * kNumWarps, 8) assemble_numeric_kernel(const __grid_constant__ NumericArgs a) {
   walk_runs(a, a.desc, [&](uint32_t d, int er, int ec) { return gather_entry(a, d, er, ec); });
 }
@@ -264,6 +319,14 @@ __device__ __forceinline__ double factor_entry(const FactorArgs& a, uint32_t d, 
 
 __global__ void __launch_bounds__(32 * kNumWarps, 8) assemble_factors_kernel(const __grid_constant__ FactorArgs a) {
   walk_runs(a, a.fdesc, [&](uint32_t d, int er, int ec) { return factor_entry(a, d, er, ec); });
+}
+
+__global__ void __launch_bounds__(32 * kNumWarps, 8) assemble_factors_trio_kernel(const __grid_constant__ FactorArgs a) {
+  walk_trios(a, a.fdesc, [&](uint32_t d, int er, int ec) { return factor_entry(a, d, er, ec); });
+}
+
+__global__ void __launch_bounds__(32 * kNumWarps, 8) assemble_numeric_trio_kernel(const __grid_constant__ NumericArgs a) {
+  walk_trios(a, a.desc, [&](uint32_t d, int er, int ec) { return gather_entry(a, d, er, ec); });
 }
 
 // ---- row-wise numeric assembly ------------------------------------------------------------------
@@ -532,7 +595,7 @@ extern "C" int b200ipc_assembly_create(b200ipc_assembly** out) {
 }
 
 extern "C" int b200ipc_assembly_set_variant(b200ipc_assembly* h, int32_t variant) {
-  if (!h || !(variant == 0 || variant == 1 || variant == 4)) return B200IPC_EINVAL;
+  if (!h || !(variant == 0 || variant == 1 || variant == 2 || variant == 4)) return B200IPC_EINVAL;
   h->variant = variant;
   return 0;
 }
@@ -775,11 +838,23 @@ extern "C" int b200ipc_assemble_numeric(b200ipc_assembly* h, const double* masse
   }
   a.nnzb = h->nnzb; a.fixed = h->fixed.ptr; a.masses = masses;
   a.useg = h->useg.ptr; a.uend = h->uend.ptr; a.desc = h->desc.ptr; a.vals = vals;
-  if ((h->variant == 0 || h->variant == 1) && packed_ok) {  // per-block runs (gather of 3x3 sub-blocks)
+  // automatic choice between the two per-block-run walkers: trios win while runs are short (cloth on sphere,
+  // 2.5 sources per block: 48 vs 60 us), the three-group walker when the diagonal runs are long (cloth stack,
+  // 9 per block, 46 on the diagonal: 299 vs 320 us); b200ipc_assemble_numeric_factors makes the same choice, so
+  // the two paths stay bitwise equal
+  const bool short_runs = h->nvalid < 4 * h->nnzb;
+  if ((h->variant == 1 || (h->variant == 0 && !short_runs)) && packed_ok) {  // per-block runs (gather of 3x3 sub-blocks)
     RC(ensure_desc(h, (cudaStream_t)stream));
     a.desc = h->desc.ptr;
     const unsigned grid = (unsigned)((h->nnzb + kNumWarps * kBlocksPerWarp - 1) / (kNumWarps * kBlocksPerWarp));
     assemble_numeric_kernel<<<grid, 32 * kNumWarps, 0, (cudaStream_t)stream>>>(a);
+    return post_launch();
+  }
+  if ((h->variant == 2 || h->variant == 0) && packed_ok) {  // per-block runs, three blocks per warp trip
+    RC(ensure_desc(h, (cudaStream_t)stream));
+    a.desc = h->desc.ptr;
+    const int64_t per_cta = (int64_t)kNumWarps * kTriosPerWarp * 3;
+    assemble_numeric_trio_kernel<<<(unsigned)((h->nnzb + per_cta - 1) / per_cta), 32 * kNumWarps, 0, (cudaStream_t)stream>>>(a);
     return post_launch();
   }
   RC(ensure_rows(h, (cudaStream_t)stream));
@@ -808,8 +883,14 @@ extern "C" int b200ipc_assemble_numeric_factors(b200ipc_assembly* h, const doubl
   RC(ensure_fdesc(h, (cudaStream_t)stream));
   a.nnzb = h->nnzb; a.fixed = h->fixed.ptr; a.masses = masses; a.useg = h->useg.ptr; a.uend = h->uend.ptr; a.fdesc = h->fdesc.ptr;
   a.vals = vals;
-  const unsigned grid = (unsigned)((h->nnzb + kNumWarps * kBlocksPerWarp - 1) / (kNumWarps * kBlocksPerWarp));
-  assemble_factors_kernel<<<grid, 32 * kNumWarps, 0, (cudaStream_t)stream>>>(a);
+  const bool short_runs = h->nvalid < 4 * h->nnzb;
+  if (h->variant == 1 || (h->variant != 2 && !short_runs)) {   // same walker as b200ipc_assemble_numeric: bitwise equal to it
+    const unsigned grid = (unsigned)((h->nnzb + kNumWarps * kBlocksPerWarp - 1) / (kNumWarps * kBlocksPerWarp));
+    assemble_factors_kernel<<<grid, 32 * kNumWarps, 0, (cudaStream_t)stream>>>(a);
+    return post_launch();
+  }
+  const int64_t per_cta = (int64_t)kNumWarps * kTriosPerWarp * 3;
+  assemble_factors_trio_kernel<<<(unsigned)((h->nnzb + per_cta - 1) / per_cta), 32 * kNumWarps, 0, (cudaStream_t)stream>>>(a);
   return post_launch();
 }
 
