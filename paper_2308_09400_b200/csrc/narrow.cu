@@ -231,24 +231,6 @@ __global__ void __launch_bounds__(kNT) narrow_gather_kernel(const GatherArgs a) 
 
 static inline unsigned nblocks(int64_t n) { return (unsigned)((n + kNT - 1) / kNT); }
 
-// Per-call scratch from the device's stream-ordered pool (cudaMallocAsync).  The pool's release
-// threshold is lifted once, so after the first call the buffers are recycled without touching the
-// driver: cudaMalloc / cudaFree per buffer cost ~30 ms per narrow phase.
-inline cudaError_t keep_pool_memory() {
-  static bool done = false;
-  if (done) return cudaSuccess;
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return e;
-  cudaMemPool_t pool;
-  e = cudaDeviceGetDefaultMemPool(&pool, dev);
-  if (e != cudaSuccess) return e;
-  uint64_t keep = ~0ull;
-  e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-  done = e == cudaSuccess;
-  return e;
-}
-
 template <typename T>
 struct Scratch {
   T* p = nullptr;

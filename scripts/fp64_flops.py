@@ -1,6 +1,6 @@
 """fp64 flops per launch of the compute-bound kernels, counted by ncu on the GPU box:
 2 x DFMA + DADD + DMUL thread-level instructions of accd_kernel (the CCD filter of the bench's cloth stack)
-and elastic_blocks_kernel (400 k tets), written to gpurun_out/fp64_flops.json (copy to profiles/).
+and the two elastic kernels (400 k tets), written to gpurun_out/fp64_flops.json (copy to profiles/).
 bench.py divides these by ITS OWN measured kernel times for the `bound: fp64` rooflines."""
 import csv
 import io
@@ -11,12 +11,13 @@ import sys
 METRICS = ["smsp__sass_thread_inst_executed_op_dfma_pred_on.sum", "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum",
            "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum", "gpu__time_duration.sum"]
 cmd = ["ncu", "--metrics", ",".join(METRICS), "--clock-control", "none", "--csv", "-k",
-       "regex:accd_kernel|elastic_blocks_kernel", sys.executable, "scripts/newton_ncu.py"]
+       "regex:accd_kernel|elastic_state_kernel|elastic_hessian_kernel", sys.executable, "scripts/newton_ncu.py"]
 out = subprocess.run(cmd, capture_output=True, text=True).stdout
 rows = list(csv.DictReader(io.StringIO(out[out.index('"ID"'):])))
 per = {}
 for r in rows:
-    name = "accd_kernel" if "accd_kernel" in r["Kernel Name"] else "elastic_blocks_kernel"
+    kn = r["Kernel Name"]
+    name = "accd_kernel" if "accd_kernel" in kn else ("elastic_state_kernel" if "elastic_state" in kn else "elastic_hessian_kernel")
     per.setdefault((name, r["ID"]), {})[r["Metric Name"]] = float(r["Metric Value"].replace(",", ""))
 res = {}
 launches = {}
@@ -29,6 +30,10 @@ for name, ls in launches.items():
                  "dfma": sum(m[METRICS[0]] for _, m in take), "dadd": sum(m[METRICS[1]] for _, m in take),
                  "dmul": sum(m[METRICS[2]] for _, m in take), "ncu_time_ns": sum(m[METRICS[3]] for _, m in take),
                  "launches_summed": len(take)}
+# the elastic blocks are two launches (eigen phase + write-out phase): one entry for the pair
+e1, e2 = res.pop("elastic_state_kernel"), res.pop("elastic_hessian_kernel")
+res["elastic_blocks_kernel"] = {k: e1[k] + e2[k] for k in e1}
+res["elastic_blocks_kernel"]["kernels"] = "elastic_state_kernel + elastic_hessian_kernel"
 res["accd_kernel"]["workload"] = "CCD filter of cloth-stack-4x140x140, random 0.3 d_hat step (bench newton.ccd)"
 res["elastic_blocks_kernel"]["workload"] = "400k random tets (bench newton.elastic)"
 json.dump(res, open("gpurun_out/fp64_flops.json", "w"), indent=1)
