@@ -15,7 +15,7 @@ import numpy as np
 
 from . import _lib, device
 from .barrier import LocalQuadratic
-from .proximity import KIND_SIZE, StencilTable
+from .proximity import KIND_CODE, KIND_SIZE, StencilKind, StencilTable
 from .stencils import BarrierBatch, DeviceStencilTable, Family, FAMILY_KINDS
 
 
@@ -206,9 +206,13 @@ def tangential_displacement(datum, positions, positions_start):
 def update_friction_state(stencils, barrier_gradients, positions, mu, eps_v, dt):
     """Twin of friction.py:148-171: list of ``FrictionDatum`` from the end-of-step contact set and the
     raw barrier gradients of its stencils."""
-    stencils = list(stencils)
-    if mu <= 0.0 or not stencils:
+    given = list(stencils)
+    if mu <= 0.0 or not given:
         return []
+    # the reference takes the stencils in any order with a positionally matched gradient list; the device table
+    # wants kind-sorted rows: sort with a (stable) permutation and hand the data back in the caller's order
+    order = sorted(range(len(given)), key=lambda i: KIND_CODE[StencilKind(given[i].kind.value)])
+    stencils = [given[i] for i in order]
     table = StencilTable.from_stencils(stencils)
     dev = DeviceStencilTable.from_host(table)
     fams = {}
@@ -216,7 +220,7 @@ def update_friction_state(stencils, barrier_gradients, positions, mu, eps_v, dt)
     for s in (2, 3, 4):
         rows = np.concatenate([np.arange(off[k], off[k + 1]) for k in FAMILY_KINDS[s]]).astype(np.int64)
         if rows.size:
-            g = np.stack([np.asarray(barrier_gradients[r], dtype=np.float64).reshape(3 * s) for r in rows])
+            g = np.stack([np.asarray(barrier_gradients[order[r]], dtype=np.float64).reshape(3 * s) for r in rows])
             fams[s] = Family(s, None, device.to_device(g), None)
     batch = BarrierBatch(dev, None, None, fams)
     state = update_state(dev, positions, mu, eps_v, dt, barrier_batch=batch)
@@ -228,5 +232,6 @@ def update_friction_state(stencils, barrier_gradients, positions, mu, eps_v, dt)
         for v in range(s):
             basis[3 * v:3 * v + 3, 0] = fr[v] * fr[4:7]
             basis[3 * v:3 * v + 3, 1] = fr[v] * fr[7:10]
-        out.append(FrictionDatum(stencil=stencils[r], lambda_n=float(fr[10]), basis_T=basis, mu=mu, eps_v=eps_v, dt=dt))
-    return out
+        out.append((order[r], FrictionDatum(stencil=stencils[r], lambda_n=float(fr[10]), basis_T=basis, mu=mu,
+                                            eps_v=eps_v, dt=dt)))
+    return [d for _, d in sorted(out, key=lambda t: t[0])]

@@ -88,7 +88,11 @@ class BarrierBatch:
 
     def raise_on_penetration(self):
         """The reference raises InterpenetrationError on d2 <= 0 (gap.py:61, solver.py:132)."""
-        if self.summary()[2]:
+        if self._summary is None and self.energy is None:   # evaluated without energies: count the flags alone
+            penetrating = int((self.status == 2).sum().item())
+        else:
+            penetrating = self.summary()[2]
+        if penetrating:
             bad = np.flatnonzero(device.to_host(self.status) == 2)
             raise InterpenetrationError(f"nonpositive squared distance on {bad.size} stencil(s), first row {bad[0]}")
 

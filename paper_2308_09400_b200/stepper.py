@@ -79,7 +79,8 @@ def _tet_materials(scene, materials, nt):
     mu, lam = np.zeros(nt), np.zeros(nt)
     if hasattr(materials, "lame_mu"):
         mu[:], lam[:] = materials.lame_mu, materials.lame_lambda
-    elif isinstance(materials, (list, tuple)) and hasattr(scene, "bodies") and len(materials) == len(scene.bodies):
+    elif (isinstance(materials, (list, tuple)) and hasattr(scene, "bodies") and len(materials) == len(scene.bodies)
+          and all(m is None or hasattr(m, "lame_mu") for m in materials)):   # not a (mu, lam) pair of arrays
         cursor = 0
         for i, body in enumerate(scene.bodies):
             k = int(np.asarray(body.tets).reshape(-1, 4).shape[0])
@@ -207,6 +208,7 @@ class SimState:
             fams.append(self.tet_mesh.evaluate(x, dt=dt, want_energy=False)[1])
         if table.n:
             batch = stencils.evaluate(table, x, self.config.barrier, dt=dt, want_energy=False)
+            batch.raise_on_penetration()   # _barrier_block -> build_diagonal_jacobian raises on d2 <= 0 (gap.py:61)
             fams += [batch.families[s] for s in sorted(batch.families)]
         if self.friction_state is not None and self.friction_state.n:
             fb = friction.evaluate(self.friction_state, x, x_start, want_energy=False)

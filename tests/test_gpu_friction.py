@@ -138,6 +138,17 @@ def test_reference_shaped_entry_points(F, z):
         r0, r1, r1p = o.f0_f1(un, float(z["eps_v"]), float(z["dt"]))
         assert abs(f0 - r0) <= 1e-12 * abs(r0) and abs(f1 - r1) <= 1e-12 and abs(f1p - r1p) <= 1e-12 * max(abs(r1p), 1)
     assert F.friction.update_friction_state(stencils, grads, z["x0"], 0.0, 1e-2, 0.01) == []
+    # the reference accepts the stencils in ANY order with a positionally matched gradient list (friction.py:148-171):
+    # a shuffled call returns the same data, in the caller's order
+    perm = np.random.default_rng(0).permutation(len(stencils))[:400]
+    sub_st, sub_g = [stencils[i] for i in perm], [grads[i] for i in perm]
+    shuffled = F.friction.update_friction_state(sub_st, sub_g, z["x0"], float(z["mu"]), float(z["eps_v"]), float(z["dt"]))
+    by_key = {(d.stencil.kind, tuple(d.stencil.verts)): d for d in data}
+    kept = [st for st in sub_st if (st.kind, tuple(st.verts)) in by_key]
+    assert [(d.stencil.kind, tuple(d.stencil.verts)) for d in shuffled] == [(st.kind, tuple(st.verts)) for st in kept]
+    for d in shuffled[::37]:
+        ref_d = by_key[(d.stencil.kind, tuple(d.stencil.verts))]
+        assert d.lambda_n == ref_d.lambda_n and np.array_equal(d.basis_T, ref_d.basis_T)
 
 
 def test_barrier_and_friction_families_assemble_together(F, z):

@@ -230,3 +230,26 @@ def test_cube_drop_with_friction_bounces_without_interpenetration(S):
     assert x[~sc.fixed, 2].min() > 0.0
     np.testing.assert_array_equal(x[sc.fixed], sc.positions[sc.fixed])
     state.close()
+
+
+def test_assembly_path_raises_on_interpenetration(S):
+    """The reference's assemble_local_quadratics -> _barrier_block -> build_diagonal_jacobian raises
+    InterpenetrationError on d2 <= 0 (gap.py:61-62); the device path must not hand back a direction built from
+    silently zeroed blocks."""
+    from paper_2308_09400_b200 import proximity
+    from paper_2308_09400_b200.gap import InterpenetrationError
+
+    z = load_golden("stepper_drop")
+    state = state_of(S, z)
+    x = state.positions().copy()
+    # a point-point stencil over two coincident vertices: d2 = 0
+    x[1] = x[0]
+    table = proximity.StencilTable(np.array([4], np.uint8), np.array([[0, 1, -1, -1]], np.int32), np.zeros(1, np.uint8),
+                                   np.zeros(1))
+    from paper_2308_09400_b200.stencils import DeviceStencilTable
+
+    dev = DeviceStencilTable.from_host(table)
+    xd = S.device.to_device(x)
+    with pytest.raises(InterpenetrationError):
+        state.assemble_local_quadratics(xd, xd, dev)
+    state.close()
