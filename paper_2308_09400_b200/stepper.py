@@ -43,6 +43,11 @@ class SolverConfig:
     accd_slack: float = 0.9
     line_search_floor: float = 1e-12
     mollify: bool = True
+    # not in the reference: which preconditioner drives pcg_solve.  "block_jacobi" is the reference's
+    # (solver.py:265-276); "mas" is the paper's alternative, domains re-ordered once per time
+    # step.  Both stop on the reference's block-Jacobi-norm rule.
+    preconditioner: str = "block_jacobi"
+    mas_levels: int = 1
 
     def __post_init__(self):
         if self.dt <= 0.0 or self.eps_d <= 0.0 or self.pcg_rel_tol <= 0.0:
@@ -51,6 +56,8 @@ class SolverConfig:
             raise ValueError(f"unknown mode {self.mode!r}")
         if self.mode == MODE_REFERENCE:
             raise NotImplementedError("the reference-IPC baseline mode is not part of the GPU path")
+        if self.preconditioner not in ("block_jacobi", "mas"):
+            raise ValueError(f"unknown preconditioner {self.preconditioner!r}")
 
 
 @dataclass
@@ -135,6 +142,7 @@ class SimState:
         self.system = NewtonSystem(masses, fixed)
         self.friction_state = None
         self._last_detect = None
+        self._mas_ordered = False
         if config.friction_mu > 0.0:
             self._refresh_friction(self.x)
 
@@ -243,11 +251,25 @@ def _search_direction(state, x, x_tilde, x_start, table):
     """Newton direction at x on the device: blocks -> BSR matrix -> gradient -> block-Jacobi PCG, fixed rows
     zeroed (solver.py:325-334).  Returns (direction (N,3) tensor, PCG iterations, PCG converged)."""
     cfg = state.config
-    fams = state.assemble_local_quadratics(x, x_start, table)
-    state.system.set_pattern([(f.s, f.vids) for f in fams])
-    state.system.assemble([f.hess for f in fams])
+    only_barrier = state.tet_mesh is None and not (state.friction_state is not None and state.friction_state.n)
+    if only_barrier and table.n:
+        # barrier blocks are rank one: assemble straight from the factors z, the dense blocks are never written
+        # (bitwise the same matrix, b200ipc_assemble_numeric_factors)
+        batch = stencils.evaluate(table, x, cfg.barrier, dt=cfg.dt, want_energy=False, want_hess=False, want_factors=True)
+        batch.raise_on_penetration()
+        fams = [batch.families[s] for s in sorted(batch.families)]
+        state.system.set_pattern([(f.s, f.vids) for f in fams])
+        state.system.assemble_from_factors([f.fac for f in fams])
+    else:
+        fams = state.assemble_local_quadratics(x, x_start, table)
+        state.system.set_pattern([(f.s, f.vids) for f in fams])
+        state.system.assemble([f.hess for f in fams])
     rhs = -state.gradient(x, x_tilde, fams)
-    flat, iters, ok, _, _ = state.system.pcg(rhs, cfg.pcg_rel_tol, cfg.pcg_max_iters)
+    if cfg.preconditioner == "mas" and not state._mas_ordered:
+        state.system.mas_order(x)          # once per time step: positions move by a fraction of d_hat per iteration
+        state._mas_ordered = True
+    flat, iters, ok, _, _ = state.system.pcg(rhs, cfg.pcg_rel_tol, cfg.pcg_max_iters,
+                                             preconditioner=cfg.preconditioner, mas_levels=cfg.mas_levels)
     direction = flat.view(-1, 3)
     direction[state._fixed_dev] = 0.0
     return direction, iters, ok
@@ -294,6 +316,7 @@ def advance_time_step(state):
     clock = time.perf_counter()
     state.x, state.v = _dev(state.x), _dev(state.v)      # host arrays assigned by the caller are welcome
     x_start = state.x        # iterates are never modified in place: no copies, and detect's cache applies
+    state._mas_ordered = False   # MAS domains follow the positions at the start of the step
     x_tilde = state._inertia_target(x_start)
     x, energy = x_start, state.evaluate_energy(x_start, x_tilde, x_start)
 
