@@ -46,6 +46,18 @@ x_t = device.to_device(rest_t + 0.1 * rng_e.normal(size=rest_t.shape))
 for _ in range(2):
     mesh_t.evaluate(x_t, dt=cloth.dt)
 sysm.block_jacobi()
+sysm.set_symbolic_mode(1)          # the sort-based symbolic phase, for comparison with the row-wise one above
+sysm.set_pattern([(f.s, f.vids) for f in fams])
+sysm.set_symbolic_mode(0)
+sysm.set_pattern([(f.s, f.vids) for f in fams])
+sysm.assemble_from_factors([f.fac for f in fams])
 if "--pcg" in sys.argv:
     sysm.pcg(-g, 1e-30, 20)
+    sysm.mas_order(pos)
+    for levels in (1, 2):
+        sysm.mas_setup(levels)
+        sysm._mas_stale = False
+        sysm.pcg(-g, 1e-30, 20, preconditioner="mas", mas_levels=levels)
+    sysm.mas_setup(1)
+    sysm.mas_apply(g)
 torch.cuda.synchronize()
