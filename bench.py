@@ -266,6 +266,104 @@ def host_scene_table(scene):
     return o.narrow_phase(scene.positions, scene.rest_positions, vt, ee, scene.d_hat)
 
 
+def _reference_package_path():
+    """Where the UNMODIFIED reference package can be imported from on this box: baseline/_ref (pip-installed by
+    __graft_entry__.build(), travels to the GPU box) or the read-only mount of the build container."""
+    for path in (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"):
+        if os.path.isdir(os.path.join(path, "tetipc")):
+            return path
+    return None
+
+
+def _reference_python_worker(job):
+    """One host process of the real-reference arm: the barrier loop of the reference's own
+    ``SimState.assemble_local_quadratics`` (solver.py:202-209 -> ``_barrier_block`` :177-184) over its chunk of
+    the table, through the reference's own functions, ``reps`` times.  Returns (seconds, blocks built)."""
+    path, kind, verts, sub, eps_x, positions, d_hat, kappa, dt, reps = job
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    import tetipc  # noqa: F401
+    from tetipc.barrier import BarrierParams, build_local_quadratic
+    from tetipc.gap import build_diagonal_jacobian
+    from tetipc.mollifier import build_mollified_local_quadratic
+    from tetipc.proximity import PARALLEL_KINDS, stencil_distance
+    from tetipc.proximity import ContactStencil, StencilKind
+
+    # table rows -> the reference's own ContactStencil objects (kind code = rank of the enum's value string; two bits
+    # per local index in `sub`); nothing of this repository is imported in the worker
+    order = sorted(StencilKind, key=lambda k: k.value)
+    size, sublen = (4, 4, 3, 4, 2, 4, 4), (0, 4, 0, 3, 0, 2, 0)
+    stencils = []
+    for i in range(len(kind)):
+        code = int(kind[i])
+        vs = tuple(int(v) for v in verts[i, :size[code]])
+        if sublen[code]:
+            sel = tuple((int(sub[i]) >> (2 * k)) & 3 for k in range(sublen[code]))
+            stencils.append(ContactStencil(kind=order[code], verts=vs, eps_x=float(eps_x[i]), edge_pair=(vs[:2], vs[2:]),
+                                           sub=sel, origin=None))
+        else:
+            stencils.append(ContactStencil(kind=order[code], verts=vs))
+    params = BarrierParams(d_hat=d_hat, kappa=kappa)
+    dt2, dhat2 = dt * dt, d_hat * d_hat
+    built = 0
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        for st in stencils:
+            if stencil_distance(st, positions).d2 >= dhat2:      # solver.py:203-205
+                continue
+            jac = build_diagonal_jacobian(st, positions, d_hat)
+            blk = (build_mollified_local_quadratic if st.kind in PARALLEL_KINDS else build_local_quadratic)(st, jac, params)
+            blk.grad *= dt2                                         # solver.py:207-208
+            blk.hess *= dt2
+            built += 1
+    return time.perf_counter() - t0, built
+
+
+class ReferencePython:
+    """The reference's own (pure-Python, single-threaded) per-stencil path fanned out over every host core on a
+    strided sample of the table; None when the package is not importable on this box."""
+
+    def __init__(self, tab, qb, cores, sample_rows):
+        self.path = _reference_package_path()
+        self.cores = cores
+        n = len(tab["kind"])
+        rows = np.unique(np.linspace(0, n - 1, min(sample_rows, n)).astype(np.int64))
+        self.n = len(rows)
+        chunks = np.array_split(rows, cores)
+        # a chunk keeps the table's kind order (rows ascend), so each is a valid kind-sorted table
+        self.jobs = []
+        for c in chunks:
+            if not len(c):
+                continue
+            verts = tab["verts"][c]
+            used, local = np.unique(verts[verts >= 0], return_inverse=True)   # ship only the vertices the chunk touches
+            lv = np.full(verts.shape, -1, dtype=verts.dtype)
+            lv[verts >= 0] = local
+            self.jobs.append((self.path, tab["kind"][c], lv, tab["sub"][c], tab["eps_x"][c],
+                              np.ascontiguousarray(qb.positions[used]), float(qb.d_hat), float(qb.kappa), 1.0, 1))
+        self.pool = None
+
+    def available(self):
+        return self.path is not None
+
+    def __enter__(self):
+        import multiprocessing as mp
+
+        # spawn, not fork: the B200 arm calls this with a CUDA context alive in the parent
+        self.pool = mp.get_context("spawn").Pool(len(self.jobs))
+        return self
+
+    def __exit__(self, *exc):
+        self.pool.close()
+        self.pool.join()
+
+    def step(self):
+        """One pass over the sample on all cores; returns wall seconds."""
+        t0 = time.perf_counter()
+        self.pool.map(_reference_python_worker, self.jobs)
+        return time.perf_counter() - t0
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -293,20 +391,39 @@ def run_reference(args):
         step()
     el = time.perf_counter() - t0
     n = len(tab["kind"])
-    value = n * args.steps / el
-    sample = (f"the whole workload table: {n} stencils per step, {args.steps} steps; oracle/oracle_c.c port with "
-              f"{cores} pthreads writing the dense block families to host RAM; the Python reference itself "
-              f"(77-132 us/stencil, single thread) cannot travel")
+    port_value = n * args.steps / el
+    port = {"value": port_value, "unit": UNIT, "cores": cores, "kind": "port", "ms_per_step": el / args.steps * 1e3,
+            "sample": (f"the whole workload table: {n} stencils per step, {args.steps} steps; oracle/oracle_c.c, a C port "
+                       f"of the reference's per-stencil path, {cores} pthreads writing the dense block families to host RAM")}
+    del out
+    # The reference's OWN implementation of the path: the pure-Python barrier loop of assemble_local_quadratics,
+    # unmodified, from the installed package (baseline/_ref), one process per host core.  It is the headline value
+    # of this arm when the package is importable; the C port above (~300 x faster than it) is reported next to it.
+    value, ms_step, baseline = port_value, port["ms_per_step"], dict(port)
+    ref_py = ReferencePython(tab, qb, cores, sample_rows=100_000)
+    if ref_py.available():
+        with ref_py:
+            for _ in range(min(args.warmup, 1)):
+                ref_py.step()
+            secs = [ref_py.step() for _ in range(args.steps)]
+        value = ref_py.n * args.steps / sum(secs)
+        ms_step = sum(secs) / args.steps * 1e3
+        baseline = {"value": value, "unit": UNIT, "cores": len(ref_py.jobs), "kind": "reference",
+                    "sample": (f"{ref_py.n} stencils per step (every {n // max(ref_py.n, 1)}th row of the {n}-row workload table, "
+                               f"all kinds in proportion), {args.steps} steps; the unmodified tetipc package from "
+                               f"{os.path.relpath(ref_py.path, ROOT) if ref_py.path.startswith(ROOT) else ref_py.path}: "
+                               f"stencil_distance -> build_diagonal_jacobian -> build_(mollified_)local_quadratic per stencil "
+                               f"(solver.py:177-209), {len(ref_py.jobs)} processes (the reference itself is single-threaded)")}
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(n, np.diff(koff), world, algorithmic_bytes(koff, qb.positions.shape[0])),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "cpu_baseline": baseline,
+        "c_port": port,
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
-    del out
     if not args.skip_newton:
         line["newton"] = {}
         for key, scene in (("cloth_stack", workloads.cloth_stack(layers=4, n=140, seed=1, d_hat_rel=0.2)),
@@ -748,6 +865,19 @@ def run_b200(args):
         except Exception as exc:
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                                     "sample": f"unavailable: {exc}"}
+        # and the reference's own pure-Python path (what `--impl reference` reports), on a small sample
+        try:
+            ref_py = ReferencePython(tab_np, qb, os.cpu_count() or 1, sample_rows=32_000)
+            if ref_py.available():
+                with ref_py:
+                    ref_py.step()
+                    sec = ref_py.step()
+                line["cpu_reference_python"] = {"value": ref_py.n / sec, "unit": UNIT, "cores": len(ref_py.jobs),
+                                                "kind": "reference",
+                                                "sample": f"{ref_py.n} stencils, one pass after a warm-up pass, "
+                                                          f"{len(ref_py.jobs)} processes of the unmodified tetipc package"}
+        except Exception as exc:
+            line["cpu_reference_python"] = {"value": None, "kind": "reference", "sample": f"unavailable: {exc}"}
     # ---- BASELINE configs[4]: N independent multilayer-cloth scenes, one per GPU --------------------
     if world > 1 and not args.skip_newton:
         batch = None
