@@ -245,7 +245,25 @@ def reference_newton(scene, tab, budget_iters=12):
     _, iters, ok = o.pcg_solve(grouped, scene.masses, fixed, -g, 1e-4, budget_iters, matvec=matvec)
     ms_pcg = (time.perf_counter() - t0) * 1e3 - ms_prec   # pcg_solve rebuilds the preconditioner, like the reference
     per_iter = ms_pcg / max(iters, 1)
+    # the reference's OWN pcg_solve (solver.py:279-315, its compiled matvec_blocks) to
+    # convergence on the same system -- wall time and iteration count -- when the package is importable
+    ref_solve = None
+    path = _reference_package_path()
+    if path is not None:
+        try:
+            if path not in sys.path:
+                sys.path.insert(0, path)
+            import tetipc.kernels as tk
+            from tetipc.solver import pcg_solve as ref_pcg_solve
+
+            t0 = time.perf_counter()
+            _, it_ref, ok_ref = ref_pcg_solve(grouped, scene.masses, fixed, -g, 1e-4, 2000)
+            ref_solve = {"ms": (time.perf_counter() - t0) * 1e3, "iters": int(it_ref), "converged": bool(ok_ref),
+                         "backend": tk.BACKEND, "note": "tetipc.solver.pcg_solve, unmodified, one process"}
+        except Exception as exc:
+            ref_solve = {"error": repr(exc)}
     return {"workload": scene.name, "vertices": int(n), "contacts": int(len(tab["kind"])),
+            "reference_pcg_solve": ref_solve,
             "blocks_ms": ms_blocks, "matvec_ms": ms_matvec, "assembly_plus_spmv_ms": ms_blocks + ms_matvec,
             "gradient_ms": ms_grad, "preconditioner_ms": ms_prec, "pcg_ms_per_iter": per_iter,
             "pcg_iters_run": int(iters), "pcg_converged_within_budget": bool(ok),
@@ -358,10 +376,13 @@ class ReferencePython:
         self.pool.join()
 
     def step(self):
-        """One pass over the sample on all cores; returns wall seconds."""
+        """One pass over the sample on all cores; returns wall seconds.  ``self.per_process`` keeps the rate each
+        worker saw for its own chunk (stencils/s of ONE reference process, the reference being single-threaded)."""
         t0 = time.perf_counter()
-        self.pool.map(_reference_python_worker, self.jobs)
-        return time.perf_counter() - t0
+        res = self.pool.map(_reference_python_worker, self.jobs)
+        el = time.perf_counter() - t0
+        self.per_process = [len(job[1]) / sec for job, (sec, _) in zip(self.jobs, res)]
+        return el
 
 
 def run_reference(args):
@@ -409,6 +430,7 @@ def run_reference(args):
         value = ref_py.n * args.steps / sum(secs)
         ms_step = sum(secs) / args.steps * 1e3
         baseline = {"value": value, "unit": UNIT, "cores": len(ref_py.jobs), "kind": "reference",
+                    "one_process": float(np.median(ref_py.per_process)),
                     "sample": (f"{ref_py.n} stencils per step (every {n // max(ref_py.n, 1)}th row of the {n}-row workload table, "
                                f"all kinds in proportion), {args.steps} steps; the unmodified tetipc package from "
                                f"{os.path.relpath(ref_py.path, ROOT) if ref_py.path.startswith(ROOT) else ref_py.path}: "
@@ -424,6 +446,33 @@ def run_reference(args):
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
+    # the vectorised NumPy oracle (one process) and the reference's own
+    # `bench-projection` command, for continuity with PAPER.md:784-802
+    try:
+        from oracle import tetipc_oracle as o_
+
+        rows = np.arange(0, n, max(1, n // 250_000))
+        t0 = time.perf_counter()
+        o_.local_quadratics_batch(tab["kind"][rows], tab["verts"][rows], tab["sub"][rows], tab["eps_x"][rows], qb.positions,
+                                  qb.d_hat, qb.kappa)
+        line["numpy_oracle"] = {"value": len(rows) / (time.perf_counter() - t0), "unit": UNIT, "cores": 1, "kind": "port",
+                                "sample": f"{len(rows)} stencils, oracle/tetipc_oracle.py local_quadratics_batch, one process"}
+    except Exception as exc:
+        line["numpy_oracle"] = {"error": repr(exc)}
+    path = _reference_package_path()
+    if path is not None:
+        import subprocess
+
+        proj = {}
+        for count in (100_000, 1_000_000):
+            try:
+                outp = subprocess.run([sys.executable, "-m", "tetipc.cli", "bench-projection", "--count", str(count), "--dim", "12"],
+                                      capture_output=True, text=True, timeout=300, env=dict(os.environ, PYTHONPATH=path),
+                                      cwd="/tmp").stdout.strip().splitlines()[-1]
+                proj[str(count)] = json.loads(outp)
+            except Exception as exc:
+                proj[str(count)] = {"error": repr(exc)}
+        line["reference_bench_projection"] = proj
     if not args.skip_newton:
         line["newton"] = {}
         for key, scene in (("cloth_stack", workloads.cloth_stack(layers=4, n=140, seed=1, d_hat_rel=0.2)),
@@ -640,7 +689,15 @@ def newton_section(torch, pkg, steps, warmup, peak, cloth, extras=True, cpu_leg=
                 "pcg_per_iter": ref["pcg_ms_per_iter"] / ms_pcg_iter,
                 "newton_direction": (ref["blocks_ms"] + ref["gradient_ms"] + ref["preconditioner_ms"]
                                      + it_full * ref["pcg_ms_per_iter"]) / ms_newton_e2e,
-                "note": "reference-side time / B200 time; the reference's Newton direction is projected as blocks + "
+                "pcg_solve": (ref["reference_pcg_solve"]["ms"] / ms_pcg_full
+                              if ref.get("reference_pcg_solve") and "ms" in ref["reference_pcg_solve"] else None),
+                "pcg_solve_vs_mas": (ref["reference_pcg_solve"]["ms"] / mas["levels_1"]["setup_plus_solve_ms"]
+                                     if ref.get("reference_pcg_solve") and "ms" in ref["reference_pcg_solve"] else None),
+                "pcg_iters_reference_vs_here": ([ref["reference_pcg_solve"].get("iters"), it_full]
+                                                if ref.get("reference_pcg_solve") else None),
+                "note": "reference-side time / B200 time; pcg_solve = the unmodified tetipc.solver.pcg_solve to 1e-4 on the "
+                        "same system against NewtonSystem.pcg (block-Jacobi) and against MAS setup + solve; "
+                        "the reference's Newton direction is projected as blocks + "
                         "gradient + preconditioner + (this solve's iteration count) x its measured per-iteration cost, "
                         "detect excluded on the reference side and included on the B200 side"}
             if extras:  # the reference's own compiled ACCD on a sample of the swept candidates

@@ -19,7 +19,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "--child":
     out = []
     for R in os.environ.get("PROBE_R", "0").split(","):
         if R != "0": os.environ["B200IPC_SPMV_ROWS_PER_CHUNK"] = R
-        sp = bench.time_steps(torch, lambda: sysm.spmv(x, out=y), 100, 5, lambda: None) / 100
+        sp = bench.time_steps(torch, lambda: sysm.spmv(x, out=y), 100, 5) / 100
         xt = device.to_device(cloth.positions + 1e-4 * np.random.default_rng(1).normal(size=cloth.positions.shape))
         rhs = -sysm.gradient(pos, xt, [f.grad for f in fams])
         sysm.block_jacobi(); sysm.pcg(rhs, 1e-30, 5)
