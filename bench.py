@@ -421,7 +421,8 @@ def run_reference(args):
     # unmodified, from the installed package (baseline/_ref), one process per host core.  It is the headline value
     # of this arm when the package is importable; the C port above (~300 x faster than it) is reported next to it.
     value, ms_step, baseline = port_value, port["ms_per_step"], dict(port)
-    ref_py = ReferencePython(tab, qb, cores, sample_rows=100_000)
+    # sample sized so that K steps of it take about a minute at ~10 k stencils/s per core, whatever K is
+    ref_py = ReferencePython(tab, qb, cores, sample_rows=min(100_000, max(8_000, int(60 * 10_000 * cores / (args.steps + 1)))))
     if ref_py.available():
         with ref_py:
             for _ in range(min(args.warmup, 1)):
