@@ -274,3 +274,19 @@ def test_mas_preconditioner_through_the_time_stepper(S):
     # both runs stop Newton at |d|_inf <= eps_d l dt (solver.py:393): they agree to that tolerance per step
     assert np.abs(xa - xb).max() <= 2 * 2 * cfg.eps_d * l * soft.dt
     assert itb < ita, (itb, ita)
+
+
+def test_mas_on_a_seven_family_matrix(S):
+    """Elastic + barrier + friction families in one matrix (the row-wise numeric kernel, > 3 families) solved with the
+    MAS preconditioner, two levels: same steps converge, the cubes land in the same place to the Newton tolerance."""
+    out = {}
+    for prec in ("block_jacobi", "mas"):
+        sc, state = _cube_state(S, 8, 0.3)
+        state.config.preconditioner = prec
+        state.config.mas_levels = 2
+        stats = [S.stepper.advance_time_step(state) for _ in range(6)]
+        assert all(st.converged and st.warning == "" for st in stats)
+        out[prec] = (state.positions(), state.l, state.config)
+        state.close()
+    (xa, l, cfg), (xb, _, _) = out["block_jacobi"], out["mas"]
+    assert np.abs(xa - xb).max() <= 2 * 6 * cfg.eps_d * l * cfg.dt
