@@ -230,6 +230,15 @@ int b200ipc_accd_max_step(int64_t n, const int32_t* ids, const uint8_t* pair_kin
 int b200ipc_ccd_filter(int64_t n_vt, const int32_t* vt, int64_t n_ee, const int32_t* ee,
                        const double* positions, const double* directions, double slack, int32_t max_iter,
                        double* alpha /* device[1] */, int64_t* n_invalid /* device[1] */, void* stream);
+/* The same filter over ANY superset of sweep_candidates' lists (e.g. one swept join with a margin of d_hat/2 that
+ * also serves as the candidate set of every line-search detection along the step): each pair is first put to the
+ * reference's own swept-box test (proximity.py:388-421) at `sweep_margin` (the reference: 1e-3 d_hat), the
+ * survivors are compacted on the device and go through ACCD -- same minimum as b200ipc_ccd_filter over the
+ * reference's list.  scratch: device, 16 (n_vt + n_ee) + 16 bytes, 16-byte aligned. */
+int b200ipc_ccd_filter_swept(int64_t n_vt, const int32_t* vt, int64_t n_ee, const int32_t* ee,
+                             const double* positions, const double* directions, double sweep_margin, double slack,
+                             int32_t max_iter, void* scratch, double* alpha /* device[1] */,
+                             int64_t* n_invalid /* device[1] */, void* stream);
 
 /* ---- narrow phase: candidate queries -> ordered contact list ------------------- */
 /* find_contact_pairs without its broad phase (proximity.py:284-358).  vt (n_vt,4) i32 =

@@ -77,6 +77,7 @@ SIGNATURES = {
                                        C.POINTER(_dbl), C.POINTER(_i64), C.POINTER(_i64), _vp],
     "b200ipc_accd_max_step": [_i64, _vp, _vp, _i32, _vp, _vp, _dbl, _i32, _vp, _vp, _vp],
     "b200ipc_ccd_filter": [_i64, _vp, _i64, _vp, _vp, _vp, _dbl, _i32, _vp, _vp, _vp],
+    "b200ipc_ccd_filter_swept": [_i64, _vp, _i64, _vp, _vp, _vp, _dbl, _dbl, _i32, _vp, _vp, _vp, _vp],
     "b200ipc_friction_state": [_i64, C.POINTER(_i64), _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "b200ipc_friction_blocks": [_i64, C.POINTER(_i64), _vp, _vp, _vp, _vp, _dbl, _dbl, _dbl, _vp, _vp, _vp, _vp, _vp,
                                 _vp, _vp, _vp],

@@ -135,6 +135,25 @@ _PAIR_OF_KIND = {"point-triangle": 0, "edge-edge": 1, "edge-edge-parallel": 1, "
                  "point-point-parallel": 1, "point-edge": 2, "point-point": 3}  # proximity.py:361-369
 
 
+def ccd_filter_superset_device(vt, ee, positions, directions, sweep_margin, slack=0.9, max_iter=512):
+    """``ccd_filter_device`` over any SUPERSET of ``sweep_candidates``' lists: each pair is first put to the
+    reference's swept-box test at ``sweep_margin`` (the reference: 1e-3 d_hat), the survivors go through ACCD --
+    the same bound as over the reference's own list (min is order-free).  One swept join with a margin of d_hat/2
+    can thus serve the CCD filter AND every line-search detection along the step."""
+    if not 0.0 < slack < 1.0:
+        raise ValueError("slack must lie in (0, 1)")
+    out = device.empty((2,))  # [alpha, n_invalid (int64 bits)]
+    scratch = device.empty((2 * (int(vt.shape[0]) + int(ee.shape[0])) + 2,))   # 16 bytes per pair + the two counts
+    _lib.check(_lib.lib().b200ipc_ccd_filter_swept(
+        int(vt.shape[0]), device.ptr(vt), int(ee.shape[0]), device.ptr(ee), device.ptr(positions),
+        device.ptr(directions), float(sweep_margin), float(slack), int(max_iter), device.ptr(scratch),
+        C.c_void_p(out.data_ptr()), C.c_void_p(out.data_ptr() + 8), device.stream()), "ccd_filter_swept")
+    host = device.to_host(out)
+    if int(host[1:2].view(np.int64)[0]) != 0:
+        raise ValueError("additive CCD requires a strictly positive initial distance")  # _core.pyx:307-308
+    return float(host[0])
+
+
 def accd_step_bound(stencil, positions, directions, slack=0.9, max_iter=512):
     """Twin of proximity.py:372-385: ACCD bound of one stencil along ``directions``."""
     from . import kernels

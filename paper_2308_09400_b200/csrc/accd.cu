@@ -110,13 +110,15 @@ struct AccdArgs {
   uint8_t* status;            // (n) or NULL
   unsigned long long* alpha_bits;  // running minimum (ordered bits of a non-negative double) or NULL
   unsigned long long* n_invalid;   // pairs with a non-positive initial distance, or NULL
+  const unsigned long long* n_dev; // when set: the pair count lives on the device (a list compacted there), n = its capacity
 };
 
 __global__ void __launch_bounds__(kCT) accd_kernel(const __grid_constant__ AccdArgs a) {
   const int64_t i = (int64_t)blockIdx.x * kCT + threadIdx.x;
   double t = 1.0;
   bool bad = false;
-  if (i < a.n) {
+  const int64_t n = a.n_dev ? (int64_t)*a.n_dev : a.n;
+  if (i < n) {
     const int kind = a.pair_kind ? a.pair_kind[i] : a.uniform_kind;
     const int s = pair_size(kind);
     const int4 id = reinterpret_cast<const int4*>(a.ids)[i];
@@ -141,6 +143,58 @@ __global__ void __launch_bounds__(kCT) accd_kernel(const __grid_constant__ AccdA
   if (a.alpha_bits && a.n_invalid) {
     const unsigned nbad = __popc(__ballot_sync(0xffffffffu, bad));
     if ((threadIdx.x & 31) == 0 && nbad) atomicAdd(a.n_invalid, (unsigned long long)nbad);
+  }
+}
+
+// sweep_candidates' own predicate (proximity.py:388-421) on a candidate pair: the swept boxes of its two
+// primitives -- pose at x and at x + d, grown by `margin` -- overlap.  Corners are formed exactly like broad.cu
+// forms them (min / max over both poses, then -margin / +margin), so a SUPERSET of the reference's candidate
+// list filtered by this test is the reference's list.  Pairs that pass are appended to `out` (one atomic per warp;
+// the order is arbitrary, the minimum taken over them afterwards is order-free).
+struct SweptFilterArgs {
+  int64_t n;
+  const int32_t* ids;      // (n,4)
+  int32_t na;              // vertices of the first primitive: 1 (point-triangle) or 2 (edge-edge)
+  const double* positions;
+  const double* directions;
+  double margin;
+  int32_t* out;            // (n,4)
+  unsigned long long* count;
+};
+
+__global__ void __launch_bounds__(kCT) swept_filter_kernel(const __grid_constant__ SweptFilterArgs a) {
+  const int64_t i = (int64_t)blockIdx.x * kCT + threadIdx.x;
+  bool pass = false;
+  int4 id = make_int4(0, 0, 0, 0);
+  if (i < a.n) {
+    id = reinterpret_cast<const int4*>(a.ids)[i];
+    const int v[4] = {id.x, id.y, id.z, id.w};
+    double lo[2][3], hi[2][3];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int b = k < a.na ? 0 : 1;
+      const bool first = k == 0 || k == a.na;
+      const V3 x = load3(a.positions, v[k]), d = load3(a.directions, v[k]);
+      const double p0[3] = {x.x, x.y, x.z}, p1[3] = {x.x + d.x, x.y + d.y, x.z + d.z};
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double l = fmin(p0[c], p1[c]), h = fmax(p0[c], p1[c]);
+        lo[b][c] = first ? l : fmin(lo[b][c], l);
+        hi[b][c] = first ? h : fmax(hi[b][c], h);
+      }
+    }
+    pass = true;
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      pass = pass && (lo[0][c] - a.margin <= hi[1][c] + a.margin) && (lo[1][c] - a.margin <= hi[0][c] + a.margin);
+  }
+  const unsigned m = __ballot_sync(0xffffffffu, pass);
+  if (m) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long base = 0;
+    if (lane == __ffs(m) - 1) base = atomicAdd(a.count, (unsigned long long)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+    if (pass) reinterpret_cast<int4*>(a.out)[base + __popc(m & ((1u << lane) - 1u))] = id;
   }
 }
 
@@ -169,7 +223,7 @@ extern "C" int b200ipc_accd_max_step(int64_t n, const int32_t* ids, const uint8_
   if (rc) return rc;
   if (n == 0) return 0;
   if (!step) return B200IPC_EINVAL;
-  AccdArgs a{n, ids, pair_kind, uniform_kind, positions, directions, slack, max_iter, step, status, nullptr, nullptr};
+  AccdArgs a{n, ids, pair_kind, uniform_kind, positions, directions, slack, max_iter, step, status, nullptr, nullptr, nullptr};
   accd_kernel<<<(unsigned)((n + kCT - 1) / kCT), kCT, 0, (cudaStream_t)stream>>>(a);
   return post_launch();
 }
@@ -189,14 +243,55 @@ extern "C" int b200ipc_ccd_filter(int64_t n_vt, const int32_t* vt, int64_t n_ee,
   rc = post_launch();
   if (rc) return rc;
   if (n_vt) {
-    AccdArgs a{n_vt, vt, nullptr, B200IPC_PAIR_PT, positions, directions, slack, max_iter, nullptr, nullptr, bits, bad};
+    AccdArgs a{n_vt, vt, nullptr, B200IPC_PAIR_PT, positions, directions, slack, max_iter, nullptr, nullptr, bits, bad, nullptr};
     accd_kernel<<<(unsigned)((n_vt + kCT - 1) / kCT), kCT, 0, st>>>(a);
     rc = post_launch();
     if (rc) return rc;
   }
   if (n_ee) {
-    AccdArgs a{n_ee, ee, nullptr, B200IPC_PAIR_EE, positions, directions, slack, max_iter, nullptr, nullptr, bits, bad};
+    AccdArgs a{n_ee, ee, nullptr, B200IPC_PAIR_EE, positions, directions, slack, max_iter, nullptr, nullptr, bits, bad, nullptr};
     accd_kernel<<<(unsigned)((n_ee + kCT - 1) / kCT), kCT, 0, st>>>(a);
+    rc = post_launch();
+    if (rc) return rc;
+  }
+  return 0;
+}
+
+// global_ccd_filter over ANY superset of sweep_candidates' lists: every pair is first put to the reference's
+// swept-box test at `sweep_margin`, the survivors (compacted on the device, no host round trip) go through ACCD.
+// `scratch`: device, 16 (n_vt + n_ee) + 16 bytes, 16-byte aligned.
+extern "C" int b200ipc_ccd_filter_swept(int64_t n_vt, const int32_t* vt, int64_t n_ee, const int32_t* ee,
+                                        const double* positions, const double* directions, double sweep_margin,
+                                        double slack, int32_t max_iter, void* scratch, double* alpha, int64_t* n_invalid,
+                                        void* stream) {
+  if (!alpha || !scratch || !(sweep_margin >= 0.0) || (((uintptr_t)scratch) & 15)) return B200IPC_EINVAL;
+  int rc = accd_args_ok(n_vt, vt, nullptr, B200IPC_PAIR_PT, positions, directions, slack, max_iter);
+  if (rc) return rc;
+  rc = accd_args_ok(n_ee, ee, nullptr, B200IPC_PAIR_EE, positions, directions, slack, max_iter);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned long long* counts = static_cast<unsigned long long*>(scratch);   // [vt kept, ee kept]
+  int32_t* keep_vt = reinterpret_cast<int32_t*>(counts + 2);
+  int32_t* keep_ee = keep_vt + 4 * n_vt;
+  cudaError_t e = cudaMemsetAsync(counts, 0, 16, st);
+  if (e != cudaSuccess) return -(int)e;
+  unsigned long long* bits = reinterpret_cast<unsigned long long*>(alpha);
+  unsigned long long* bad = reinterpret_cast<unsigned long long*>(n_invalid);
+  accd_init_kernel<<<1, 1, 0, st>>>(bits, bad);
+  rc = post_launch();
+  if (rc) return rc;
+  for (int pass = 0; pass < 2; ++pass) {
+    const int64_t n = pass == 0 ? n_vt : n_ee;
+    if (!n) continue;
+    const int32_t* ids = pass == 0 ? vt : ee;
+    int32_t* keep = pass == 0 ? keep_vt : keep_ee;
+    SweptFilterArgs f{n, ids, pass == 0 ? 1 : 2, positions, directions, sweep_margin, keep, counts + pass};
+    swept_filter_kernel<<<(unsigned)((n + kCT - 1) / kCT), kCT, 0, st>>>(f);
+    rc = post_launch();
+    if (rc) return rc;
+    AccdArgs a{n, keep, nullptr, pass == 0 ? B200IPC_PAIR_PT : B200IPC_PAIR_EE, positions, directions, slack, max_iter,
+               nullptr, nullptr, bits, bad, counts + pass};
+    accd_kernel<<<(unsigned)((n + kCT - 1) / kCT), kCT, 0, st>>>(a);
     rc = post_launch();
     if (rc) return rc;
   }

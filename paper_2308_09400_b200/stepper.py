@@ -157,17 +157,19 @@ class SimState:
         return device.to_host(self.v)
 
     # -- contact set (solver.py:112-116) ----------------------------------------------------
-    def detect(self, x):
+    def detect(self, x, candidates=None):
         """``DeviceStencilTable`` of every stencil closer than d_hat, in the reference's list order.
 
         The reference detects at the accepted line-search candidate and again, on the same positions, at
         the top of the next Newton iteration and at the end of the step (solver.py:324, :343, :400); the
-        last result is kept and returned when the very same, unmodified tensor comes back."""
+        last result is kept and returned when the very same, unmodified tensor comes back.  ``candidates``:
+        (vt, ee) known to contain every pair within d_hat at ``x`` (the swept join of the step this ``x``
+        lies on): the broad phase is skipped, the list is the same (any superset of candidates gives it)."""
         last = self._last_detect
         if last is not None and last[0] is x and last[1] == x._version:
             return last[2]
         promote = self.config.mollify and self.config.mode == MODE_GIPC
-        vt, ee = self.broad.query(x)
+        vt, ee = candidates if candidates is not None else self.broad.query(x)
         table, extra = contacts.narrow_phase_device(x, self._rest, vt, ee, self.config.barrier.d_hat,
                                                     promote_parallel=promote, want_origin=False)
         table.kind_dev = extra.kind
@@ -196,10 +198,10 @@ class SimState:
         energy, _ = self.tet_mesh.evaluate(x, want_grad=False, want_hess=False)
         return float(energy.sum().item())
 
-    def evaluate_energy(self, x, x_tilde, x_start, stencils=None):
-        """Incremental potential at x; detects contacts unless a table is given."""
+    def evaluate_energy(self, x, x_tilde, x_start, stencils=None, candidates=None):
+        """Incremental potential at x; detects contacts unless a table is given (``candidates``: see ``detect``)."""
         x, x_tilde, x_start = _dev(x), _dev(x_tilde), _dev(x_start)
-        table = self.detect(x) if stencils is None else stencils
+        table = self.detect(x, candidates) if stencils is None else stencils
         dx = x - x_tilde
         inertia = 0.5 * float((self._free_mass * dx * dx).sum().item())
         dt2 = self.config.dt ** 2
@@ -275,13 +277,14 @@ def _search_direction(state, x, x_tilde, x_start, table):
     return direction, iters, ok
 
 
-def _backtrack(state, x, direction, alpha, x_tilde, x_start, energy_prev):
+def _backtrack(state, x, direction, alpha, x_tilde, x_start, energy_prev, candidates=None):
     """Halve alpha from the CCD bound until the incremental potential does not rise, contacts re-detected
-    at every candidate (solver.py:342-351).  Returns (x_new, energy_new, alpha) or None on collapse."""
+    at every candidate (solver.py:342-351).  Returns (x_new, energy_new, alpha) or None on collapse.
+    ``candidates``: the swept join of the step (every trial x + alpha d, alpha <= 1, lies inside it)."""
     floor = state.config.line_search_floor
     while alpha >= floor:
         trial = x + alpha * direction
-        energy = state.evaluate_energy(trial, x_tilde, x_start)
+        energy = state.evaluate_energy(trial, x_tilde, x_start, candidates=candidates if alpha <= 1.0 else None)
         if energy <= energy_prev:
             return trial, energy, alpha
         alpha *= 0.5
@@ -297,8 +300,16 @@ def newton_step(state, x, x_tilde, x_start, energy_prev):
     x, x_tilde, x_start = _dev(x), _dev(x_tilde), _dev(x_start)
     table = state.detect(x)
     direction, pcg_iters, pcg_ok = _search_direction(state, x, x_tilde, x_start, table)
-    bound = state.broad.ccd_step_bound(x, direction, slack=state.config.accd_slack)
-    found = _backtrack(state, x, direction, min(1.0, bound), x_tilde, x_start, energy_prev)
+    # ONE swept join per Newton iteration: boxes over x and x + d grown by 0.51 d_hat contain every pair that is
+    # within d_hat anywhere on the step, so the list serves (a) the CCD filter, after the reference's own
+    # swept-box test at 1e-3 d_hat has cut it down to sweep_candidates' exact set (proximity.py:388-421), and
+    # (b) the contact detection of every line-search candidate, which then skips its broad phase.  Same bound,
+    # same contact lists; one grid join instead of two.
+    d_hat = state.config.barrier.d_hat
+    swept = state.broad.sweep(x, direction, margin=0.51 * d_hat)
+    bound = contacts.ccd_filter_superset_device(swept[0], swept[1], x, direction, 1e-3 * d_hat,
+                                                slack=state.config.accd_slack)
+    found = _backtrack(state, x, direction, min(1.0, bound), x_tilde, x_start, energy_prev, candidates=swept)
     info = {"pcg_iters": pcg_iters, "pcg_converged": pcg_ok, "alpha": 0.0, "accepted": found is not None,
             "d_inf": float(direction.abs().max().item()) if direction.numel() else 0.0, "n_contacts": table.n}
     if found is None:

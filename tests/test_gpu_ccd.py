@@ -120,3 +120,26 @@ def test_ccd_filter_large_scene_against_oracle(G):
     xe = x + alpha * d
     d2 = o.pt_classify_batch(xe[vt[:, 0]], xe[vt[:, 1]], xe[vt[:, 2]], xe[vt[:, 3]])[1]
     assert d2.min() > 0.0
+
+
+def test_superset_filter_equals_the_reference_candidate_filter(G):
+    """One swept join with a margin of 0.51 d_hat, cut down by the reference's own swept-box test at 1e-3 d_hat on
+    the device, gives the bound of sweep_candidates + global_ccd_filter bit for bit; and it contains every pair a
+    static detection finds anywhere on the step (the line search then skips its broad phase)."""
+    cloth = G.workloads.cloth_stack(layers=4, n=24, seed=21)
+    rng = np.random.default_rng(3)
+    dirs = 0.4 * cloth.d_hat * rng.normal(size=cloth.positions.shape)
+    bp = G.contacts.BroadPhase(None, cloth.tris, cloth.edges, cloth.d_hat, cloth.positions)
+    pos, dd = G.device.to_device(cloth.positions), G.device.to_device(dirs)
+    exact = bp.ccd_step_bound(pos, dd)
+    vt, ee = bp.sweep(pos, dd, margin=0.51 * cloth.d_hat)
+    ref_vt, ref_ee = bp.sweep(pos, dd)
+    assert vt.shape[0] > ref_vt.shape[0] and ee.shape[0] > ref_ee.shape[0]
+    got = G.contacts.ccd_filter_superset_device(vt, ee, pos, dd, 1e-3 * cloth.d_hat)
+    assert got == exact
+    as_set = lambda t: set(map(tuple, G.device.to_host(t).tolist()))  # noqa: E731
+    big_vt, big_ee = as_set(vt), as_set(ee)
+    for alpha in (0.0, 0.37, 1.0):
+        q_vt, q_ee = bp.query(G.device.to_device(cloth.positions + alpha * dirs))
+        assert as_set(q_vt) <= big_vt and as_set(q_ee) <= big_ee
+    bp.close()
