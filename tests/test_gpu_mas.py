@@ -134,3 +134,33 @@ def test_mas_cuts_the_iteration_count_on_a_contact_stack(M):
     d2, it2, ok2, _, _ = sysm.pcg(rhs, 1e-4, 5000, preconditioner="mas")
     assert ok2 and abs(it2 - it_mas) <= 3
     sysm.close()
+
+
+@pytest.mark.parametrize("n", [1, 5, 32, 33])
+def test_tiny_systems(M, n):
+    """Fewer vertices than one domain (MAS is then the exact inverse: one iteration), exactly one domain, one vertex
+    into the second domain; two levels requested where only one domain exists fall back to one."""
+    rng = np.random.default_rng(n)
+    grouped = []
+    if n >= 2:
+        nb = 3 * n
+        vids = np.stack([rng.choice(n, size=2, replace=False) for _ in range(nb)]).astype(np.int64)
+        z = rng.normal(size=(nb, 6))
+        grouped.append((z[:, :, None] * z[:, None, :], vids))
+    masses, fixed = rng.uniform(0.5, 2.0, size=n), np.zeros(n, bool)
+    if n >= 5:
+        fixed[2] = True
+    sysm = M.solver.NewtonSystem(masses, fixed)
+    sysm.set_pattern([(v.shape[1], v) for _, v in grouped])
+    sysm.assemble([h for h, _ in grouped])
+    rhs = rng.normal(size=3 * n)
+    a = o.assemble_dense(grouped, masses, fixed)
+    b = rhs.copy()
+    b.reshape(n, 3)[fixed] = 0.0
+    sol = np.linalg.solve(a, b)
+    for levels in (1, 2):
+        d, iters, ok, _, _ = sysm.pcg(rhs, 1e-20, 200, preconditioner="mas", mas_levels=levels)
+        assert ok and np.abs(M.device.to_host(d) - sol).max() <= 1e-9 * max(np.abs(sol).max(), 1e-300)
+        if n <= 32:
+            assert iters <= 2          # one domain holds the whole matrix (fp32-stored inverse: a second sweep at most)
+    sysm.close()
