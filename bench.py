@@ -461,7 +461,7 @@ def run_reference(args):
     except Exception as exc:
         line["numpy_oracle"] = {"error": repr(exc)}
     path = _reference_package_path()
-    if path is not None:
+    if path is not None and not args.skip_newton:    # the long legs ride with the full run only
         import subprocess
 
         proj = {}
