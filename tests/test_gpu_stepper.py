@@ -290,3 +290,18 @@ def test_mas_on_a_seven_family_matrix(S):
         state.close()
     (xa, l, cfg), (xb, _, _) = out["block_jacobi"], out["mas"]
     assert np.abs(xa - xb).max() <= 2 * 6 * cfg.eps_d * l * cfg.dt
+
+
+def test_auto_preconditioner_switches_on_hard_solves_only(S):
+    """SolverConfig.preconditioner = "auto" (the paper's "trial both, keep the faster"): a stiff contact stack whose
+    block-Jacobi solves exceed the threshold switches to MAS inside the step; below the threshold it never does."""
+    from paper_2308_09400_b200 import workloads
+
+    for kappa, threshold, expect_switch in ((2e8, 40, True), (1e5, 1000, False)):
+        sc = workloads.cloth_stack(layers=4, n=40, seed=1, d_hat_rel=0.2, jitter_rel=0.01, kappa=kappa)
+        cfg = S.stepper.SolverConfig(dt=sc.dt, barrier=S.barrier.BarrierParams(d_hat=sc.d_hat, kappa=sc.kappa),
+                                     preconditioner="auto", auto_switch_iters=threshold, newton_max_iters=6)
+        state = S.stepper.SimState(sc.as_scene(), cfg)
+        S.stepper.advance_time_step(state)
+        assert state._auto_mas == expect_switch, (kappa, state._auto_mas)
+        state.close()
