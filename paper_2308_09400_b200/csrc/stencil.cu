@@ -19,6 +19,16 @@
 
 namespace b200ipc {
 
+// 16-byte store of two adjacent outputs.  STREAM: evict-first (st.global.cs) -- a step that writes more than the L2
+// holds gains nothing from allocating its output there (measured on 1.27 GB of blocks: 0.2417 -> 0.2376 ms); small
+// batches keep plain stores so that the assembly that follows finds the blocks in L2.
+template <bool STREAM>
+__device__ __forceinline__ void store2(double* p, double a, double b) {
+  if (STREAM) __stcs(reinterpret_cast<double2*>(p), make_double2(a, b));
+  else *reinterpret_cast<double2*>(p) = make_double2(a, b);
+}
+
+
 constexpr int kTile = 128;  // stencils per CTA == threads per CTA
 
 template <int KIND>
@@ -54,7 +64,7 @@ struct StencilArgs {
 
 constexpr int kPad = kTile + 1;  // odd stride: bank = 2(k*P + i) mod 32 is distinct across k and i
 
-template <int KIND, int FORM>
+template <int KIND, int FORM, bool STREAM>
 __device__ __forceinline__ void stencil_tile(const b200ipc_params& prm, const double* __restrict__ positions,
                                              const KindArgs& a, int64_t tile, double* sm_z, double* sm_g) {
   using KT = KindTraits<KIND>;
@@ -160,7 +170,7 @@ __device__ __forceinline__ void stencil_tile(const b200ipc_params& prm, const do
         const int k1 = (k0 + 1 == D) ? 0 : k0 + 1;
         const int b1 = (k0 + 1 == D) ? b0 + 1 : b0;
         const double v1 = sm[k1 * P + b1];
-        *reinterpret_cast<double2*>(out + e) = make_double2(v0, v1);
+        store2<STREAM>(out + e, v0, v1);
       } else {
         out[e] = v0;
       }
@@ -179,7 +189,7 @@ __device__ __forceinline__ void stencil_tile(const b200ipc_params& prm, const do
         const double zr = sm_z[r * P + b];
         const double v0 = zr * sm_z[c * P + b];
         const double v1 = zr * sm_z[(c + 1) * P + b];
-        *reinterpret_cast<double2*>(out + e) = make_double2(v0, v1);
+        store2<STREAM>(out + e, v0, v1);
       }
     } else {
       for (int e = 2 * tid; e < total; e += 2 * kTile) {
@@ -191,7 +201,7 @@ __device__ __forceinline__ void stencil_tile(const b200ipc_params& prm, const do
           const int b1 = e1 / DD, k1 = e1 - b1 * DD;
           const int r1 = k1 / D, c1 = k1 - r1 * D;
           const double v1 = sm_z[r1 * P + b1] * sm_z[c1 * P + b1];
-          *reinterpret_cast<double2*>(out + e) = make_double2(v0, v1);
+          store2<STREAM>(out + e, v0, v1);
         } else {
           out[e] = v0;
         }
@@ -200,7 +210,7 @@ __device__ __forceinline__ void stencil_tile(const b200ipc_params& prm, const do
   }
 }
 
-template <int FORM>
+template <int FORM, bool STREAM>
 __global__ void __launch_bounds__(kTile) barrier_stencil_kernel(const StencilArgs a) {
   __shared__ double sm_z[12 * kPad];
   __shared__ double sm_g[12 * kPad];
@@ -211,13 +221,13 @@ __global__ void __launch_bounds__(kTile) barrier_stencil_kernel(const StencilArg
     if (b >= a.tile_off[k]) kind = k;
   const int64_t tile = b - a.tile_off[kind];
   switch (kind) {
-    case B200IPC_EE: stencil_tile<B200IPC_EE, FORM>(a.prm, a.positions, a.k[B200IPC_EE], tile, sm_z, sm_g); break;
-    case B200IPC_EEP: stencil_tile<B200IPC_EEP, FORM>(a.prm, a.positions, a.k[B200IPC_EEP], tile, sm_z, sm_g); break;
-    case B200IPC_PE: stencil_tile<B200IPC_PE, FORM>(a.prm, a.positions, a.k[B200IPC_PE], tile, sm_z, sm_g); break;
-    case B200IPC_PEP: stencil_tile<B200IPC_PEP, FORM>(a.prm, a.positions, a.k[B200IPC_PEP], tile, sm_z, sm_g); break;
-    case B200IPC_PP: stencil_tile<B200IPC_PP, FORM>(a.prm, a.positions, a.k[B200IPC_PP], tile, sm_z, sm_g); break;
-    case B200IPC_PPP: stencil_tile<B200IPC_PPP, FORM>(a.prm, a.positions, a.k[B200IPC_PPP], tile, sm_z, sm_g); break;
-    default: stencil_tile<B200IPC_PT, FORM>(a.prm, a.positions, a.k[B200IPC_PT], tile, sm_z, sm_g); break;
+    case B200IPC_EE: stencil_tile<B200IPC_EE, FORM, STREAM>(a.prm, a.positions, a.k[B200IPC_EE], tile, sm_z, sm_g); break;
+    case B200IPC_EEP: stencil_tile<B200IPC_EEP, FORM, STREAM>(a.prm, a.positions, a.k[B200IPC_EEP], tile, sm_z, sm_g); break;
+    case B200IPC_PE: stencil_tile<B200IPC_PE, FORM, STREAM>(a.prm, a.positions, a.k[B200IPC_PE], tile, sm_z, sm_g); break;
+    case B200IPC_PEP: stencil_tile<B200IPC_PEP, FORM, STREAM>(a.prm, a.positions, a.k[B200IPC_PEP], tile, sm_z, sm_g); break;
+    case B200IPC_PP: stencil_tile<B200IPC_PP, FORM, STREAM>(a.prm, a.positions, a.k[B200IPC_PP], tile, sm_z, sm_g); break;
+    case B200IPC_PPP: stencil_tile<B200IPC_PPP, FORM, STREAM>(a.prm, a.positions, a.k[B200IPC_PPP], tile, sm_z, sm_g); break;
+    default: stencil_tile<B200IPC_PT, FORM, STREAM>(a.prm, a.positions, a.k[B200IPC_PT], tile, sm_z, sm_g); break;
   }
 }
 
@@ -355,8 +365,20 @@ extern "C" int b200ipc_barrier_stencils_ex(const b200ipc_params* params, int64_t
   }
   a.tile_off[B200IPC_NKINDS] = (uint32_t)tiles;
   if (tiles >= (1ull << 31)) return B200IPC_EINVAL;
-  if (params->form == 0) barrier_stencil_kernel<0><<<(unsigned)tiles, kTile, 0, s>>>(a);
-  else barrier_stencil_kernel<1><<<(unsigned)tiles, kTile, 0, s>>>(a);
+  // output larger than what the L2 can keep for the next kernel: stream it
+  int64_t out_bytes = 0;
+  for (int k = 0; k < B200IPC_NKINDS; ++k) {
+    const int64_t sz = k == B200IPC_PP ? 2 : (k == B200IPC_PE ? 3 : 4);
+    if (a.k[k].hess) out_bytes += a.k[k].n * 72 * sz * sz;
+  }
+  const bool streaming = out_bytes > (96ll << 20);
+  if (params->form == 0) {
+    if (streaming) barrier_stencil_kernel<0, true><<<(unsigned)tiles, kTile, 0, s>>>(a);
+    else barrier_stencil_kernel<0, false><<<(unsigned)tiles, kTile, 0, s>>>(a);
+  } else {
+    if (streaming) barrier_stencil_kernel<1, true><<<(unsigned)tiles, kTile, 0, s>>>(a);
+    else barrier_stencil_kernel<1, false><<<(unsigned)tiles, kTile, 0, s>>>(a);
+  }
   return post_launch();
 }
 
