@@ -53,7 +53,11 @@ __global__ void __launch_bounds__(kAT) matrix_keys_kernel(FamDesc fd, int64_t nv
     col = v[c];
   }
   uint64_t key = (uint64_t)row * (uint64_t)nverts + (uint64_t)col;
-  if (row != col && (fixed[row] | fixed[col])) key = (uint64_t)nverts * (uint64_t)nverts;  // Dirichlet: dropped (sorts last)
+  // Dirichlet: an off-diagonal slot with a fixed end is dropped (sorts last), and so are the block slots on the
+  // diagonal of a fixed row -- its block is the unit matrix whatever they hold; only the mass slot stays, as in
+  // the row-wise phase (same run contents and the same source count in both phases)
+  if ((row != col && (fixed[row] | fixed[col])) || (row == col && e >= nverts && fixed[row]))
+    key = (uint64_t)nverts * (uint64_t)nverts;
   keys[e] = key;
   slots[e] = (uint32_t)e;
 }

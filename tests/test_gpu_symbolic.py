@@ -90,6 +90,7 @@ def test_row_wise_symbolic_equals_sort_path_and_oracle(S, name, n, counts, hub, 
     if a.stats()["symbolic"] == "rows":
         st = a.stats()
         assert st["max_row"] == int(np.diff(ra).max()) and st["nnzb"] == len(ca)
+        assert st["sources"] == b.stats()["sources"]      # same runs: the numeric walker choice cannot differ
     # the factor path and the row-wise numeric kernel on the row-wise pattern
     if grouped and a.stats()["symbolic"] == "rows":
         r4 = build(S, grouped, masses, fixed, mode=0, variant=4)
@@ -148,3 +149,34 @@ def test_row_wise_numeric_kernel_refuses_rows_beyond_16_bits(S):
     with pytest.raises(S.lib.B200IpcError):
         sysm.assemble([hess])
     sysm.close()
+
+
+def test_random_scenes_both_phases_and_oracle(S):
+    """Randomised stress (scripts/symbolic_stress.py, shortened): clustered vertex choices so that rows get long
+    and share columns, 0 - 30 % Dirichlet vertices -- both symbolic phases and the oracle, pattern and values."""
+    rng = np.random.default_rng(12345)
+    for case in range(25):
+        n = int(rng.integers(2, 3000))
+        fams = []
+        for s in (2, 3, 4):
+            nb = int(rng.integers(0, 6 * n))
+            if n < s or nb == 0:
+                continue
+            centre = rng.integers(0, n, size=nb)
+            width = max(s, int(rng.integers(s, max(s + 1, n // int(rng.integers(1, 40)) + s))))
+            vids = np.stack([(c + rng.choice(width, size=s, replace=False)) % n for c in centre]).astype(np.int64)
+            vids = vids[np.array([len(set(v)) == s for v in vids])]
+            if len(vids):
+                z = rng.normal(size=(len(vids), 3 * s))
+                fams.append((z[:, :, None] * z[:, None, :], vids))
+        masses = rng.uniform(0.5, 2.0, size=n)
+        fixed = rng.uniform(size=n) < rng.choice([0.0, 0.02, 0.3])
+        a, b = build(S, fams, masses, fixed, mode=0), build(S, fams, masses, fixed, mode=1)
+        ra, ca, va = a.to_scipy_like()
+        rb, cb, vb = b.to_scipy_like()
+        o_rowptr, o_colidx, o_vals = o.assemble_bsr(fams, masses, fixed)
+        assert np.array_equal(ra, rb) and np.array_equal(ca, cb) and np.array_equal(va, vb), case
+        assert np.array_equal(ra, o_rowptr) and np.array_equal(ca, o_colidx), case
+        assert np.abs(va - o_vals).max() <= 1e-12 * max(np.abs(o_vals).max(), 1.0), case
+        a.close()
+        b.close()
