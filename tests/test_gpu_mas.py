@@ -124,6 +124,10 @@ def test_mas_cuts_the_iteration_count_on_a_contact_stack(M):
     _, it_mas, ok_mas, _, _ = sysm.pcg(rhs, 1e-4, 5000, preconditioner="mas", mas_levels=1)
     assert ok_bj and ok_mas
     assert it_mas < 0.6 * it_bj, (it_mas, it_bj)
+    # deterministic: fixed summation orders, no atomics -- a second solve returns the same bits
+    d_a, it_a, _, _, _ = sysm.pcg(rhs, 1e-4, 5000, preconditioner="mas", mas_levels=1)
+    d_b, it_b, _, _, _ = sysm.pcg(rhs, 1e-4, 5000, preconditioner="mas", mas_levels=1)
+    assert it_a == it_b == it_mas and bool((d_a == d_b).all())
     # zero right-hand side: no iterations, converged (solver.py:296-297)
     d, iters, ok, _, _ = sysm.pcg(np.zeros(3 * sysm.n), 1e-4, 100, preconditioner="mas")
     assert ok and iters == 0 and not M.device.to_host(d).any()
