@@ -160,6 +160,22 @@ int b200ipc_barrier_stencils_ex(const b200ipc_params* params /* host */, int64_t
                                 double* grad4, double* hess4,
                                 double* fac2, double* fac3, double* fac4, void* stream);
 
+/* Same as b200ipc_barrier_stencils_ex with a choice of the dense blocks' DEVICE layout.  The reference's
+ * LocalQuadratic.hess (solver.py:202-209) is the row-major (3s,3s) array, B200IPC_LAYOUT_DENSE; with
+ * B200IPC_LAYOUT_SUBBLOCK the same numbers leave as (nb, s, s, 3, 3): element [b][a][c][i][j] = hess_b[3a+i][3c+j],
+ * every 3x3 vertex-pair sub-block 72 contiguous bytes -- what the BSR assembly gathers (one line per source
+ * instead of three).  An internal format between this call and b200ipc_assemble_numeric (see
+ * b200ipc_assembly_set_layout); the host-facing view is a permute of it.  grad / fac / energy / status unchanged. */
+#define B200IPC_LAYOUT_DENSE 0
+#define B200IPC_LAYOUT_SUBBLOCK 1
+int b200ipc_barrier_stencils_layout(const b200ipc_params* params /* host */, int64_t nverts,
+                                    const double* positions, int64_t n, const int64_t* kind_off /* host[8] */,
+                                    const int32_t* verts, const uint8_t* sub, const double* eps_x,
+                                    double* energy, uint8_t* status,
+                                    double* grad2, double* hess2, double* grad3, double* hess3,
+                                    double* grad4, double* hess4,
+                                    double* fac2, double* fac3, double* fac4, int32_t hess_layout, void* stream);
+
 /* Sum of energy[0..n) (the scalar of SimState._barrier_energy, solver.py:127-146) and the
  * counts of status==1 / status==2, deterministic two-pass.  result: device double[1];
  * counts: device int64[2] (inactive, penetration); workspace: device scratch of at least
@@ -328,6 +344,12 @@ int b200ipc_assembly_set_variant(b200ipc_assembly* h, int32_t variant);
  * sort of the 16 n_c slots), falling back to 1 when a row has more than 256 distinct columns.  1 = sort by
  * key (stable radix sort of every (row, col) slot).  Identical pattern, run order and matrices. */
 int b200ipc_assembly_set_symbolic(b200ipc_assembly* h, int32_t mode);
+/* Layout of the dense blocks b200ipc_assemble_numeric will be given: bit f of tiled_mask set = family f (the
+ * f-th of b200ipc_assemble_symbolic) is B200IPC_LAYOUT_SUBBLOCK, clear = the reference's row-major blocks
+ * (default).  The source descriptors are written by the symbolic phase, so the mask takes effect at the NEXT
+ * b200ipc_assemble_symbolic.  Walkers 1 / 2 only: with a sub-block-major family the row-wise kernel (variant 4,
+ * or more than three families) returns B200IPC_EINVAL.  Same sums in the same order: bitwise equal matrices. */
+int b200ipc_assembly_set_layout(b200ipc_assembly* h, uint32_t tiled_mask);
 /* out[4] (host) = {symbolic path that built the current pattern (1 sort, 2 row-wise), longest block row
  * (-1: not measured), nnzb, kept source slots}.  B200IPC_ESTATE before the first symbolic call. */
 int b200ipc_assembly_stats(b200ipc_assembly* h, int64_t* out);

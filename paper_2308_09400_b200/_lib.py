@@ -59,6 +59,8 @@ SIGNATURES = {
                                  _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "b200ipc_barrier_stencils_ex": [C.POINTER(Params), _i64, _vp, _i64, C.POINTER(_i64), _vp, _vp, _vp,
                                     _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "b200ipc_barrier_stencils_layout": [C.POINTER(Params), _i64, _vp, _i64, C.POINTER(_i64), _vp, _vp, _vp,
+                                        _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp],
     "b200ipc_reduce_energy": [_i64, _vp, _vp, _vp, _vp, _vp, _vp],
     "b200ipc_diagonal_jacobian": [C.POINTER(Params), _i64, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                   _vp, _vp, _vp, _vp, _vp, _vp],
@@ -88,6 +90,7 @@ SIGNATURES = {
     "b200ipc_assembly_destroy": [_vp],
     "b200ipc_assembly_set_variant": [_vp, _i32],
     "b200ipc_assembly_set_symbolic": [_vp, _i32],
+    "b200ipc_assembly_set_layout": [_vp, C.c_uint32],
     "b200ipc_assembly_stats": [_vp, C.POINTER(_i64)],
     "b200ipc_assemble_symbolic": [_vp, _i64, _vp, _i32, C.POINTER(_i32), C.POINTER(_i64), C.POINTER(_vp),
                                   C.POINTER(_i64), _vp],

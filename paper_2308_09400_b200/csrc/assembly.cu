@@ -132,14 +132,14 @@ __global__ void __launch_bounds__(kAT) source_desc_kernel(FamDesc fd, int64_t nv
     int64_t b;
     decode_slot(fd, slot - nverts, f, b, a, c);
     const int64_t s = fd.s[f];
-    // ((b*D + 3a)*D + 3c) / 3 with D = 3s
-    desc[j] = ((uint32_t)f << 30) | (uint32_t)((b * 3 * s + 3 * a) * s + c);
+    // row-major: ((b*D + 3a)*D + 3c) / 3 with D = 3s; sub-block-major: 9 (b s^2 + a s + c) / 3
+    desc[j] = ((uint32_t)f << 30) | (uint32_t)((b * 3 * s + 3 * a) * s + fd.cmul[f] * c);
   }
 }
 
 struct NumericArgs {
   HessPtrs hp;
-  int32_t ld[4];        // row length D of families 0..2 (slot 3 unused)
+  int32_t ld[4];        // row stride of a 3x3 sub-block in families 0..2: D row-major, 3 sub-block-major (slot 3 unused)
   int64_t nnzb;
   const uint8_t* fixed;
   const double* masses;
@@ -702,6 +702,12 @@ extern "C" int b200ipc_assembly_set_symbolic(b200ipc_assembly* h, int32_t mode) 
   return 0;
 }
 
+extern "C" int b200ipc_assembly_set_layout(b200ipc_assembly* h, uint32_t tiled_mask) {
+  if (!h || tiled_mask >= (1u << kMaxFam)) return B200IPC_EINVAL;
+  h->tiled_next = tiled_mask;   // descriptors are written by the symbolic phase: takes effect at the next pattern
+  return 0;
+}
+
 extern "C" int b200ipc_assembly_stats(b200ipc_assembly* h, int64_t* out) {
   if (!h || !out) return B200IPC_EINVAL;
   if (!h->ready) return B200IPC_ESTATE;
@@ -730,7 +736,9 @@ extern "C" int b200ipc_assemble_symbolic(b200ipc_assembly* h, int64_t nverts, co
     fd.vids[f] = fam_vids[f];
     fd.ent_off[f + 1] = fd.ent_off[f] + fam_nb[f] * fam_s[f] * fam_s[f];
     fd.vert_off[f + 1] = fd.vert_off[f] + fam_nb[f] * fam_s[f];
+    fd.cmul[f] = (h->tiled_next >> f) & 1u ? 3 : 1;
   }
+  h->tiled = nfam ? h->tiled_next & ((1u << nfam) - 1u) : 0u;
   h->nverts = nverts;
   h->nslots = nverts + fd.ent_off[nfam];
   h->ngslots = fd.vert_off[nfam];
@@ -837,7 +845,7 @@ extern "C" int b200ipc_assemble_numeric(b200ipc_assembly* h, const double* masse
   for (int f = 0; f < h->fam.nfam; ++f) {
     if (h->fam.nb[f] && !fam_hess[f]) return B200IPC_EINVAL;
     a.hp.p[f] = fam_hess[f];
-    if (f < 3) a.ld[f] = 3 * h->fam.s[f];
+    if (f < 3) a.ld[f] = h->fam.cmul[f] == 3 ? 3 : 3 * h->fam.s[f];
     if (h->fam.nb[f] * 9 * h->fam.s[f] * h->fam.s[f] >= (3ll << 30)) packed_ok = false;
   }
   a.nnzb = h->nnzb; a.fixed = h->fixed.ptr; a.masses = masses;
@@ -861,6 +869,7 @@ extern "C" int b200ipc_assemble_numeric(b200ipc_assembly* h, const double* masse
     assemble_numeric_trio_kernel<<<(unsigned)((h->nnzb + per_cta - 1) / per_cta), 32 * kNumWarps, 0, (cudaStream_t)stream>>>(a);
     return post_launch();
   }
+  if (h->tiled) return B200IPC_EINVAL;   // the row-wise kernel reads whole rows of row-major blocks
   RC(ensure_rows(h, (cudaStream_t)stream));
   RowArgs r;
   r.hp = a.hp;

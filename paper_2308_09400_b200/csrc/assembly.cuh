@@ -17,6 +17,10 @@ struct FamDesc {
   int64_t vert_off[kMaxFam + 1];  // prefix of nb*s    (gradient slots)
   const int64_t* vids[kMaxFam];
   int32_t nfam;
+  // dense-block layout of a family: 1 = the reference's row-major (nb, 3s, 3s); 3 = sub-block-major
+  // (nb, s, s, 3, 3), every 3x3 sub-block 72 contiguous bytes.  It is the factor of c in the element
+  // offset / 3 of sub-block (a, c): 3 (b s + a) s + cmul c.
+  int32_t cmul[kMaxFam];
 };
 
 struct HessPtrs {
@@ -55,6 +59,8 @@ struct b200ipc_assembly {
   bool have_desc = false, have_fdesc = false, have_rows = false;   // descriptor tables are built on first use
   int variant = 0;         // numeric kernel: 0 auto (per-block runs when applicable), 1 runs, 4 row-wise
   int symbolic_mode = 0;   // 0 auto (row-wise, sort path when a row is too long), 1 sort path always
+  uint32_t tiled_next = 0; // bit f: family f of the NEXT pattern delivers its dense blocks sub-block-major
+  uint32_t tiled = 0;      // the same for the current pattern
   int symbolic_used = 0;   // which path built the current pattern: 1 sort, 2 row-wise
   int64_t max_row = -1;    // longest block row of the current pattern (-1: not measured yet)
   b200ipc::FamDesc fam;

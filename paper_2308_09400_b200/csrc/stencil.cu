@@ -64,9 +64,13 @@ struct StencilArgs {
 
 constexpr int kPad = kTile + 1;  // odd stride: bank = 2(k*P + i) mod 32 is distinct across k and i
 
-template <int KIND, int FORM, bool STREAM>
+// TILED: the dense block leaves sub-block-major, (nb, S, S, 3, 3) -- every 3x3 sub-block 72 contiguous bytes, what
+// the assembly's gather wants (one line per source instead of three); the reference's (nb, 3S, 3S) view is then
+// produced only at the host boundary.  Same products, same bytes, another order.
+template <int KIND, int FORM, bool STREAM, bool TILED>
 __device__ __forceinline__ void stencil_tile(const b200ipc_params& prm, const double* __restrict__ positions,
-                                             const KindArgs& a, int64_t tile, double* sm_z, double* sm_g) {
+                                             const KindArgs& a, int64_t tile, double* sm_z, double* sm_g,
+                                             uint32_t* sm_lut) {
   using KT = KindTraits<KIND>;
   constexpr int S = KT::S;
   constexpr int D = 3 * S;
@@ -76,6 +80,16 @@ __device__ __forceinline__ void stencil_tile(const b200ipc_params& prm, const do
   const int tid = threadIdx.x;
   const int64_t tile0 = tile * kTile;
   const int64_t i = tile0 + tid;
+
+  if (TILED && a.hess) {
+    // element k = ((va S + vc) 3 + i) 3 + j of a tiled block is z[3 va + i] z[3 vc + j]: shared-memory rows, once per CTA
+    for (int k = tid; k < DD; k += kTile) {
+      const int t = k / 9, q = k - 9 * t;
+      const int va = t / S, vc = t - S * va;
+      const int qi = q / 3, qj = q - 3 * qi;
+      sm_lut[k] = (uint32_t)((3 * va + qi) * P) | ((uint32_t)((3 * vc + qj) * P) << 16);
+    }
+  }
 
   if (i < a.n) {
     const int4 vid = __ldg(reinterpret_cast<const int4*>(a.verts) + i);
@@ -181,7 +195,22 @@ __device__ __forceinline__ void stencil_tile(const b200ipc_params& prm, const do
   if (a.hess) {
     double* out = a.hess + tile0 * DD;
     const int total = ntile * DD;
-    if (D % 2 == 0) {
+    if (TILED) {
+      for (int e = 2 * tid; e < total; e += 2 * kTile) {
+        const int b0 = e / DD, k0 = e - b0 * DD;
+        const uint32_t l0 = sm_lut[k0];
+        const double v0 = sm_z[(l0 & 0xffffu) + b0] * sm_z[(l0 >> 16) + b0];
+        if (e + 1 < total) {
+          const int k1 = (k0 + 1 == DD) ? 0 : k0 + 1;
+          const int b1 = (k0 + 1 == DD) ? b0 + 1 : b0;
+          const uint32_t l1 = sm_lut[k1];
+          const double v1 = sm_z[(l1 & 0xffffu) + b1] * sm_z[(l1 >> 16) + b1];
+          store2<STREAM>(out + e, v0, v1);
+        } else {
+          out[e] = v0;
+        }
+      }
+    } else if (D % 2 == 0) {
       // rows have even length: a pair never straddles a row
       for (int e = 2 * tid; e < total; e += 2 * kTile) {
         const int b = e / DD, k = e - b * DD;
@@ -210,10 +239,11 @@ __device__ __forceinline__ void stencil_tile(const b200ipc_params& prm, const do
   }
 }
 
-template <int FORM, bool STREAM>
+template <int FORM, bool STREAM, bool TILED>
 __global__ void __launch_bounds__(kTile) barrier_stencil_kernel(const StencilArgs a) {
   __shared__ double sm_z[12 * kPad];
   __shared__ double sm_g[12 * kPad];
+  __shared__ uint32_t sm_lut[TILED ? 144 : 1];
   const uint32_t b = blockIdx.x;
   int kind = 0;
 #pragma unroll
@@ -221,13 +251,13 @@ __global__ void __launch_bounds__(kTile) barrier_stencil_kernel(const StencilArg
     if (b >= a.tile_off[k]) kind = k;
   const int64_t tile = b - a.tile_off[kind];
   switch (kind) {
-    case B200IPC_EE: stencil_tile<B200IPC_EE, FORM, STREAM>(a.prm, a.positions, a.k[B200IPC_EE], tile, sm_z, sm_g); break;
-    case B200IPC_EEP: stencil_tile<B200IPC_EEP, FORM, STREAM>(a.prm, a.positions, a.k[B200IPC_EEP], tile, sm_z, sm_g); break;
-    case B200IPC_PE: stencil_tile<B200IPC_PE, FORM, STREAM>(a.prm, a.positions, a.k[B200IPC_PE], tile, sm_z, sm_g); break;
-    case B200IPC_PEP: stencil_tile<B200IPC_PEP, FORM, STREAM>(a.prm, a.positions, a.k[B200IPC_PEP], tile, sm_z, sm_g); break;
-    case B200IPC_PP: stencil_tile<B200IPC_PP, FORM, STREAM>(a.prm, a.positions, a.k[B200IPC_PP], tile, sm_z, sm_g); break;
-    case B200IPC_PPP: stencil_tile<B200IPC_PPP, FORM, STREAM>(a.prm, a.positions, a.k[B200IPC_PPP], tile, sm_z, sm_g); break;
-    default: stencil_tile<B200IPC_PT, FORM, STREAM>(a.prm, a.positions, a.k[B200IPC_PT], tile, sm_z, sm_g); break;
+    case B200IPC_EE: stencil_tile<B200IPC_EE, FORM, STREAM, TILED>(a.prm, a.positions, a.k[B200IPC_EE], tile, sm_z, sm_g, sm_lut); break;
+    case B200IPC_EEP: stencil_tile<B200IPC_EEP, FORM, STREAM, TILED>(a.prm, a.positions, a.k[B200IPC_EEP], tile, sm_z, sm_g, sm_lut); break;
+    case B200IPC_PE: stencil_tile<B200IPC_PE, FORM, STREAM, TILED>(a.prm, a.positions, a.k[B200IPC_PE], tile, sm_z, sm_g, sm_lut); break;
+    case B200IPC_PEP: stencil_tile<B200IPC_PEP, FORM, STREAM, TILED>(a.prm, a.positions, a.k[B200IPC_PEP], tile, sm_z, sm_g, sm_lut); break;
+    case B200IPC_PP: stencil_tile<B200IPC_PP, FORM, STREAM, TILED>(a.prm, a.positions, a.k[B200IPC_PP], tile, sm_z, sm_g, sm_lut); break;
+    case B200IPC_PPP: stencil_tile<B200IPC_PPP, FORM, STREAM, TILED>(a.prm, a.positions, a.k[B200IPC_PPP], tile, sm_z, sm_g, sm_lut); break;
+    default: stencil_tile<B200IPC_PT, FORM, STREAM, TILED>(a.prm, a.positions, a.k[B200IPC_PT], tile, sm_z, sm_g, sm_lut); break;
   }
 }
 
@@ -308,12 +338,25 @@ __global__ void reduce_energy_pass2(int nparts, const double* __restrict__ part_
 
 using namespace b200ipc;
 
-extern "C" int b200ipc_barrier_stencils_ex(const b200ipc_params* params, int64_t nverts, const double* positions,
-                                           int64_t n, const int64_t* kind_off, const int32_t* verts,
-                                           const uint8_t* sub, const double* eps_x, double* energy, uint8_t* status,
-                                           double* grad2, double* hess2, double* grad3, double* hess3, double* grad4,
-                                           double* hess4, double* fac2, double* fac3, double* fac4, void* stream) {
+template <int FORM>
+static void launch_stencils(bool streaming, bool tiled, unsigned tiles, cudaStream_t s, const StencilArgs& a) {
+  if (tiled) {
+    if (streaming) barrier_stencil_kernel<FORM, true, true><<<tiles, kTile, 0, s>>>(a);
+    else barrier_stencil_kernel<FORM, false, true><<<tiles, kTile, 0, s>>>(a);
+  } else {
+    if (streaming) barrier_stencil_kernel<FORM, true, false><<<tiles, kTile, 0, s>>>(a);
+    else barrier_stencil_kernel<FORM, false, false><<<tiles, kTile, 0, s>>>(a);
+  }
+}
+
+extern "C" int b200ipc_barrier_stencils_layout(const b200ipc_params* params, int64_t nverts, const double* positions,
+                                               int64_t n, const int64_t* kind_off, const int32_t* verts,
+                                               const uint8_t* sub, const double* eps_x, double* energy,
+                                               uint8_t* status, double* grad2, double* hess2, double* grad3,
+                                               double* hess3, double* grad4, double* hess4, double* fac2, double* fac3,
+                                               double* fac4, int32_t hess_layout, void* stream) {
   if (!params || !kind_off || n < 0 || nverts < 0) return B200IPC_EINVAL;
+  if (hess_layout != B200IPC_LAYOUT_DENSE && hess_layout != B200IPC_LAYOUT_SUBBLOCK) return B200IPC_EINVAL;
   if (n == 0) return 0;
   if (!positions || !verts) return B200IPC_EINVAL;
   if (kind_off[0] != 0 || kind_off[B200IPC_NKINDS] != n) return B200IPC_EINVAL;
@@ -372,14 +415,20 @@ extern "C" int b200ipc_barrier_stencils_ex(const b200ipc_params* params, int64_t
     if (a.k[k].hess) out_bytes += a.k[k].n * 72 * sz * sz;
   }
   const bool streaming = out_bytes > (96ll << 20);
-  if (params->form == 0) {
-    if (streaming) barrier_stencil_kernel<0, true><<<(unsigned)tiles, kTile, 0, s>>>(a);
-    else barrier_stencil_kernel<0, false><<<(unsigned)tiles, kTile, 0, s>>>(a);
-  } else {
-    if (streaming) barrier_stencil_kernel<1, true><<<(unsigned)tiles, kTile, 0, s>>>(a);
-    else barrier_stencil_kernel<1, false><<<(unsigned)tiles, kTile, 0, s>>>(a);
-  }
+  const bool tiled = hess_layout == B200IPC_LAYOUT_SUBBLOCK;
+  if (params->form == 0) launch_stencils<0>(streaming, tiled, (unsigned)tiles, s, a);
+  else launch_stencils<1>(streaming, tiled, (unsigned)tiles, s, a);
   return post_launch();
+}
+
+extern "C" int b200ipc_barrier_stencils_ex(const b200ipc_params* params, int64_t nverts, const double* positions,
+                                           int64_t n, const int64_t* kind_off, const int32_t* verts,
+                                           const uint8_t* sub, const double* eps_x, double* energy, uint8_t* status,
+                                           double* grad2, double* hess2, double* grad3, double* hess3, double* grad4,
+                                           double* hess4, double* fac2, double* fac3, double* fac4, void* stream) {
+  return b200ipc_barrier_stencils_layout(params, nverts, positions, n, kind_off, verts, sub, eps_x, energy, status,
+                                         grad2, hess2, grad3, hess3, grad4, hess4, fac2, fac3, fac4,
+                                         B200IPC_LAYOUT_DENSE, stream);
 }
 
 extern "C" int b200ipc_barrier_stencils(const b200ipc_params* params, int64_t nverts, const double* positions,

@@ -270,7 +270,8 @@ __device__ __forceinline__ bool emit_row(const SymArgs& a, int64_t row, int lane
     __syncwarp();
     if (keep) {
       const uint32_t za = 3u * k.r;                      // element index of z_a = 3 (b s + a)
-      if (a.desc) a.desc[slab + p] = (k.f << 30) | (za * k.s + (uint32_t)c);   // ((b D + 3a) D + 3c) / 3, D = 3s
+      // row-major ((b D + 3a) D + 3c) / 3, D = 3s; sub-block-major 9 (b s^2 + a s + c) / 3
+      if (a.desc) a.desc[slab + p] = (k.f << 30) | (za * k.s + (uint32_t)(a.fd.cmul[k.f] * c));
       if (a.fdesc) a.fdesc[slab + p] = (k.f << 30) | ((uint32_t)(c - (int)k.la + 3) << 27) | za;
     }
     return true;

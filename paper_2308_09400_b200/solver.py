@@ -55,6 +55,7 @@ class NewtonSystem:
         self.nnzb = 0
         self.rowptr = self.colidx = self.vals = self.pinv = None
         self._fam = []        # [(s, nb, vids tensor)]
+        self._tiled = []      # per family: dense blocks arrive sub-block-major
         self._pcg_ws = None
         self._mas, self._mas_ordered, self._mas_levels, self._mas_stale = None, False, 0, True
 
@@ -89,8 +90,18 @@ class NewtonSystem:
             pass
 
     # -- symbolic ---------------------------------------------------------------------------
-    def set_pattern(self, families):
-        """``families``: iterable of (s, vids) with vids an (nb, s) int64 array/tensor."""
+    def set_pattern(self, families, tiled=None):
+        """``families``: iterable of (s, vids) with vids an (nb, s) int64 array/tensor.  ``tiled``: one flag per
+        family -- ``assemble`` will be given that family's dense blocks sub-block-major, (nb,s,s,3,3)
+        (``stencils.evaluate(..., hess_layout="subblock")``), instead of the reference's (nb,3s,3s)."""
+        families = list(families)
+        flags = [False] * len(families) if tiled is None else [bool(t) for t in tiled]
+        if len(flags) != len(families):
+            raise ValueError("one tiled flag per family")
+        flags = [t for t, (s, vids) in zip(flags, families) if len(vids)]   # empty families are dropped below
+        mask = sum(1 << f for f, t in enumerate(flags) if t)
+        _lib.check(_lib.lib().b200ipc_assembly_set_layout(self._h, mask), "assembly_set_layout")
+        self._tiled = flags
         fam = []
         for s, vids in families:
             v = device.to_device(vids, np.int64)
@@ -130,6 +141,10 @@ class NewtonSystem:
     def assemble(self, fam_hess):
         """vals = diag(m I) + segmented sums of the families' blocks (fixed rows: identity)."""
         hs = self._match([h for h in fam_hess if h is not None and len(h)], lambda s: 9 * s * s)
+        for h, t in zip(hs, self._tiled):
+            if (h.dim() == 5) != t:    # same byte count either way: a mix-up would assemble a wrong matrix silently
+                raise ValueError("family blocks are %s but the pattern was set for %s" %
+                                 (("sub-block-major", "row-major") if h.dim() == 5 else ("row-major", "sub-block-major")))
         _lib.check(_lib.lib().b200ipc_assemble_numeric(self._h, device.ptr(self.masses), _ptr_array(hs),
                                                        device.ptr(self.vals), device.stream()), "assemble_numeric")
         self.pinv = None

@@ -59,8 +59,16 @@ class Family:
     s: int
     vids: object   # (nb,s) int64 device
     grad: object   # (nb,3s) device or None
-    hess: object   # (nb,3s,3s) device or None
+    hess: object   # (nb,3s,3s) device or None; (nb,s,s,3,3) when ``tiled``
     fac: object = None   # (nb,3s) device or None: rank-1 factor z, hess == z z^T
+    tiled: bool = False  # hess is sub-block-major (the assembly's internal layout), not the reference's
+
+    def dense_hess(self):
+        """The reference's (nb,3s,3s) blocks whatever the device layout (a permuted copy when ``tiled``)."""
+        if self.hess is None or not self.tiled:
+            return self.hess
+        nb, s = self.hess.shape[0], self.s
+        return self.hess.permute(0, 1, 3, 2, 4).reshape(nb, 3 * s, 3 * s).contiguous()
 
 
 @dataclass
@@ -98,7 +106,7 @@ class BarrierBatch:
 
     def grouped(self):
         """``[(hess, vids)]`` by ascending stencil size, as ``group_blocks`` returns (device tensors)."""
-        return [(self.families[s].hess, self.families[s].vids) for s in sorted(self.families)]
+        return [(self.families[s].dense_hess(), self.families[s].vids) for s in sorted(self.families)]
 
     def to_local_quadratics(self, keep_inactive=False):
         """Host ``LocalQuadratic`` list in the reference's block order, inactive rows dropped
@@ -112,7 +120,7 @@ class BarrierBatch:
             rows = np.concatenate([np.arange(off[k], off[k + 1]) for k in FAMILY_KINDS[s]])
             vids = device.to_host(fam.vids)
             grad = device.to_host(fam.grad) if fam.grad is not None else None
-            hess = device.to_host(fam.hess) if fam.hess is not None else None
+            hess = device.to_host(fam.dense_hess()) if fam.hess is not None else None
             for j, r in enumerate(rows):
                 if status[r] == 0 or keep_inactive:
                     out[r] = LocalQuadratic(vert_ids=vids[j].copy(), grad=None if grad is None else grad[j].copy(),
@@ -125,7 +133,7 @@ def _lib_ws_doubles():
 
 
 def evaluate(table, positions, params, dt=1.0, want_energy=True, want_grad=True, want_hess=True,
-             want_factors=False, out=None):
+             want_factors=False, out=None, hess_layout="dense"):
     """Evaluate every stencil of ``table`` at ``positions``.
 
     ``table``: ``StencilTable`` or ``DeviceStencilTable``; ``positions``: (N,3) host array or
@@ -133,8 +141,13 @@ def evaluate(table, positions, params, dt=1.0, want_energy=True, want_grad=True,
     dt**2, energy is not, like solver.py:207-208).  ``out``: a previous ``BarrierBatch`` for the
     same table whose buffers are reused.  ``want_factors`` adds the rank-1 factors z (hess = z z^T);
     with ``want_hess=False`` the dense blocks are skipped and ``NewtonSystem.assemble_from_factors``
-    builds the matrix from z alone.  Returns a ``BarrierBatch`` (asynchronous).
+    builds the matrix from z alone.  ``hess_layout="subblock"`` leaves the dense blocks on the device as
+    (nb,s,s,3,3) -- the layout ``NewtonSystem.set_pattern(..., tiled=...)`` + ``assemble`` gather fastest; ``Family.dense_hess()``
+    and everything host-facing still give the reference's (nb,3s,3s).  Returns a ``BarrierBatch`` (asynchronous).
     """
+    if hess_layout not in ("dense", "subblock"):
+        raise ValueError("hess_layout must be 'dense' or 'subblock'")
+    tiled = hess_layout == "subblock"
     if isinstance(table, StencilTable):
         table = DeviceStencilTable.from_host(table)
     if not isinstance(params, BarrierParams):
@@ -151,9 +164,11 @@ def evaluate(table, positions, params, dt=1.0, want_energy=True, want_grad=True,
                 continue
             fams[s] = Family(s, table.family_vids(s),
                              device.empty((nb, 3 * s)) if want_grad else None,
-                             device.empty((nb, 3 * s, 3 * s)) if want_hess else None,
-                             device.empty((nb, 3 * s)) if want_factors else None)
+                             device.empty((nb, s, s, 3, 3) if tiled else (nb, 3 * s, 3 * s)) if want_hess else None,
+                             device.empty((nb, 3 * s)) if want_factors else None, tiled)
         out = BarrierBatch(table, device.empty((n,)) if want_energy else None, device.empty((n,), np.uint8), fams)
+    elif any(f.tiled != tiled for f in out.families.values()):
+        raise ValueError("out was evaluated with another hess_layout")
     out._summary = None
     prm = c_params(params, dt)
     koff = (C.c_int64 * 8)(*[int(v) for v in table.kind_off])
@@ -162,12 +177,12 @@ def evaluate(table, positions, params, dt=1.0, want_energy=True, want_grad=True,
         fam = out.families.get(s)
         return device.ptr(getattr(fam, name) if fam is not None else None)
 
-    _lib.check(_lib.lib().b200ipc_barrier_stencils_ex(
+    _lib.check(_lib.lib().b200ipc_barrier_stencils_layout(
         prm, pos.shape[0], device.ptr(pos), n, koff, device.ptr(table.verts), device.ptr(table.sub),
         device.ptr(table.eps_x), device.ptr(out.energy), device.ptr(out.status),
         fam_ptr(2, "grad"), fam_ptr(2, "hess"), fam_ptr(3, "grad"), fam_ptr(3, "hess"),
         fam_ptr(4, "grad"), fam_ptr(4, "hess"), fam_ptr(2, "fac"), fam_ptr(3, "fac"), fam_ptr(4, "fac"),
-        device.stream()), "barrier_stencils")
+        1 if tiled else 0, device.stream()), "barrier_stencils")
     return out
 
 
