@@ -137,3 +137,119 @@ def batched_solver(tetipc):
         yield
     finally:
         ref.pcg_solve, rp.sweep_candidates, rp.global_ccd_filter = saved
+
+
+# ---------------------------------------------------------------------------------------------------------------
+# 3. function overlay: every function of the reference's modules that this package mirrors, swapped in place
+# ---------------------------------------------------------------------------------------------------------------
+# (reference module, name) -> the mirror.  Arguments are duck-typed on the reference's field names, so the
+# reference's own objects (ContactStencil, BarrierParams, DiagonalJacobian, FrictionDatum, Scene ...) go straight in;
+# results and exceptions are handed back as the REFERENCE's classes.
+
+def _overlay_table():
+    from . import barrier, elasticity, friction, gap, mollifier
+
+    return {
+        "barrier": {n: getattr(barrier, n) for n in ("barrier_value", "barrier_dg", "barrier_d2g", "lambda1", "lambda23",
+                                                      "filtered_lambda1", "build_local_quadratic")},
+        "gap": {n: getattr(gap, n) for n in ("build_diagonal_jacobian", "gap_function")},
+        "proximity": {"stencil_distance": gap.stencil_distance, "parallel_measure": gap.parallel_measure,
+                      "find_contact_pairs": contacts.find_contact_pairs, "accd_step_bound": contacts.accd_step_bound,
+                      "sweep_candidates": contacts.sweep_candidates, "global_ccd_filter": contacts.global_ccd_filter},
+        "mollifier": {n: getattr(mollifier, n) for n in ("mollified_eigensystem", "mollified_barrier_value",
+                                                          "mollified_gradient", "build_mollified_local_quadratic")},
+        "friction": {n: getattr(friction, n) for n in ("f0_f1", "potential", "friction_force", "friction_hessian_psd",
+                                                        "tangential_displacement", "update_friction_state")},
+        "elasticity": {n: getattr(elasticity, n) for n in ("rest_data", "batch_grad_hess", "tet_energy_grad_hess")},
+        "solver": {n: getattr(bsolver, n) for n in ("group_blocks", "matvec_matrix_free", "block_jacobi_preconditioner",
+                                                    "pcg_solve")},
+        "kernels": {n: getattr(b200_kernels, n) for n in _SEAM},
+    }
+
+
+def _reference_classes(tetipc):
+    """name -> class for every dataclass / enum / exception the reference's modules define."""
+    import enum
+    import importlib
+
+    out = {}
+    for mod in ("proximity", "gap", "barrier", "mollifier", "friction", "elasticity"):
+        m = importlib.import_module(f"{tetipc.__name__}.{mod}")
+        for name, val in vars(m).items():
+            if isinstance(val, type) and val.__module__ == m.__name__ and (
+                    hasattr(val, "__dataclass_fields__") or issubclass(val, (enum.Enum, Exception))):
+                out[name] = val
+    return out
+
+
+def _as_reference(obj, classes):
+    """This package's records / enums -> the reference's classes of the same name (recursively through lists,
+    tuples and record fields); arrays and scalars pass through."""
+    import dataclasses
+    import enum
+
+    if isinstance(obj, list):
+        return [_as_reference(o, classes) for o in obj]
+    if type(obj) is tuple:
+        return tuple(_as_reference(o, classes) for o in obj)
+    cls = classes.get(type(obj).__name__)
+    if cls is None or isinstance(obj, cls) or not type(obj).__module__.startswith(__package__):
+        return obj
+    if isinstance(obj, enum.Enum):
+        return cls(obj.value)
+    if dataclasses.is_dataclass(obj):
+        return cls(**{f.name: _as_reference(getattr(obj, f.name), classes) for f in dataclasses.fields(cls)
+                      if hasattr(obj, f.name)})
+    return obj
+
+
+@contextlib.contextmanager
+def function_overlay(tetipc, calls=None):
+    """Within the block every function of ``tetipc.{barrier, gap, proximity, mollifier, friction, elasticity,
+    solver, kernels}`` that this package mirrors IS the mirror -- in the defining module and in every other
+    ``tetipc`` module that imported it by name -- so the reference's own callers and its own test-suite
+    (``tests/test_gpu_reference_suite.py``) exercise the B200 backend.  ``calls``: optional dict, filled with
+    ``"module.function" -> number of calls``."""
+    import functools
+    import importlib
+    import sys
+
+    classes = _reference_classes(tetipc)
+    root = tetipc.__name__
+
+    def wrap(key, fn):
+        @functools.wraps(fn)
+        def mirrored(*args, **kwargs):
+            if calls is not None:
+                calls[key] = calls.get(key, 0) + 1
+            try:
+                return _as_reference(fn(*args, **kwargs), classes)
+            except Exception as exc:
+                cls = classes.get(type(exc).__name__)
+                if (cls is not None and not isinstance(exc, cls) and isinstance(cls, type)
+                        and issubclass(cls, Exception) and type(exc).__module__.startswith(__package__)):
+                    raise cls(*exc.args) from exc
+                raise
+        return mirrored
+
+    saved = []
+    try:
+        for mod, table in _overlay_table().items():
+            ref_mod = importlib.import_module(f"{root}.{mod}")
+            for name, fn in table.items():
+                orig = getattr(ref_mod, name)
+                new = wrap(f"{mod}.{name}", fn)
+                for mname, m in list(sys.modules.items()):
+                    if m is None or not (mname == root or mname.startswith(root + ".")):
+                        continue
+                    for attr, val in list(vars(m).items()):
+                        if val is orig:
+                            saved.append((m, attr, orig))
+                            setattr(m, attr, new)
+        kernels_mod = importlib.import_module(f"{root}.kernels")
+        saved.append((kernels_mod, "BACKEND", kernels_mod.BACKEND))
+        kernels_mod.BACKEND = b200_kernels.BACKEND
+        yield
+    finally:
+        for m, attr, orig in reversed(saved):
+            setattr(m, attr, orig)

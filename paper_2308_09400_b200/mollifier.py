@@ -11,22 +11,33 @@ from .barrier import _blocks_from_jac, c_params
 from .proximity import PARALLEL_KINDS, StencilKind
 
 
+_IDX_G1 = 4   # slot (2,2) of the 3x3 J-space layout: gamma channel diagonal (mollifier.py:21)
+_IDX_F1 = 8   # slot (3,3): gap channel diagonal (mollifier.py:22)
+
+
 @dataclass
 class MollifiedEigenSystem:
-    """Channel eigenvalues and the retained coupled pair (mollifier.py:35-52)."""
+    """The reference's record, field for field (mollifier.py:35-52): ``lambda_gamma`` / ``lambda_g`` hold
+    (primary, twist, twist) of the two channels, ``lambda7p <= lambda8p`` the eigenvalues of the 2x2 coupling
+    block and ``q8p`` its normalised eigenmatrix (9-vector, entries at slots (2,2) and (3,3)); ``q_gamma2`` /
+    ``q_gamma3`` are the constant twist directions.  After them, what the kernel computes besides: the two
+    entries of ``q8p`` as scalars, the channel derivatives and the mollifier value / slope."""
 
-    lambda_gamma1: float
-    lambda_g1: float
+    lambda_gamma: tuple
+    lambda_g: tuple
     t: float
     p: float
     lambda7p: float
     lambda8p: float
-    q_gamma: float
-    q_f: float
-    b_gamma: float
-    b_g: float
-    e_k: float
-    de_dgamma: float
+    q_gamma2: np.ndarray
+    q_gamma3: np.ndarray
+    q8p: np.ndarray
+    q_gamma: float = 0.0
+    q_f: float = 0.0
+    b_gamma: float = 0.0
+    b_g: float = 0.0
+    e_k: float = 0.0
+    de_dgamma: float = 0.0
 
 
 def mollified_eigensystem_batch(g, c, eps_x, params):
@@ -48,7 +59,18 @@ def mollified_eigensystem_batch(g, c, eps_x, params):
 
 def mollified_eigensystem(g, c, params, eps_x):
     """Closed-form eigensystem of the mollified J-space Hessian (mollifier.py:106-144)."""
-    return MollifiedEigenSystem(*[float(v) for v in mollified_eigensystem_batch(g, c, eps_x, params)[0]])
+    lam_gamma1, lam_g1, t, p, lam7p, lam8p, q_gamma, q_f, b_gamma, b_g, e_k, de = (
+        float(v) for v in mollified_eigensystem_batch(g, c, eps_x, params)[0])
+    q8p = np.zeros(9)
+    q8p[_IDX_G1], q8p[_IDX_F1] = q_gamma, q_f
+    q_gamma2 = np.zeros(9)
+    q_gamma2[5] = -1.0     # twist onto slot (3,2) (mollifier.py:129-130)
+    q_gamma3 = np.zeros(9)
+    q_gamma3[3] = 1.0      # twist onto slot (1,2) (mollifier.py:131-132)
+    lam_gamma23, lam_g23 = 2.0 * b_gamma, 2.0 * b_g           # mollifier.py:110, :112
+    return MollifiedEigenSystem(lambda_gamma=(lam_gamma1, lam_gamma23, lam_gamma23), lambda_g=(lam_g1, lam_g23, lam_g23),
+                                t=t, p=p, lambda7p=lam7p, lambda8p=lam8p, q_gamma2=q_gamma2, q_gamma3=q_gamma3, q8p=q8p,
+                                q_gamma=q_gamma, q_f=q_f, b_gamma=b_gamma, b_g=b_g, e_k=e_k, de_dgamma=de)
 
 
 def mollified_barrier_value(g, c, params, eps_x):
