@@ -204,12 +204,13 @@ def _as_reference(obj, classes):
 
 
 @contextlib.contextmanager
-def function_overlay(tetipc, calls=None):
+def function_overlay(tetipc, calls=None, batched=False):
     """Within the block every function of ``tetipc.{barrier, gap, proximity, mollifier, friction, elasticity,
     solver, kernels}`` that this package mirrors IS the mirror -- in the defining module and in every other
     ``tetipc`` module that imported it by name -- so the reference's own callers and its own test-suite
     (``tests/test_gpu_reference_suite.py``) exercise the B200 backend.  ``calls``: optional dict, filled with
-    ``"module.function" -> number of calls``."""
+    ``"module.function" -> number of calls``.  ``batched``: additionally ``tetipc.solver.SimState`` IS
+    ``b200_sim_state(tetipc)`` (contact detection and the per-stencil barrier loops as single batched launches)."""
     import functools
     import importlib
     import sys
@@ -246,6 +247,22 @@ def function_overlay(tetipc, calls=None):
                         if val is orig:
                             saved.append((m, attr, orig))
                             setattr(m, attr, new)
+        if batched:
+            solver_mod = importlib.import_module(f"{root}.solver")
+            orig_cls = solver_mod.SimState
+            new_cls = b200_sim_state(tetipc)
+            if calls is not None:
+                for meth in ("detect", "_barrier_energy", "barrier_gradient_blocks", "assemble_local_quadratics"):
+                    def counted(self, *a, _m=getattr(new_cls, meth), _k="SimState." + meth, **kw):
+                        calls[_k] = calls.get(_k, 0) + 1
+                        return _m(self, *a, **kw)
+                    setattr(new_cls, meth, counted)
+            for mname, m in list(sys.modules.items()):
+                if m is not None and (mname == root or mname.startswith(root + ".")):
+                    for attr, val in list(vars(m).items()):
+                        if val is orig_cls:
+                            saved.append((m, attr, orig_cls))
+                            setattr(m, attr, new_cls)
         kernels_mod = importlib.import_module(f"{root}.kernels")
         saved.append((kernels_mod, "BACKEND", kernels_mod.BACKEND))
         kernels_mod.BACKEND = b200_kernels.BACKEND

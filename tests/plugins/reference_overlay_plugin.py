@@ -1,8 +1,9 @@
-"""pytest plugin (``-p reference_overlay_plugin``), loaded only by tests/test_gpu_reference_suite.py in a child
+"""pytest plugin (``-p reference_overlay_plugin``, this directory on PYTHONPATH), loaded only by tests/test_gpu_reference_suite.py in a child
 pytest that runs the REFERENCE's own test-suite: before the reference's test modules are imported, every function
 of ``tetipc`` that ``paper_2308_09400_b200`` mirrors is swapped for the mirror
 (``paper_2308_09400_b200.integration.function_overlay``).  Writes the per-function call counts to
-``$B200_OVERLAY_REPORT`` when the session ends."""
+``$B200_OVERLAY_REPORT`` when the session ends.  ``$B200_OVERLAY_BATCHED``: the reference's ``SimState`` is the batched
+subclass of ``integration.b200_sim_state`` as well."""
 
 import json
 import os
@@ -18,7 +19,7 @@ def pytest_configure(config):
     from paper_2308_09400_b200 import integration
 
     _STATE["calls"] = {}
-    _STATE["cm"] = integration.function_overlay(tetipc, _STATE["calls"])
+    _STATE["cm"] = integration.function_overlay(tetipc, _STATE["calls"], batched=bool(os.environ.get("B200_OVERLAY_BATCHED")))
     _STATE["cm"].__enter__()
 
 

@@ -42,16 +42,15 @@ MUST_BE_CALLED = ["barrier.barrier_value", "barrier.lambda1", "barrier.build_loc
                   "kernels.ee_classify_batch"]
 
 
-def test_reference_test_suite_passes_on_this_backend(tmp_path):
-    pkg, tests = _locate()
-    if pkg is None:
-        pytest.skip("the reference package and its tests are not available here")
+def _run_reference_suite(tmp_path, pkg, tests, select, batched):
     report = tmp_path / "overlay_calls.json"
     env = dict(os.environ)
-    env["PYTHONPATH"] = os.pathsep.join([os.path.join(ROOT, "tests"), ROOT, pkg] + env.get("PYTHONPATH", "").split(os.pathsep))
+    if batched:
+        env["B200_OVERLAY_BATCHED"] = "1"
+    env["PYTHONPATH"] = os.pathsep.join([os.path.join(ROOT, "tests", "plugins"), ROOT, pkg] + env.get("PYTHONPATH", "").split(os.pathsep))
     env["B200_OVERLAY_REPORT"] = str(report)
     env["HYPOTHESIS_STORAGE_DIRECTORY"] = str(tmp_path / "hypothesis")
-    cmd = [sys.executable, "-m", "pytest", tests, "-q", "-p", "reference_overlay_plugin", "-p", "no:cacheprovider",
+    cmd = [sys.executable, "-m", "pytest", select, "-q", "-p", "reference_overlay_plugin", "-p", "no:cacheprovider",
            "--rootdir", tests, "-o", "addopts=", "--tb=short",
            # fails on the unmodified reference alone (a CLI diagnostic curve, 9.0e-5 against its own 1e-6 bound; no
            # function of the path is involved): 170 of the reference's 171 tests pass on the reference itself
@@ -60,8 +59,29 @@ def test_reference_test_suite_passes_on_this_backend(tmp_path):
     tail = "\n".join(run.stdout.splitlines()[-60:])
     m = re.search(r"(\d+) passed", run.stdout)
     assert run.returncode == 0, f"reference test-suite on the B200 backend:\n{tail}\n{run.stderr[-2000:]}"
-    assert m and int(m.group(1)) >= 170, tail
-    calls = json.loads(report.read_text())
+    return (int(m.group(1)) if m else 0), json.loads(report.read_text()), tail
+
+
+def test_reference_test_suite_passes_on_this_backend(tmp_path):
+    pkg, tests = _locate()
+    if pkg is None:
+        pytest.skip("the reference package and its tests are not available here")
+    passed, calls, tail = _run_reference_suite(tmp_path, pkg, tests, tests, batched=False)
+    assert passed >= 170, tail
     missing = [k for k in MUST_BE_CALLED if calls.get(k, 0) == 0]
     assert not missing, f"mirrors the reference's tests never reached: {missing}\n{json.dumps(calls, indent=1)}"
     print(json.dumps(calls, sort_keys=True))
+
+
+def test_reference_solver_tests_pass_on_the_batched_sim_state(tmp_path):
+    """The reference's ``tests/test_solver.py`` once more, with ``SimState`` itself replaced by the batched
+    subclass (``integration.b200_sim_state``): detect, barrier energy and the barrier blocks of every Newton
+    iteration are single device launches under the reference's own ``newton_step`` / ``advance_time_step``."""
+    pkg, tests = _locate()
+    if pkg is None:
+        pytest.skip("the reference package and its tests are not available here")
+    passed, calls, tail = _run_reference_suite(tmp_path, pkg, tests, os.path.join(tests, "test_solver.py"), batched=True)
+    assert passed >= 15, tail
+    for k in ("SimState.detect", "SimState._barrier_energy", "SimState.assemble_local_quadratics", "solver.pcg_solve"):
+        assert calls.get(k, 0) > 0, f"{k} never ran\n{json.dumps(calls, indent=1)}"
+    print(json.dumps({k: v for k, v in calls.items() if k.startswith("SimState")}, sort_keys=True))
