@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) bsr_spmv_stream_kernel(cons
 
 int stream_rows_per_chunk(int64_t n, int64_t nnzb) {
   const double avg = n > 0 ? (double)nnzb / (double)n : 1.0;
-  int r = (int)(0.7 * kStageBlocks / (avg > 1.0 ? avg : 1.0)) / 3 * 3;  // three rows per warp trip
+  int r = (int)(0.72 * kStageBlocks / (avg > 1.0 ? avg : 1.0)) / 3 * 3;  // three rows per warp trip (cloth stack: 27 rows = 9 of a group's 10 warps busy; 24 / 27 / 30 rows: 35.1 / 34.1 / 35.1 us per PCG iteration)
   if (const char* env = getenv("B200IPC_SPMV_ROWS_PER_CHUNK")) r = atoi(env);
   return r < 3 ? 3 : (r > kMaxChunkRows ? kMaxChunkRows : r);
 }
