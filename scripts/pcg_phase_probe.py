@@ -16,6 +16,7 @@ sysm.set_pattern([(f.s, f.vids) for f in fams]); sysm.assemble([f.hess for f in 
 xt = device.to_device(cloth.positions + 1e-4 * np.random.default_rng(1).normal(size=cloth.positions.shape))
 rhs = -sysm.gradient(pos, xt, [f.grad for f in fams])
 sysm.block_jacobi()
+for _ in range(3): sysm.spmv(rhs)
 sysm.pcg(rhs, 1e-30, 5)
 torch.cuda.synchronize(); t0 = time.perf_counter()
 d, iters, ok, _, _ = sysm.pcg(rhs, 1e-30, 200)
