@@ -36,4 +36,11 @@ print("tets", len(h), "hess err max %.3e  p99.9 %.3e   grad err max %.3e" % (err
 w = np.flatnonzero(err > 1e-9)
 print("rows over 1e-9:", len(w), "kinds", np.bincount(kind[good][w], minlength=5) if len(w) else "-")
 ev = np.linalg.eigvalsh(0.5 * (h + np.swapaxes(h, 1, 2)))
-print("min eig / max eig worst: %.3e" % (ev.min(axis=1) / np.maximum(ev.max(axis=1), 1e-300)).min(), "finite", bool(np.isfinite(h).all()))
+# block = vol * G^T P G with P the projected F-space Hessian (elasticity.py:114-137): PSD for a positively oriented
+# REST tet; the random rest shapes here are negatively oriented half of the time (mesh loading rejects those), and
+# both the reference and this kernel then return the same negative-semidefinite block
+pos = vols[good] > 0
+rel_min = ev.min(axis=1) / np.maximum(scale, 1e-300)
+rel_max = ev.max(axis=1) / np.maximum(scale, 1e-300)
+print("positively oriented rest tets: %d, min eig / block scale worst %.3e;  negatively oriented: %d, max eig / block scale worst %.3e;  finite %s"
+      % (int(pos.sum()), rel_min[pos].min(), int((~pos).sum()), rel_max[~pos].max(), bool(np.isfinite(h).all())))
