@@ -63,6 +63,10 @@ int b200ipc_abi_version(void);
 const char* b200ipc_build_info(void);
 /* Number of kernel launches issued by this library since load (all threads). */
 int64_t b200ipc_launch_count(void);
+/* dst[i] = src[idx[i]], rows of row_bytes bytes (a multiple of 4), all device pointers; idx (n) i64.  The row
+ * compaction of the lagged friction state (friction.py:148-171 keeps the stencils with lambda_n > 0) and any other
+ * place where the host mirror needs whole rows by index. */
+int b200ipc_gather_rows(int64_t n, int64_t row_bytes, const void* src, const int64_t* idx, void* dst, void* stream);
 
 /* Measured FP64 FMA throughput of the current device in TFLOP/s (2 flop per DFMA): a register-resident
  * DFMA microbenchmark, best of five launches.  The denominator of the fp64 rooflines.

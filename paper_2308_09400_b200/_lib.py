@@ -48,6 +48,7 @@ SIGNATURES = {
     "b200ipc_abi_version": [],
     "b200ipc_build_info": [],
     "b200ipc_launch_count": [],
+    "b200ipc_gather_rows": [_i64, _i64, _vp, _vp, _vp, _vp],
     "b200ipc_fp64_probe": [C.POINTER(_dbl), _vp],
     "b200ipc_pt_classify": [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "b200ipc_ee_classify": [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],

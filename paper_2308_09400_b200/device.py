@@ -65,3 +65,19 @@ def ptr(x):
 
 def stream():
     return C.c_void_p(torch().cuda.current_stream().cuda_stream)
+
+
+def gather_rows(src, idx):
+    """``src[idx]`` along dim 0 for a contiguous device tensor (rows of any width), by ``b200ipc_gather_rows``."""
+    from . import _lib
+
+    t = torch()
+    src = src.contiguous()
+    idx = idx.to(t.int64).contiguous()
+    out = t.empty((idx.shape[0],) + tuple(src.shape[1:]), dtype=src.dtype, device=src.device)
+    row_bytes = src.element_size() * (int(src.numel() // src.shape[0]) if src.shape[0] else 1)
+    if row_bytes % 4 or idx.shape[0] == 0 or src.shape[0] == 0:
+        return src.index_select(0, idx)          # byte-wide rows (the u8 columns): torch's 1-D path is fine there
+    _lib.check(_lib.lib().b200ipc_gather_rows(idx.shape[0], row_bytes, ptr(src), ptr(idx), ptr(out), stream()),
+               "gather_rows")
+    return out

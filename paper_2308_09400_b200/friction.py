@@ -114,9 +114,11 @@ def update_state(table, positions, mu, eps_v, dt, barrier_batch=None, params=Non
         raise ValueError("undefined contact normal for friction basis")
     keep = t.nonzero(ok).squeeze(1)
     koff = np.concatenate([[0], np.cumsum(host[:7])]).astype(np.int64)
-    sub = DeviceStencilTable(int(keep.shape[0]), koff, table.verts[keep].contiguous(), table.sub[keep].contiguous(),
-                             table.eps_x[keep].contiguous())
-    return FrictionState(sub, frame[keep].contiguous(), keep, float(mu), float(eps_v), float(dt))
+    # whole rows by index (torch's 2-D index_select / advanced indexing: 0.55 ms each for the (n,12) frames and the
+    # (n,4) vertex rows of 1 M contacts)
+    sub = DeviceStencilTable(int(keep.shape[0]), koff, device.gather_rows(table.verts, keep), table.sub.index_select(0, keep),
+                             device.gather_rows(table.eps_x, keep))
+    return FrictionState(sub, device.gather_rows(frame, keep), keep, float(mu), float(eps_v), float(dt))
 
 
 def evaluate(state, positions, positions_start, want_energy=True, want_grad=True, want_hess=True):

@@ -186,3 +186,22 @@ def test_barrier_and_friction_families_assemble_together(F, z):
     gref = o.scatter_gradient(masses, fixed, z["x1"], xt, [(f.s, None, F.device.to_host(f.vids), F.device.to_host(f.grad), None) for f in fams])
     assert np.abs(g - gref).max() <= TOL * np.abs(gref).max()
     sysm.close()
+
+
+def test_gather_rows_matches_indexing():
+    """``b200ipc_gather_rows`` (the row compaction of the lagged friction state): any row width that is a multiple of
+    4 bytes, 16- / 8- / 4-byte word paths, repeated and out-of-order indices, empty inputs."""
+    import torch
+
+    from paper_2308_09400_b200 import device
+
+    g = torch.Generator(device="cuda").manual_seed(5)
+    for shape, dtype in (((5000, 12), torch.float64), ((5000, 4), torch.int32), ((5000,), torch.float64),
+                         ((4097, 3), torch.int32), ((300, 3, 3), torch.float64), ((1000, 5), torch.float32)):
+        src = (torch.rand(shape, generator=g, device="cuda", dtype=torch.float64) * 1000).to(dtype)
+        idx = torch.randint(0, shape[0], (7001,), generator=g, device="cuda")
+        assert torch.equal(device.gather_rows(src, idx), src[idx])
+        assert torch.equal(device.gather_rows(src[1:], idx.clamp(max=shape[0] - 2)), src[1:][idx.clamp(max=shape[0] - 2)])
+        assert device.gather_rows(src, idx[:0]).shape == (0,) + tuple(shape[1:])
+    u8 = torch.randint(0, 255, (100,), device="cuda", dtype=torch.uint8)       # byte rows fall back to torch
+    assert torch.equal(device.gather_rows(u8, torch.arange(99, -1, -1, device="cuda")), u8.flip(0))
