@@ -50,6 +50,10 @@ def init(backend="nccl"):
     if backend == "nccl":
         import torch
 
+        have = torch.cuda.device_count()
+        if local >= have:
+            raise SystemExit(f"rank {rank}: local rank {local} needs GPU {local}, but this node has {have} "
+                             f"(one process per GPU: --gpus must not exceed the GPUs of the node)")
         torch.cuda.set_device(local)
     if world > 1:
         import torch
