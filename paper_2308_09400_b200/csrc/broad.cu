@@ -9,7 +9,8 @@
 //      on the device alongside;
 //   2. every "A" box (vertex box [p - d_hat, p + d_hat]; inflated edge AABB) probes the cells that can
 //      hold the lower corner of an overlapping B box, [A.lo - max extent, A.hi], finds each cell
-//      column's run by binary search, and keeps a pair when
+//      column's run (dense cell table, or binary search on large grids), and -- eight lanes per A box
+//      walking the runs laid end to end -- keeps a pair when
 //        - the boxes overlap (the reference's own predicate lo_a <= hi_b && lo_b <= hi_a on the same
 //          fp64 box corners, so the candidate SET equals the reference's),
 //        - the reference's incidence filters pass (vertex not a corner of the triangle, :286;
@@ -194,19 +195,13 @@ struct JoinArgs {
   const uint32_t* ids;
   const Box* bbox;          // boxes of the B elements
   const double* ext;        // largest B extent per axis (device, 3)
+  const int32_t* rev;       // dense cell table or null: rev[ncell - c] = first sorted entry with key >= c
+  int64_t ncell;            // 2^key_bits
   unsigned long long* total;  // pairs found (device counter)
   int4* out;                // staging list of (pairs, 4) global vertex ids
   unsigned long long cap;   // its capacity: pairs beyond it are counted, not stored
 };
 
-// EE = false: A = vertex boxes, B = triangles.  EE = true: A = B = inflated edge boxes.
-// One thread per (A box, slot): slot (rx, ry) of kJoinSlots = 3 x 3 walks the cell columns
-// (x0 + rx + 3p, y0 + ry + 3q) of the box's span, so a box covering up to 3 x 3 columns is spread over
-// nine threads (4 - 8 x more threads and correspondingly shorter loops than one thread per box; larger
-// spans just loop).  A thread keeps up to kHold hit ids in registers; the warp reserves room for all of
-// them with one atomicAdd when its lanes have finished (a lane whose registers fill up mid-walk flushes
-// with the other lanes in the same state).
-constexpr int kJoinSlots = 9;
 constexpr int kHold = 4;
 
 template <bool EE>
@@ -215,20 +210,38 @@ __device__ __forceinline__ int4 pair_row(const JoinArgs& a, int av0, int av1, in
   return make_int4(av0, a.b_elems[3 * j], a.b_elems[3 * j + 1], a.b_elems[3 * j + 2]);
 }
 
+// The join.  EE = false: A = vertex boxes, B = triangles.  EE = true: A = B = inflated edge boxes.
+// EIGHT lanes per A box.  (Round 1's form, one thread per (box, 3 x 3 probe slot) walking its own cell column, left
+// lanes idle whenever a box spans fewer than 3 x 3 columns and whenever the columns of a warp's slots hold different
+// numbers of boxes -- ncu, cloth stack: 13 of 32 lanes active on average -- and paid a binary search per slot plus a
+// key test per visit.)  The group first finds, one lane per column, the sorted-bin range [t0, t1) of every column
+// (cx, cy, z0..z1) of the span -- two reads of the dense cell table when the grid has at most 2^21 cells, two
+// binary searches otherwise -- lays the ranges end to end (prefix sum over the group, table in shared memory) and
+// then walks the FLATTENED list with stride 8: every lane has a candidate until the list runs out, and the lanes
+// read consecutive (id) entries.  The reference's own overlap predicate on the same fp64 corners decides, so the
+// pairs are the reference's; the list order is arbitrary, which no consumer depends on (it is a set).  A lane keeps
+// up to kHold hit ids in registers; the warp reserves room for all of them with one atomicAdd when its lanes have
+// finished (a lane whose registers fill up mid-walk flushes with the other lanes in the same state).
+#ifndef B200IPC_JOIN_GROUP
+#define B200IPC_JOIN_GROUP 8
+#endif
+constexpr int kJoinGroup = B200IPC_JOIN_GROUP;   // lanes per A box (8 / 16 / 32 measured: see DESIGN 4.4)
+
 template <bool EE>
 __global__ void __launch_bounds__(kBT) join_kernel(const __grid_constant__ JoinArgs a) {
-  const int64_t T = (int64_t)blockIdx.x * kBT + threadIdx.x;
-  const bool live = T < a.na * kJoinSlots;
+  __shared__ int32_t tab_t0[kBT / kJoinGroup][kJoinGroup];     // first bin entry of the column
+  __shared__ int32_t tab_end[kBT / kJoinGroup][kJoinGroup];    // end of the column in the flattened list
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (kJoinGroup - 1);
+  const int grp = threadIdx.x / kJoinGroup;
+  const unsigned gmask = kJoinGroup == 32 ? 0xffffffffu : (((1u << kJoinGroup) - 1u) << (lane & ~(kJoinGroup - 1)));
+  const int64_t i = ((int64_t)blockIdx.x * kBT + threadIdx.x) / kJoinGroup;
+  const bool live = i < a.na;
   int32_t n = 0;
   int h0 = 0, h1 = 0, h2 = 0, h3 = 0;
   int av0 = -1, av1 = -1;
-  if (live) {
-    const int64_t i = T / kJoinSlots;
-    const int slot = (int)(T - i * kJoinSlots);
-    const int rx = slot / 3, ry = slot - 3 * rx;
+  if (live) {   // uniform over the group
     const Box A = EE ? a.bbox[i] : make_box<0>(a.in, a.a_elems, i);
-    // cells that can hold the lower corner of an overlapping B box: [A.lo - max extent, A.hi]; the extent
-    // is widened by 1e-9 relative so that the roundings of hi - lo and lo - extent cannot lose a cell
     constexpr double kWiden = 1.000000001;
     Span s;
     s.x0 = cell_of(A.lx - kWiden * a.ext[0], a.g.ox, a.g.inv, a.g.mx); s.x1 = cell_of(A.hx, a.g.ox, a.g.inv, a.g.mx);
@@ -240,48 +253,78 @@ __global__ void __launch_bounds__(kBT) join_kernel(const __grid_constant__ JoinA
     } else {
       av0 = a.a_elems[i];
     }
-    for (int cx = s.x0 + rx; cx <= s.x1; cx += 3)
-      for (int cy = s.y0 + ry; cy <= s.y1; cy += 3) {
-        // cells (cx, cy, z0..z1) are consecutive keys: one search, one walk
+    const int ncy = s.y1 - s.y0 + 1;
+    const int ncol = (s.x1 - s.x0 + 1) * ncy;
+    for (int c0 = 0; c0 < ncol; c0 += kJoinGroup) {   // a group's worth of columns at a time (a cloth box spans at most nine)
+      const int c = c0 + gl;
+      int32_t t0 = 0, len = 0;
+      if (c < ncol) {
+        const int cx = s.x0 + c / ncy, cy = s.y0 + c % ncy;
+        // cells (cx, cy, z0..z1) are consecutive keys
         const uint64_t k0 = cell_key(a.g, cx, cy, s.z0), k1 = cell_key(a.g, cx, cy, s.z1);
-        for (int64_t t = lower_bound_u64(a.keys, a.nbins, k0); t < a.nbins; ++t) {
-          const uint64_t key = a.keys[t];
-          if (key > k1) break;
-          const int64_t j = a.ids[t];
-          if (EE && j <= i) continue;  // each unordered pair once, lower edge index first (:310)
-          const Box B = a.bbox[j];
-          if (!(A.lx <= B.hx && B.lx <= A.hx && A.ly <= B.hy && B.ly <= A.hy && A.lz <= B.hz && B.lz <= A.hz)) continue;
-          if (EE) {
-            const int b0 = a.b_elems[2 * j], b1 = a.b_elems[2 * j + 1];
-            if (av0 == b0 || av0 == b1 || av1 == b0 || av1 == b1) continue;
-          } else {
-            const int t0 = a.b_elems[3 * j], t1 = a.b_elems[3 * j + 1], t2 = a.b_elems[3 * j + 2];
-            if (av0 == t0 || av0 == t1 || av0 == t2) continue;
-          }
-          if (n == kHold) {  // registers full: flush with whichever lanes are here too
-            const unsigned m = __activemask();
-            const int lead = __ffs(m) - 1, rank = __popc(m & ((1u << (threadIdx.x & 31)) - 1));
-            unsigned long long base = 0;
-            if ((int)(threadIdx.x & 31) == lead) base = atomicAdd(a.total, (unsigned long long)kHold * __popc(m));
-            base = __shfl_sync(m, base, lead) + (unsigned long long)kHold * rank;
-            if (base + kHold <= a.cap) {
-              a.out[base] = pair_row<EE>(a, av0, av1, h0);
-              a.out[base + 1] = pair_row<EE>(a, av0, av1, h1);
-              a.out[base + 2] = pair_row<EE>(a, av0, av1, h2);
-              a.out[base + 3] = pair_row<EE>(a, av0, av1, h3);
-            }
-            n = 0;
-          }
-          if (n == 0) h0 = (int)j;
-          else if (n == 1) h1 = (int)j;
-          else if (n == 2) h2 = (int)j;
-          else h3 = (int)j;
-          ++n;
+        if (a.rev) {   // dense grid: two table reads instead of two binary searches
+          t0 = a.rev[a.ncell - (int64_t)k0];
+          len = a.rev[a.ncell - (int64_t)k1 - 1] - t0;
+        } else {
+          t0 = (int32_t)lower_bound_u64(a.keys, a.nbins, k0);
+          len = (int32_t)lower_bound_u64(a.keys, a.nbins, k1 + 1) - t0;
         }
       }
+      int32_t incl = len;
+#pragma unroll
+      for (int o = 1; o < kJoinGroup; o <<= 1) {
+        const int32_t v = __shfl_up_sync(gmask, incl, o, kJoinGroup);
+        if (gl >= o) incl += v;
+      }
+      const int32_t total = __shfl_sync(gmask, incl, kJoinGroup - 1, kJoinGroup);
+      __syncwarp(gmask);                 // the previous batch's readers are done with the table
+      tab_t0[grp][gl] = t0;
+      tab_end[grp][gl] = incl;
+      __syncwarp(gmask);
+      int col = 0;
+      int32_t cend = tab_end[grp][0], cbeg = 0, ct0 = tab_t0[grp][0];
+      for (int32_t f = gl; f < total; f += kJoinGroup) {
+        while (f >= cend) {              // this lane's cursor moves on to the column that holds f
+          ++col;
+          cbeg = cend;
+          cend = tab_end[grp][col];
+          ct0 = tab_t0[grp][col];
+        }
+        const int64_t j = a.ids[ct0 + (f - cbeg)];
+        if (EE && j <= i) continue;  // each unordered pair once, lower edge index first (:310)
+        const Box B = a.bbox[j];
+        if (!(A.lx <= B.hx && B.lx <= A.hx && A.ly <= B.hy && B.ly <= A.hy && A.lz <= B.hz && B.lz <= A.hz)) continue;
+        if (EE) {
+          const int b0 = a.b_elems[2 * j], b1 = a.b_elems[2 * j + 1];
+          if (av0 == b0 || av0 == b1 || av1 == b0 || av1 == b1) continue;
+        } else {
+          const int t0v = a.b_elems[3 * j], t1v = a.b_elems[3 * j + 1], t2v = a.b_elems[3 * j + 2];
+          if (av0 == t0v || av0 == t1v || av0 == t2v) continue;
+        }
+        if (n == kHold) {  // registers full: flush with whichever lanes are here too
+          const unsigned m = __activemask();
+          const int lead = __ffs(m) - 1, rank = __popc(m & ((1u << lane) - 1));
+          unsigned long long base = 0;
+          if (lane == lead) base = atomicAdd(a.total, (unsigned long long)kHold * __popc(m));
+          base = __shfl_sync(m, base, lead) + (unsigned long long)kHold * rank;
+          if (base + kHold <= a.cap) {
+            a.out[base] = pair_row<EE>(a, av0, av1, h0);
+            a.out[base + 1] = pair_row<EE>(a, av0, av1, h1);
+            a.out[base + 2] = pair_row<EE>(a, av0, av1, h2);
+            a.out[base + 3] = pair_row<EE>(a, av0, av1, h3);
+          }
+          n = 0;
+        }
+        if (n == 0) h0 = (int)j;
+        else if (n == 1) h1 = (int)j;
+        else if (n == 2) h2 = (int)j;
+        else h3 = (int)j;
+        ++n;
+      }
+    }
   }
+  __syncwarp();
   // the whole warp is here: exclusive prefix of the held counts, one reservation per warp
-  const int lane = threadIdx.x & 31;
   int incl = n;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -311,6 +354,7 @@ struct b200ipc_broad {
   b200ipc::BroadBuf<uint8_t> temp;
   b200ipc::BroadBuf<b200ipc::Box> box_t, box_e;
   b200ipc::BroadBuf<double> ext;   // [0..2] triangles, [3..5] edges: largest box extent per axis
+  b200ipc::BroadBuf<int32_t> rev_t, rev_e;   // dense cell tables of the two bin lists (grids of <= 2^21 cells)
   // state between count and fill
   bool counted = false;
   int64_t nverts = 0, n_sv = 0, n_tri = 0, n_edge = 0, n_vt = 0, n_ee = 0;
@@ -335,6 +379,37 @@ using namespace b200ipc;
   } while (0)
 
 static inline unsigned bblocks(int64_t n) { return (unsigned)((n + kBT - 1) / kBT); }
+
+// Dense cell table of a sorted bin list, for grids of at most 2^kDenseBits cells: rev[ncell - c] = lower_bound(keys,
+// c), built as fill(n) -> every run head writes its index -> inclusive min-scan (the table is stored back to front so
+// that "first entry with key >= c" is a forward prefix minimum).
+constexpr int kDenseBits = 21;
+namespace b200ipc {
+__global__ void __launch_bounds__(kBT) fill_i32_kernel(int64_t n, int32_t v, int32_t* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * kBT + threadIdx.x;
+  if (i < n) out[i] = v;
+}
+__global__ void __launch_bounds__(kBT) run_heads_kernel(int64_t n, int64_t ncell, const uint64_t* __restrict__ keys,
+                                                        int32_t* __restrict__ rev) {
+  const int64_t t = (int64_t)blockIdx.x * kBT + threadIdx.x;
+  if (t < n && (t == 0 || keys[t] != keys[t - 1])) rev[ncell - (int64_t)keys[t]] = (int32_t)t;
+}
+}  // namespace b200ipc
+
+static int cell_table(b200ipc_broad* h, const uint64_t* keys, int64_t n, BroadBuf<int32_t>& rev, cudaStream_t st) {
+  const int64_t ncell = 1ll << h->key_bits;
+  CK(rev.reserve(ncell + 1));
+  fill_i32_kernel<<<bblocks(ncell + 1), kBT, 0, st>>>(ncell + 1, (int32_t)n, rev.ptr);
+  RC(post_launch());
+  run_heads_kernel<<<bblocks(n), kBT, 0, st>>>(n, ncell, keys, rev.ptr);
+  RC(post_launch());
+  size_t tb = 0;
+  CK(cub::DeviceScan::InclusiveScan(nullptr, tb, rev.ptr, rev.ptr, cub::Min(), (int)(ncell + 1), st));
+  CK(h->temp.reserve(tb));
+  CK(cub::DeviceScan::InclusiveScan(h->temp.ptr, tb, rev.ptr, rev.ptr, cub::Min(), (int)(ncell + 1), st));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return 0;
+}
 
 // File every B box under its home cell (sorted keys / ids) and reduce the largest extent per axis.
 static int bin_boxes(b200ipc_broad* h, const Box* box, int64_t n, BroadBuf<uint64_t>& keys, BroadBuf<uint32_t>& ids,
@@ -364,7 +439,7 @@ extern "C" int b200ipc_broad_destroy(b200ipc_broad* h) {
   h->stage_vt.release(); h->stage_ee.release(); h->counters.release();
   h->keys_a.release(); h->keys_t.release(); h->keys_e.release();
   h->ids_a.release(); h->ids_t.release(); h->ids_e.release();
-  h->temp.release(); h->box_t.release(); h->box_e.release(); h->ext.release();
+  h->temp.release(); h->box_t.release(); h->box_e.release(); h->ext.release(); h->rev_t.release(); h->rev_e.release();
   delete h;
   return 0;
 }
@@ -383,7 +458,7 @@ static int broad_count(b200ipc_broad* h, int64_t nverts, const Boxes& in, int64_
     return B200IPC_EINVAL;
   if ((n_sv && !surf_verts) || (n_tri && !tris) || (n_edge && !edges)) return B200IPC_EINVAL;
   if (!(cell > 0.0)) return B200IPC_EINVAL;
-  if (n_sv >= (1ll << 27) || n_tri >= (1ll << 31) || n_edge >= (1ll << 27)) return B200IPC_EINVAL;  // (box, slot) ids are int32-scanned
+  if (n_sv >= (1ll << 27) || n_tri >= (1ll << 31) || n_edge >= (1ll << 27)) return B200IPC_EINVAL;  // (box, lane) thread ids stay below 2^31
   cudaStream_t st = (cudaStream_t)stream;
   h->counted = false;
   h->nverts = nverts; h->in = in; h->n_sv = n_sv; h->surf_verts = surf_verts; h->n_tri = n_tri; h->tris = tris;
@@ -401,33 +476,36 @@ static int broad_count(b200ipc_broad* h, int64_t nverts, const Boxes& in, int64_
 
   // boxes and bins of both joins first, then the two passes, then ONE synchronisation for both counts
   const bool do_vt = n_sv && n_tri, do_ee = n_edge > 1;
+  const bool dense = h->key_bits <= kDenseBits;
   CK(h->counters.reserve(2));
   if (do_vt) {
     CK(h->box_t.reserve(n_tri));
     make_boxes_kernel<1><<<bblocks(n_tri), kBT, 0, st>>>(in, tris, n_tri, h->box_t.ptr);
     RC(post_launch());
     RC(bin_boxes(h, h->box_t.ptr, n_tri, h->keys_t, h->ids_t, h->ext.ptr, st));
+    if (dense) RC(cell_table(h, h->keys_t.ptr, n_tri, h->rev_t, st));
   }
   if (do_ee) {
     CK(h->box_e.reserve(n_edge));
     make_boxes_kernel<2><<<bblocks(n_edge), kBT, 0, st>>>(in, edges, n_edge, h->box_e.ptr);
     RC(post_launch());
     RC(bin_boxes(h, h->box_e.ptr, n_edge, h->keys_e, h->ids_e, h->ext.ptr + 3, st));
+    if (dense) RC(cell_table(h, h->keys_e.ptr, n_edge, h->rev_e, st));
   }
   bool run_vt = do_vt, run_ee = do_ee;
   for (int attempt = 0; attempt < 2 && (run_vt || run_ee); ++attempt) {
     if (run_vt) {
       CK(cudaMemsetAsync(h->counters.ptr, 0, sizeof(unsigned long long), st));
       JoinArgs a{in, surf_verts, tris, n_sv, n_tri, h->grid, h->keys_t.ptr, h->ids_t.ptr, h->box_t.ptr, h->ext.ptr,
-                 h->counters.ptr, h->stage_vt.ptr, (unsigned long long)h->stage_vt.cap};
-      join_kernel<false><<<bblocks(n_sv * kJoinSlots), kBT, 0, st>>>(a);
+                 dense ? h->rev_t.ptr : nullptr, 1ll << h->key_bits, h->counters.ptr, h->stage_vt.ptr, (unsigned long long)h->stage_vt.cap};
+      join_kernel<false><<<bblocks(n_sv * kJoinGroup), kBT, 0, st>>>(a);
       RC(post_launch());
     }
     if (run_ee) {
       CK(cudaMemsetAsync(h->counters.ptr + 1, 0, sizeof(unsigned long long), st));
       JoinArgs a{in, edges, edges, n_edge, n_edge, h->grid, h->keys_e.ptr, h->ids_e.ptr, h->box_e.ptr, h->ext.ptr + 3,
-                 h->counters.ptr + 1, h->stage_ee.ptr, (unsigned long long)h->stage_ee.cap};
-      join_kernel<true><<<bblocks(n_edge * kJoinSlots), kBT, 0, st>>>(a);
+                 dense ? h->rev_e.ptr : nullptr, 1ll << h->key_bits, h->counters.ptr + 1, h->stage_ee.ptr, (unsigned long long)h->stage_ee.cap};
+      join_kernel<true><<<bblocks(n_edge * kJoinGroup), kBT, 0, st>>>(a);
       RC(post_launch());
     }
     unsigned long long found[2] = {0, 0};
