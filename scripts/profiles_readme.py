@@ -29,7 +29,7 @@ rows = [
      f"{n['assembly_numeric_ms']:.3f} / {n['fused']['assembly_from_factors_ms']:.3f} / {n['spmv_ms']:.4f} ms "
      f"({n['roofline_assembly']['frac']:.2f} / {n['roofline_assembly_factors']['frac']:.2f} / {n['roofline_spmv']['frac']:.2f} of HBM)"),
     ("assembly + SpMV a Newton iteration pays (symbolic + numeric from factors + SpMV)", "1.59 ms", f"**{n['per_newton_iteration_ms']['total']:.2f} ms**"),
-    ("PCG per iteration, block-Jacobi", "34 - 38 us", f"**{n['pcg_ms_per_iter']*1e3:.1f} us** (L2 eviction hints)"),
+    ("PCG per iteration, block-Jacobi", "34 - 38 us", f"**{n['pcg_ms_per_iter']*1e3:.1f} us** (L2 eviction hints, 27-row chunks)"),
     ("PCG to 1e-4, block-Jacobi", "244 iterations, 9.0 - 9.2 ms", f"{n['pcg_iters']} iterations, {n['pcg_solve_ms']:.2f} ms"),
     ("PCG to 1e-4 (same stopping rule), MAS preconditioner, 1 level", "--",
      f"**{m1['iters']} iterations, {m1['setup_ms']:.2f} ms setup + {m1['solve_ms']:.2f} ms solve = {m1['setup_plus_solve_ms']:.2f} ms** "
