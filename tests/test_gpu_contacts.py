@@ -152,6 +152,20 @@ def test_gpu_broad_phase_list_regrows_and_shrinks(Cn):
     vt, ee = bp.query(device.to_device(dense))
     np.testing.assert_array_equal(_rows(device.to_host(vt)), _rows(ref_vt))
     np.testing.assert_array_equal(_rows(device.to_host(ee)), _rows(ref_ee))
+
+    # a grid of more than 2^21 cells (here: the widest hint, 63 key bits) has no dense cell table: the join finds
+    # its column runs by binary search instead -- same candidate set
+    def huge(span, margin):
+        origin = grid(span, margin)
+        _lib.check(_lib.lib().b200ipc_broad_set_grid_cells(bp._h, 1 << 21, 1 << 21, 1 << 21), "broad_set_grid_cells")
+        return origin
+
+    bp._grid = huge
+    for x in (dense, sparse):
+        vt, ee = bp.query(device.to_device(x))
+        ref_vt, ref_ee = o.aabb_candidates(x, surf, cloth.tris, cloth.edges, d_hat)
+        np.testing.assert_array_equal(_rows(device.to_host(vt)), _rows(ref_vt))
+        np.testing.assert_array_equal(_rows(device.to_host(ee)), _rows(ref_ee))
     bp.close()
     assert sizes[1] > 3 * sizes[0] and sizes[1] > 9 * 4 * len(cloth.edges)   # > 4 hits per (box, slot) on average
 
