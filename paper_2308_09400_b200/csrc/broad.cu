@@ -266,8 +266,22 @@ __global__ void __launch_bounds__(kBT) join_kernel(const __grid_constant__ JoinA
           t0 = a.rev[a.ncell - (int64_t)k0];
           len = a.rev[a.ncell - (int64_t)k1 - 1] - t0;
         } else {
-          t0 = (int32_t)lower_bound_u64(a.keys, a.nbins, k0);
-          len = (int32_t)lower_bound_u64(a.keys, a.nbins, k1 + 1) - t0;
+          // the run's end is close to its start (runs are short, most columns of a sparse grid are empty):
+          // gallop from t0 instead of a second full search
+          const int64_t b = lower_bound_u64(a.keys, a.nbins, k0);
+          int64_t lo = b, step = 1;
+          while (lo + step <= a.nbins && a.keys[lo + step - 1] <= k1) {
+            lo += step;
+            step <<= 1;
+          }
+          int64_t hi = lo + step - 1 < a.nbins ? lo + step - 1 : a.nbins;   // keys[lo - 1] <= k1 (or lo == b), keys[hi] > k1 (or hi == nbins)
+          while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (a.keys[mid] <= k1) lo = mid + 1;
+            else hi = mid;
+          }
+          t0 = (int32_t)b;
+          len = (int32_t)(lo - b);
         }
       }
       int32_t incl = len;

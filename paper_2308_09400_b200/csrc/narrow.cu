@@ -119,7 +119,8 @@ struct KeyArgs {
   const int4* verts;
   const int32_t* vt;
   const int32_t* ee;
-  int word;            // 0: (o2,o3)  1: (otype,o0,o1)  2: (v2,v3)  3: (kind,v0,v1)
+  int word;            // 0: (o2,o3)  1: (otype,o0,o1)  2: low word of (kind,v0..v3)  3: its high word
+  int lowbits;         // width of the low word (words 2 / 3)
   uint64_t* keys;
 };
 
@@ -135,8 +136,13 @@ __global__ void __launch_bounds__(kNT) narrow_keys_kernel(const KeyArgs a) {
     else key = ((uint64_t)(is_vt ? 2 : 1) << (2 * a.bits)) | ((uint64_t)(uint32_t)o.x << a.bits) | (uint64_t)(uint32_t)o.y;
   } else {
     const int4 v = a.verts[q];
-    if (a.word == 2) key = ((uint64_t)(uint32_t)(v.z + 1) << a.bits) | (uint64_t)(uint32_t)(v.w + 1);
-    else key = ((uint64_t)a.kind[q] << (2 * a.bits)) | ((uint64_t)(uint32_t)(v.x + 1) << a.bits) | (uint64_t)(uint32_t)(v.y + 1);
+    // (kind, v0, v1, v2, v3) is one 4 bits + 4 x `bits` wide number, sorted LSD in two calls: the low word takes
+    // the largest multiple of 8 bits (a radix pass sorts 8) below 2 x bits, the rest of (v2, v3) rides at the bottom
+    // of the high word -- 72 bits at 17 bits per vertex are then 4 + 5 passes instead of 5 + 5
+    const uint64_t lo = ((uint64_t)(uint32_t)(v.z + 1) << a.bits) | (uint64_t)(uint32_t)(v.w + 1);
+    if (a.word == 2) key = lo & ((1ull << a.lowbits) - 1ull);
+    else key = ((((uint64_t)a.kind[q] << (2 * a.bits)) | ((uint64_t)(uint32_t)(v.x + 1) << a.bits) | (uint64_t)(uint32_t)(v.y + 1))
+                << (2 * a.bits - a.lowbits)) | (lo >> a.lowbits);
   }
   a.keys[i] = key;
 }
@@ -318,11 +324,13 @@ extern "C" int b200ipc_narrow_phase(int64_t nverts, const double* positions, con
   CK(temp2.alloc(ts, st));
   uint32_t* cur = idx_a.p;
   uint32_t* nxt = idx_b.p;
+  int lowbits = (2 * bits) / 8 * 8;
+  if (lowbits == 0 || 4 * bits + 4 - lowbits > 64) lowbits = 2 * bits;   // the high word must fit 64 bits
   for (int word = 2; word < 4; ++word) {
-    KeyArgs ka{n, n_vt, bits, cur, kq.p, vq.p, vt, ee, word, key_a.p};
+    KeyArgs ka{n, n_vt, bits, cur, kq.p, vq.p, vt, ee, word, lowbits, key_a.p};
     narrow_keys_kernel<<<nblocks(n), kNT, 0, st>>>(ka);
     RC(post_launch());
-    const int end_bit = (word == 0 || word == 2) ? 2 * bits : 2 * bits + 4;
+    const int end_bit = word == 2 ? lowbits : 2 * bits + 4 + (2 * bits - lowbits);
     CK(cub::DeviceRadixSort::SortPairs(temp2.p, ts, key_a.p, key_b.p, cur, nxt, (int)n, 0, end_bit, st));
     g_launches.fetch_add(1, std::memory_order_relaxed);
     uint32_t* t = cur;
