@@ -210,6 +210,13 @@ int b200ipc_broad_destroy(b200ipc_broad* h);
  * runs 3 radix passes instead of 8.  Coordinates beyond the hinted span fall into the boundary cells:
  * slower there, the candidate set is unchanged. */
 int b200ipc_broad_set_grid_cells(b200ipc_broad* h, int32_t nx, int32_t ny, int32_t nz);
+/* Size classes of the grid join (speed only; the candidate set is the reference's either way).  coarse_cell = 0
+ * (default): every box is filed on the one grid of `cell`-sized cells.  coarse_cell > 2 cell: boxes whose largest
+ * extent exceeds two cells are filed on a second grid of coarse_cell-sized cells and joined separately, so that a
+ * few long collider edges do not widen the probe range of every cloth vertex (the probe range of a bin list is
+ * its largest box).  The host mirror sets it from the longest edge of the scene when that is much longer than a
+ * cell (cloth draped on a coarse sphere: broad phase 1.50 -> see DESIGN 4.4). */
+int b200ipc_broad_set_coarse_cell(b200ipc_broad* h, double coarse_cell);
 int b200ipc_broad_phase_count(b200ipc_broad* h, int64_t nverts, const double* positions,
                               int64_t n_sv, const int32_t* surf_verts, int64_t n_tri, const int32_t* tris,
                               int64_t n_edge, const int32_t* edges, double d_hat, double cell,

@@ -73,6 +73,7 @@ SIGNATURES = {
     "b200ipc_broad_create": [C.POINTER(_vp)],
     "b200ipc_broad_destroy": [_vp],
     "b200ipc_broad_set_grid_cells": [_vp, C.c_int32, C.c_int32, C.c_int32],
+    "b200ipc_broad_set_coarse_cell": [_vp, _dbl],
     "b200ipc_broad_phase_count": [_vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _dbl, _dbl, C.POINTER(_dbl),
                                   C.POINTER(_i64), C.POINTER(_i64), _vp],
     "b200ipc_broad_phase_fill": [_vp, _vp, _vp, _vp],

@@ -44,6 +44,15 @@ class BroadPhase:
         self.cell = float(cell)
         self._h = C.c_void_p()
         _lib.check(_lib.lib().b200ipc_broad_create(C.byref(self._h)), "broad_create")
+        # a scene with edges much longer than a cell (cloth on a coarse collider): the long boxes get a grid of their
+        # own, or every vertex would probe the cells a LONG box could start in (speed only)
+        self.coarse_cell = 0.0
+        if positions is not None and len(edges):
+            x = np.asarray(positions, dtype=np.float64)
+            longest = float(np.linalg.norm(x[edges[:, 1]] - x[edges[:, 0]], axis=1).max())
+            if longest + self.d_hat > 2.0 * self.cell:
+                self.coarse_cell = 1.25 * longest + 2.0 * self.d_hat
+        _lib.check(_lib.lib().b200ipc_broad_set_coarse_cell(self._h, self.coarse_cell), "broad_set_coarse_cell")
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h:

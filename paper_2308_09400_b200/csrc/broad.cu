@@ -23,6 +23,7 @@
 // a total order over (kind, vertices, origin query), the CCD filter takes a minimum.
 // The same join with swept boxes (both ends of a step, margin 1e-3 d_hat) is sweep_candidates
 // (proximity.py:388-421), the candidate set of the CCD step filter (accd.cu).
+#include <cmath>
 #include <cub/cub.cuh>
 
 #include "launch.cuh"
@@ -149,18 +150,23 @@ __global__ void __launch_bounds__(kBT) make_boxes_kernel(const Boxes in, const i
   if (i < n) out[i] = make_box<KIND>(in, elems, i);
 }
 
-// Home cell (cell of the lower corner) of every B box, and the largest extent per axis (ordered-bits
-// atomicMax: extents are non-negative doubles).
-__global__ void __launch_bounds__(kBT) home_cell_kernel(const Box* __restrict__ box, int64_t n, Grid g,
-                                                        uint64_t* __restrict__ keys, uint32_t* __restrict__ ids,
-                                                        unsigned long long* __restrict__ ext) {
+// Home cell (cell of the lower corner) of every B box of one SIZE CLASS -- largest extent in (lo_thr, hi_thr] -- and
+// the class's largest extent per axis (ordered-bits atomicMax: extents are non-negative doubles).  A box of another
+// class gets the key `sentinel` (one past the largest cell key: it sorts behind every cell and no probe reaches it).
+__global__ void __launch_bounds__(kBT) home_cell_kernel(const Box* __restrict__ box, int64_t n, Grid g, double lo_thr,
+                                                        double hi_thr, uint64_t sentinel, uint64_t* __restrict__ keys,
+                                                        uint32_t* __restrict__ ids, unsigned long long* __restrict__ ext) {
   const int64_t i = (int64_t)blockIdx.x * kBT + threadIdx.x;
   double ex = 0.0, ey = 0.0, ez = 0.0;
   if (i < n) {
     const Box b = box[i];
-    keys[i] = cell_key(g, cell_of(b.lx, g.ox, g.inv, g.mx), cell_of(b.ly, g.oy, g.inv, g.my), cell_of(b.lz, g.oz, g.inv, g.mz));
-    ids[i] = (uint32_t)i;
     ex = b.hx - b.lx; ey = b.hy - b.ly; ez = b.hz - b.lz;
+    const double big = fmax(ex, fmax(ey, ez));
+    const bool member = big > lo_thr && big <= hi_thr;
+    keys[i] = member ? cell_key(g, cell_of(b.lx, g.ox, g.inv, g.mx), cell_of(b.ly, g.oy, g.inv, g.my), cell_of(b.lz, g.oz, g.inv, g.mz))
+                     : sentinel;
+    ids[i] = (uint32_t)i;
+    if (!member) ex = ey = ez = 0.0;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -360,23 +366,32 @@ __global__ void __launch_bounds__(kBT) join_kernel(const __grid_constant__ JoinA
 
 }  // namespace b200ipc
 
+// One sorted bin list: the B boxes of one kind (triangles / edges) and one size class on their own grid.
+struct BinSet {
+  b200ipc::BroadBuf<uint64_t> keys;
+  b200ipc::BroadBuf<uint32_t> ids;
+  b200ipc::BroadBuf<int32_t> rev;   // dense cell table (grids of <= 2^21 cells)
+  b200ipc::Grid grid{};
+  int key_bits = 63;
+  bool dense = false;
+};
+
 struct b200ipc_broad {
   b200ipc::BroadBuf<int4> stage_vt, stage_ee;            // candidate lists of the last query
   b200ipc::BroadBuf<unsigned long long> counters;        // [0] point-triangle, [1] edge-edge pairs found
-  b200ipc::BroadBuf<uint64_t> keys_a, keys_t, keys_e;   // scratch, sorted triangle bins, sorted edge bins
-  b200ipc::BroadBuf<uint32_t> ids_a, ids_t, ids_e;
+  b200ipc::BroadBuf<uint64_t> keys_a;                    // unsorted keys (scratch)
+  b200ipc::BroadBuf<uint32_t> ids_a;
+  BinSet bins[2][2];                                     // [triangles, edges][small boxes, large boxes]
   b200ipc::BroadBuf<uint8_t> temp;
   b200ipc::BroadBuf<b200ipc::Box> box_t, box_e;
-  b200ipc::BroadBuf<double> ext;   // [0..2] triangles, [3..5] edges: largest box extent per axis
-  b200ipc::BroadBuf<int32_t> rev_t, rev_e;   // dense cell tables of the two bin lists (grids of <= 2^21 cells)
+  b200ipc::BroadBuf<double> ext;   // [(kind * 2 + class) * 3 ..]: largest box extent per axis of every bin list
   // state between count and fill
   bool counted = false;
   int64_t nverts = 0, n_sv = 0, n_tri = 0, n_edge = 0, n_vt = 0, n_ee = 0;
   b200ipc::Boxes in{};
   const int32_t *surf_verts = nullptr, *tris = nullptr, *edges = nullptr;
-  b200ipc::Grid grid{};
   int32_t cells[3] = {1 << 21, 1 << 21, 1 << 21};   // b200ipc_broad_set_grid_cells
-  int key_bits = 63;
+  double coarse_cell = 0.0;                          // b200ipc_broad_set_coarse_cell: 0 = one size class
 };
 
 using namespace b200ipc;
@@ -410,35 +425,53 @@ __global__ void __launch_bounds__(kBT) run_heads_kernel(int64_t n, int64_t ncell
 }
 }  // namespace b200ipc
 
-static int cell_table(b200ipc_broad* h, const uint64_t* keys, int64_t n, BroadBuf<int32_t>& rev, cudaStream_t st) {
-  const int64_t ncell = 1ll << h->key_bits;
-  CK(rev.reserve(ncell + 1));
-  fill_i32_kernel<<<bblocks(ncell + 1), kBT, 0, st>>>(ncell + 1, (int32_t)n, rev.ptr);
+static int cell_table(b200ipc_broad* h, BinSet& b, int64_t n, cudaStream_t st) {
+  const int64_t ncell = 1ll << b.key_bits;
+  CK(b.rev.reserve(ncell + 1));
+  fill_i32_kernel<<<bblocks(ncell + 1), kBT, 0, st>>>(ncell + 1, (int32_t)n, b.rev.ptr);
   RC(post_launch());
-  run_heads_kernel<<<bblocks(n), kBT, 0, st>>>(n, ncell, keys, rev.ptr);
+  run_heads_kernel<<<bblocks(n), kBT, 0, st>>>(n, ncell, b.keys.ptr, b.rev.ptr);   // the sentinel run lands in rev[0]
   RC(post_launch());
   size_t tb = 0;
-  CK(cub::DeviceScan::InclusiveScan(nullptr, tb, rev.ptr, rev.ptr, cub::Min(), (int)(ncell + 1), st));
+  CK(cub::DeviceScan::InclusiveScan(nullptr, tb, b.rev.ptr, b.rev.ptr, cub::Min(), (int)(ncell + 1), st));
   CK(h->temp.reserve(tb));
-  CK(cub::DeviceScan::InclusiveScan(h->temp.ptr, tb, rev.ptr, rev.ptr, cub::Min(), (int)(ncell + 1), st));
+  CK(cub::DeviceScan::InclusiveScan(h->temp.ptr, tb, b.rev.ptr, b.rev.ptr, cub::Min(), (int)(ncell + 1), st));
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return 0;
 }
 
-// File every B box under its home cell (sorted keys / ids) and reduce the largest extent per axis.
-static int bin_boxes(b200ipc_broad* h, const Box* box, int64_t n, BroadBuf<uint64_t>& keys, BroadBuf<uint32_t>& ids,
+// Grid of `cell`-sized cells over the span the host announced in fine cells (b200ipc_broad_set_grid_cells).
+static void make_grid(BinSet& b, const double* origin, double cell, const int32_t* fine_cells, double fine_cell) {
+  int nbits[3], cells[3];
+  for (int k = 0; k < 3; ++k) {
+    const double want = ceil((double)fine_cells[k] * fine_cell / cell) + 1.0;
+    cells[k] = want < 1.0 ? 1 : (want > (double)(1 << 21) ? (1 << 21) : (int)want);
+    if (cell == fine_cell) cells[k] = fine_cells[k];
+    nbits[k] = 1;
+    while ((1 << nbits[k]) < cells[k]) ++nbits[k];
+  }
+  b.grid = Grid{origin[0], origin[1], origin[2], 1.0 / cell, cells[0] - 1, cells[1] - 1, cells[2] - 1, nbits[2], nbits[1] + nbits[2]};
+  b.key_bits = nbits[0] + nbits[1] + nbits[2];
+  b.dense = b.key_bits <= kDenseBits;
+}
+
+// File every B box of one size class under its home cell (sorted keys / ids; the other class's boxes sort behind
+// every cell) and reduce the class's largest extent per axis.
+static int bin_boxes(b200ipc_broad* h, const Box* box, int64_t n, BinSet& b, double lo_thr, double hi_thr, bool classes,
                      double* ext, cudaStream_t st) {
   CK(cudaMemsetAsync(ext, 0, 3 * sizeof(double), st));
   if (n == 0) return 0;
-  CK(h->keys_a.reserve(n)); CK(h->ids_a.reserve(n)); CK(keys.reserve(n)); CK(ids.reserve(n));
-  home_cell_kernel<<<bblocks(n), kBT, 0, st>>>(box, n, h->grid, h->keys_a.ptr, h->ids_a.ptr,
-                                               reinterpret_cast<unsigned long long*>(ext));
+  CK(h->keys_a.reserve(n)); CK(h->ids_a.reserve(n)); CK(b.keys.reserve(n)); CK(b.ids.reserve(n));
+  home_cell_kernel<<<bblocks(n), kBT, 0, st>>>(box, n, b.grid, lo_thr, hi_thr, 1ull << b.key_bits, h->keys_a.ptr,
+                                               h->ids_a.ptr, reinterpret_cast<unsigned long long*>(ext));
   RC(post_launch());
+  const int end_bit = b.key_bits + (classes ? 1 : 0);   // the sentinel needs one more bit
   size_t tb = 0;
-  CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, h->keys_a.ptr, keys.ptr, h->ids_a.ptr, ids.ptr, (int)n, 0, h->key_bits, st));
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, h->keys_a.ptr, b.keys.ptr, h->ids_a.ptr, b.ids.ptr, (int)n, 0, end_bit, st));
   CK(h->temp.reserve(tb));
-  CK(cub::DeviceRadixSort::SortPairs(h->temp.ptr, tb, h->keys_a.ptr, keys.ptr, h->ids_a.ptr, ids.ptr, (int)n, 0, h->key_bits, st));
+  CK(cub::DeviceRadixSort::SortPairs(h->temp.ptr, tb, h->keys_a.ptr, b.keys.ptr, h->ids_a.ptr, b.ids.ptr, (int)n, 0, end_bit, st));
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (b.dense) RC(cell_table(h, b, n, st));
   return 0;
 }
 
@@ -451,9 +484,12 @@ extern "C" int b200ipc_broad_create(b200ipc_broad** out) {
 extern "C" int b200ipc_broad_destroy(b200ipc_broad* h) {
   if (!h) return 0;
   h->stage_vt.release(); h->stage_ee.release(); h->counters.release();
-  h->keys_a.release(); h->keys_t.release(); h->keys_e.release();
-  h->ids_a.release(); h->ids_t.release(); h->ids_e.release();
-  h->temp.release(); h->box_t.release(); h->box_e.release(); h->ext.release(); h->rev_t.release(); h->rev_e.release();
+  h->keys_a.release(); h->ids_a.release();
+  for (int k = 0; k < 2; ++k)
+    for (int c = 0; c < 2; ++c) {
+      h->bins[k][c].keys.release(); h->bins[k][c].ids.release(); h->bins[k][c].rev.release();
+    }
+  h->temp.release(); h->box_t.release(); h->box_e.release(); h->ext.release();
   delete h;
   return 0;
 }
@@ -462,6 +498,12 @@ extern "C" int b200ipc_broad_set_grid_cells(b200ipc_broad* h, int32_t nx, int32_
   if (!h) return B200IPC_EINVAL;
   const int32_t want[3] = {nx, ny, nz};
   for (int k = 0; k < 3; ++k) h->cells[k] = want[k] <= 0 ? (1 << 21) : (want[k] > (1 << 21) ? (1 << 21) : want[k]);
+  return 0;
+}
+
+extern "C" int b200ipc_broad_set_coarse_cell(b200ipc_broad* h, double coarse_cell) {
+  if (!h || !(coarse_cell >= 0.0)) return B200IPC_EINVAL;
+  h->coarse_cell = coarse_cell;
   return 0;
 }
 
@@ -477,50 +519,66 @@ static int broad_count(b200ipc_broad* h, int64_t nverts, const Boxes& in, int64_
   h->counted = false;
   h->nverts = nverts; h->in = in; h->n_sv = n_sv; h->surf_verts = surf_verts; h->n_tri = n_tri; h->tris = tris;
   h->n_edge = n_edge; h->edges = edges;
-  int nbits[3];
-  for (int k = 0; k < 3; ++k) {
-    nbits[k] = 1;
-    while ((1 << nbits[k]) < h->cells[k]) ++nbits[k];
-  }
-  h->grid = Grid{origin[0], origin[1], origin[2], 1.0 / cell, h->cells[0] - 1, h->cells[1] - 1, h->cells[2] - 1,
-                 nbits[2], nbits[1] + nbits[2]};
-  h->key_bits = nbits[0] + nbits[1] + nbits[2];
   h->n_vt = h->n_ee = 0;
-  CK(h->ext.reserve(6));
+  CK(h->ext.reserve(12));
 
-  // boxes and bins of both joins first, then the two passes, then ONE synchronisation for both counts
+  // Size classes.  One class: every B box on the fine grid, as the reference's scenes of uniform resolution want.
+  // Two classes (the host saw edges much longer than a cell, b200ipc_broad_set_coarse_cell): boxes of up to two
+  // cells stay on the fine grid, the few large ones go to a coarse grid of their own -- the probe range of a join is
+  // set by the LARGEST box of its bin list, and a handful of long collider edges would otherwise make every cloth
+  // vertex probe dozens of empty columns.  Each A box is joined with both lists; a pair is found in the list its B
+  // box lives in, once.
+  const bool classes = h->coarse_cell > 2.0 * cell;
+  const int ncls = classes ? 2 : 1;
+  const double split = 2.0 * cell;
+  for (int k = 0; k < 2; ++k) {
+    make_grid(h->bins[k][0], origin, cell, h->cells, cell);
+    if (classes) make_grid(h->bins[k][1], origin, h->coarse_cell, h->cells, cell);
+  }
+
+  // boxes and bins of both joins first, then the passes, then ONE synchronisation for both counts
   const bool do_vt = n_sv && n_tri, do_ee = n_edge > 1;
-  const bool dense = h->key_bits <= kDenseBits;
   CK(h->counters.reserve(2));
+  const double inf = HUGE_VAL;
   if (do_vt) {
     CK(h->box_t.reserve(n_tri));
     make_boxes_kernel<1><<<bblocks(n_tri), kBT, 0, st>>>(in, tris, n_tri, h->box_t.ptr);
     RC(post_launch());
-    RC(bin_boxes(h, h->box_t.ptr, n_tri, h->keys_t, h->ids_t, h->ext.ptr, st));
-    if (dense) RC(cell_table(h, h->keys_t.ptr, n_tri, h->rev_t, st));
+    for (int c = 0; c < ncls; ++c)
+      RC(bin_boxes(h, h->box_t.ptr, n_tri, h->bins[0][c], c == 0 ? -1.0 : split, c == 0 && classes ? split : inf, classes,
+                   h->ext.ptr + 3 * c, st));
   }
   if (do_ee) {
     CK(h->box_e.reserve(n_edge));
     make_boxes_kernel<2><<<bblocks(n_edge), kBT, 0, st>>>(in, edges, n_edge, h->box_e.ptr);
     RC(post_launch());
-    RC(bin_boxes(h, h->box_e.ptr, n_edge, h->keys_e, h->ids_e, h->ext.ptr + 3, st));
-    if (dense) RC(cell_table(h, h->keys_e.ptr, n_edge, h->rev_e, st));
+    for (int c = 0; c < ncls; ++c)
+      RC(bin_boxes(h, h->box_e.ptr, n_edge, h->bins[1][c], c == 0 ? -1.0 : split, c == 0 && classes ? split : inf, classes,
+                   h->ext.ptr + 6 + 3 * c, st));
   }
   bool run_vt = do_vt, run_ee = do_ee;
   for (int attempt = 0; attempt < 2 && (run_vt || run_ee); ++attempt) {
     if (run_vt) {
       CK(cudaMemsetAsync(h->counters.ptr, 0, sizeof(unsigned long long), st));
-      JoinArgs a{in, surf_verts, tris, n_sv, n_tri, h->grid, h->keys_t.ptr, h->ids_t.ptr, h->box_t.ptr, h->ext.ptr,
-                 dense ? h->rev_t.ptr : nullptr, 1ll << h->key_bits, h->counters.ptr, h->stage_vt.ptr, (unsigned long long)h->stage_vt.cap};
-      join_kernel<false><<<bblocks(n_sv * kJoinGroup), kBT, 0, st>>>(a);
-      RC(post_launch());
+      for (int c = 0; c < ncls; ++c) {
+        const BinSet& b = h->bins[0][c];
+        JoinArgs a{in, surf_verts, tris, n_sv, n_tri, b.grid, b.keys.ptr, b.ids.ptr, h->box_t.ptr, h->ext.ptr + 3 * c,
+                   b.dense ? b.rev.ptr : nullptr, 1ll << b.key_bits, h->counters.ptr, h->stage_vt.ptr,
+                   (unsigned long long)h->stage_vt.cap};
+        join_kernel<false><<<bblocks(n_sv * kJoinGroup), kBT, 0, st>>>(a);
+        RC(post_launch());
+      }
     }
     if (run_ee) {
       CK(cudaMemsetAsync(h->counters.ptr + 1, 0, sizeof(unsigned long long), st));
-      JoinArgs a{in, edges, edges, n_edge, n_edge, h->grid, h->keys_e.ptr, h->ids_e.ptr, h->box_e.ptr, h->ext.ptr + 3,
-                 dense ? h->rev_e.ptr : nullptr, 1ll << h->key_bits, h->counters.ptr + 1, h->stage_ee.ptr, (unsigned long long)h->stage_ee.cap};
-      join_kernel<true><<<bblocks(n_edge * kJoinGroup), kBT, 0, st>>>(a);
-      RC(post_launch());
+      for (int c = 0; c < ncls; ++c) {
+        const BinSet& b = h->bins[1][c];
+        JoinArgs a{in, edges, edges, n_edge, n_edge, b.grid, b.keys.ptr, b.ids.ptr, h->box_e.ptr, h->ext.ptr + 6 + 3 * c,
+                   b.dense ? b.rev.ptr : nullptr, 1ll << b.key_bits, h->counters.ptr + 1, h->stage_ee.ptr,
+                   (unsigned long long)h->stage_ee.cap};
+        join_kernel<true><<<bblocks(n_edge * kJoinGroup), kBT, 0, st>>>(a);
+        RC(post_launch());
+      }
     }
     unsigned long long found[2] = {0, 0};
     CK(cudaMemcpyAsync(found, h->counters.ptr, sizeof(found), cudaMemcpyDeviceToHost, st));

@@ -170,6 +170,34 @@ def test_gpu_broad_phase_list_regrows_and_shrinks(Cn):
     assert sizes[1] > 3 * sizes[0] and sizes[1] > 9 * 4 * len(cloth.edges)   # > 4 hits per (box, slot) on average
 
 
+def test_gpu_broad_phase_two_size_classes(Cn):
+    """Cloth draped on a coarse sphere (collider edges many cells long): the broad phase files the long boxes on a
+    coarse grid of their own and joins every A box with both bin lists -- the candidate set is still exactly the
+    reference's, for the static query and for the swept one, and whatever the class boundary does to the split
+    (coarse cell barely above / far above the threshold, classes off)."""
+    from paper_2308_09400_b200 import _lib, device
+
+    scene = Cn.workloads.cloth_on_sphere(n=26, subdiv=2, seed=4)
+    surf = np.unique(scene.tris)
+    ref_vt, ref_ee = o.aabb_candidates(scene.positions, surf, scene.tris, scene.edges, scene.d_hat)
+    assert len(ref_vt) > 50 and len(ref_ee) > 50
+    bp = Cn.contacts.BroadPhase(surf, scene.tris, scene.edges, scene.d_hat, scene.positions)
+    assert bp.coarse_cell > 2.0 * bp.cell                       # the scene does trigger the second class
+    for coarse in (bp.coarse_cell, 2.01 * bp.cell, 40.0 * bp.cell, 0.0):
+        _lib.check(_lib.lib().b200ipc_broad_set_coarse_cell(bp._h, coarse), "broad_set_coarse_cell")
+        vt, ee = bp.query(scene.positions)
+        np.testing.assert_array_equal(_rows(device.to_host(vt)), _rows(ref_vt))
+        np.testing.assert_array_equal(_rows(device.to_host(ee)), _rows(ref_ee))
+    _lib.check(_lib.lib().b200ipc_broad_set_coarse_cell(bp._h, bp.coarse_cell), "broad_set_coarse_cell")
+    rng = np.random.default_rng(8)
+    d = 0.4 * scene.d_hat * rng.normal(size=scene.positions.shape)
+    s_vt, s_ee = bp.sweep(scene.positions, d)
+    r_vt, r_ee = o.sweep_candidates(scene.positions, d, surf, scene.tris, scene.edges, scene.d_hat)
+    np.testing.assert_array_equal(_rows(device.to_host(s_vt)), _rows(r_vt))
+    np.testing.assert_array_equal(_rows(device.to_host(s_ee)), _rows(r_ee))
+    bp.close()
+
+
 def test_gpu_broad_phase_moving_scene_and_find_contact_pairs(Cn):
     """One handle, several detects (positions change); find_contact_pairs end to end on the GPU."""
     from types import SimpleNamespace
