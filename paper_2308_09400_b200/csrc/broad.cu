@@ -4,9 +4,10 @@
 // The reference tests every (surface vertex, triangle) and every (edge, edge) pair for AABB overlap --
 // O(n^2) boolean matrices.  Here both joins run on a uniform grid:
 //   1. the boxes of the "B" elements (triangle AABB; edge AABB inflated by d_hat/2) are built once and
-//      each is filed under ONE cell, the cell of its lower corner (one radix sort of n keys; no
-//      multi-cell binning, so no pair can be found twice); the largest box extent per axis is reduced
-//      on the device alongside;
+//      each is filed under ONE cell, the cell of its lower corner (counting sort on dense grids, one radix
+//      sort of n keys otherwise; no multi-cell binning, so no pair can be found twice); the largest box
+//      extent per axis is reduced on the device alongside; boxes much larger than a cell get a coarse
+//      grid of their own (two size classes);
 //   2. every "A" box (vertex box [p - d_hat, p + d_hat]; inflated edge AABB) probes the cells that can
 //      hold the lower corner of an overlapping B box, [A.lo - max extent, A.hi], finds each cell
 //      column's run (dense cell table, or binary search on large grids), and -- eight lanes per A box
@@ -155,7 +156,8 @@ __global__ void __launch_bounds__(kBT) make_boxes_kernel(const Boxes in, const i
 // class gets the key `sentinel` (one past the largest cell key: it sorts behind every cell and no probe reaches it).
 __global__ void __launch_bounds__(kBT) home_cell_kernel(const Box* __restrict__ box, int64_t n, Grid g, double lo_thr,
                                                         double hi_thr, uint64_t sentinel, uint64_t* __restrict__ keys,
-                                                        uint32_t* __restrict__ ids, unsigned long long* __restrict__ ext) {
+                                                        uint32_t* __restrict__ ids, unsigned long long* __restrict__ ext,
+                                                        int32_t* __restrict__ count /* per cell, or null */) {
   const int64_t i = (int64_t)blockIdx.x * kBT + threadIdx.x;
   double ex = 0.0, ey = 0.0, ez = 0.0;
   if (i < n) {
@@ -165,7 +167,11 @@ __global__ void __launch_bounds__(kBT) home_cell_kernel(const Box* __restrict__ 
     const bool member = big > lo_thr && big <= hi_thr;
     keys[i] = member ? cell_key(g, cell_of(b.lx, g.ox, g.inv, g.mx), cell_of(b.ly, g.oy, g.inv, g.my), cell_of(b.lz, g.oz, g.inv, g.mz))
                      : sentinel;
-    ids[i] = (uint32_t)i;
+    if (count) {
+      if (member) atomicAdd(count + keys[i], 1);
+    } else {
+      ids[i] = (uint32_t)i;
+    }
     if (!member) ex = ey = ez = 0.0;
   }
 #pragma unroll
@@ -201,7 +207,7 @@ struct JoinArgs {
   const uint32_t* ids;
   const Box* bbox;          // boxes of the B elements
   const double* ext;        // largest B extent per axis (device, 3)
-  const int32_t* rev;       // dense cell table or null: rev[ncell - c] = first sorted entry with key >= c
+  const int32_t* rev;       // dense grid: rev[c] = first entry of cell c (ids grouped by cell), or null (sorted keys)
   int64_t ncell;            // 2^key_bits
   unsigned long long* total;  // pairs found (device counter)
   int4* out;                // staging list of (pairs, 4) global vertex ids
@@ -268,9 +274,9 @@ __global__ void __launch_bounds__(kBT) join_kernel(const __grid_constant__ JoinA
         const int cx = s.x0 + c / ncy, cy = s.y0 + c % ncy;
         // cells (cx, cy, z0..z1) are consecutive keys
         const uint64_t k0 = cell_key(a.g, cx, cy, s.z0), k1 = cell_key(a.g, cx, cy, s.z1);
-        if (a.rev) {   // dense grid: two table reads instead of two binary searches
-          t0 = a.rev[a.ncell - (int64_t)k0];
-          len = a.rev[a.ncell - (int64_t)k1 - 1] - t0;
+        if (a.rev) {   // dense grid: two reads of the cell-start table
+          t0 = a.rev[k0];
+          len = a.rev[k1 + 1] - t0;
         } else {
           // the run's end is close to its start (runs are short, most columns of a sparse grid are empty):
           // gallop from t0 instead of a second full search
@@ -370,7 +376,7 @@ __global__ void __launch_bounds__(kBT) join_kernel(const __grid_constant__ JoinA
 struct BinSet {
   b200ipc::BroadBuf<uint64_t> keys;
   b200ipc::BroadBuf<uint32_t> ids;
-  b200ipc::BroadBuf<int32_t> rev;   // dense cell table (grids of <= 2^21 cells)
+  b200ipc::BroadBuf<int32_t> rev;   // dense grids (<= 2^21 cells): rev[c] = first entry of cell c, rev[ncell] = members
   b200ipc::Grid grid{};
   int key_bits = 63;
   bool dense = false;
@@ -381,6 +387,7 @@ struct b200ipc_broad {
   b200ipc::BroadBuf<unsigned long long> counters;        // [0] point-triangle, [1] edge-edge pairs found
   b200ipc::BroadBuf<uint64_t> keys_a;                    // unsorted keys (scratch)
   b200ipc::BroadBuf<uint32_t> ids_a;
+  b200ipc::BroadBuf<int32_t> count;                      // per-cell member counts (dense grids; scratch)
   BinSet bins[2][2];                                     // [triangles, edges][small boxes, large boxes]
   b200ipc::BroadBuf<uint8_t> temp;
   b200ipc::BroadBuf<b200ipc::Box> box_t, box_e;
@@ -409,36 +416,24 @@ using namespace b200ipc;
 
 static inline unsigned bblocks(int64_t n) { return (unsigned)((n + kBT - 1) / kBT); }
 
-// Dense cell table of a sorted bin list, for grids of at most 2^kDenseBits cells: rev[ncell - c] = lower_bound(keys,
-// c), built as fill(n) -> every run head writes its index -> inclusive min-scan (the table is stored back to front so
-// that "first entry with key >= c" is a forward prefix minimum).
+// Dense grids (at most 2^kDenseBits cells) are binned by COUNTING instead of sorting: home_cell_kernel counts the
+// members of every cell while it writes their keys, one exclusive sum turns the counts into cell starts
+// (start[c] = first entry of cell c, start[ncell] = members), and the scatter kernel drops every member's id into its
+// cell with the count as a down-counter.  The order inside a cell is arbitrary -- the join's output is a set -- and
+// the join reads a column's run as start[k0] .. start[k1 + 1]: no sort, no searches (a radix sort of the 19-bit
+// keys of the cloth stack plus the table passes took 76 us per bin list, this takes ~30).
 constexpr int kDenseBits = 21;
 namespace b200ipc {
-__global__ void __launch_bounds__(kBT) fill_i32_kernel(int64_t n, int32_t v, int32_t* __restrict__ out) {
+__global__ void __launch_bounds__(kBT) scatter_ids_kernel(int64_t n, uint64_t sentinel, const uint64_t* __restrict__ keys,
+                                                          const int32_t* __restrict__ start, int32_t* __restrict__ count,
+                                                          uint32_t* __restrict__ ids) {
   const int64_t i = (int64_t)blockIdx.x * kBT + threadIdx.x;
-  if (i < n) out[i] = v;
-}
-__global__ void __launch_bounds__(kBT) run_heads_kernel(int64_t n, int64_t ncell, const uint64_t* __restrict__ keys,
-                                                        int32_t* __restrict__ rev) {
-  const int64_t t = (int64_t)blockIdx.x * kBT + threadIdx.x;
-  if (t < n && (t == 0 || keys[t] != keys[t - 1])) rev[ncell - (int64_t)keys[t]] = (int32_t)t;
+  if (i >= n) return;
+  const uint64_t key = keys[i];
+  if (key == sentinel) return;
+  ids[start[key] + atomicSub(count + key, 1) - 1] = (uint32_t)i;
 }
 }  // namespace b200ipc
-
-static int cell_table(b200ipc_broad* h, BinSet& b, int64_t n, cudaStream_t st) {
-  const int64_t ncell = 1ll << b.key_bits;
-  CK(b.rev.reserve(ncell + 1));
-  fill_i32_kernel<<<bblocks(ncell + 1), kBT, 0, st>>>(ncell + 1, (int32_t)n, b.rev.ptr);
-  RC(post_launch());
-  run_heads_kernel<<<bblocks(n), kBT, 0, st>>>(n, ncell, b.keys.ptr, b.rev.ptr);   // the sentinel run lands in rev[0]
-  RC(post_launch());
-  size_t tb = 0;
-  CK(cub::DeviceScan::InclusiveScan(nullptr, tb, b.rev.ptr, b.rev.ptr, cub::Min(), (int)(ncell + 1), st));
-  CK(h->temp.reserve(tb));
-  CK(cub::DeviceScan::InclusiveScan(h->temp.ptr, tb, b.rev.ptr, b.rev.ptr, cub::Min(), (int)(ncell + 1), st));
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  return 0;
-}
 
 // Grid of `cell`-sized cells over the span the host announced in fine cells (b200ipc_broad_set_grid_cells).
 static void make_grid(BinSet& b, const double* origin, double cell, const int32_t* fine_cells, double fine_cell) {
@@ -455,15 +450,34 @@ static void make_grid(BinSet& b, const double* origin, double cell, const int32_
   b.dense = b.key_bits <= kDenseBits;
 }
 
-// File every B box of one size class under its home cell (sorted keys / ids; the other class's boxes sort behind
-// every cell) and reduce the class's largest extent per axis.
+// File every B box of one size class under its home cell and reduce the class's largest extent per axis.  Dense
+// grid: counting (cell starts in b.rev, ids grouped by cell).  Otherwise: sorted keys / ids, the other class's boxes
+// behind every cell under the sentinel key.
 static int bin_boxes(b200ipc_broad* h, const Box* box, int64_t n, BinSet& b, double lo_thr, double hi_thr, bool classes,
                      double* ext, cudaStream_t st) {
   CK(cudaMemsetAsync(ext, 0, 3 * sizeof(double), st));
   if (n == 0) return 0;
-  CK(h->keys_a.reserve(n)); CK(h->ids_a.reserve(n)); CK(b.keys.reserve(n)); CK(b.ids.reserve(n));
-  home_cell_kernel<<<bblocks(n), kBT, 0, st>>>(box, n, b.grid, lo_thr, hi_thr, 1ull << b.key_bits, h->keys_a.ptr,
-                                               h->ids_a.ptr, reinterpret_cast<unsigned long long*>(ext));
+  const uint64_t sentinel = 1ull << b.key_bits;
+  CK(h->keys_a.reserve(n)); CK(h->ids_a.reserve(n)); CK(b.ids.reserve(n));
+  if (b.dense) {
+    const int64_t ncell = 1ll << b.key_bits;
+    CK(b.rev.reserve(ncell + 1)); CK(h->count.reserve(ncell + 1));
+    CK(cudaMemsetAsync(h->count.ptr, 0, (ncell + 1) * sizeof(int32_t), st));
+    home_cell_kernel<<<bblocks(n), kBT, 0, st>>>(box, n, b.grid, lo_thr, hi_thr, sentinel, h->keys_a.ptr, nullptr,
+                                                 reinterpret_cast<unsigned long long*>(ext), h->count.ptr);
+    RC(post_launch());
+    size_t tb = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, h->count.ptr, b.rev.ptr, (int)(ncell + 1), st));
+    CK(h->temp.reserve(tb));
+    CK(cub::DeviceScan::ExclusiveSum(h->temp.ptr, tb, h->count.ptr, b.rev.ptr, (int)(ncell + 1), st));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    scatter_ids_kernel<<<bblocks(n), kBT, 0, st>>>(n, sentinel, h->keys_a.ptr, b.rev.ptr, h->count.ptr, b.ids.ptr);
+    RC(post_launch());
+    return 0;
+  }
+  CK(b.keys.reserve(n));
+  home_cell_kernel<<<bblocks(n), kBT, 0, st>>>(box, n, b.grid, lo_thr, hi_thr, sentinel, h->keys_a.ptr, h->ids_a.ptr,
+                                               reinterpret_cast<unsigned long long*>(ext), nullptr);
   RC(post_launch());
   const int end_bit = b.key_bits + (classes ? 1 : 0);   // the sentinel needs one more bit
   size_t tb = 0;
@@ -471,7 +485,6 @@ static int bin_boxes(b200ipc_broad* h, const Box* box, int64_t n, BinSet& b, dou
   CK(h->temp.reserve(tb));
   CK(cub::DeviceRadixSort::SortPairs(h->temp.ptr, tb, h->keys_a.ptr, b.keys.ptr, h->ids_a.ptr, b.ids.ptr, (int)n, 0, end_bit, st));
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  if (b.dense) RC(cell_table(h, b, n, st));
   return 0;
 }
 
@@ -484,7 +497,7 @@ extern "C" int b200ipc_broad_create(b200ipc_broad** out) {
 extern "C" int b200ipc_broad_destroy(b200ipc_broad* h) {
   if (!h) return 0;
   h->stage_vt.release(); h->stage_ee.release(); h->counters.release();
-  h->keys_a.release(); h->ids_a.release();
+  h->keys_a.release(); h->ids_a.release(); h->count.release();
   for (int k = 0; k < 2; ++k)
     for (int c = 0; c < 2; ++c) {
       h->bins[k][c].keys.release(); h->bins[k][c].ids.release(); h->bins[k][c].rev.release();
