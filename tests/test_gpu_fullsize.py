@@ -223,3 +223,48 @@ def test_cloth_on_sphere_newton_direction(P):
     assert 0.0 < alpha <= 1.0
     bp.close()
     sysm.close()
+
+
+def test_block_offsets_beyond_2_31_elements(P):
+    """Maximum sizes: 15.2 M four-vertex stencils are 2.19 G Hessian entries (17.5 GB), past what a 32-bit element
+    offset addresses.  The table is a small oracle-checked one with every row repeated R times in place (kind order
+    kept), so the blocks of a group of R rows must be bit-identical to the group's first row, whatever the offset,
+    and the first rows themselves are held to the oracle at 1e-9."""
+    t = P.torch
+    free, _ = t.cuda.mem_get_info()
+    if free < 40 * 2**30:
+        pytest.skip("needs 40 GB of free device memory")
+    qb = P.workloads.config1_batch(n_pt=1000, n_ee=1000)
+    tab = o.narrow_phase(qb.positions, qb.rest_positions, qb.vt, qb.ee, qb.d_hat)
+    n0 = len(tab["kind"])
+    base = P.proximity.StencilTable(tab["kind"], tab["verts"], tab["sub"], tab["eps_x"])
+    R = -(-15_200_000 // len(base.family_rows(4)))
+    rep = np.repeat(np.arange(n0), R)
+    table = P.proximity.StencilTable(tab["kind"][rep], tab["verts"][rep], tab["sub"][rep], tab["eps_x"][rep])
+    params = P.barrier.BarrierParams(d_hat=qb.d_hat, kappa=qb.kappa)
+    batch = P.stencils.evaluate(table, qb.positions, params)
+    ref = o.local_quadratics_batch(tab["kind"], tab["verts"], tab["sub"], tab["eps_x"], qb.positions, qb.d_hat, qb.kappa)
+    total, inactive, bad = batch.summary()
+    assert bad == 0
+    assert abs(total - R * ref["energy"].sum()) <= 1e-9 * abs(R * ref["energy"].sum())
+    assert np.array_equal(P.device.to_host(batch.status.reshape(n0, R)[:, 0]), ref["status"])
+    entries = 0
+    for s, fam in batch.families.items():
+        nb = fam.hess.shape[0]
+        assert nb % R == 0
+        entries = max(entries, fam.hess.numel())
+        h = fam.hess.reshape(nb // R, R, 3 * s, 3 * s)
+        g = fam.grad.reshape(nb // R, R, 3 * s)
+        for lo in range(0, nb // R, 64):                                     # chunked: no multi-GB temporaries
+            assert bool((h[lo:lo + 64] == h[lo:lo + 64, :1]).all())
+            assert bool((g[lo:lo + 64] == g[lo:lo + 64, :1]).all())
+        rows = base.family_rows(s)                                           # base-table rows of this family
+        href, gref = ref["hess"][rows][:, :3 * s, :3 * s], ref["grad"][rows][:, :3 * s]
+        assert href.shape[0] == nb // R
+        h0 = P.device.to_host(h[:, 0].contiguous())
+        g0 = P.device.to_host(g[:, 0].contiguous())
+        scale = np.abs(href).reshape(len(href), -1).max(axis=1)
+        assert (np.abs(h0 - href).reshape(len(href), -1).max(axis=1) <= 1e-9 * scale + 1e-300).all()
+        gscale = np.abs(gref).max(axis=1)
+        assert (np.abs(g0 - gref).max(axis=1) <= 1e-9 * gscale + 1e-300).all()
+    assert entries > 2**31
