@@ -268,3 +268,85 @@ def test_block_offsets_beyond_2_31_elements(P):
         gscale = np.abs(gref).max(axis=1)
         assert (np.abs(g0 - gref).max(axis=1) <= 1e-9 * gscale + 1e-300).all()
     assert entries > 2**31
+
+
+def test_cloth_stack_four_times_the_bench_scale(P):
+    """Beyond configs[3]: an 8 x 180 x 180 cloth stack (259 k vertices, ~4 M contacts, ~5 M blocks) through detect ->
+    blocks -> both symbolic phases -> both numeric paths -> SpMV -> PCG (block-Jacobi and MAS).  Device-side
+    properties only plus the oracle on a strided sample of the contact table: nothing may change with the scale
+    (chunk rings over a 400 MB matrix, 32-bit descriptor fields, row slabs, domain counts)."""
+    t = P.torch
+    cloth = P.workloads.cloth_stack(layers=8, n=180, seed=3, d_hat_rel=0.2)
+    bp = P.contacts.BroadPhase(None, cloth.tris, cloth.edges, cloth.d_hat, cloth.positions)
+    vt, ee = bp.query(cloth.positions)
+    bp.close()
+    table, extra = P.contacts.narrow_phase_device(cloth.positions, cloth.rest_positions, vt, ee, cloth.d_hat)
+    assert 3.2e6 < table.n < 4.8e6, table.n
+    kind = P.device.to_host(extra.kind)
+    verts = P.device.to_host(table.verts)
+    assert bool((np.diff(kind.astype(np.int16)) >= 0).all())
+    for k in range(7):                                                          # reference order inside every kind
+        seg = verts[table.kind_off[k]:table.kind_off[k + 1]].astype(np.int64)
+        dif = np.diff(seg, axis=0)
+        first = np.argmax(dif != 0, axis=1)                                     # first differing vertex (0 on ties)
+        assert bool((dif[np.arange(len(dif)), first] >= 0).all()), k           # lexicographic, ties allowed
+    params = P.barrier.BarrierParams(d_hat=cloth.d_hat, kappa=cloth.kappa)
+    batch = P.stencils.evaluate(table, cloth.positions, params, dt=cloth.dt, want_factors=True)
+    assert batch.summary()[2] == 0
+    block_properties(P, batch)
+    rows = np.arange(0, table.n, 97)
+    ref = o.local_quadratics_batch(kind[rows], verts[rows], P.device.to_host(table.sub)[rows],
+                                   P.device.to_host(table.eps_x)[rows], cloth.positions, cloth.d_hat, cloth.kappa,
+                                   dt2=cloth.dt * cloth.dt)
+    energy = P.device.to_host(batch.energy)[rows]
+    assert np.abs(energy - ref["energy"]).max() <= 1e-9 * np.abs(ref["energy"]).max()
+    assert np.array_equal(P.device.to_host(batch.status)[rows], ref["status"])
+    fams = [batch.families[s] for s in sorted(batch.families)]
+    sysm = P.solver.NewtonSystem(cloth.masses, cloth.fixed)
+    nnzb = sysm.set_pattern([(f.s, f.vids) for f in fams])
+    assert nnzb > 4_000_000
+    rowptr_rows, colidx_rows = sysm.rowptr.clone(), sysm.colidx.clone()
+    dense_path = sysm.assemble([f.hess for f in fams]).clone()
+    factor_path = sysm.assemble_from_factors([f.fac for f in fams])
+    assert bool((dense_path == factor_path).all())                             # bitwise, ~5 M blocks
+    assert int(rowptr_rows[-1]) == nnzb and bool((rowptr_rows[1:] > rowptr_rows[:-1]).all())
+    # strictly increasing columns inside every row, diagonal present in every row
+    inner = t.ones(nnzb, dtype=t.bool, device=colidx_rows.device)
+    inner[rowptr_rows[:-1].long()] = False
+    assert bool((colidx_rows[1:] > colidx_rows[:-1])[inner[1:]].all())
+    row_of = t.repeat_interleave(t.arange(sysm.n, device=colidx_rows.device), (rowptr_rows[1:] - rowptr_rows[:-1]).long())
+    assert int((colidx_rows.long() == row_of).sum()) == sysm.n
+    # assembled SpMV == matrix-free matvec of the reference kernel seam
+    rng = np.random.default_rng(0)
+    x = P.device.to_device(rng.normal(size=3 * sysm.n))
+    y = sysm.spmv(x)
+    free = t.from_numpy(~cloth.fixed).cuda().repeat_interleave(3)
+    xm = t.where(free, x, t.zeros_like(x))
+    out = t.repeat_interleave(sysm.masses, 3) * xm
+    for f in fams:
+        P.kernels.matvec_blocks_device(f.hess, f.vids, xm, out)
+    out = t.where(free, out, x)
+    assert float((y - out).abs().max()) <= 1e-11 * float(out.abs().max())
+    w = P.device.to_device(rng.normal(size=3 * sysm.n))
+    aw = sysm.spmv(w)
+    assert abs(float(x @ aw) - float(w @ y)) <= 1e-10 * abs(float(w @ y))
+    # PCG: both preconditioners meet the reference's stopping rule on the re-evaluated residual
+    xt = P.device.to_device(cloth.positions + 1e-4 * rng.normal(size=cloth.positions.shape))
+    rhs = -sysm.gradient(cloth.positions, xt, [f.grad for f in fams])
+    pinv = sysm.block_jacobi()
+    r0 = t.where(free, rhs, t.zeros_like(rhs))
+    d0 = float(r0 @ (pinv @ r0.reshape(-1, 3, 1)).reshape(-1))
+    d, iters, ok, _, _ = sysm.pcg(rhs, 1e-4, 4000)
+    assert ok and iters > 20
+    sysm.mas_order(cloth.positions)
+    d_mas, it_mas, ok_mas, _, _ = sysm.pcg(rhs, 1e-4, 4000, preconditioner="mas")
+    assert ok_mas and 0 < it_mas < iters, (it_mas, iters)
+    for sol in (d, d_mas):
+        res = t.where(free, rhs - sysm.spmv(sol), t.zeros_like(rhs))
+        assert float(res @ (pinv @ res.reshape(-1, 3, 1)).reshape(-1)) <= 1.05e-4 * d0
+    # the sort-based symbolic phase gives the same pattern and the same matrix, bit for bit
+    sysm.set_symbolic_mode(1)
+    assert sysm.set_pattern([(f.s, f.vids) for f in fams]) == nnzb
+    assert bool((sysm.rowptr == rowptr_rows).all()) and bool((sysm.colidx == colidx_rows).all())
+    assert bool((sysm.assemble_from_factors([f.fac for f in fams]) == dense_path).all())
+    sysm.close()
