@@ -151,6 +151,14 @@ class NewtonSystem:
         self._mas_stale = True
         return self.vals
 
+    FACTOR_INDEX_BITS = 27   # element index field of the factor descriptors (assembly.cu factor_desc_kernel)
+
+    @classmethod
+    def factors_fit(cls, family_counts):
+        """True when ``assemble_from_factors`` can address every family: nb * 3 s below 2**27 elements
+        (``family_counts``: {s: nb}); beyond that the dense path (``assemble``) applies."""
+        return all(int(nb) * 3 * int(s) < (1 << cls.FACTOR_INDEX_BITS) for s, nb in family_counts.items())
+
     def assemble_from_factors(self, fam_fac):
         """Same matrix from the rank-1 factors z of the barrier blocks (hess = z z^T), without the
         dense blocks: the gathers read 24 s instead of 72 s^2 bytes per block and stay in L2."""

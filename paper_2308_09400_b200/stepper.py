@@ -259,7 +259,7 @@ def _search_direction(state, x, x_tilde, x_start, table):
     zeroed (solver.py:325-334).  Returns (direction (N,3) tensor, PCG iterations, PCG converged)."""
     cfg = state.config
     only_barrier = state.tet_mesh is None and not (state.friction_state is not None and state.friction_state.n)
-    if only_barrier and table.n:
+    if only_barrier and table.n and state.system.factors_fit({s: table.family_count(s) for s in (2, 3, 4)}):
         # barrier blocks are rank one: assemble straight from the factors z, the dense blocks are never written
         # (bitwise the same matrix, b200ipc_assemble_numeric_factors)
         batch = stencils.evaluate(table, x, cfg.barrier, dt=cfg.dt, want_energy=False, want_hess=False, want_factors=True)

@@ -197,3 +197,14 @@ def test_cube_drop_workload_is_well_formed():
     assert tris.shape == (12, 3) and edges.shape == (18, 2)                    # a cube's surface
     np.testing.assert_allclose(sc.masses[:8].sum(), 1000.0 * 0.4 ** 3)
     assert sc.fixed[72:].all() and not sc.fixed[:72].any() and sc.surf_verts.size == sc.positions.shape[0]
+
+
+def test_factor_path_limit_is_a_host_side_choice():
+    """The factor descriptors hold a 27-bit element index (assembly.cu): the stepper picks the rank-1 factor path
+    only while every family fits and assembles from the dense blocks beyond that, instead of running into the
+    C ABI's EINVAL."""
+    fit = solver.NewtonSystem.factors_fit
+    assert fit({2: 0, 3: 0, 4: 0}) and fit({2: 10**6, 3: 10**6, 4: 10**6})
+    assert fit({4: (1 << 27) // 12 - 1 + (1 if ((1 << 27) % 12) else 0)})
+    assert not fit({4: (1 << 27) // 12 + 1})
+    assert not fit({2: 1, 3: (1 << 27) // 9 + 1, 4: 1})
