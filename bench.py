@@ -624,10 +624,11 @@ def newton_section(torch, pkg, steps, warmup, peak, cloth, extras=True, cpu_leg=
 
     e2e = {}
     for prec in ("block_jacobi", "mas"):
-        newton_direction(prec)
+        for _ in range(2):   # the second call still pays first-use costs (list regrowth, descriptor tables, allocator)
+            newton_direction(prec)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        reps_e2e = 3
+        reps_e2e = 5
         for _ in range(reps_e2e):
             d_host, its_e2e, ok_e2e, energy_e2e = newton_direction(prec)
         e2e[prec] = ((time.perf_counter() - t0) * 1e3 / reps_e2e, its_e2e, ok_e2e)
