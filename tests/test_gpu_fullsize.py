@@ -350,3 +350,43 @@ def test_cloth_stack_four_times_the_bench_scale(P):
     assert bool((sysm.rowptr == rowptr_rows).all()) and bool((sysm.colidx == colidx_rows).all())
     assert bool((sysm.assemble_from_factors([f.fac for f in fams]) == dense_path).all())
     sysm.close()
+
+
+def test_stepper_direction_past_the_factor_descriptor_limit(P):
+    """24.7 M contacts (8 x 450 x 450 cloth stack, 1.62 M vertices): the four-vertex family has more than 2^27 / 12
+    blocks, so the rank-1 factor path no longer applies (its C entry point answers EINVAL).  The stepper has to see
+    that on the host (NewtonSystem.factors_fit), assemble from the dense blocks and still return a converged,
+    finite direction that solves its own system to the stopping rule."""
+    t = P.torch
+    if t.cuda.mem_get_info()[0] < 60 * 2**30:
+        pytest.skip("needs 60 GB of free device memory")
+    from paper_2308_09400_b200 import stepper
+
+    scene = P.workloads.cloth_stack(layers=8, n=450, seed=3, d_hat_rel=0.2, jitter_rel=0.01, kappa=1e5)
+    cfg = stepper.SolverConfig(dt=scene.dt, barrier=P.barrier.BarrierParams(d_hat=scene.d_hat, kappa=scene.kappa),
+                               preconditioner="mas")
+    state = stepper.SimState(scene.as_scene(), cfg)
+    try:
+        x = state.x
+        table = state.detect(x)
+        counts = {s: table.family_count(s) for s in (2, 3, 4)}
+        assert table.n > 2.2e7 and not state.system.factors_fit(counts)
+        xt = x + 1e-4 * t.randn_like(x)
+        d, iters, ok = stepper._search_direction(state, x, xt, x, table)
+        assert ok and iters > 0 and bool(t.isfinite(d).all())
+        # the direction solves the assembled system: residual in the block-Jacobi norm below the rule
+        fams = state.assemble_local_quadratics(x, x, table)
+        rhs = -state.gradient(x, xt, fams)
+        free = (~state.system.fixed.bool()).repeat_interleave(3)
+        res = t.where(free, rhs - state.system.spmv(d.reshape(-1)), t.zeros_like(rhs))
+        pinv = state.system.block_jacobi()
+        r0 = t.where(free, rhs, t.zeros_like(rhs))
+        d0 = float(r0 @ (pinv @ r0.reshape(-1, 3, 1)).reshape(-1))
+        assert float(res @ (pinv @ res.reshape(-1, 3, 1)).reshape(-1)) <= 1.05 * cfg.pcg_rel_tol * d0
+        # and the factor entry point itself refuses the table instead of wrapping its 27-bit index
+        batch = P.stencils.evaluate(table, x, cfg.barrier, dt=cfg.dt, want_energy=False, want_hess=False, want_factors=True)
+        fl = [batch.families[s] for s in sorted(batch.families)]
+        with pytest.raises(Exception):
+            state.system.assemble_from_factors([f.fac for f in fl])
+    finally:
+        state.close()
